@@ -1,0 +1,152 @@
+/* rsvd_b200.h — C-ABI of the B200-native randomized truncated SVD.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   randsvd::randomized_ksvd(const DenseMatrix&, const RsvdConfig&)
+ *       (/root/reference/proj/include/randsvd/rsvd.hpp:58, src/rsvd.cpp:150-156)
+ *   randsvd::singular_values_only(const DenseMatrix&, const RsvdConfig&)
+ *       (rsvd.hpp:62-63, rsvd.cpp:158-174)
+ * and the step functions its tests drive (rsvd.hpp:36-53). Plain pointers and
+ * sizes only: every matrix is row-major FP64 exactly like randsvd::DenseMatrix
+ * (matrix.hpp:12-31, element (i, j) at data[i * cols + j]) unless a leading
+ * dimension is given. The C++ drop-in (include/randsvd/rsvd.hpp) and the Python
+ * host mirror (paper_2110_03423_b200/rsvd.py) are thin layers over this file.
+ *
+ * Errors: every entry point returns an rsvd_b200_status. The reference's
+ * exception types map 1:1 — ArgumentError, DimensionError, ConvergenceError
+ * (errors.hpp:16-37) — plus CUDA/NCCL/allocation failures. The message of the
+ * last failure on the calling thread is rsvd_b200_last_error().
+ *
+ * Threading: a handle owns one CUDA stream and its workspace; one solve at a
+ * time per handle, independent handles are independent (cf. SPEC "safe
+ * concurrent independent solves").
+ */
+#ifndef RSVD_B200_H
+#define RSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RSVD_B200_OK = 0,
+    RSVD_B200_ARGUMENT_ERROR = 1,    /* randsvd::ArgumentError    */
+    RSVD_B200_DIMENSION_ERROR = 2,   /* randsvd::DimensionError   */
+    RSVD_B200_CONVERGENCE_ERROR = 3, /* randsvd::ConvergenceError */
+    RSVD_B200_CUDA_ERROR = 4,
+    RSVD_B200_NCCL_ERROR = 5,
+    RSVD_B200_ALLOC_ERROR = 6
+} rsvd_b200_status;
+
+/* Mirrors randsvd::RsvdConfig (rsvd.hpp:13-23) field for field. */
+typedef struct {
+    size_t k;          /* target rank, >= 1                         */
+    size_t oversample; /* p, reference default 10                   */
+    size_t power_q;    /* q, reference default 2                    */
+    uint64_t seed;     /* reference default 0                       */
+    double epsilon;    /* must lie in (0, 1); reference default 0.5 */
+    int epsilon_mode;  /* sketch width ceil(k / epsilon)            */
+} rsvd_b200_config;
+
+/* Fills the reference defaults (k = 1, p = 10, q = 2, seed 0, eps 0.5, off). */
+void rsvd_b200_config_default(rsvd_b200_config* cfg);
+
+/* RsvdConfig::sketch_width (rsvd.cpp:28-35). */
+size_t rsvd_b200_sketch_width(const rsvd_b200_config* cfg, size_t m, size_t n);
+
+typedef struct rsvd_b200_handle rsvd_b200_handle;
+
+/* Create a solver bound to CUDA device `device` (its own stream and workspace). */
+rsvd_b200_status rsvd_b200_create(int device, rsvd_b200_handle** out);
+rsvd_b200_status rsvd_b200_destroy(rsvd_b200_handle* h);
+const char* rsvd_b200_last_error(void);
+/* The handle's CUDA stream (a cudaStream_t) so callers can order work around it. */
+void* rsvd_b200_stream(rsvd_b200_handle* h);
+
+/* Validation mode: use the caller's Omega (n x s row-major, host memory) for the
+ * next solves instead of the on-device generator, making the sketch bit-identical
+ * to the reference's (rng.cpp's glibc log/sin/cos can differ from the device's in
+ * the last bit). Pass NULL to return to the device generator. */
+rsvd_b200_status rsvd_b200_set_omega(rsvd_b200_handle* h, const double* omega_host, size_t rows,
+                                     size_t cols);
+
+/* ---------------------------------------------------------------------------
+ * The drop-in entry points, host buffers (H2D/D2H inside the call):
+ *   a      m x n input (borrowed)
+ *   u      m x k, sigma k, v n x k outputs (caller allocated); sketch_width may be NULL.
+ * Wide inputs (m < n) are solved on the transpose with U/V swapped back, exactly
+ * as rsvd.cpp:150-156 does.
+ * ------------------------------------------------------------------------- */
+rsvd_b200_status rsvd_b200_randomized_ksvd(rsvd_b200_handle* h, const double* a, size_t m,
+                                           size_t n, const rsvd_b200_config* cfg, double* u,
+                                           double* sigma, double* v, size_t* sketch_width);
+
+/* sigma (k) only; bit-identical to randomized_ksvd's sigma under the same config. */
+rsvd_b200_status rsvd_b200_singular_values_only(rsvd_b200_handle* h, const double* a, size_t m,
+                                                size_t n, const rsvd_b200_config* cfg,
+                                                double* sigma);
+
+/* Same solve with every buffer already in device memory (A resident in HBM):
+ * a_dev with leading dimension lda (>= n, lda*8 a multiple of 16 bytes, 16-byte
+ * aligned base), u_dev (m x k) / v_dev (n x k) may be NULL for values-only.
+ * Work is enqueued on the handle's stream; the call returns after the solve
+ * completes (status flags are checked on the host). */
+rsvd_b200_status rsvd_b200_randomized_ksvd_device(rsvd_b200_handle* h, const double* a_dev,
+                                                  size_t m, size_t n, size_t lda,
+                                                  const rsvd_b200_config* cfg, double* u_dev,
+                                                  double* sigma_dev, double* v_dev,
+                                                  size_t* sketch_width);
+
+/* ---------------------------------------------------------------------------
+ * Step functions (rsvd.hpp:36-53), host buffers, for the reference's step-level
+ * tests.  range_basis writes the kept width to *cols_out (q must hold m x s).
+ * ------------------------------------------------------------------------- */
+rsvd_b200_status rsvd_b200_gaussian_matrix(rsvd_b200_handle* h, uint64_t seed, size_t rows,
+                                           size_t cols, double* out);
+rsvd_b200_status rsvd_b200_sketch(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
+                                  size_t s, uint64_t seed, double* y0);
+rsvd_b200_status rsvd_b200_power_iterate(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
+                                         const double* y0, size_t s, size_t q, double* w);
+rsvd_b200_status rsvd_b200_range_basis(rsvd_b200_handle* h, const double* y, size_t m, size_t s,
+                                       double* q, size_t* cols_out);
+rsvd_b200_status rsvd_b200_project_and_solve(rsvd_b200_handle* h, const double* a, size_t m,
+                                             size_t n, const double* qb, size_t sq, size_t k,
+                                             double* u, double* sigma, double* v,
+                                             size_t* sketch_width);
+
+/* ---------------------------------------------------------------------------
+ * Raw sampler stream on the device (rng.cpp:22-32), for bit-exactness tests:
+ * words / uniforms for counters first_counter .. first_counter + count - 1.
+ * ------------------------------------------------------------------------- */
+rsvd_b200_status rsvd_b200_splitmix_words(rsvd_b200_handle* h, uint64_t seed,
+                                          uint64_t first_counter, size_t count, uint64_t* out);
+rsvd_b200_status rsvd_b200_uniforms(rsvd_b200_handle* h, uint64_t seed, uint64_t first_counter,
+                                    size_t count, double* out);
+
+/* ---------------------------------------------------------------------------
+ * Instrumentation: per-stage device times (ms) of the last solve on this handle,
+ * measured with CUDA events on the handle's stream, and the dominant GEMM's
+ * launch count/total ms.  names[i] are static strings.  Returns the count.
+ * ------------------------------------------------------------------------- */
+int rsvd_b200_last_profile(rsvd_b200_handle* h, const char** names, double* ms, int max);
+/* Event timing level: 0 off (default), 1 per-stage events, 2 additionally one event
+ * pair around every launch of the passes over A (tag "gemm_A"). Adds event records only. */
+void rsvd_b200_set_profiling(rsvd_b200_handle* h, int level);
+/* Accumulated per-launch stats for a tag since the last reset: launches, summed device
+ * ms (CUDA events on the handle's stream) and summed algorithmic flops (2*m*n*s per pass).
+ * Returns 1 if the tag was seen. */
+int rsvd_b200_kernel_stats(rsvd_b200_handle* h, const char* tag, long* count, double* total_ms,
+                           double* total_flops);
+void rsvd_b200_reset_stats(rsvd_b200_handle* h);
+/* Number of kernels launched by the last solve. */
+long rsvd_b200_last_launch_count(rsvd_b200_handle* h);
+
+/* Library build identification (sm_100a). */
+const char* rsvd_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVD_B200_H */

@@ -1,0 +1,80 @@
+"""Loader for the in-tree C-ABI library paper_2110_03423_b200/_lib/librsvd_b200.so.
+
+Fails loudly when the library is missing: the product path never falls back to CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "librsvd_b200.so")
+
+# Every symbol include/rsvd_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "rsvd_b200_config_default", "rsvd_b200_sketch_width", "rsvd_b200_create",
+    "rsvd_b200_destroy", "rsvd_b200_last_error", "rsvd_b200_stream", "rsvd_b200_set_omega",
+    "rsvd_b200_randomized_ksvd", "rsvd_b200_singular_values_only",
+    "rsvd_b200_randomized_ksvd_device", "rsvd_b200_gaussian_matrix", "rsvd_b200_sketch",
+    "rsvd_b200_power_iterate", "rsvd_b200_range_basis", "rsvd_b200_project_and_solve",
+    "rsvd_b200_splitmix_words", "rsvd_b200_uniforms", "rsvd_b200_last_profile",
+    "rsvd_b200_set_profiling", "rsvd_b200_last_launch_count", "rsvd_b200_version",
+    "rsvd_b200_kernel_stats", "rsvd_b200_reset_stats",
+]
+
+
+class Config(C.Structure):
+    """rsvd_b200_config (include/rsvd_b200.h)."""
+    _fields_ = [("k", C.c_size_t), ("oversample", C.c_size_t), ("power_q", C.c_size_t),
+                ("seed", C.c_uint64), ("epsilon", C.c_double), ("epsilon_mode", C.c_int)]
+
+
+_dp = C.POINTER(C.c_double)
+_sz = C.c_size_t
+_vp = C.c_void_p
+_LIB = None
+
+
+def load() -> C.CDLL:
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2110_03423_b200.build` "
+                          "(the rSVD has no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    cfgp = C.POINTER(Config)
+    sig = {
+        "rsvd_b200_config_default": (None, [cfgp]),
+        "rsvd_b200_sketch_width": (_sz, [cfgp, _sz, _sz]),
+        "rsvd_b200_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+        "rsvd_b200_destroy": (C.c_int, [_vp]),
+        "rsvd_b200_last_error": (C.c_char_p, []),
+        "rsvd_b200_stream": (_vp, [_vp]),
+        "rsvd_b200_set_omega": (C.c_int, [_vp, _dp, _sz, _sz]),
+        "rsvd_b200_randomized_ksvd": (C.c_int, [_vp, _dp, _sz, _sz, cfgp, _dp, _dp, _dp,
+                                                C.POINTER(_sz)]),
+        "rsvd_b200_singular_values_only": (C.c_int, [_vp, _dp, _sz, _sz, cfgp, _dp]),
+        "rsvd_b200_randomized_ksvd_device": (C.c_int, [_vp, _dp, _sz, _sz, _sz, cfgp, _dp, _dp,
+                                                       _dp, C.POINTER(_sz)]),
+        "rsvd_b200_gaussian_matrix": (C.c_int, [_vp, C.c_uint64, _sz, _sz, _dp]),
+        "rsvd_b200_sketch": (C.c_int, [_vp, _dp, _sz, _sz, _sz, C.c_uint64, _dp]),
+        "rsvd_b200_power_iterate": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _sz, _sz, _dp]),
+        "rsvd_b200_range_basis": (C.c_int, [_vp, _dp, _sz, _sz, _dp, C.POINTER(_sz)]),
+        "rsvd_b200_project_and_solve": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _sz, _sz, _dp, _dp,
+                                                  _dp, C.POINTER(_sz)]),
+        "rsvd_b200_splitmix_words": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _sz,
+                                               C.POINTER(C.c_uint64)]),
+        "rsvd_b200_uniforms": (C.c_int, [_vp, C.c_uint64, C.c_uint64, _sz, _dp]),
+        "rsvd_b200_last_profile": (C.c_int, [_vp, C.POINTER(C.c_char_p), _dp, C.c_int]),
+        "rsvd_b200_set_profiling": (None, [_vp, C.c_int]),
+        "rsvd_b200_last_launch_count": (C.c_long, [_vp]),
+        "rsvd_b200_version": (C.c_char_p, []),
+        "rsvd_b200_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_long), _dp, _dp]),
+        "rsvd_b200_reset_stats": (None, [_vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _LIB = lib
+    return lib

@@ -1,0 +1,453 @@
+// FP64 tensor-core GEMMs for the rSVD hot path on B200 (sm_100a).
+//
+// The reference does every product of Algorithm 1 with one blocked CPU GEMM
+// that materialises transposed operands (gemm.cpp:48-100). Here the two
+// shapes that occur are separate kernels, both fed by TMA (128-byte swizzled
+// boxes, 4-stage mbarrier pipeline, one producer warp) and computed on the FP64
+// tensor cores with mma.sync m16n8k16 (DMMA; tcgen05 has no f64 kind):
+//
+//   ax  : Y = A * X      A row-major (M x K, lda), X given as Xt (NP x K, ldx),
+//                        Y row-major (M x NP, ldy).  Contraction over A's rows'
+//                        contiguous dimension.  Used for Y = A*Omega, Y = A*Z
+//                        (rsvd.cpp:58,70), U = Q*U_B (rsvd.cpp:105), the TRSM
+//                        Q = Y*R^-1 of CholeskyQR and the Gram B*B^T.
+//   atx : Z = A^T * W    A row-major (K x N, lda) read in place (no transpose
+//                        copy, cf. gemm.cpp:75-78), W row-major (K x NP, ldw);
+//                        output either Z^T (NP x N) or Z (N x NP).  Used for
+//                        A^T*W (rsvd.cpp:69), B = Q^T*A (rsvd.cpp:100) and the
+//                        tall Gram Y^T*Y of CholeskyQR.
+//
+// Both support split-K into fixed partial slabs that rsvd_reduce_partials
+// sums in a fixed order, so every result is deterministic run to run.
+//
+// Bank-conflict-free fragment loads from the 128B-swizzled boxes come from
+// permuting which physical k each MMA k-slot reads (the same permutation on
+// both operands, so the product is unchanged):
+//   ax : k = (t&1) + 8*(t>>1) + 2*q      (K-major A and K-major Xt)
+//   atx: k = 2*t + (q&1) + 8*(q>>1)      (M-major A and N-major W)
+// with t = lane&3 and q the 4-wide k-slot group.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvdb200 {
+
+constexpr int kBK = 32;           // k extent of one pipeline stage (two 16-wide boxes)
+constexpr int kBoxBytesRow = 128; // 16 doubles
+
+__device__ __forceinline__ int k_ax(int t, int q) { return (t & 1) + 8 * (t >> 1) + 2 * q; }
+__device__ __forceinline__ int k_atx(int t, int q) { return 2 * t + (q & 1) + 8 * (q >> 1); }
+
+__device__ __forceinline__ bool nonfinite(double x) {
+    return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;
+}
+
+// ============================================================================ ax
+template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    gemm_ax_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {K, M}, box {16, BM}
+                   const __grid_constant__ CUtensorMap mapX,  // dims {K, NP}, box {16, NP}
+                   double* __restrict__ Y, long ldy, long split_stride, int M, int k_tiles,
+                   int k_tiles_per_split, int* __restrict__ flag) {
+    constexpr int NP = NT * 8;
+    constexpr int MI = BM / WM / 16;
+    constexpr int NI = NT / WN;
+    constexpr int kConsumers = WM * WN;
+    constexpr uint32_t kABox = BM * kBoxBytesRow;
+    constexpr uint32_t kXBox = NP * kBoxBytesRow;
+    constexpr uint32_t kStage = 2 * kABox + 2 * kXBox;
+    static_assert(MI >= 1 && NI >= 1 && BM % (16 * WM) == 0 && NT % WN == 0, "tiling");
+    static_assert(kABox % 1024 == 0 && kXBox % 1024 == 0, "swizzle alignment");
+
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
+    uint64_t* empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM;
+    const int kt0 = blockIdx.y * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int n_iter = max(0, kt1 - kt0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumers) {
+        // ----------------------------------------------------------- producer
+        if (lane == 0) {
+            tma_prefetch_desc(&mapA);
+            tma_prefetch_desc(&mapX);
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                char* st = smem + s * kStage;
+                mbar_arrive_expect_tx(&full[s], kStage);
+                const int k = (kt0 + it) * kBK;
+                tma_load_2d(st, &mapA, &full[s], k, m0);
+                tma_load_2d(st + kABox, &mapA, &full[s], k + 16, m0);
+                tma_load_2d(st + 2 * kABox, &mapX, &full[s], k, 0);
+                tma_load_2d(st + 2 * kABox + kXBox, &mapX, &full[s], k + 16, 0);
+            }
+        }
+        return;
+    }
+
+    // --------------------------------------------------------------- consumers
+    const int wm = warp / WN, wn = warp % WN;
+    const int g = lane >> 2, t = lane & 3;
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+    bool bad = false;
+
+    for (int it = 0; it < n_iter; ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        const char* st = smem + s * kStage;
+#pragma unroll 1
+        for (int ks = 0; ks < 2; ++ks) {
+            const char* boxA = st + ks * kABox;
+            const char* boxX = st + 2 * kABox + ks * kXBox;
+            double a[MI][8];
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+                const int r0 = wm * (BM / WM) + mi * 16 + g;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const int row = r0 + 8 * (v & 1);
+                    a[mi][v] = lds_f64(boxA, swz128(row, k_ax(t, v >> 1)));
+                }
+            }
+            if (CHECK && wn == 0) {
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) bad |= nonfinite(a[mi][v]);
+            }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const int n = (wn * NI + ni) * 8 + g;
+                double b[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) b[v] = lds_f64(boxX, swz128(n, k_ax(t, v)));
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], a[mi], b);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (CHECK && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+
+    // --------------------------------------------------------------- epilogue
+    double* out = Y + blockIdx.y * split_stride;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int row = m0 + wm * (BM / WM) + mi * 16 + g + 8 * h;
+            if (row < M) {
+                double* yrow = out + row * ldy;
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) {
+                    const int col = (wn * NI + ni) * 8 + 2 * t;
+                    *reinterpret_cast<double2*>(yrow + col) =
+                        make_double2(acc[mi][ni][2 * h], acc[mi][ni][2 * h + 1]);
+                }
+            }
+        }
+    }
+}
+
+// =========================================================================== atx
+template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T>
+__global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
+    gemm_atx_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {N, K}, box {16, 32}
+                    const __grid_constant__ CUtensorMap mapW,  // dims {NP, K}, box {16, 32}
+                    double* __restrict__ Z, long ldz, long split_stride, int N, int k_tiles,
+                    int k_tiles_per_split) {
+    constexpr int NP = NT * 8;
+    constexpr int MI = BJ / WM / 16;
+    constexpr int NI = NT / WN;
+    constexpr int kConsumers = WM * WN;
+    constexpr int kABoxes = BJ / 16;
+    constexpr int kWBoxes = NP / 16;
+    constexpr uint32_t kBox = kBK * kBoxBytesRow;  // 4 KB: 32 rows x 16 doubles
+    constexpr uint32_t kStage = (kABoxes + kWBoxes) * kBox;
+    static_assert(NP % 16 == 0 && BJ % (16 * WM) == 0 && NT % WN == 0, "tiling");
+
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
+    uint64_t* empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j0 = blockIdx.x * BJ;
+    const int kt0 = blockIdx.y * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int n_iter = max(0, kt1 - kt0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumers);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumers) {
+        if (lane == 0) {
+            tma_prefetch_desc(&mapA);
+            tma_prefetch_desc(&mapW);
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                char* st = smem + s * kStage;
+                mbar_arrive_expect_tx(&full[s], kStage);
+                const int k = (kt0 + it) * kBK;
+#pragma unroll
+                for (int bx = 0; bx < kABoxes; ++bx)
+                    tma_load_2d(st + bx * kBox, &mapA, &full[s], j0 + 16 * bx, k);
+#pragma unroll
+                for (int bx = 0; bx < kWBoxes; ++bx)
+                    tma_load_2d(st + (kABoxes + bx) * kBox, &mapW, &full[s], 16 * bx, k);
+            }
+        }
+        return;
+    }
+
+    const int wm = warp / WN, wn = warp % WN;
+    const int g = lane >> 2, t = lane & 3;
+    double acc[MI][NI][4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    for (int it = 0; it < n_iter; ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        const char* st = smem + s * kStage;
+#pragma unroll 1
+        for (int ks = 0; ks < 2; ++ks) {
+            double a[MI][8];
+#pragma unroll
+            for (int mi = 0; mi < MI; ++mi) {
+                const char* boxA = st + (wm * (BJ / WM / 16) + mi) * kBox;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const int col = g + 8 * (v & 1);
+                    const int row = ks * 16 + k_atx(t, v >> 1);
+                    a[mi][v] = lds_f64(boxA, swz128(row, col));
+                }
+            }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const int c = (wn * NI + ni) * 8 + g;
+                const char* boxW = st + (kABoxes + (c >> 4)) * kBox;
+                double b[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int row = ks * 16 + k_atx(t, v);
+                    b[v] = lds_f64(boxW, swz128(row, c & 15));
+                }
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], a[mi], b);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    double* out = Z + blockIdx.y * split_stride;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = j0 + wm * (BJ / WM) + mi * 16 + g + 8 * h;
+            if (j < N) {
+#pragma unroll
+                for (int ni = 0; ni < NI; ++ni) {
+                    const int c = (wn * NI + ni) * 8 + 2 * t;
+                    if (OUT_T) {
+                        out[(long)c * ldz + j] = acc[mi][ni][2 * h];
+                        out[(long)(c + 1) * ldz + j] = acc[mi][ni][2 * h + 1];
+                    } else {
+                        *reinterpret_cast<double2*>(out + (long)j * ldz + c) =
+                            make_double2(acc[mi][ni][2 * h], acc[mi][ni][2 * h + 1]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Fixed-order sum of split-K slabs: out[e] = sum_s part[s * stride + e].
+__global__ void reduce_partials_kernel(const double* __restrict__ part, long stride, int splits,
+                                       double* __restrict__ out, long count) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count;
+         e += (long)gridDim.x * blockDim.x) {
+        double acc = part[e];
+        for (int s = 1; s < splits; ++s) acc += part[s * stride + e];
+        out[e] = acc;
+    }
+}
+
+// ================================================================ host launchers
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// Row-major (rows x cols, ld elements) FP64 matrix, box {16 cols, box_rows rows}, 128B swizzle.
+int make_map(CUtensorMap* map, const double* base, long rows, long cols, long ld, int box_rows) {
+    auto encode = get_encode();
+    if (!encode) return -1;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 8) & 15)) return -2;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+    cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -3;
+}
+
+template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK>
+cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
+    constexpr int NP = NT * 8;
+    constexpr size_t kStage = 2 * BM * 128 + 2 * NP * 128;
+    constexpr size_t smem = STAGES * kStage + 2 * STAGES * 8 + 1024;
+    auto kern = gemm_ax_kernel<BM, NT, WM, WN, STAGES, CHECK>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mA, mX;
+    if (make_map(&mA, p.A, p.M, p.K, p.lda, BM) || make_map(&mX, p.Xt, NP, p.K, p.ldx, NP))
+        return cudaErrorInvalidValue;
+    const int k_tiles = (int)((p.K + kBK - 1) / kBK);
+    const int splits = p.splits < 1 ? 1 : p.splits;
+    const int per = (k_tiles + splits - 1) / splits;
+    dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)splits);
+    kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mX, p.Y, p.ldy, p.split_stride, (int)p.M,
+                                                 k_tiles, per, p.flag);
+    return cudaGetLastError();
+}
+
+template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T>
+cudaError_t launch_atx_t(const GemmAtx& p, cudaStream_t st) {
+    constexpr int NP = NT * 8;
+    constexpr size_t kStage = (BJ / 16 + NP / 16) * kBK * 128;
+    constexpr size_t smem = STAGES * kStage + 2 * STAGES * 8 + 1024;
+    auto kern = gemm_atx_kernel<BJ, NT, WM, WN, STAGES, OUT_T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mA, mW;
+    if (make_map(&mA, p.A, p.K, p.N, p.lda, kBK) || make_map(&mW, p.W, p.K, NP, p.ldw, kBK))
+        return cudaErrorInvalidValue;
+    const int k_tiles = (int)((p.K + kBK - 1) / kBK);
+    const int splits = p.splits < 1 ? 1 : p.splits;
+    const int per = (k_tiles + splits - 1) / splits;
+    dim3 grid((unsigned)((p.N + BJ - 1) / BJ), (unsigned)splits);
+    kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mW, p.Z, p.ldz, p.split_stride, (int)p.N,
+                                                 k_tiles, per);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// NP (padded sketch width) dispatch. Widths up to 96 use 128-row tiles with a
+// 4x2 warp grid and 4 stages; wider sketches use 64-row tiles, 2x4 warps, 3 stages.
+template <int NT>
+cudaError_t dispatch_ax(const GemmAx& p, cudaStream_t st) {
+    if constexpr (NT <= 12) {
+        return p.flag ? launch_ax_t<128, NT, 4, 2, 4, true>(p, st)
+                      : launch_ax_t<128, NT, 4, 2, 4, false>(p, st);
+    } else {
+        return p.flag ? launch_ax_t<64, NT, 2, 4, 3, true>(p, st)
+                      : launch_ax_t<64, NT, 2, 4, 3, false>(p, st);
+    }
+}
+
+template <int NT>
+cudaError_t dispatch_atx(const GemmAtx& p, cudaStream_t st) {
+    if constexpr (NT <= 12) {
+        return p.out_transposed ? launch_atx_t<128, NT, 4, 2, 4, true>(p, st)
+                                : launch_atx_t<128, NT, 4, 2, 4, false>(p, st);
+    } else {
+        return p.out_transposed ? launch_atx_t<64, NT, 2, 4, 3, true>(p, st)
+                                : launch_atx_t<64, NT, 2, 4, 3, false>(p, st);
+    }
+}
+
+cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st) {
+    switch (p.NP / 8) {
+        case 2: return dispatch_ax<2>(p, st);
+        case 4: return dispatch_ax<4>(p, st);
+        case 6: return dispatch_ax<6>(p, st);
+        case 8: return dispatch_ax<8>(p, st);
+        case 10: return dispatch_ax<10>(p, st);
+        case 12: return dispatch_ax<12>(p, st);
+        case 16: return dispatch_ax<16>(p, st);
+        case 20: return dispatch_ax<20>(p, st);
+        case 24: return dispatch_ax<24>(p, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st) {
+    switch (p.NP / 8) {
+        case 2: return dispatch_atx<2>(p, st);
+        case 4: return dispatch_atx<4>(p, st);
+        case 6: return dispatch_atx<6>(p, st);
+        case 8: return dispatch_atx<8>(p, st);
+        case 10: return dispatch_atx<10>(p, st);
+        case 12: return dispatch_atx<12>(p, st);
+        case 16: return dispatch_atx<16>(p, st);
+        case 20: return dispatch_atx<20>(p, st);
+        case 24: return dispatch_atx<24>(p, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
+                                   long count, cudaStream_t st) {
+    const int threads = 256;
+    long blocks = (count + threads - 1) / threads;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    reduce_partials_kernel<<<(unsigned)blocks, threads, 0, st>>>(part, stride, splits, out, count);
+    return cudaGetLastError();
+}
+
+}  // namespace rsvdb200

@@ -1,0 +1,106 @@
+// Internal (C++) launch interface of the sm_100a kernels. Not part of the C-ABI:
+// include/rsvd_b200.h is the public boundary; rsvd_b200.cpp orchestrates these.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rsvdb200 {
+
+// Y = A * X.  A: M x K row-major (lda), Xt: NP x K row-major (ldx) holding X^T,
+// Y: M x NP row-major (ldy).  splits > 1 writes split slab s at Y + s*split_stride.
+// flag != nullptr additionally ORs 1 into *flag if any element of A is NaN/Inf.
+struct GemmAx {
+    const double* A;
+    long M, K, lda;
+    const double* Xt;
+    long ldx;
+    int NP;
+    double* Y;
+    long ldy;
+    int splits = 1;
+    long split_stride = 0;
+    int* flag = nullptr;
+};
+
+// Z = A^T * W.  A: K x N row-major (lda), W: K x NP row-major (ldw).
+// out_transposed: Z^T stored NP x N (ldz) else Z stored N x NP (ldz).
+struct GemmAtx {
+    const double* A;
+    long K, N, lda;
+    const double* W;
+    long ldw;
+    int NP;
+    double* Z;
+    long ldz;
+    bool out_transposed = true;
+    int splits = 1;
+    long split_stride = 0;
+};
+
+cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
+cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);
+cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
+                                   long count, cudaStream_t st);
+
+// Omega^T (NP x n, ld) for the reference's SplitMix64 + Box-Muller stream:
+// Omega(r, c) = normal #(r*s + c) of GaussianSampler(seed); rows c >= s of
+// Omega^T are zero.
+cudaError_t launch_omega(uint64_t seed, long n, int s, int NP, double* omega_t, long ld,
+                         cudaStream_t st);
+// Raw stream pieces for the bit-exactness tests.
+cudaError_t launch_splitmix_words(uint64_t seed, uint64_t first_counter, long count,
+                                  uint64_t* out, cudaStream_t st);
+cudaError_t launch_uniforms(uint64_t seed, uint64_t first_counter, long count, double* out,
+                            cudaStream_t st);
+cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double* out,
+                                     cudaStream_t st);
+
+// Small dense linear algebra, one CTA, matrices in shared memory.
+// Cholesky of the s x s Gram G (ld ldg): writes R (upper, NP x NP, ld NP, zero padded)
+// and Rinv^T (NP x NP, ld NP, zero padded: usable directly as the Xt operand of ax).
+// status[0] = 0 ok, 1 breakdown (min pivot below tol * max diag); status is int[4].
+cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
+                            int* status, double tol, cudaStream_t st);
+// out (NP x NP) = X (NP x NP) * Y (NP x NP), row-major, s-leading block only (rest zero).
+cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP, double* out,
+                                bool transpose_out, cudaStream_t st);
+// One-sided Jacobi SVD of the s x s matrix R (row-major, ld NP) with the reference's
+// thresholds (svd.cpp:35-36): sigma (s, sorted non-increasing), U (s x s -> NP x NP ld NP,
+// left vectors), W (right vectors, NP x NP ld NP).  status[0] = sweeps or -1 on no convergence.
+cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U,
+                              double* W, int* status, cudaStream_t st);
+size_t jacobi_max_width();
+
+// Sign convention (svd.cpp:237-254): for each column c < s of V (rows x NP, ld ldv),
+// if the largest-|.| entry (first index on ties) is negative, negate V[:, c] and
+// column c of Ub (NP x NP, ld NP).
+cudaError_t launch_sign_fix(double* V, long rows, long ldv, int s, double* Ub, int NP,
+                            cudaStream_t st);
+
+// out (cols x rows, ld ldo) = in^T (in: rows x cols, ld ldi).
+cudaError_t launch_transpose(const double* in, long rows, long cols, long ldi, double* out,
+                             long ldo, cudaStream_t st);
+// Copy rows x cols block between strided buffers.
+cudaError_t launch_copy2d(const double* in, long ldi, double* out, long ldo, long rows, long cols,
+                          cudaStream_t st);
+// Zero-fill.
+cudaError_t launch_fill(double* p, long count, double v, cudaStream_t st);
+// NaN/Inf scan: ORs 1 into *flag.
+cudaError_t launch_nonfinite_scan(const double* A, long rows, long cols, long lda, int* flag,
+                                  cudaStream_t st);
+
+// Cooperative (grid-synchronised) unblocked Householder QR of a tall M x s matrix
+// (row-major, ld), the CholeskyQR2 fallback. Same algorithm as qr.cpp:27-102
+// (diag R >= 0, backward Q accumulation). Q overwrites Y's first s columns? No: Q to Qout.
+cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, double* Qout,
+                                  long ldq, double* R, int NP, double* work, cudaStream_t st);
+size_t householder_work_doubles(long M, int s);
+
+// Deterministic orthonormal completion (svd.cpp:111-151): fills columns [r0, r1) of
+// U (rows x ld, row-major) by Gram-Schmidt of canonical vectors ordered by row load.
+cudaError_t launch_complete_basis(double* U, long rows, long ld, int r0, int r1, double* work,
+                                  int* status, cudaStream_t st);
+size_t complete_basis_work_doubles(long rows);
+
+}  // namespace rsvdb200

@@ -1,0 +1,231 @@
+// Gaussian sketch generator: the reference's counter-based SplitMix64 stream and
+// Box-Muller transform (rng.cpp:9-51), evaluated in parallel and written straight
+// into the transposed operand layout the ax GEMM consumes (Omega^T, NP x n).
+//
+// Stream facts restated from the reference:
+//   word(c)  = mix64(seed + c * 0x9E3779B97F4A7C15), counters start at 1 (rng.cpp:24-27)
+//   uniform  = ((word >> 11) + 1) * 2^-53 in (0, 1]                   (rng.cpp:29-32)
+//   normals come in pairs: pair p uses counters 2p+1 (u1) and 2p+2 (u2);
+//   normal 2p = r*cos(2*pi*u2), normal 2p+1 = r*sin(2*pi*u2), r = sqrt(-2 log u1)
+//   (the sine half is cached for the next draw, rng.cpp:34-46)
+//   Omega(r, c) = normal #(r*s + c) of a fresh sampler (rng.cpp:48-53, rsvd.cpp:128).
+// Words and uniforms are exact integer / power-of-two arithmetic and match the
+// reference bit for bit; sqrt and the two products are single IEEE roundings on
+// both sides. log, sin and cos are evaluated here in double-double arithmetic
+// (~104 bits) and rounded once, i.e. correctly rounded; the reference calls glibc,
+// whose results are within ~0.52 ulp, so the two agree except where glibc itself
+// misrounds (~0.2% of Omega entries, by 1 ulp; the reference's own Omega already
+// differs between glibc's FMA and non-FMA code paths). Bit-exact Omega parity is
+// available through validation mode (rsvd_b200_set_omega).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvdb200 {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z;
+}
+
+__device__ __forceinline__ uint64_t word_at(uint64_t seed, uint64_t counter) {
+    return mix64(seed + counter * 0x9E3779B97F4A7C15ULL);
+}
+
+__device__ __forceinline__ double uniform_from_word(uint64_t w) {
+    return static_cast<double>((w >> 11) + 1) * 0x1.0p-53;
+}
+
+// ------------------------------------------------ double-double arithmetic
+struct dd {
+    double hi, lo;
+};
+
+__device__ __forceinline__ dd two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+    return {s, e};
+}
+__device__ __forceinline__ dd fast_two_sum(double a, double b) {  // |a| >= |b|
+    const double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+    const double p = __dmul_rn(a, b);
+    return {p, __fma_rn(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+    dd s = two_sum(a.hi, b.hi);
+    const dd t = two_sum(a.lo, b.lo);
+    s.lo = __dadd_rn(s.lo, t.hi);
+    s = fast_two_sum(s.hi, s.lo);
+    s.lo = __dadd_rn(s.lo, t.lo);
+    return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+__device__ __forceinline__ dd dd_sub(dd a, dd b) { return dd_add(a, dd_neg(b)); }
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+    dd p = two_prod(a.hi, b.hi);
+    p.lo = __fma_rn(a.hi, b.lo, __fma_rn(a.lo, b.hi, p.lo));
+    return fast_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_mul_d(dd a, double b) {
+    dd p = two_prod(a.hi, b);
+    p.lo = __fma_rn(a.lo, b, p.lo);
+    return fast_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_div(dd a, dd b) {
+    const double q1 = __ddiv_rn(a.hi, b.hi);
+    dd r = dd_sub(a, dd_mul_d(b, q1));
+    const double q2 = __ddiv_rn(r.hi, b.hi);
+    r = dd_sub(r, dd_mul_d(b, q2));
+    const double q3 = __ddiv_rn(r.hi, b.hi);
+    return dd_add(fast_two_sum(q1, q2), dd{q3, 0.0});
+}
+
+// Correctly rounded (to ~2^-104 before the final rounding) natural log of u in (0, 1]:
+// u = 2^e m, m in [sqrt(2)/2, sqrt(2)); log m = 2 atanh(f), f = (m - 1)/(m + 1).
+__device__ double log_cr(double u) {
+    if (u == 1.0) return 0.0;
+    int e;
+    double m = frexp(u, &e);  // m in [0.5, 1)
+    if (m < 0.70710678118654752440) {
+        m *= 2.0;
+        e -= 1;
+    }
+    const dd num = {__dsub_rn(m, 1.0), 0.0};  // exact (Sterbenz)
+    const dd den = two_sum(m, 1.0);
+    const dd f = dd_div(num, den);
+    const dd f2 = dd_mul(f, f);
+    // atanh(f)/f = sum_j f^(2j) / (2j + 1), |f| <= 0.1716: 24 terms reach 2^-120
+    dd acc = dd_div(dd{1.0, 0.0}, dd{49.0, 0.0});
+    for (int j = 23; j >= 0; --j)
+        acc = dd_add(dd_mul(acc, f2), dd_div(dd{1.0, 0.0}, dd{2.0 * j + 1.0, 0.0}));
+    dd lm = dd_mul(dd_mul_d(f, 2.0), acc);
+    const dd ln2 = {0.69314718055994528623, 2.3190468138462996e-17};
+    return dd_add(dd_mul_d(ln2, (double)e), lm).hi;
+}
+
+// Correctly rounded sin and cos of x in [0, 2*pi]: reduce by pi/2 with a
+// triple-double pi/2, then Taylor series in double-double.
+__device__ void sincos_cr(double x, double* sn, double* cs) {
+    const double p1 = 1.5707963267948966192, p2 = 6.123233995736766036e-17,
+                 p3 = -1.4973849048591698e-33;
+    const double kq = rint(x * 0.63661977236758134308);
+    dd r = dd_sub(dd{x, 0.0}, two_prod(kq, p1));
+    r = dd_sub(r, two_prod(kq, p2));
+    r = dd_sub(r, dd{kq * p3, 0.0});
+    const dd r2 = dd_mul(r, r);
+    // sin r = r * sum (-1)^j r^(2j) / (2j+1)!,  cos r = sum (-1)^j r^(2j) / (2j)!, j <= 15
+    dd inv_fact[32];
+    inv_fact[0] = dd{1.0, 0.0};
+    for (int n = 1; n < 32; ++n) inv_fact[n] = dd_div(inv_fact[n - 1], dd{(double)n, 0.0});
+    dd s = inv_fact[31], c = inv_fact[30];
+    for (int j = 14; j >= 0; --j) {
+        s = dd_add(dd_neg(dd_mul(s, r2)), inv_fact[2 * j + 1]);
+        c = dd_add(dd_neg(dd_mul(c, r2)), inv_fact[2 * j]);
+    }
+    s = dd_mul(s, r);
+    const int q = ((int)kq) & 3;
+    double sv = s.hi, cv = c.hi;
+    switch (q) {
+        case 0: *sn = sv; *cs = cv; break;
+        case 1: *sn = cv; *cs = -sv; break;
+        case 2: *sn = -sv; *cs = -cv; break;
+        default: *sn = -cv; *cs = sv; break;
+    }
+}
+
+// Both normals of pair p.
+__device__ __forceinline__ void box_muller_pair(uint64_t seed, uint64_t p, double& n0,
+                                                double& n1) {
+    const double u1 = uniform_from_word(word_at(seed, 2 * p + 1));
+    const double u2 = uniform_from_word(word_at(seed, 2 * p + 2));
+    const double radius = __dsqrt_rn(__dmul_rn(-2.0, log_cr(u1)));
+    const double angle = __dmul_rn(2.0 * 3.14159265358979323846, u2);
+    double s, c;
+    sincos_cr(angle, &s, &c);
+    n0 = __dmul_rn(radius, c);
+    n1 = __dmul_rn(radius, s);
+}
+
+__global__ void omega_t_kernel(uint64_t seed, long n, int s, int NP, double* __restrict__ out,
+                               long ld) {
+    const long total = n * (long)s;
+    const long pairs = (total + 1) / 2;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < pairs;
+         p += (long)gridDim.x * blockDim.x) {
+        double v0, v1;
+        box_muller_pair(seed, (uint64_t)p, v0, v1);
+        const long i0 = 2 * p;
+        out[(i0 % s) * ld + i0 / s] = v0;
+        const long i1 = i0 + 1;
+        if (i1 < total) out[(i1 % s) * ld + i1 / s] = v1;
+    }
+    // zero the padding rows s..NP-1 of Omega^T
+    const long pad = (long)(NP - s) * n;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < pad;
+         e += (long)gridDim.x * blockDim.x)
+        out[(s + e / n) * ld + e % n] = 0.0;
+}
+
+__global__ void gaussian_rowmajor_kernel(uint64_t seed, long total, double* __restrict__ out) {
+    const long pairs = (total + 1) / 2;
+    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < pairs;
+         p += (long)gridDim.x * blockDim.x) {
+        double v0, v1;
+        box_muller_pair(seed, (uint64_t)p, v0, v1);
+        out[2 * p] = v0;
+        if (2 * p + 1 < total) out[2 * p + 1] = v1;
+    }
+}
+
+__global__ void words_kernel(uint64_t seed, uint64_t first, long count, uint64_t* out) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count;
+         i += (long)gridDim.x * blockDim.x)
+        out[i] = word_at(seed, first + (uint64_t)i);
+}
+
+__global__ void uniforms_kernel(uint64_t seed, uint64_t first, long count, double* out) {
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count;
+         i += (long)gridDim.x * blockDim.x)
+        out[i] = uniform_from_word(word_at(seed, first + (uint64_t)i));
+}
+
+static unsigned grid_for(long work, int threads) {
+    long b = (work + threads - 1) / threads;
+    if (b > 148L * 16) b = 148L * 16;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_omega(uint64_t seed, long n, int s, int NP, double* omega_t, long ld,
+                         cudaStream_t st) {
+    const long work = (n * (long)s + 1) / 2;
+    omega_t_kernel<<<grid_for(work, 256), 256, 0, st>>>(seed, n, s, NP, omega_t, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double* out,
+                                     cudaStream_t st) {
+    const long total = rows * cols;
+    gaussian_rowmajor_kernel<<<grid_for((total + 1) / 2, 256), 256, 0, st>>>(seed, total, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_splitmix_words(uint64_t seed, uint64_t first_counter, long count,
+                                  uint64_t* out, cudaStream_t st) {
+    words_kernel<<<grid_for(count, 256), 256, 0, st>>>(seed, first_counter, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_uniforms(uint64_t seed, uint64_t first_counter, long count, double* out,
+                            cudaStream_t st) {
+    uniforms_kernel<<<grid_for(count, 256), 256, 0, st>>>(seed, first_counter, count, out);
+    return cudaGetLastError();
+}
+
+}  // namespace rsvdb200

@@ -1,0 +1,293 @@
+"""Python host mirror of the reference API over the C-ABI (include/rsvd_b200.h).
+
+Same names, argument meaning and error behaviour as the reference's C++ entry points
+(/root/reference/proj/include/randsvd/rsvd.hpp:13-63): ``RsvdConfig``,
+``randomized_ksvd``, ``singular_values_only``, ``sketch``, ``power_iterate``,
+``range_basis``, ``project_and_solve``; failures raise ``ArgumentError``,
+``DimensionError`` or ``ConvergenceError`` like errors.hpp:16-37. Matrices are
+row-major float64 numpy arrays (host) or CUDA torch tensors (device path).
+
+Every call runs the sm_100a kernels in ``_lib/librsvd_b200.so``; there is no CPU
+fallback. If the library or a B200 is missing the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+class Error(RuntimeError):
+    """randsvd::Error"""
+
+
+class ArgumentError(Error):
+    """randsvd::ArgumentError"""
+
+
+class DimensionError(Error):
+    """randsvd::DimensionError"""
+
+
+class ConvergenceError(Error):
+    """randsvd::ConvergenceError"""
+
+
+class DeviceError(Error):
+    """CUDA / NCCL / allocation failure (no reference counterpart)."""
+
+
+_STATUS = {1: ArgumentError, 2: DimensionError, 3: ConvergenceError}
+
+
+def _check(lib, st: int) -> None:
+    if st != 0:
+        msg = lib.rsvd_b200_last_error().decode()
+        raise _STATUS.get(st, DeviceError)(msg)
+
+
+@dataclass
+class RsvdConfig:
+    """randsvd::RsvdConfig (rsvd.hpp:13-23) with the reference defaults."""
+    k: int = 1
+    oversample: int = 10
+    power_q: int = 2
+    seed: int = 0
+    epsilon: float = 0.5
+    epsilon_mode: bool = False
+
+    def sketch_width(self, m: int, n: int) -> int:
+        cap = min(m, n)
+        if self.epsilon_mode:
+            import math
+            return min(int(math.ceil(self.k / self.epsilon)), cap)
+        return min(self.k + self.oversample, cap)
+
+    def _c(self) -> _lib.Config:
+        return _lib.Config(self.k, self.oversample, self.power_q, self.seed & (2**64 - 1),
+                           self.epsilon, int(bool(self.epsilon_mode)))
+
+
+@dataclass
+class SvdFactors:
+    u: np.ndarray
+    sigma: np.ndarray
+    v: np.ndarray
+
+
+@dataclass
+class RsvdResult:
+    factors: SvdFactors
+    sketch_width: int = 0
+
+    def residual_fro(self, a) -> float:
+        """||a - u diag(sigma) v^T||_F (rsvd.cpp:37-49), evaluated with numpy on the host."""
+        a = np.asarray(a, dtype=np.float64)
+        f = self.factors
+        if f.u.shape[0] != a.shape[0] or f.v.shape[0] != a.shape[1]:
+            raise DimensionError(f"residual_fro: factors for {f.u.shape[0]}x{f.v.shape[0]} "
+                                 f"against input {a.shape[0]}x{a.shape[1]}")
+        return float(np.linalg.norm(a - (f.u * f.sigma) @ f.v.T))
+
+
+def _arr(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise DimensionError(f"DenseMatrix requires rows >= 1 and cols >= 1, got shape {a.shape}")
+    return a
+
+
+def _dp(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Solver:
+    """One rsvd_b200_handle: a CUDA device, its stream and HBM workspace."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        _check(self.lib, self.lib.rsvd_b200_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.rsvd_b200_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- options
+    def set_omega(self, omega: np.ndarray | None) -> None:
+        """Validation mode: consume this Omega (n x s) instead of the device generator."""
+        if omega is None:
+            _check(self.lib, self.lib.rsvd_b200_set_omega(self.h, None, 0, 0))
+            return
+        om = _arr(omega)
+        _check(self.lib, self.lib.rsvd_b200_set_omega(self.h, _dp(om), om.shape[0], om.shape[1]))
+
+    def set_profiling(self, level: int) -> None:
+        self.lib.rsvd_b200_set_profiling(self.h, int(level))
+
+    def kernel_stats(self, tag: str = "gemm_A") -> dict:
+        cnt, ms, fl = C.c_long(0), C.c_double(0), C.c_double(0)
+        self.lib.rsvd_b200_kernel_stats(self.h, tag.encode(), C.byref(cnt), C.byref(ms),
+                                        C.byref(fl))
+        return {"count": cnt.value, "ms": ms.value, "flops": fl.value}
+
+    def reset_stats(self) -> None:
+        self.lib.rsvd_b200_reset_stats(self.h)
+
+    def last_profile(self) -> dict:
+        names = (C.c_char_p * 32)()
+        ms = (C.c_double * 32)()
+        n = self.lib.rsvd_b200_last_profile(self.h, names, ms, 32)
+        return {names[i].decode(): ms[i] for i in range(n)}
+
+    def last_launch_count(self) -> int:
+        return int(self.lib.rsvd_b200_last_launch_count(self.h))
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.rsvd_b200_stream(self.h) or 0)
+
+    # --------------------------------------------------------------- hot path
+    def randomized_ksvd(self, a, cfg: RsvdConfig) -> RsvdResult:
+        a = _arr(a)
+        m, n = a.shape
+        k = max(int(cfg.k), 1)
+        u = np.empty((m, k))
+        v = np.empty((n, k))
+        s = np.empty(k)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        _check(self.lib, self.lib.rsvd_b200_randomized_ksvd(self.h, _dp(a), m, n, C.byref(c),
+                                                            _dp(u), _dp(s), _dp(v), C.byref(sw)))
+        return RsvdResult(SvdFactors(u, s, v), sw.value)
+
+    def singular_values_only(self, a, cfg: RsvdConfig) -> np.ndarray:
+        a = _arr(a)
+        m, n = a.shape
+        s = np.empty(max(int(cfg.k), 1))
+        c = cfg._c()
+        _check(self.lib, self.lib.rsvd_b200_singular_values_only(self.h, _dp(a), m, n, C.byref(c),
+                                                                 _dp(s)))
+        return s[: cfg.k]
+
+    def randomized_ksvd_device(self, a, cfg: RsvdConfig, values_only: bool = False):
+        """A already resident in HBM (a CUDA float64 torch tensor, row-major, possibly with a
+        leading-dimension stride). Returns (u, sigma, v, sketch_width) as CUDA tensors."""
+        import torch
+        assert a.is_cuda and a.dtype == torch.float64 and a.dim() == 2 and a.stride(1) == 1
+        m, n = a.shape
+        k = int(cfg.k)
+        dev = a.device
+        sig = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+        u = None if values_only else torch.empty((m, max(k, 1)), dtype=torch.float64, device=dev)
+        v = None if values_only else torch.empty((n, max(k, 1)), dtype=torch.float64, device=dev)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        dptr = lambda t: None if t is None else C.cast(t.data_ptr(), C.POINTER(C.c_double))
+        _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_device(
+            self.h, dptr(a), m, n, a.stride(0), C.byref(c), dptr(u), dptr(sig), dptr(v),
+            C.byref(sw)))
+        return u, sig[:k], v, sw.value
+
+    # ---------------------------------------------------------- step functions
+    def gaussian_matrix(self, seed: int, rows: int, cols: int) -> np.ndarray:
+        out = np.empty((rows, cols))
+        _check(self.lib, self.lib.rsvd_b200_gaussian_matrix(self.h, seed & (2**64 - 1), rows,
+                                                            cols, _dp(out)))
+        return out
+
+    def splitmix_words(self, seed: int, count: int, first_counter: int = 1) -> np.ndarray:
+        out = np.empty(count, dtype=np.uint64)
+        _check(self.lib, self.lib.rsvd_b200_splitmix_words(
+            self.h, seed & (2**64 - 1), first_counter, count,
+            out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return out
+
+    def uniforms(self, seed: int, count: int, first_counter: int = 1) -> np.ndarray:
+        out = np.empty(count)
+        _check(self.lib, self.lib.rsvd_b200_uniforms(self.h, seed & (2**64 - 1), first_counter,
+                                                     count, _dp(out)))
+        return out
+
+    def sketch(self, a, s: int, seed: int) -> np.ndarray:
+        a = _arr(a)
+        y = np.empty((a.shape[0], max(int(s), 1)))
+        _check(self.lib, self.lib.rsvd_b200_sketch(self.h, _dp(a), a.shape[0], a.shape[1], s,
+                                                   seed & (2**64 - 1), _dp(y)))
+        return y
+
+    def power_iterate(self, a, y0, q: int) -> np.ndarray:
+        a, y0 = _arr(a), _arr(y0)
+        if y0.shape[0] != a.shape[0]:
+            raise DimensionError(f"power_iterate: y0 has {y0.shape[0]} rows, a has {a.shape[0]}")
+        w = np.empty_like(y0)
+        _check(self.lib, self.lib.rsvd_b200_power_iterate(self.h, _dp(a), a.shape[0], a.shape[1],
+                                                          _dp(y0), y0.shape[1], q, _dp(w)))
+        return w
+
+    def range_basis(self, y) -> np.ndarray:
+        y = _arr(y)
+        q = np.empty(y.size)
+        cols = C.c_size_t(0)
+        _check(self.lib, self.lib.rsvd_b200_range_basis(self.h, _dp(y), y.shape[0], y.shape[1],
+                                                        _dp(q), C.byref(cols)))
+        return q[: y.shape[0] * cols.value].reshape(y.shape[0], cols.value)
+
+    def project_and_solve(self, a, qbasis, k: int) -> RsvdResult:
+        a, qb = _arr(a), _arr(qbasis)
+        m, n = a.shape
+        kk = max(int(k), 1)
+        u, s, v = np.empty((m, kk)), np.empty(kk), np.empty((n, kk))
+        sw = C.c_size_t(0)
+        _check(self.lib, self.lib.rsvd_b200_project_and_solve(
+            self.h, _dp(a), m, n, _dp(qb), qb.shape[1], k, _dp(u), _dp(s), _dp(v), C.byref(sw)))
+        return RsvdResult(SvdFactors(u, s, v), sw.value)
+
+
+_default: Solver | None = None
+
+
+def default_solver() -> Solver:
+    global _default
+    if _default is None:
+        _default = Solver(int(os.environ.get("RSVD_B200_DEVICE", "0")))
+    return _default
+
+
+def randomized_ksvd(a, cfg: RsvdConfig) -> RsvdResult:
+    """randsvd::randomized_ksvd (rsvd.hpp:58) on the B200."""
+    return default_solver().randomized_ksvd(a, cfg)
+
+
+def singular_values_only(a, cfg: RsvdConfig) -> np.ndarray:
+    """randsvd::singular_values_only (rsvd.hpp:62-63) on the B200."""
+    return default_solver().singular_values_only(a, cfg)
+
+
+def sketch(a, s: int, seed: int) -> np.ndarray:
+    return default_solver().sketch(a, s, seed)
+
+
+def power_iterate(a, y0, q: int) -> np.ndarray:
+    return default_solver().power_iterate(a, y0, q)
+
+
+def range_basis(y) -> np.ndarray:
+    return default_solver().range_basis(y)
+
+
+def project_and_solve(a, qbasis, k: int) -> RsvdResult:
+    return default_solver().project_and_solve(a, qbasis, k)

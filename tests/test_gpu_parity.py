@@ -1,0 +1,278 @@
+"""GPU parity of the B200 rSVD against the reference (golden fixtures) and the oracle.
+
+Tolerances (BASELINE.json north_star, FP64): Omega bit-exact (validation mode; the device
+generator's words/uniforms are bit-exact and its normals are correctly rounded),
+singular values within 1e-10 relative, U and V subspaces within a principal angle of 1e-8.
+Singular values at the noise floor (<= 1e-13 sigma_1, exact low-rank inputs) are compared
+with an absolute tolerance of 1e-12 sigma_1 since their relative value is noise on both sides.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, principal_angle
+
+pytestmark = pytest.mark.gpu
+
+SIG_RTOL = 1e-10
+ANGLE_TOL = 1e-8
+
+
+def cfg_of(c):
+    import paper_2110_03423_b200 as P
+    return P.RsvdConfig(k=c["k"], oversample=c["oversample"], power_q=c["power_q"],
+                        seed=c["seed"], epsilon=c["epsilon"], epsilon_mode=c["epsilon_mode"])
+
+
+def check_against(res, sigma, u, v, name):
+    s = res.factors.sigma
+    assert s.shape == sigma.shape, name
+    floor = 1e-13 * sigma[0]
+    live = sigma > floor
+    rel = np.abs(s[live] - sigma[live]) / np.abs(sigma[live])
+    assert rel.max() <= SIG_RTOL, (name, rel.max())
+    assert np.all(np.abs(s[~live] - sigma[~live]) <= 1e-12 * sigma[0]), name
+    assert np.all(np.diff(s) <= 0), name
+    # subspaces are compared on the leading block that ends at a spectral gap (a
+    # degenerate cluster, e.g. the identity, has no unique singular subspace)
+    nl = int(live.sum())
+    while nl > 0 and nl < len(sigma) and sigma[nl - 1] <= sigma[nl] * (1 + 1e-6):
+        nl -= 1
+    if nl > 0:
+        assert principal_angle(res.factors.u[:, :nl], u[:, :nl]) <= ANGLE_TOL, name
+        assert principal_angle(res.factors.v[:, :nl], v[:, :nl]) <= ANGLE_TOL, name
+    k = u.shape[1]
+    assert np.abs(res.factors.u.T @ res.factors.u - np.eye(k)).max() <= 1e-10, name
+    assert np.abs(res.factors.v.T @ res.factors.v - np.eye(k)).max() <= 1e-10, name
+
+
+# ------------------------------------------------------------------ sampler
+def test_words_and_uniforms_bit_exact(solver, kat):
+    g = np.load(os.path.join(GOLDEN, "sampler.npz"))
+    assert int(solver.splitmix_words(0, 1)[0]) == 0xE220A8397B1DCDAF
+    assert np.array_equal(solver.splitmix_words(0, 1024), g["words_seed0"])
+    assert np.array_equal(solver.splitmix_words(42, 1024), g["words_seed42"])
+    assert np.array_equal(solver.uniforms(7, 4096), g["uniforms_seed7"])
+    # arbitrary counter offsets (the device evaluates the stream at any position)
+    assert np.array_equal(solver.splitmix_words(42, 16, first_counter=1009),
+                          g["words_seed42"][1008:1024])
+
+
+def test_device_normals_vs_reference(solver):
+    g = np.load(os.path.join(GOLDEN, "sampler.npz"))
+    for key, (seed, r, c) in {"omega_s42_1024x74": (42, 1024, 74), "omega_s3_5x2": (3, 5, 2),
+                              "omega_s9_1001x7": (9, 1001, 7)}.items():
+        dev = solver.gaussian_matrix(seed, r, c)
+        ref = g[key]
+        ulp = np.abs(dev.view(np.int64) - ref.view(np.int64))
+        assert ulp.max() <= 2, key
+        assert np.mean(dev != ref) < 0.005, key  # glibc misrounds ~0.1-0.2%
+
+
+def test_device_normals_correctly_rounded(solver, port):
+    mp = pytest.importorskip("mpmath")
+    import math
+    mp.mp.prec = 200
+    count = 1500
+    w = port.uniforms(42, 2 * count)
+    dev = solver.gaussian_matrix(42, 1, 2 * count).ravel()
+    exact = np.empty(2 * count)
+    for p in range(count):
+        radius = math.sqrt(-2.0 * float(mp.log(mp.mpf(w[2 * p]))))
+        angle = (2.0 * math.pi) * w[2 * p + 1]
+        exact[2 * p] = radius * float(mp.cos(mp.mpf(angle)))
+        exact[2 * p + 1] = radius * float(mp.sin(mp.mpf(angle)))
+    assert np.array_equal(dev, exact)
+
+
+def test_sketch_of_identity_is_omega(solver):
+    # test_rsvd.cpp:46-52; with the device generator up to the libm last bit, in
+    # validation mode bit for bit
+    s = np.load(os.path.join(GOLDEN, "steps.npz"))
+    y = solver.sketch(np.eye(5), 2, 3)
+    assert np.abs(y - s["sketch_identity"]).max() <= 4.5e-16 * np.abs(y).max()
+    solver.set_omega(s["sketch_identity"])
+    try:
+        assert np.array_equal(solver.sketch(np.eye(5), 2, 3), s["sketch_identity"])
+    finally:
+        solver.set_omega(None)
+
+
+# ------------------------------------------------------------------ full solve
+def test_rsvd_golden(solver, golden_cases):
+    for c, d in golden_cases:
+        res = solver.randomized_ksvd(d["a"], cfg_of(c))
+        assert res.sketch_width == int(d["sketch_width"]), c["name"]
+        check_against(res, d["sigma"], d["u"], d["v"], c["name"])
+
+
+def test_rsvd_golden_validation_mode(solver, golden_cases):
+    for c, d in golden_cases:
+        solver.set_omega(d["omega"])
+        try:
+            res = solver.randomized_ksvd(d["a"], cfg_of(c))
+        finally:
+            solver.set_omega(None)
+        check_against(res, d["sigma"], d["u"], d["v"], c["name"] + "/validation")
+
+
+def test_values_only_bit_identical(solver, golden_cases):
+    for c, d in golden_cases:
+        full = solver.randomized_ksvd(d["a"], cfg_of(c))
+        sv = solver.singular_values_only(d["a"], cfg_of(c))
+        assert np.array_equal(sv, full.factors.sigma), c["name"]
+
+
+def test_determinism_bit_for_bit(solver, golden_cases):
+    c, d = golden_cases[4]
+    r1 = solver.randomized_ksvd(d["a"], cfg_of(c))
+    r2 = solver.randomized_ksvd(d["a"], cfg_of(c))
+    assert np.array_equal(r1.factors.u, r2.factors.u)
+    assert np.array_equal(r1.factors.v, r2.factors.v)
+    assert np.array_equal(r1.factors.sigma, r2.factors.sigma)
+
+
+def test_transpose_consistency(solver, port):
+    import paper_2110_03423_b200 as P
+    a = port.gaussian_matrix(13, 40, 25)
+    cfg = P.RsvdConfig(k=5, seed=11)
+    tall = solver.randomized_ksvd(a, cfg)
+    wide = solver.randomized_ksvd(a.T.copy(), cfg)
+    # the wide solve runs on the device transpose: same kernels, same bits
+    assert np.array_equal(wide.factors.u, tall.factors.v)
+    assert np.array_equal(wide.factors.v, tall.factors.u)
+
+
+@pytest.mark.parametrize("m,n,k,q", [(4096, 4096, 64, 2), (3000, 700, 40, 1), (777, 333, 17, 3),
+                                     (2500, 1200, 100, 2)])
+def test_rsvd_vs_oracle_sizes(solver, port, m, n, k, q):
+    import paper_2110_03423_b200 as P
+    rng = np.random.default_rng(m + n)
+    r = min(m, n)
+    uu, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    sig = np.exp(-np.arange(r) * (np.log(1e4) / (k + 10)))  # sigma_1/sigma_s = 1e4
+    a = (uu * sig) @ vv.T
+    res = solver.randomized_ksvd(a, P.RsvdConfig(k=k, power_q=q, seed=42))
+    ref = port.randomized_ksvd(a, k, power_q=q, seed=42)
+    check_against(res, ref.sigma, ref.u, ref.v, f"{m}x{n}")
+
+
+# ------------------------------------------------------------------ step functions
+def test_steps(solver, port):
+    s = np.load(os.path.join(GOLDEN, "steps.npz"))
+    q = solver.range_basis(s["dup"])  # test_rsvd.cpp:122-129: duplicate column dropped
+    assert q.shape == (15, 1)
+    assert np.abs(q.T @ q - 1).max() < 1e-14
+    assert principal_angle(q, s["dup_basis"]) < 1e-12
+    qr = solver.range_basis(s["y_rand"])
+    assert qr.shape == s["y_rand_basis"].shape
+    assert np.abs(qr - s["y_rand_basis"]).max() < 1e-13  # same sign convention (diag R >= 0)
+    y = np.zeros((4, 2))
+    y[0, 0] = y[1, 1] = 1.0
+    assert np.abs(solver.range_basis(y) - y).max() == 0.0  # test_rsvd.cpp:114-120
+    w1 = solver.power_iterate(s["a20"], s["y0"], 1)
+    assert principal_angle(w1, s["w_q1"]) < 1e-10
+    w0 = solver.power_iterate(s["a20"], s["y0"], 0)
+    assert np.abs(w0 - s["w_q0"]).max() < 1e-13
+    a = np.diag([5.0, 3.0, 1.0])
+    qb = np.zeros((3, 2))
+    qb[0, 0] = qb[1, 1] = 1.0
+    res = solver.project_and_solve(a, qb, 2)  # test_rsvd.cpp:138-147
+    assert abs(res.factors.sigma[0] - 5.0) <= 5e-13 and abs(res.factors.sigma[1] - 3.0) <= 3e-13
+
+
+# ------------------------------------------------------------------ error contract
+def test_errors(solver):
+    import paper_2110_03423_b200 as P
+    a = np.eye(10)
+    for k in (0, 11):
+        with pytest.raises(P.ArgumentError):
+            solver.randomized_ksvd(a, P.RsvdConfig(k=k))
+    with pytest.raises(P.ArgumentError):
+        solver.randomized_ksvd(a, P.RsvdConfig(k=1, epsilon=1.0))
+    for bad in (np.nan, np.inf, -np.inf):
+        b = np.random.default_rng(0).standard_normal((300, 200))
+        b[123, 45] = bad
+        with pytest.raises(P.ArgumentError, match="NaN or Inf"):
+            solver.randomized_ksvd(b, P.RsvdConfig(k=5))
+    with pytest.raises(P.ArgumentError):
+        solver.sketch(np.zeros((10, 6)), 7, 0)
+    with pytest.raises(P.DimensionError):
+        solver.power_iterate(np.zeros((10, 5)), np.zeros((9, 3)), 1)
+    with pytest.raises(P.ArgumentError):
+        solver.project_and_solve(np.eye(6), np.eye(6)[:, :3], 4)
+    # the solver stays usable after errors
+    r = solver.randomized_ksvd(np.diag([3.0, 2.0, 1.0]), P.RsvdConfig(k=2, seed=3))
+    assert abs(r.factors.sigma[0] - 3.0) < 1e-12
+
+
+def test_zero_matrix(solver):
+    import paper_2110_03423_b200 as P
+    y = solver.sketch(np.zeros((10, 8)), 3, 1)  # test_rsvd.cpp:54-58
+    assert np.abs(y).max() == 0.0
+    r = solver.randomized_ksvd(np.zeros((30, 20)), P.RsvdConfig(k=3))
+    assert np.all(r.factors.sigma == 0.0)
+
+
+# ------------------------------------------------------------------ robust paths
+def test_householder_fallback_ill_conditioned(solver, port):
+    """cond(Y) >> 1e6 forces the CholeskyQR2 -> Householder fallback (q = 0 keeps the
+    sketch's conditioning); results still match the reference."""
+    import paper_2110_03423_b200 as P
+    rng = np.random.default_rng(5)
+    m, n, k = 600, 300, 20
+    uu, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = 10.0 ** (-np.arange(n) * 12.0 / 29)  # 1e-12 range across the sketch
+    a = (uu * sig) @ vv.T
+    res = solver.randomized_ksvd(a, P.RsvdConfig(k=k, power_q=0, seed=4))
+    ref = port.randomized_ksvd(a, k, power_q=0, seed=4)
+    lead = 8  # singular values well above the eps * sigma_1 floor
+    rel = np.abs(res.factors.sigma[:lead] - ref.sigma[:lead]) / ref.sigma[:lead]
+    assert rel.max() <= SIG_RTOL
+    assert principal_angle(res.factors.u[:, :lead], ref.u[:, :lead]) <= ANGLE_TOL
+    assert np.abs(res.factors.u.T @ res.factors.u - np.eye(k)).max() <= 1e-10
+
+
+def test_lowrank_beyond_rank(solver, port):
+    import paper_2110_03423_b200 as P
+    a = port.gemm(1.0, port.gaussian_matrix(55, 80, 4), False, port.gaussian_matrix(56, 4, 50),
+                  False)
+    r = solver.randomized_ksvd(a, P.RsvdConfig(k=6, seed=8))
+    assert r.factors.sigma[4] <= 1e-13 * r.factors.sigma[0]
+    assert r.factors.sigma[5] <= 1e-13 * r.factors.sigma[0]
+    assert r.residual_fro(a) / np.linalg.norm(a) <= 1e-10
+    assert np.abs(r.factors.u.T @ r.factors.u - np.eye(6)).max() <= 1e-10
+    assert np.abs(r.factors.v.T @ r.factors.v - np.eye(6)).max() <= 1e-10
+
+
+# ------------------------------------------------------------------ device path, full size
+def test_c2_device_properties(solver):
+    """BASELINE config C2 (202599 x 4096, k=64, p=10, q=2) at full size: size-independent
+    properties (the CPU oracle needs minutes here): planted spectrum recovered, factors
+    orthonormal, values-only bit-identical, deterministic."""
+    torch = pytest.importorskip("torch")
+    import paper_2110_03423_b200 as P
+    m, n, k = 202599, 4096, 64
+    g = torch.Generator(device="cuda").manual_seed(0)
+    # A = U diag(s) V^T with U = orthonormal m x 70 slice, V = n x 70 (rank 70 < s = 74,
+    # so the sketch captures the range exactly and sigma is recovered to rounding)
+    r = 70
+    uu = torch.linalg.qr(torch.randn(m, r, dtype=torch.float64, device="cuda", generator=g))[0]
+    vv = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device="cuda", generator=g))[0]
+    sig = torch.exp(-torch.arange(r, dtype=torch.float64, device="cuda") / 10.0)
+    a = (uu * sig) @ vv.T
+    cfg = P.RsvdConfig(k=k, oversample=10, power_q=2, seed=42)
+    u, s, v, sw = solver.randomized_ksvd_device(a, cfg)
+    assert sw == 74
+    rel = ((s - sig[:k]).abs() / sig[:k]).max().item()
+    assert rel < 1e-10
+    eye = torch.eye(k, dtype=torch.float64, device="cuda")
+    assert (u.T @ u - eye).abs().max().item() < 1e-10
+    assert (v.T @ v - eye).abs().max().item() < 1e-10
+    _, s2, _, _ = solver.randomized_ksvd_device(a, cfg, values_only=True)
+    assert torch.equal(s, s2)
+    u3, s3, v3, _ = solver.randomized_ksvd_device(a, cfg)
+    assert torch.equal(u, u3) and torch.equal(v, v3)
