@@ -143,6 +143,13 @@ void rsvd_b200_reset_stats(rsvd_b200_handle* h);
 /* Number of kernels launched by the last solve. */
 long rsvd_b200_last_launch_count(rsvd_b200_handle* h);
 
+/* Diagnostics of the last solve: "jacobi_sweeps", "householder_fallbacks",
+ * "robust_reruns" (optimistic pipeline repeated on the robust path), "launches".
+ * Returns -1 for an unknown key. */
+long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key);
+/* Force the robust path (host-checked Cholesky, Householder fallback) for every solve. */
+void rsvd_b200_set_robust(rsvd_b200_handle* h, int on);
+
 /* Library build identification (sm_100a). */
 const char* rsvd_b200_version(void);
 

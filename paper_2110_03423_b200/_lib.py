@@ -18,7 +18,8 @@ EXPORTS = [
     "rsvd_b200_power_iterate", "rsvd_b200_range_basis", "rsvd_b200_project_and_solve",
     "rsvd_b200_splitmix_words", "rsvd_b200_uniforms", "rsvd_b200_last_profile",
     "rsvd_b200_set_profiling", "rsvd_b200_last_launch_count", "rsvd_b200_version",
-    "rsvd_b200_kernel_stats", "rsvd_b200_reset_stats",
+    "rsvd_b200_kernel_stats", "rsvd_b200_reset_stats", "rsvd_b200_last_info",
+    "rsvd_b200_set_robust",
 ]
 
 
@@ -71,6 +72,8 @@ def load() -> C.CDLL:
         "rsvd_b200_version": (C.c_char_p, []),
         "rsvd_b200_kernel_stats": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_long), _dp, _dp]),
         "rsvd_b200_reset_stats": (None, [_vp]),
+        "rsvd_b200_last_info": (C.c_long, [_vp, C.c_char_p]),
+        "rsvd_b200_set_robust": (None, [_vp, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

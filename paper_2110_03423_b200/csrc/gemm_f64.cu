@@ -41,13 +41,109 @@ __device__ __forceinline__ bool nonfinite(double x) {
     return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;
 }
 
+// Fused Gram epilogue of the ax kernel: G_tile = Y_tile^T Y_tile (NP x NP, upper
+// triangle) for the BM x NP output tile still held in the consumer warps' accumulators,
+// so the CholeskyQR Gram of a freshly produced Y needs no extra pass over it. The tile
+// is staged in the (now idle) pipeline buffers in the same 128B-swizzled box layout TMA
+// produces and multiplied with the atx fragment maps (contraction over the BM rows).
+// Only the 16x8 tiles that touch the upper triangle are computed, spread evenly over
+// the warps; the rest of the partial is zero. Rows beyond M were zero-filled by TMA.
+// One partial per CTA; the host reduces the partials in a fixed order.
+template <int BM, int NT, int WM, int WN>
+__device__ __forceinline__ void gram_epilogue(char* smem, const double (&acc)[BM / WM / 16][NT / WN][4],
+                                              double* __restrict__ gpart) {
+    constexpr int NP = NT * 8;
+    constexpr int MI = BM / WM / 16;
+    constexpr int NI = NT / WN;
+    constexpr uint32_t kBox = BM * 128;  // BM rows x 16 doubles
+    constexpr int MT = NP / 16;          // m16 tiles of G
+    constexpr int NW = WM * WN;
+    // upper-triangle tiles (a, b): b*8 + 7 >= a*16
+    constexpr int kTiles = [] {
+        int n = 0;
+        for (int a = 0; a < MT; ++a)
+            for (int b = 0; b < NT; ++b) n += (b * 8 + 7 >= a * 16);
+        return n;
+    }();
+    constexpr int TPW = (kTiles + NW - 1) / NW;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp / WN, wn = warp % WN;
+    const int g = lane >> 2, t = lane & 3;
+    // all consumers are done reading the pipeline stages before they are overwritten
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int row = wm * (BM / WM) + mi * 16 + g + 8 * h;
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const int col = (wn * NI + ni) * 8 + 2 * t;
+                *reinterpret_cast<double2*>(smem + (col >> 4) * kBox + swz128(row, col & 15)) =
+                    make_double2(acc[mi][ni][2 * h], acc[mi][ni][2 * h + 1]);
+            }
+        }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    // tile idx -> (a, b): row a of the upper triangle holds tiles b = 2a .. NT-1
+    auto tile_of = [](int idx, int& a, int& b) {
+        a = 0;
+        while (a < MT && idx >= NT - 2 * a) {
+            idx -= NT - 2 * a;
+            ++a;
+        }
+        b = 2 * a + idx;
+    };
+    double gacc[TPW][4];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) gacc[i][v] = 0.0;
+#pragma unroll 1
+    for (int ks = 0; ks < BM / 16; ++ks) {
+#pragma unroll
+        for (int i = 0; i < TPW; ++i) {
+            const int idx = warp + i * NW;
+            if (idx >= kTiles) continue;
+            int a, b;
+            tile_of(idx, a, b);
+            const int c = b * 8 + g;
+            double bf[4], af[8];
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+                bf[v] = lds_f64(smem + (c >> 4) * kBox, swz128(ks * 16 + k_atx(t, v), c & 15));
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+                af[v] = lds_f64(smem + a * kBox, swz128(ks * 16 + k_atx(t, v >> 1), g + 8 * (v & 1)));
+            dmma_16x8x16(gacc[i], af, bf);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+        const int idx = warp + i * NW;
+        if (idx >= kTiles) continue;
+        int a, b;
+        tile_of(idx, a, b);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = a * 16 + g + 8 * h, c = b * 8 + 2 * t;
+            *reinterpret_cast<double2*>(gpart + r * NP + c) =
+                make_double2(gacc[i][2 * h], gacc[i][2 * h + 1]);
+        }
+    }
+    // zero the tiles strictly below the diagonal (never read, kept finite for the reduce)
+    for (int e = threadIdx.x; e < NP * NP; e += NW * 32) {
+        const int r = e / NP, c = e % NP;
+        if ((c >> 3) * 8 + 7 < (r >> 4) * 16) gpart[e] = 0.0;
+    }
+}
+
 // ============================================================================ ax
 template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_ax_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {K, M}, box {16, BM}
                    const __grid_constant__ CUtensorMap mapX,  // dims {K, NP}, box {16, NP}
                    double* __restrict__ Y, long ldy, long split_stride, int M, int k_tiles,
-                   int k_tiles_per_split, int* __restrict__ flag) {
+                   int k_tiles_per_split, int* __restrict__ flag, double* __restrict__ gram) {
     constexpr int NP = NT * 8;
     constexpr int MI = BM / WM / 16;
     constexpr int NI = NT / WN;
@@ -166,6 +262,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
                 }
             }
         }
+    }
+    if constexpr (NT <= 12) {
+        if (gram != nullptr) gram_epilogue<BM, NT, WM, WN>(smem, acc, gram + (long)blockIdx.x * NP * NP);
     }
 }
 
@@ -295,14 +394,29 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     }
 }
 
-// Fixed-order sum of split-K slabs: out[e] = sum_s part[s * stride + e].
-__global__ void reduce_partials_kernel(const double* __restrict__ part, long stride, int splits,
-                                       double* __restrict__ out, long count) {
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count;
-         e += (long)gridDim.x * blockDim.x) {
-        double acc = part[e];
-        for (int s = 1; s < splits; ++s) acc += part[s * stride + e];
-        out[e] = acc;
+// Fixed-order sum of split-K slabs: out[e] = sum_s part[s * stride + e]. Threads are
+// laid out 32 elements x 8 split-groups; group g sums splits g, g+8, ... and the 8 group
+// sums are added in a fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ part,
+                                                              long stride, int splits,
+                                                              double* __restrict__ out,
+                                                              long count) {
+    __shared__ double red[8][33];
+    const int lx = threadIdx.x & 31, gy = threadIdx.x >> 5;
+    for (long base = blockIdx.x * 32L; base < count; base += gridDim.x * 32L) {
+        const long e = base + lx;
+        double acc = 0.0;
+        if (e < count)
+            for (int sp = gy; sp < splits; sp += 8) acc += part[sp * stride + e];
+        red[gy][lx] = acc;
+        __syncthreads();
+        if (gy == 0 && e < count) {
+            double t = red[0][lx];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) t += red[q][lx];
+            out[e] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -359,8 +473,9 @@ cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     const int splits = p.splits < 1 ? 1 : p.splits;
     const int per = (k_tiles + splits - 1) / splits;
     dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)splits);
+    if (p.gram && (splits != 1 || NT > 12)) return cudaErrorInvalidValue;
     kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mX, p.Y, p.ldy, p.split_stride, (int)p.M,
-                                                 k_tiles, per, p.flag);
+                                                 k_tiles, per, p.flag, p.gram);
     return cudaGetLastError();
 }
 
@@ -442,11 +557,10 @@ cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st) {
 
 cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
                                    long count, cudaStream_t st) {
-    const int threads = 256;
-    long blocks = (count + threads - 1) / threads;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    long blocks = (count + 31) / 32;
+    if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    reduce_partials_kernel<<<(unsigned)blocks, threads, 0, st>>>(part, stride, splits, out, count);
+    reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, stride, splits, out, count);
     return cudaGetLastError();
 }
 

@@ -1,20 +1,19 @@
 // Robust paths of the rSVD on B200:
 //
-//  * householder_qr_kernel — the CholeskyQR2 fallback. A cooperative (grid-
-//    synchronised) restatement of the reference's unblocked Householder QR
-//    (qr.cpp:27-102): reflector v ~ x + sign(x_1)||x|| e_1 per column, applied to
-//    the trailing columns, thin Q accumulated backwards from the identity, then
-//    diag(R) >= 0 by flipping R rows / Q columns. One CTA per SM owns a contiguous
-//    row slab; every reduction is a fixed-order sum over per-CTA partials, so the
-//    result is deterministic. Two grid barriers per column in the factorisation and
-//    one per column in the Q accumulation.
+//  * the Householder QR fallback of CholeskyQR2 — a restatement of the reference's
+//    unblocked Householder QR (qr.cpp:27-102): reflector v ~ x + sign(x_1)||x|| e_1
+//    per column, applied to the trailing columns, thin Q accumulated backwards from
+//    the identity, then diag(R) >= 0 by flipping R rows / Q columns. Each CTA owns a
+//    contiguous row slab; every reduction is a fixed-order sum over per-CTA partials,
+//    so the result is deterministic. Two launches per column (factorisation) and two
+//    per column (Q accumulation); it only runs on ill-conditioned input.
 //
 //  * complete_basis_kernel — the reference's deterministic orthonormal completion
 //    (svd.cpp:111-151): for each missing column, canonical vectors e_t are tried in
 //    ascending order of row load (sum of squares of the row over the valid columns,
 //    ties by index, i.e. the stable sort of svd.cpp:126-130), orthogonalised by two
 //    modified Gram-Schmidt passes and accepted when the remaining norm >= 1e-4.
-#include <cooperative_groups.h>
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -25,28 +24,8 @@ constexpr int kHHThreads = 256;
 constexpr int kHHWarps = kHHThreads / 32;
 constexpr int kMaxCh = 6;  // up to 192 columns, 32 per lane-chunk
 
-// Sense-reversing grid barrier for a cooperative launch.
-__device__ __forceinline__ void grid_barrier(unsigned* count, volatile unsigned* gen,
-                                             unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned my = *gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == nblocks - 1) {
-            *count = 0;
-            __threadfence();
-            atomicAdd((unsigned*)gen, 1u);
-        } else {
-            while (*gen == my) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-// Block-wide partial sums of sum_{rows i in [lo,hi)} x_i * w[i][j] for j in [j0, s):
-// x_i = xcol ? w[i][xcol_idx] * xscale : vbuf[i]... generalised through a functor.
+// Block-wide partial sums of sum_{rows i in [lo,hi)} x_i * w[i][j] for j in [j0, s),
+// x_i given by a functor; written to out[j].
 template <typename XF>
 __device__ void block_col_dots(const double* __restrict__ w, long ld, long lo, long hi, int j0,
                                int s, XF xval, double* __restrict__ out /* [s] */,
@@ -78,167 +57,218 @@ __device__ void block_col_dots(const double* __restrict__ w, long ld, long lo, l
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kHHThreads) householder_qr_kernel(
-    const double* __restrict__ Y, long M, int s, long ldy, double* __restrict__ Q, long ldq,
-    double* __restrict__ R, int NP, double* __restrict__ work /* M x NP */,
-    double* __restrict__ refl /* M x NP */, double* __restrict__ part /* 2 x nb x (NP+2) */,
-    int* __restrict__ act /* NP */, unsigned* __restrict__ bar) {
-    __shared__ double red[kHHWarps * 192];
-    __shared__ double dj[192];
-    const unsigned nb = gridDim.x;
-    const long rpb = (M + nb - 1) / nb;
-    const long lo = blockIdx.x * rpb, hi = min(M, lo + rpb);
-    const long pstride = (long)nb * (NP + 2);
-    unsigned* count = bar;
-    volatile unsigned* gen = bar + 1;
+// The factorisation is a sequence of ordinary launches (two per column, one grid-wide
+// reduction each), so no grid-wide barrier or co-residency assumption is needed.
+// Partial sums live in part[block][0..NP-1] (column dots) and part[block][NP] (tail
+// norm^2); every block re-reduces the partials in the same fixed order, so all blocks
+// derive bit-identical reflectors.
+struct HH {
+    const double* Y;
+    long M;
+    int s;
+    long ldy;
+    double* Q;
+    long ldq;
+    double* R;
+    int NP;
+    double* work;  // M x NP row-major working copy
+    double* refl;  // M x NP reflector columns
+    double* part;  // nb x (NP + 2)
+    int* act;      // NP
+};
 
-    // working copy (row-major, ld NP) and zeroed reflectors
-    for (long i = lo; i < hi; ++i)
-        for (int j = threadIdx.x; j < NP; j += blockDim.x) {
-            work[i * NP + j] = j < s ? Y[i * ldy + j] : 0.0;
-            refl[i * NP + j] = 0.0;
-        }
-    // Partial-sum layout: part[buf][block][0..NP-1] = column dots, [NP] = tail norm^2.
-    // Buffers alternate per step; every reader of a buffer is separated from its next
-    // writer by at least one grid barrier.
-    auto tail_norm = [&](int k, double* dst) {
-        double acc = 0.0;
-        for (long i = max(lo, (long)k + 1) + threadIdx.x; i < hi; i += blockDim.x) {
-            const double x = work[i * NP + k];
-            acc += x * x;
-        }
-        acc = warp_sum(acc);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int q = 0; q < kHHWarps; ++q) t += red[q];
-            dst[blockIdx.x * (NP + 2) + NP] = t;
-        }
-        __syncthreads();
-    };
+__device__ __forceinline__ void hh_rows(const HH& h, long& lo, long& hi) {
+    const long rpb = (h.M + gridDim.x - 1) / gridDim.x;
+    lo = blockIdx.x * rpb;
+    hi = min(h.M, lo + rpb);
+}
+
+// tail norm^2 of column k (rows > k) into slot NP + (k & 1): consecutive columns use
+// different slots, so a launch never overwrites a value another block may still read.
+__device__ void hh_tail_norm(const HH& h, int k, long lo, long hi, double* red) {
+    double acc = 0.0;
+    for (long i = max(lo, (long)k + 1) + threadIdx.x; i < hi; i += blockDim.x) {
+        const double x = h.work[i * h.NP + k];
+        acc += x * x;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    tail_norm(0, part);
-    grid_barrier(count, gen, nb);
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < kHHWarps; ++q) t += red[q];
+        h.part[blockIdx.x * (h.NP + 2) + h.NP + (k & 1)] = t;
+    }
+    __syncthreads();
+}
 
-    for (int k = 0; k < s; ++k) {
-        double* pk = part + (k & 1) * pstride;        // norms of column k, dots of step k
-        double* pn = part + ((k + 1) & 1) * pstride;  // norms of column k + 1
-        double tail2 = 0.0;
-        for (unsigned b = 0; b < nb; ++b) tail2 += pk[b * (NP + 2) + NP];
-        const double x0 = work[(long)k * NP + k];
-        const double norm_x = sqrt(tail2 + x0 * x0);
-        if (norm_x == 0.0) {  // zero column: H_k = I, r_kk = 0 (qr.cpp:47)
-            if (blockIdx.x == 0 && threadIdx.x == 0) act[k] = 0;
-            if (k + 1 < s) {
-                tail_norm(k + 1, pn);
-                grid_barrier(count, gen, nb);
-            }
-            continue;
+__global__ void __launch_bounds__(kHHThreads) hh_init_kernel(HH h) {
+    __shared__ double red[kHHWarps];
+    long lo, hi;
+    hh_rows(h, lo, hi);
+    for (long i = lo; i < hi; ++i)
+        for (int j = threadIdx.x; j < h.NP; j += blockDim.x) {
+            h.work[i * h.NP + j] = j < h.s ? h.Y[i * h.ldy + j] : 0.0;
+            h.refl[i * h.NP + j] = 0.0;
         }
-        const double sign = x0 >= 0.0 ? 1.0 : -1.0;
-        const double alpha = x0 + sign * norm_x;
-        const double inv_nv = 1.0 / sqrt(tail2 + alpha * alpha);
-        if (blockIdx.x == 0 && threadIdx.x == 0) act[k] = 1;
-        for (long i = max(lo, (long)k) + threadIdx.x; i < hi; i += blockDim.x)
-            refl[i * NP + k] = (i == k ? alpha : work[i * NP + k]) * inv_nv;
-        __syncthreads();
-        block_col_dots(work, NP, max(lo, (long)k), hi, k + 1, s,
-                       [&](long i) { return refl[i * NP + k]; }, pk + blockIdx.x * (NP + 2), red);
-        grid_barrier(count, gen, nb);
-        for (int j = k + 1 + threadIdx.x; j < s; j += blockDim.x) {
+    __syncthreads();
+    hh_tail_norm(h, 0, lo, hi, red);
+}
+
+// column k, phase A: reflector v_k (qr.cpp:44-58) and partial dots v_k . w_j, j > k
+__global__ void __launch_bounds__(kHHThreads) hh_col_a_kernel(HH h, int k) {
+    __shared__ double red[kHHWarps * 192];
+    long lo, hi;
+    hh_rows(h, lo, hi);
+    const int NP = h.NP;
+    double tail2 = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) tail2 += h.part[b * (NP + 2) + NP + (k & 1)];
+    const double x0 = h.work[(long)k * NP + k];
+    const double norm_x = sqrt(tail2 + x0 * x0);
+    if (norm_x == 0.0) {  // zero column: H_k = I, r_kk = 0 (qr.cpp:47)
+        if (blockIdx.x == 0 && threadIdx.x == 0) h.act[k] = 0;
+        return;
+    }
+    const double sign = x0 >= 0.0 ? 1.0 : -1.0;
+    const double alpha = x0 + sign * norm_x;
+    const double inv_nv = 1.0 / sqrt(tail2 + alpha * alpha);
+    if (blockIdx.x == 0 && threadIdx.x == 0) h.act[k] = 1;
+    for (long i = max(lo, (long)k) + threadIdx.x; i < hi; i += blockDim.x)
+        h.refl[i * NP + k] = (i == k ? alpha : h.work[i * NP + k]) * inv_nv;
+    __syncthreads();
+    block_col_dots(h.work, NP, max(lo, (long)k), hi, k + 1, h.s,
+                   [&](long i) { return h.refl[i * NP + k]; }, h.part + blockIdx.x * (NP + 2), red);
+}
+
+// column k, phase B: w_j -= 2 (v.w_j) v for j > k, r_kk, tail norm of column k + 1
+__global__ void __launch_bounds__(kHHThreads) hh_col_b_kernel(HH h, int k) {
+    __shared__ double dj[192];
+    __shared__ double red[kHHWarps];
+    long lo, hi;
+    hh_rows(h, lo, hi);
+    const int NP = h.NP;
+    const bool active = h.act[k] != 0;
+    if (active) {
+        for (int j = k + 1 + threadIdx.x; j < h.s; j += blockDim.x) {
             double t = 0.0;
-            for (unsigned b = 0; b < nb; ++b) t += pk[b * (NP + 2) + j];
+            for (unsigned b = 0; b < gridDim.x; ++b) t += h.part[b * (NP + 2) + j];
             dj[j] = 2.0 * t;
         }
+        double tail2 = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) tail2 += h.part[b * (NP + 2) + NP + (k & 1)];
         __syncthreads();
         for (long i = max(lo, (long)k); i < hi; ++i) {
-            const double vi = refl[i * NP + k];
-            for (int j = k + 1 + threadIdx.x; j < s; j += blockDim.x) work[i * NP + j] -= dj[j] * vi;
+            const double vi = h.refl[i * NP + k];
+            for (int j = k + 1 + threadIdx.x; j < h.s; j += blockDim.x)
+                h.work[i * NP + j] -= dj[j] * vi;
         }
-        if (k >= lo && k < hi && threadIdx.x == 0) work[(long)k * NP + k] = -sign * norm_x;
+        if (k >= lo && k < hi && threadIdx.x == 0) {
+            const double x0 = h.work[(long)k * NP + k];
+            const double norm_x = sqrt(tail2 + x0 * x0);
+            h.work[(long)k * NP + k] = -(x0 >= 0.0 ? 1.0 : -1.0) * norm_x;
+        }
         __syncthreads();
-        if (k + 1 < s) tail_norm(k + 1, pn);
-        grid_barrier(count, gen, nb);
     }
+    if (k + 1 < h.s) hh_tail_norm(h, k + 1, lo, hi, red);
+}
 
-    // ---- thin Q by backward accumulation (qr.cpp:71-84), Q rows owned per block
+__global__ void __launch_bounds__(kHHThreads) hh_q_init_kernel(HH h) {
+    long lo, hi;
+    hh_rows(h, lo, hi);
     for (long i = lo; i < hi; ++i)
-        for (int j = threadIdx.x; j < NP; j += blockDim.x)
-            Q[i * ldq + j] = (i == j && j < s) ? 1.0 : 0.0;
-    __syncthreads();
-    int phase = 0;
-    for (int kk = s - 1; kk >= 0; --kk) {
-        if (!act[kk]) continue;
-        double* pd = part + (phase & 1) * pstride;
-        ++phase;
-        block_col_dots(Q, ldq, max(lo, (long)kk), hi, kk, s,
-                       [&](long i) { return refl[i * NP + kk]; }, pd + blockIdx.x * (NP + 2), red);
-        grid_barrier(count, gen, nb);
-        for (int j = kk + threadIdx.x; j < s; j += blockDim.x) {
-            double t = 0.0;
-            for (unsigned b = 0; b < nb; ++b) t += pd[b * (NP + 2) + j];
-            dj[j] = 2.0 * t;
-        }
-        __syncthreads();
-        for (long i = max(lo, (long)kk); i < hi; ++i) {
-            const double vi = refl[i * NP + kk];
-            for (int j = kk + threadIdx.x; j < s; j += blockDim.x) Q[i * ldq + j] -= dj[j] * vi;
-        }
-        __syncthreads();
-    }
-    grid_barrier(count, gen, nb);
+        for (int j = threadIdx.x; j < h.NP; j += blockDim.x)
+            h.Q[i * h.ldq + j] = (i == j && j < h.s) ? 1.0 : 0.0;
+}
 
-    // ---- diag(R) >= 0 (qr.cpp:86-93); R written from the rows each block owns
+// backward accumulation (qr.cpp:71-84), reflector kk: partial dots, then the update
+__global__ void __launch_bounds__(kHHThreads) hh_q_a_kernel(HH h, int kk) {
+    __shared__ double red[kHHWarps * 192];
+    if (!h.act[kk]) return;
+    long lo, hi;
+    hh_rows(h, lo, hi);
+    block_col_dots(h.Q, h.ldq, max(lo, (long)kk), hi, kk, h.s,
+                   [&](long i) { return h.refl[i * h.NP + kk]; },
+                   h.part + blockIdx.x * (h.NP + 2), red);
+}
+
+__global__ void __launch_bounds__(kHHThreads) hh_q_b_kernel(HH h, int kk) {
+    __shared__ double dj[192];
+    if (!h.act[kk]) return;
+    long lo, hi;
+    hh_rows(h, lo, hi);
+    const int NP = h.NP;
+    for (int j = kk + threadIdx.x; j < h.s; j += blockDim.x) {
+        double t = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) t += h.part[b * (NP + 2) + j];
+        dj[j] = 2.0 * t;
+    }
+    __syncthreads();
+    for (long i = max(lo, (long)kk); i < hi; ++i) {
+        const double vi = h.refl[i * NP + kk];
+        for (int j = kk + threadIdx.x; j < h.s; j += blockDim.x) h.Q[i * h.ldq + j] -= dj[j] * vi;
+    }
+}
+
+// diag(R) >= 0 (qr.cpp:86-93): flip R rows / Q columns; R written from the owned rows
+__global__ void __launch_bounds__(kHHThreads) hh_finish_kernel(HH h) {
+    long lo, hi;
+    hh_rows(h, lo, hi);
+    const int NP = h.NP;
     for (long i = lo; i < hi && i < NP; ++i)
         for (int j = threadIdx.x; j < NP; j += blockDim.x) {
-            double r = (i < s && j < s && j >= i) ? work[i * NP + j] : 0.0;
-            if (i < s && work[i * NP + i] < 0.0) r = -r;
-            R[i * NP + j] = r;
+            double r = (i < h.s && j < h.s && j >= i) ? h.work[i * NP + j] : 0.0;
+            if (i < h.s && h.work[i * NP + i] < 0.0) r = -r;
+            h.R[i * NP + j] = r;
         }
     for (long i = lo; i < hi; ++i)
-        for (int j = threadIdx.x; j < s; j += blockDim.x)
-            if (work[(long)j * NP + j] < 0.0) Q[i * ldq + j] = -Q[i * ldq + j];
+        for (int j = threadIdx.x; j < h.s; j += blockDim.x)
+            if (h.work[(long)j * NP + j] < 0.0) h.Q[i * h.ldq + j] = -h.Q[i * h.ldq + j];
 }
 
 size_t householder_work_doubles(long M, int s) {
     const int NP = 192;
     (void)s;
-    return 2 * (size_t)M * NP + 2 * 148 * 8 * (size_t)(NP + 2) + NP + 64;
+    return 2 * (size_t)M * NP + 2 * 296 * (size_t)(NP + 2) + NP + 64;
 }
 
 cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, double* Qout, long ldq,
                                   double* R, int NP, double* work, cudaStream_t st) {
     if (s > 192 || NP > 192) return cudaErrorInvalidValue;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, householder_qr_kernel, kHHThreads, 0);
-    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    unsigned nb = (unsigned)sms;
-    if ((long)nb > M) nb = (unsigned)(M < 1 ? 1 : M);
-    double* w = work;
-    double* refl = work + (size_t)M * NP;
-    double* part = refl + (size_t)M * NP;
-    int* act = reinterpret_cast<int*>(part + 2 * (size_t)nb * (NP + 2));
-    unsigned* bar = reinterpret_cast<unsigned*>(act + NP);
-    cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
+    const unsigned nb = (unsigned)std::max(1L, std::min(296L, M));
+    HH h;
+    h.Y = Y;
+    h.M = M;
+    h.s = s;
+    h.ldy = ldy;
+    h.Q = Qout;
+    h.ldq = ldq;
+    h.R = R;
+    h.NP = NP;
+    h.work = work;
+    h.refl = work + (size_t)M * NP;
+    h.part = h.refl + (size_t)M * NP;
+    h.act = reinterpret_cast<int*>(h.part + (size_t)nb * (NP + 2));
+    cudaError_t e = cudaMemsetAsync(R, 0, (size_t)NP * NP * sizeof(double), st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(R, 0, (size_t)NP * NP * sizeof(double), st);
-    if (e != cudaSuccess) return e;
-    void* args[] = {(void*)&Y, (void*)&M, (void*)&s, (void*)&ldy, (void*)&Qout, (void*)&ldq,
-                    (void*)&R, (void*)&NP, (void*)&w, (void*)&refl, (void*)&part, (void*)&act,
-                    (void*)&bar};
-    e = cudaLaunchCooperativeKernel((const void*)householder_qr_kernel, dim3(nb), dim3(kHHThreads),
-                                    args, 0, st);
-    return e;
+    hh_init_kernel<<<nb, kHHThreads, 0, st>>>(h);
+    for (int k = 0; k < s; ++k) {
+        hh_col_a_kernel<<<nb, kHHThreads, 0, st>>>(h, k);
+        hh_col_b_kernel<<<nb, kHHThreads, 0, st>>>(h, k);
+    }
+    hh_q_init_kernel<<<nb, kHHThreads, 0, st>>>(h);
+    for (int kk = s - 1; kk >= 0; --kk) {
+        hh_q_a_kernel<<<nb, kHHThreads, 0, st>>>(h, kk);
+        hh_q_b_kernel<<<nb, kHHThreads, 0, st>>>(h, kk);
+    }
+    hh_finish_kernel<<<nb, kHHThreads, 0, st>>>(h);
+    return cudaGetLastError();
 }
 
 // ========================================================= orthonormal completion
-__global__ void __launch_bounds__(1024) complete_basis_kernel(double* __restrict__ U, long rows,
-                                                              long ld, int r0, int r1,
-                                                              double* __restrict__ work,
-                                                              int* __restrict__ status) {
+__global__ void __launch_bounds__(1024) complete_basis_kernel(
+    double* __restrict__ U, long rows, long ld, int s, const double* __restrict__ sigma,
+    long null_dim, double* __restrict__ work, int* __restrict__ status,
+    const int* __restrict__ abort_flag) {
     double* load = work;         // rows
     double* cand = work + rows;  // rows
     unsigned char* tried = reinterpret_cast<unsigned char*>(work + 2 * rows);
@@ -247,6 +277,20 @@ __global__ void __launch_bounds__(1024) complete_basis_kernel(double* __restrict
     __shared__ double bcast;
     __shared__ long bidx;
     const int tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    if (abort_flag && *abort_flag) return;
+    // null block of the small SVD (svd.cpp:221-234)
+    const double null_thresh = sigma[0] * (double)null_dim * 2.220446049250313e-16;
+    int r0 = s;
+    for (int j = 0; j < s; ++j)
+        if (!(sigma[j] > null_thresh)) {
+            r0 = j;
+            break;
+        }
+    const int r1 = s;
+    if (r0 >= r1) {
+        if (tid == 0) status[0] = 0;
+        return;
+    }
     auto block_sum = [&](double v) {
         v = warp_sum(v);
         if (lane == 0) sv[warp] = v;
@@ -335,9 +379,11 @@ __global__ void __launch_bounds__(1024) complete_basis_kernel(double* __restrict
 
 size_t complete_basis_work_doubles(long rows) { return 2 * (size_t)rows + (size_t)rows / 8 + 8; }
 
-cudaError_t launch_complete_basis(double* U, long rows, long ld, int r0, int r1, double* work,
-                                  int* status, cudaStream_t st) {
-    complete_basis_kernel<<<1, 1024, 0, st>>>(U, rows, ld, r0, r1, work, status);
+cudaError_t launch_complete_basis(double* U, long rows, long ld, int s, const double* sigma,
+                                  long null_dim, double* work, int* status,
+                                  const int* abort_flag, cudaStream_t st) {
+    complete_basis_kernel<<<1, 1024, 0, st>>>(U, rows, ld, s, sigma, null_dim, work, status,
+                                              abort_flag);
     return cudaGetLastError();
 }
 

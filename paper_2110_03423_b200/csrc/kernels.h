@@ -21,6 +21,9 @@ struct GemmAx {
     int splits = 1;
     long split_stride = 0;
     int* flag = nullptr;
+    // Fused Gram epilogue (NP <= 96, splits == 1): per-CTA partials Y_tile^T Y_tile,
+    // NP x NP each, at gram + blockIdx * NP * NP (ceil(M / 128) partials).
+    double* gram = nullptr;
 };
 
 // Z = A^T * W.  A: K x N row-major (lda), W: K x NP row-major (ldw).
@@ -61,16 +64,20 @@ cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double
 // and Rinv^T (NP x NP, ld NP, zero padded: usable directly as the Xt operand of ax).
 // status[0] = 0 ok, 1 breakdown (min pivot below tol * max diag); status is int[4].
 cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
-                            int* status, double tol, cudaStream_t st);
+                            int* status, int* abort_flag, double tol, cudaStream_t st);
 // out (NP x NP) = X (NP x NP) * Y (NP x NP), row-major, s-leading block only (rest zero).
 cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP, double* out,
                                 bool transpose_out, cudaStream_t st);
 // One-sided Jacobi SVD of the s x s matrix R (row-major, ld NP) with the reference's
 // thresholds (svd.cpp:35-36): sigma (s, sorted non-increasing), U (s x s -> NP x NP ld NP,
 // left vectors), W (right vectors, NP x NP ld NP).  status[0] = sweeps or -1 on no convergence.
+// `scratch` must hold jacobi_global_scratch_doubles(s) doubles; the kernel returns at
+// once (status 0) if *abort_flag is set.
 cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U,
-                              double* W, int* status, cudaStream_t st);
+                              double* W, int* status, double* scratch, const int* abort_flag,
+                              cudaStream_t st);
 size_t jacobi_max_width();
+size_t jacobi_global_scratch_doubles(int s);
 
 // Sign convention (svd.cpp:237-254): for each column c < s of V (rows x NP, ld ldv),
 // if the largest-|.| entry (first index on ties) is negative, negate V[:, c] and
@@ -97,10 +104,14 @@ cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, doub
                                   long ldq, double* R, int NP, double* work, cudaStream_t st);
 size_t householder_work_doubles(long M, int s);
 
-// Deterministic orthonormal completion (svd.cpp:111-151): fills columns [r0, r1) of
-// U (rows x ld, row-major) by Gram-Schmidt of canonical vectors ordered by row load.
-cudaError_t launch_complete_basis(double* U, long rows, long ld, int r0, int r1, double* work,
-                                  int* status, cudaStream_t st);
+// Deterministic orthonormal completion (svd.cpp:111-151) of the null columns of the
+// small SVD: the first j with !(sigma[j] > sigma[0] * null_dim * eps) starts the null
+// block [j, s) (svd.cpp:221-234, decided on the device); those columns of U (rows x ld,
+// row-major) are filled by Gram-Schmidt of canonical vectors ordered by row load.
+// status[0] = 1 if no candidate survived. Returns at once if *abort_flag is set.
+cudaError_t launch_complete_basis(double* U, long rows, long ld, int s, const double* sigma,
+                                  long null_dim, double* work, int* status,
+                                  const int* abort_flag, cudaStream_t st);
 size_t complete_basis_work_doubles(long rows);
 
 }  // namespace rsvdb200

@@ -14,79 +14,118 @@
 namespace rsvdb200 {
 
 // =================================================================== Cholesky
-// G (s x s, ldg) symmetric positive definite -> G = R^T R, R upper with positive
-// diagonal.  Breakdown (status[0] = 1) when a pivot falls below tol * max_i G_ii.
-// Writes R (NP x NP, zero padded) and Rinv^T (NP x NP, zero padded).  Only R is
-// staged in shared memory (s <= 168); each thread back-substitutes one column of
-// R^-1 straight into its row of Rinv^T.
-__global__ void __launch_bounds__(512) cholesky_kernel(const double* __restrict__ G, long ldg,
-                                                       int s, int NP, double* __restrict__ R,
-                                                       double* __restrict__ RinvT,
-                                                       int* __restrict__ status, double tol) {
-    extern __shared__ double a[];  // s x s row-major, upper triangle used
+// G (s x s, ldg) symmetric positive definite -> G = R^T R with R upper and a positive
+// diagonal, plus Rinv^T = (R^-1)^T. Breakdown when a pivot falls below tol * max_i G_ii
+// (status[0] = 1 and, if `abort` is given, *abort |= 1).
+// Latency-lean single-CTA kernel (1024 threads): one __syncthreads per column, every
+// element update of a step independent (a few per thread), no division in the inner
+// loops. The s x s shared buffer (odd leading dimension) holds the unscaled LDL^T rows
+// in its upper triangle (R[j][c] = a[j][c] / sqrt(a[j][j])); the inversion R X = I runs
+// bottom-up, keeping the not-yet-scaled rows of X transposed in the strict lower
+// triangle with their scale 1/R_ii in dinv[]. An upper-triangle index table (row-major)
+// lets step j address the trailing triangle as one flat range.
+constexpr int kCholThreads = 1024;
+
+__global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
+    const double* __restrict__ G, long ldg, int s, int NP, double* __restrict__ R,
+    double* __restrict__ RinvT, int* __restrict__ status, int* __restrict__ abort_flag,
+    double tol) {
+    extern __shared__ double S[];
+    const int ld = s | 1;
+    double* dinv = S + (size_t)s * ld;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(dinv + s);  // (r << 16 | c), c >= r, row-major
+    int* rstart = reinterpret_cast<int*>(tab + s * (s + 1) / 2);  // first table index of row r
     __shared__ double gmax;
-    __shared__ int broke;
     const int tid = threadIdx.x, nth = blockDim.x;
-    for (int e = tid; e < s * s; e += nth) a[e] = G[(e / s) * ldg + e % s];
-    if (tid == 0) {
-        broke = 0;
+    const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
+    for (int e = tid; e < s * s; e += nth) {
+        const int r = e / s, c = e % s;
+        S[r * ld + c] = (c >= r) ? G[r * ldg + c] : 0.0;
+    }
+    for (int r = tid; r <= s; r += nth) rstart[r] = r * s - r * (r - 1) / 2;
+    __syncthreads();
+    for (int r = warp; r < s; r += nw)
+        for (int c = r + lane; c < s; c += 32) tab[rstart[r] + (c - r)] = ((uint32_t)r << 16) | c;
+    if (warp == 0) {
         double m = 0.0;
-        for (int i = 0; i < s; ++i) m = fmax(m, G[i * ldg + i]);
-        gmax = m;
+        for (int i = lane; i < s; i += 32) m = fmax(m, G[i * ldg + i]);
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) gmax = m;
     }
     __syncthreads();
     const double thresh = tol * gmax;
+    const int total = s * (s + 1) / 2;
+    bool broke = false;
     for (int j = 0; j < s; ++j) {
-        const double d = a[j * s + j];
-        if (!(d > thresh)) {  // also catches NaN
-            if (tid == 0) broke = 1;
+        const double d = S[j * ld + j];
+        if (!(d > thresh)) {  // uniform across threads; also catches NaN
+            broke = true;
             break;
         }
-        const double rjj = sqrt(d);
-        __syncthreads();
-        for (int c = j + tid; c < s; c += nth) a[j * s + c] = (c == j) ? rjj : a[j * s + c] / rjj;
-        __syncthreads();
-        const int rem = s - j - 1;
-        for (int e = tid; e < rem * rem; e += nth) {
-            const int r = j + 1 + e / rem, c = j + 1 + e % rem;
-            if (c >= r) a[r * s + c] -= a[j * s + r] * a[j * s + c];
+        const double rd = 1.0 / d;
+        const double* rowj = S + j * ld;
+        for (int e = rstart[j + 1] + tid; e < total; e += nth) {
+            const uint32_t rc = tab[e];
+            const int r = rc >> 16, c = rc & 0xffff;
+            S[r * ld + c] -= (rowj[r] * rd) * rowj[c];
         }
         __syncthreads();
     }
-    __syncthreads();
     if (broke) {
-        if (tid == 0) status[0] = 1;
+        if (tid == 0) {
+            status[0] = 1;
+            if (abort_flag) atomicOr(abort_flag, 1);
+        }
         return;
+    }
+    // normalise: R[j][c] = a[j][c] / sqrt(a[j][j]); zero the strict lower triangle
+    for (int j = warp; j < s; j += nw) {
+        const double rs = rsqrt(S[j * ld + j]);
+        const double rjj = S[j * ld + j] * rs;  // sqrt(d)
+        for (int c = j + lane; c < s; c += 32) S[j * ld + c] = (c == j) ? rjj : S[j * ld + c] * rs;
+        for (int c = lane; c < j; c += 32) S[j * ld + c] = 0.0;
+        if (lane == 0) dinv[j] = 1.0 / rjj;
+    }
+    __syncthreads();
+    // X = R^-1, rows bottom-up: B[i][c] (c > i) lives at S[c][i]; X[i][c] = B[i][c] * dinv[i];
+    // step i subtracts R[r][i] X[i][c] from B[r][c] for every r < i <= c (an i x (s-i) block).
+    for (int i = s - 1; i > 0; --i) {
+        const double di = dinv[i];
+        const int w = s - i;
+        for (int e = tid; e < i * w; e += nth) {
+            const int r = e / w, c = i + e % w;
+            const double xic = (c == i) ? di : S[c * ld + i] * di;
+            S[c * ld + r] -= S[r * ld + i] * xic;
+        }
+        __syncthreads();
     }
     for (int e = tid; e < NP * NP; e += nth) {
         const int r = e / NP, c = e % NP;
-        R[e] = (r < s && c < s && c >= r) ? a[r * s + c] : 0.0;
-    }
-    // Rinv column c -> RinvT row c: x_i = (delta_ic - sum_{k=i+1..c} R_ik x_k) / R_ii
-    for (int c = tid; c < NP; c += nth) {
-        double* x = RinvT + (long)c * NP;
-        for (int i = c + 1; i < NP; ++i) x[i] = 0.0;
-        if (c >= s) {
-            for (int i = 0; i <= c; ++i) x[i] = 0.0;
-            continue;
+        double rv = 0.0, xv = 0.0;
+        if (r < s && c < s) {
+            if (c >= r) rv = S[r * ld + c];
+            if (c < r) xv = S[r * ld + c] * dinv[c];  // RinvT[r][c] = X[c][r], stored at S[r][c]
+            else if (c == r) xv = dinv[r];
         }
-        for (int i = c; i >= 0; --i) {
-            double acc = (i == c) ? 1.0 : 0.0;
-            for (int k = i + 1; k <= c; ++k) acc -= a[i * s + k] * x[k];
-            x[i] = acc / a[i * s + i];
-        }
+        R[e] = rv;
+        RinvT[e] = xv;
     }
     if (tid == 0) status[0] = 0;
 }
 
+size_t cholesky_smem(int s) {
+    return ((size_t)s * (s | 1) + (size_t)s) * sizeof(double) +
+           ((size_t)s * (s + 1) / 2 + s + 1) * sizeof(uint32_t);
+}
+
 cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
-                            int* status, double tol, cudaStream_t st) {
-    const size_t smem = (size_t)s * s * sizeof(double);
+                            int* status, int* abort_flag, double tol, cudaStream_t st) {
+    const size_t smem = cholesky_smem(s);
     if (smem > 225 * 1024) return cudaErrorInvalidValue;
     cudaError_t e =
         cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cholesky_kernel<<<1, 512, smem, st>>>(G, ldg, s, NP, R, RinvT, status, tol);
+    cholesky_kernel<<<1, kCholThreads, smem, st>>>(G, ldg, s, NP, R, RinvT, status, abort_flag, tol);
     return cudaGetLastError();
 }
 
@@ -112,12 +151,13 @@ cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP,
 // Hestenes one-sided Jacobi on the columns of R (s x s): R J = U diag(sigma).
 // Rotation rule and skip thresholds restate svd.cpp:35-36,60-90:
 //   skip the pair (i, j) iff |d| <= 1e-14 * ||R||_F^2  and  d^2 <= (1e-13)^2 ||r_i||^2 ||r_j||^2
-// The sweep visits all pairs in round-robin (tournament) order so that the s/2
-// pairs of a round run concurrently, one warp per pair; a sweep with no rotation
-// ends the iteration (svd.cpp:196-199); more than 30 sweeps is a convergence
-// failure (svd.hpp:20).  Columns are stored contiguously (column-major) in smem;
-// the rotation accumulator J lives in smem when it fits, else in global scratch.
-constexpr int kJacobiThreads = 512;
+// (the norms and d are recomputed from the columns for every pair). A sweep visits
+// all pairs in round-robin (tournament) order so the s/2 pairs of a round run
+// concurrently, one warp per pair; a sweep without any rotation ends the iteration
+// (svd.cpp:196-199); more than 30 sweeps is a convergence failure (svd.hpp:20).
+// Columns are stored contiguously in shared memory; the rotation accumulator J lives
+// in shared memory when both fit, else in global scratch (L2 resident).
+constexpr int kJacobiThreads = 1024;
 constexpr int kMaxSweeps = 30;
 
 __device__ __forceinline__ int rr_index(int slot, int round, int sp) {
@@ -127,20 +167,35 @@ __device__ __forceinline__ int rr_index(int slot, int round, int sp) {
 __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
     const double* __restrict__ Rin, int s, int NP, double* __restrict__ sigma_out,
     double* __restrict__ Uout, double* __restrict__ Wout, int* __restrict__ status,
-    double* __restrict__ Jglobal) {
+    double* __restrict__ Jglobal, const int* __restrict__ abort_flag) {
     extern __shared__ double sh[];
-    double* Rc = sh;                                  // s columns of length s
-    double* J = Jglobal ? Jglobal : sh + s * s;       // s columns of length s
-    __shared__ int rotations;
+    double* Rc = sh;                             // s columns of length s
+    double* J = Jglobal ? Jglobal : sh + s * s;  // s columns of length s
     __shared__ double abs_thresh;
-    __shared__ double norms[288];
-    __shared__ int order[288];
+    __shared__ double norms[256];
+    __shared__ int order[256];
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
-
+    if (abort_flag && *abort_flag) {  // an earlier stage failed; the host reruns robustly
+        if (tid == 0) status[0] = 0;
+        return;
+    }
+    __shared__ double scale_sh;
+    if (warp == 0) {  // exact power-of-two scale so that the largest entry is O(1)
+        double mx = 0.0;
+        for (int e = lane; e < s * s; e += 32) mx = fmax(mx, fabs(Rin[(e % s) * NP + e / s]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) {
+            int ex = 0;
+            frexp(mx, &ex);
+            scale_sh = mx > 0.0 ? ldexp(1.0, -ex) : 1.0;
+        }
+    }
+    __syncthreads();
+    const double scale = scale_sh;
     for (int e = tid; e < s * s; e += nth) {
         const int c = e / s, r = e % s;
-        Rc[e] = Rin[r * NP + c];
+        Rc[e] = Rin[r * NP + c] * scale;
         J[e] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
@@ -151,55 +206,68 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
         if (lane == 0) abs_thresh = 1e-14 * acc;
     }
     __syncthreads();
+    const double athr = abs_thresh;
 
     const int sp = (s + 1) & ~1;  // even number of tournament slots (slot s is a bye)
+    // one half-warp (16 lanes) per pair: 64 pairs per pass of the 1024 threads
+    const int hw = tid >> 4, hl = tid & 15, nhw = nth >> 4;
     int sweeps = 0;
     bool converged = false;
     while (sweeps < kMaxSweeps) {
         ++sweeps;
-        if (tid == 0) rotations = 0;
-        __syncthreads();
+        int rotated = 0;
         for (int round = 0; round < sp - 1; ++round) {
-            for (int k = warp; k < sp / 2; k += nwarps) {
-                int i = rr_index(k, round, sp), j = rr_index(sp - 1 - k, round, sp);
-                if (i > j) { const int tmp = i; i = j; j = tmp; }
-                if (j >= s) continue;
+            for (int k0 = 0; k0 < sp / 2; k0 += nhw) {
+                const int k = k0 + hw;
+                int i = 0, j = 0;
+                bool live = k < sp / 2;
+                if (live) {
+                    i = rr_index(k, round, sp);
+                    j = rr_index(sp - 1 - k, round, sp);
+                    if (i > j) { const int t = i; i = j; j = t; }
+                    live = j < s;
+                }
                 double* ci = Rc + i * s;
                 double* cj = Rc + j * s;
                 double aii = 0.0, ajj = 0.0, d = 0.0;
-                for (int r = lane; r < s; r += 32) {
-                    const double x = ci[r], y = cj[r];
-                    aii += x * x;
-                    ajj += y * y;
-                    d += x * y;
+                if (live)
+                    for (int r = hl; r < s; r += 16) {
+                        const double x = ci[r], y = cj[r];
+                        aii = fma(x, x, aii);
+                        ajj = fma(y, y, ajj);
+                        d = fma(x, y, d);
+                    }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) {  // xor offsets < 16 stay inside the half
+                    aii += __shfl_xor_sync(0xffffffffu, aii, o);
+                    ajj += __shfl_xor_sync(0xffffffffu, ajj, o);
+                    d += __shfl_xor_sync(0xffffffffu, d, o);
                 }
-                aii = warp_sum(aii);
-                ajj = warp_sum(ajj);
-                d = warp_sum(d);
-                if (fabs(d) <= abs_thresh && d * d <= (1e-13 * 1e-13) * aii * ajj) continue;
-                const double zeta = (ajj - aii) / (2.0 * d);
-                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + t * t);
+                if (!live || (fabs(d) <= athr && d * d <= (1e-13 * 1e-13) * aii * ajj)) continue;
+                // zeta = (ajj - aii) / (2d), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))
+                //      = sign(zeta) 2|d| / (|ajj - aii| + sqrt((ajj - aii)^2 + 4 d^2))
+                const double diff = ajj - aii;
+                const double sgn = ((diff >= 0.0) == (d >= 0.0)) || diff == 0.0 ? 1.0 : -1.0;
+                const double t = sgn * 2.0 * fabs(d) / (fabs(diff) + sqrt(fma(diff, diff, 4.0 * d * d)));
+                const double c = rsqrt(fma(t, t, 1.0));
                 const double sn = c * t;
-                for (int r = lane; r < s; r += 32) {
+                for (int r = hl; r < s; r += 16) {
                     const double x = ci[r], y = cj[r];
                     ci[r] = c * x - sn * y;
                     cj[r] = sn * x + c * y;
                 }
                 double* ji = J + i * s;
                 double* jj = J + j * s;
-                for (int r = lane; r < s; r += 32) {
+                for (int r = hl; r < s; r += 16) {
                     const double x = ji[r], y = jj[r];
                     ji[r] = c * x - sn * y;
                     jj[r] = sn * x + c * y;
                 }
-                if (lane == 0) atomicAdd(&rotations, 1);
+                rotated = 1;
             }
             __syncthreads();
         }
-        const int rot = rotations;
-        __syncthreads();
-        if (rot == 0) {
+        if (!__syncthreads_or(rotated)) {
             converged = true;
             break;
         }
@@ -235,31 +303,30 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
         Uout[e] = u;
         Wout[e] = w;
     }
-    for (int c = tid; c < s; c += nth) sigma_out[c] = norms[order[c]];
+    for (int c = tid; c < NP; c += nth) sigma_out[c] = c < s ? norms[order[c]] / scale : 0.0;
     if (tid == 0) status[0] = sweeps;
 }
 
-size_t jacobi_max_width() { return 288; }
+size_t jacobi_max_width() { return 256; }
+
+size_t jacobi_global_scratch_doubles(int s) {
+    return 2 * (size_t)s * s * sizeof(double) > 200 * 1024 ? (size_t)s * s : 0;
+}
 
 cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U, double* W,
-                              int* status, cudaStream_t st) {
+                              int* status, double* scratch, const int* abort_flag,
+                              cudaStream_t st) {
     if (s > (int)jacobi_max_width()) return cudaErrorInvalidValue;
     const size_t one = (size_t)s * s * sizeof(double);
-    double* jglobal = nullptr;
-    size_t smem = 2 * one;
-    if (smem > 200 * 1024) {  // keep J in global memory (L2 resident)
-        smem = one;
-        if (smem > 200 * 1024) return cudaErrorInvalidValue;
-        cudaError_t e = cudaMallocAsync(&jglobal, one, st);
-        if (e != cudaSuccess) return e;
-    }
+    const bool global_j = jacobi_global_scratch_doubles(s) > 0;
+    const size_t smem = global_j ? one : 2 * one;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
     cudaError_t e =
         cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    jacobi_kernel<<<1, kJacobiThreads, smem, st>>>(R, s, NP, sigma, U, W, status, jglobal);
-    e = cudaGetLastError();
-    if (jglobal) cudaFreeAsync(jglobal, st);
-    return e;
+    jacobi_kernel<<<1, kJacobiThreads, smem, st>>>(R, s, NP, sigma, U, W, status,
+                                                   global_j ? scratch : nullptr, abort_flag);
+    return cudaGetLastError();
 }
 
 // ============================================================== sign convention

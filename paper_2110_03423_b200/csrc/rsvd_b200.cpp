@@ -32,6 +32,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,17 +88,22 @@ int pad_np(long s) {
     fail(RSVD_B200_ARGUMENT_ERROR, "sketch width %ld exceeds the supported maximum of 192", s);
 }
 
-// Split-K count so that tiles * splits fills whole waves of 148 SMs.
+// Split-K count so that tiles * splits fills whole waves of 148 SMs, with at least two
+// k-tiles (of 32) per split.
 int choose_splits(long tiles, long k_tiles) {
     if (tiles >= 2 * 148 || k_tiles <= 1) return 1;
+    const long cap = std::max(1L, k_tiles / 2);
     int best = 1;
+    double best_eff = 0.0;
     for (int w = 1; w <= 16; ++w) {
-        const long s = std::max(1L, std::lround(148.0 * w / (double)tiles));
-        if (s > std::max(1L, k_tiles / 2)) break;
-        const long ctas = s * tiles;
+        const long sp = std::min(cap, std::max(1L, std::lround(148.0 * w / (double)tiles)));
+        const long ctas = sp * tiles;
         const double eff = (double)ctas / (148.0 * ((ctas + 147) / 148));
-        best = (int)s;
-        if (eff > 0.93 && w >= 2) break;
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = (int)sp;
+        }
+        if (sp == cap || (eff > 0.93 && w >= 2)) break;
     }
     return best;
 }
@@ -131,8 +137,15 @@ struct rsvd_b200_handle {
     int device = 0;
     cudaStream_t stream = nullptr;
     // workspace
-    DevBuf a_copy, a_t, xt, y, q, part, b, qbt, vbuf, small, flags, u_out, v_out, sig_out, hh_work,
-        omega_host_dev;
+    DevBuf a_copy, a_t, xt, y, q, part, b, b2, qbt, vbuf, small, flags, u_out, v_out, sig_out,
+        hh_work, omega_host_dev, jscratch, cwork, ubt;
+    long fallbacks = 0, reruns = 0;
+    int last_sweeps = 0;
+    bool force_robust = false;
+    bool c_identity = true;  // the current basis Q = Q1 C has C = I
+    double* basis = nullptr;  // Q1 of the current basis (h->y or h->q)
+    bool gram_ready = false;  // slot kG holds Y^T Y of the last produced Y
+    DevBuf gpart;             // per-tile Gram partials of the fused epilogue
     int* flags_host = nullptr;
     std::vector<double> omega_host;  // validation mode (n x s row-major)
     size_t omega_rows = 0, omega_cols = 0;
@@ -210,7 +223,10 @@ struct rsvd_b200_handle {
         timers.clear();
     }
 
-    void sync() { ck(cudaStreamSynchronize(stream), "stream synchronize"); }
+    void sync() {
+        if (trace) fprintf(stderr, "[rsvd_b200] -- sync\n");
+        ck(cudaStreamSynchronize(stream), "stream synchronize");
+    }
     int read_flag(int idx) {
         sync();
         return flags_host[idx];
@@ -218,23 +234,50 @@ struct rsvd_b200_handle {
     void launched(cudaError_t e, const char* what, int count = 1) {
         ck(e, what);
         launches += count;
+        if (trace) {
+            fprintf(stderr, "[rsvd_b200] %s\n", what);
+            if (trace > 1) ck(cudaStreamSynchronize(stream), what);
+        }
     }
+    // RSVD_B200_TRACE=1 logs every launch, =2 also synchronises after each one
+    int trace = 0;
 };
 
 namespace {
 
 // Slots in h->flags (device int array, mirrored in pinned flags_host).
-enum { kFlagNonfinite = 0, kFlagChol = 1, kFlagJacobi = 2, kFlagHH = 3, kNumFlags = 8 };
+enum {
+    kFlagNonfinite = 0,  // NaN/Inf seen in A (fused into the first pass)
+    kFlagAbort = 1,      // a Cholesky broke down on the optimistic path -> rerun robustly
+    kFlagChol = 2,       // status of the last Cholesky (robust path)
+    kFlagCholScratch = 3,
+    kFlagJacobi = 4,     // sweeps, or -1 if the Jacobi SVD did not converge
+    kFlagComplete = 5,   // 1 if the orthonormal completion failed
+    kNumFlags = 8
+};
 
 // Small s-by-s scratch layout inside h->small (each NP x NP doubles).
 enum { kG = 0, kR1 = 1, kR1iT = 2, kR2 = 3, kR2iT = 4, kRB = 5, kUR = 6, kWR = 7, kTmp = 8,
-       kSig = 9, kNumSmall = 10 };
+       kSig = 9, kC = 10, kX = 11, kNumSmall = 12 };
 
 struct Plan {
     long m, n;   // tall problem: m >= n
     long lda;    // leading dimension of A on device
     int s, NP;   // sketch width and padded width
     long ldn;    // leading dimension of n-length rows (Xt, B, Q_B^T): round_up(n, 2)
+};
+
+// One pipeline run. `robust`: synchronise after every Cholesky and take the
+// Householder fallback on breakdown. Otherwise (the optimistic path) nothing
+// synchronises: a breakdown only raises kFlagAbort, later kernels carry on (their
+// results are discarded), and the host reruns the solve robustly after the single
+// synchronisation at the end.
+struct Ctx {
+    rsvd_b200_handle* h;
+    Plan p;
+    bool robust;
+    int* flags;
+    double* slot(int i) const { return h->small.d() + (size_t)i * p.NP * p.NP; }
 };
 
 double* small_slot(rsvd_b200_handle* h, const Plan& p, int slot) {
@@ -247,24 +290,38 @@ void download_flags(rsvd_b200_handle* h) {
        "flag download");
 }
 
+long ax_tiles(long M, int NP) { return (M + (NP <= 96 ? 127 : 63)) / (NP <= 96 ? 128 : 64); }
+
 // ------------------------------------------------------------ GEMM wrappers
-// Y (M x NP) = A (M x K) * X where Xt (NP x K) holds X^T.
-void gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, const double* Xt,
+// Y (M x NP) = A (M x K) * X where Xt (NP x K) holds X^T. If `gram_out` is given and the
+// launch can fuse it (NP <= 96, no split-K), the Gram Y^T Y is produced by the GEMM's
+// epilogue and reduced into gram_out (NP x NP); returns whether that happened.
+bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, const double* Xt,
              long ldx, int NP, double* Y, long ldy, int* flag = nullptr,
-             const char* tag = nullptr, double flops = 0.0) {
+             const char* tag = nullptr, double flops = 0.0, double* gram_out = nullptr) {
     GemmAx g{A, M, K, lda, Xt, ldx, NP, Y, ldy};
     g.flag = flag;
-    const long m_tiles = (M + (NP <= 96 ? 127 : 63)) / (NP <= 96 ? 128 : 64);
-    const long k_tiles = (K + 31) / 32;
-    const int splits = choose_splits(m_tiles, k_tiles);
+    const int splits = choose_splits(ax_tiles(M, NP), (K + 31) / 32);
     if (splits == 1) {
+        const bool fuse = gram_out && NP <= 96;
+        const long tiles = ax_tiles(M, NP);
+        if (fuse) {
+            if (h->gpart.bytes < (size_t)tiles * NP * NP * sizeof(double))
+                fail(RSVD_B200_ALLOC_ERROR, "Gram workspace too small");
+            g.gram = h->gpart.d();
+        }
         h->kernel_begin(tag, flops);
         h->launched(launch_gemm_ax(g, h->stream), "gemm_ax");
         h->kernel_end(tag);
-        return;
+        if (fuse)
+            h->launched(launch_reduce_partials(h->gpart.d(), (long)NP * NP, (int)tiles, gram_out,
+                                               (long)NP * NP, h->stream),
+                        "reduce_partials");
+        return fuse;
     }
     const long slab = M * ldy;
-    h->part.reserve((size_t)splits * slab * sizeof(double));
+    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
     g.Y = h->part.d();
     g.splits = splits;
     g.split_stride = slab;
@@ -273,6 +330,7 @@ void gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, con
     h->kernel_end(tag);
     h->launched(launch_reduce_partials(h->part.d(), slab, splits, Y, slab, h->stream),
                 "reduce_partials");
+    return false;
 }
 
 // Z = A^T W.  A (K x N, lda), W (K x NP, ldw); out_t: Z^T (NP x N, ldz) else Z (N x NP, ldz).
@@ -280,9 +338,7 @@ void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, co
               long ldw, int NP, double* Z, long ldz, bool out_t, const char* tag = nullptr,
               double flops = 0.0) {
     GemmAtx g{A, K, N, lda, W, ldw, NP, Z, ldz, out_t};
-    const long tiles = (N + (NP <= 96 ? 127 : 63)) / (NP <= 96 ? 128 : 64);
-    const long k_tiles = (K + 31) / 32;
-    const int splits = choose_splits(tiles, k_tiles);
+    const int splits = choose_splits(ax_tiles(N, NP), (K + 31) / 32);
     if (splits == 1) {
         h->kernel_begin(tag, flops);
         h->launched(launch_gemm_atx(g, h->stream), "gemm_atx");
@@ -290,7 +346,8 @@ void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, co
         return;
     }
     const long slab = out_t ? (long)NP * ldz : N * ldz;
-    h->part.reserve((size_t)splits * slab * sizeof(double));
+    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
     g.Z = h->part.d();
     g.splits = splits;
     g.split_stride = slab;
@@ -301,96 +358,169 @@ void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, co
                 "reduce_partials");
 }
 
+// Largest split-K slab set any GEMM of a plan needs.
+size_t partial_doubles(const Plan& p) {
+    const long NP = p.NP;
+    size_t need = 0;
+    auto atx = [&](long K, long N, long ldz, bool out_t) {
+        const int sp = choose_splits(ax_tiles(N, p.NP), (K + 31) / 32);
+        if (sp > 1) need = std::max(need, (size_t)sp * (out_t ? NP * ldz : N * ldz));
+    };
+    auto ax = [&](long M, long K, long ldy) {
+        const int sp = choose_splits(ax_tiles(M, p.NP), (K + 31) / 32);
+        if (sp > 1) need = std::max(need, (size_t)sp * M * ldy);
+    };
+    atx(p.m, p.n, p.ldn, true);  // A-pass (A^T W)^T, Q^T A
+    atx(p.m, NP, NP, false);     // tall Gram
+    atx(NP, p.n, p.ldn, true);   // wide TRSM / C^T correction
+    atx(NP, p.n, NP, false);     // V = Q_B U_R
+    ax(p.m, p.n, NP);            // A-pass A Z
+    ax(p.m, NP, NP);             // tall TRSM, back-projection
+    ax(NP, p.n, NP);             // wide Gram
+    return std::max<size_t>(need, 1);
+}
+
 constexpr double kCholTol = 1e-12;  // pivot / max diag: beyond cond ~1e6 use Householder
 
-// ---------------------------------------------------------------- tall QR
-// Q (M x NP, ld NP) = thin-QR(Y).q for Y (M x NP, ld NP, columns >= s zero).
-// CholeskyQR2; Householder fallback on breakdown. Returns true if the fallback ran.
-bool tall_qr(rsvd_b200_handle* h, const Plan& p, const double* Y, long M, double* Q) {
-    const int NP = p.NP, s = p.s;
-    double* G = small_slot(h, p, kG);
-    double* R1 = small_slot(h, p, kR1);
-    double* R1iT = small_slot(h, p, kR1iT);
-    int* flags = static_cast<int*>(h->flags.p);
-    // G = Y^T Y
-    gemm_atx(h, Y, M, NP, NP, Y, NP, NP, G, NP, false);
-    h->launched(launch_cholesky(G, NP, s, NP, R1, R1iT, flags + kFlagChol, kCholTol, h->stream),
+void cholesky(const Ctx& c, int g_slot, int r_slot, int rit_slot) {
+    rsvd_b200_handle* h = c.h;
+    h->launched(launch_cholesky(c.slot(g_slot), c.p.NP, c.p.s, c.p.NP, c.slot(r_slot),
+                                c.slot(rit_slot), c.flags + (c.robust ? kFlagChol : kFlagCholScratch),
+                                c.robust ? nullptr : c.flags + kFlagAbort, kCholTol, h->stream),
                 "cholesky");
-    download_flags(h);
-    if (h->read_flag(kFlagChol) == 0) {
-        // Q1 = Y R1^-1 (into Q); second pass Q = Q1 R2^-1 in place (each ax CTA reads
-        // exactly the rows it writes, all K = NP columns, before its epilogue)
-        gemm_ax(h, Y, M, NP, NP, R1iT, NP, NP, Q, NP);
-        gemm_atx(h, Q, M, NP, NP, Q, NP, NP, G, NP, false);
-        double* R2 = small_slot(h, p, kR2);
-        double* R2iT = small_slot(h, p, kR2iT);
-        h->launched(launch_cholesky(G, NP, s, NP, R2, R2iT, flags + kFlagChol, kCholTol, h->stream),
-                    "cholesky");
-        download_flags(h);
-        if (h->read_flag(kFlagChol) == 0) {
-            gemm_ax(h, Q, M, NP, NP, R2iT, NP, NP, Q, NP);
-            h->launched(launch_small_matmul(R2, R1, s, NP, small_slot(h, p, kRB), false, h->stream),
-                        "small_matmul");
+}
+
+bool chol_broke(const Ctx& c) {
+    if (!c.robust) return false;
+    download_flags(c.h);
+    return c.h->read_flag(kFlagChol) != 0;
+}
+
+void set_identity(const Ctx& c, int slot) {
+    std::vector<double> eye((size_t)c.p.NP * c.p.NP, 0.0);
+    for (int i = 0; i < c.p.NP; ++i) eye[(size_t)i * c.p.NP + i] = 1.0;
+    ck(cudaMemcpyAsync(c.slot(slot), eye.data(), eye.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, c.h->stream),
+       "identity upload");
+    c.h->sync();  // eye is a stack temporary
+}
+
+// ---------------------------------------------------------------- tall QR
+// Thin QR of Y (M x NP, ld NP, columns >= s zero) by CholeskyQR, returned in factored
+// form Q = Q1 * C with Q1 at h->basis and C in slot kC (h->c_identity when C = I):
+//  * passes = 1 (intermediate power-iteration QRs): Q1 = Y itself and C = R1^-1; no
+//    pass over Y at all. The next product only needs span(Y R1^-1) and applies R1^-1
+//    to its small output (A^T Y R1^-1); the final QR re-orthonormalises.
+//  * passes = 2 (CholeskyQR2, the final basis): Q1 = Y R1^-1 is formed by a GEMM whose
+//    epilogue also produces G2 = Q1^T Q1, and C = R2^-1 is again left to the
+//    consumers (Q = Q1 R2^-1 without the second tall TRSM).
+// `gram_ready`: slot kG already holds Y^T Y (fused into the GEMM that produced Y).
+// `materialize` forms Q explicitly in `Q1out` (step-function API).
+// The Householder fallback (robust path) writes Q itself to Q1out, C = I, R in kRB.
+// Returns true if the fallback ran.
+bool tall_qr(const Ctx& c, double* Y, long M, double* Q1out, int passes, bool materialize,
+             bool gram_ready) {
+    rsvd_b200_handle* h = c.h;
+    const int NP = c.p.NP, s = c.p.s;
+    h->c_identity = true;
+    h->basis = Q1out;
+    if (!gram_ready) gemm_atx(h, Y, M, NP, NP, Y, NP, NP, c.slot(kG), NP, false);  // G1 = Y^T Y
+    cholesky(c, kG, kR1, kR1iT);
+    if (!chol_broke(c)) {
+        if (passes == 1 && !materialize) {
+            h->basis = Y;
+            h->launched(launch_transpose(c.slot(kR1iT), NP, NP, NP, c.slot(kC), NP, h->stream),
+                        "transpose");  // C = R1^-1
+            h->c_identity = false;
+            h->launched(launch_copy2d(c.slot(kR1), NP, c.slot(kRB), NP, NP, NP, h->stream),
+                        "copy2d");
+            return false;
+        }
+        // Q1 = Y R1^-1 with G2 = Q1^T Q1 from the same kernel's epilogue
+        const bool g2 = gemm_ax(h, Y, M, NP, NP, c.slot(kR1iT), NP, NP, Q1out, NP, nullptr, nullptr,
+                                0.0, passes == 2 ? c.slot(kG) : nullptr);
+        if (passes == 1) {
+            h->launched(launch_copy2d(c.slot(kR1), NP, c.slot(kRB), NP, NP, NP, h->stream),
+                        "copy2d");
+            return false;
+        }
+        if (!g2) gemm_atx(h, Q1out, M, NP, NP, Q1out, NP, NP, c.slot(kG), NP, false);
+        cholesky(c, kG, kR2, kR2iT);
+        if (!chol_broke(c)) {
+            if (materialize) {  // in place: each ax CTA reads exactly the rows it writes
+                gemm_ax(h, Q1out, M, NP, NP, c.slot(kR2iT), NP, NP, Q1out, NP);
+            } else {
+                h->launched(launch_transpose(c.slot(kR2iT), NP, NP, NP, c.slot(kC), NP, h->stream),
+                            "transpose");  // C = R2^-1
+                h->c_identity = false;
+            }
+            h->launched(launch_small_matmul(c.slot(kR2), c.slot(kR1), s, NP, c.slot(kRB), false,
+                                            h->stream),
+                        "small_matmul");  // R = R2 R1
             return false;
         }
     }
-    // Householder fallback (the reference's algorithm, qr.cpp:27-102)
     h->hh_work.reserve(householder_work_doubles(M, s) * sizeof(double));
-    h->launched(launch_householder_qr(Y, M, s, NP, Q, NP, small_slot(h, p, kRB), NP,
-                                      h->hh_work.d(), h->stream),
+    h->launched(launch_householder_qr(Y, M, s, NP, Q1out, NP, c.slot(kRB), NP, h->hh_work.d(),
+                                      h->stream),
                 "householder_qr");
+    h->basis = Q1out;
+    h->c_identity = true;
+    h->fallbacks += 1;
     return true;
 }
 
-// QR of an n x s matrix held transposed: Zt (NP x N, ld ldz). Writes Q^T to Qt (NP x N, ld ldz)
-// and R (NP x NP) to slot r_slot. Returns true if the fallback ran.
-bool wide_qr(rsvd_b200_handle* h, const Plan& p, const double* Zt, long N, long ldz, double* Qt,
-             int r_slot) {
-    const int NP = p.NP, s = p.s;
-    double* G = small_slot(h, p, kG);
-    double* R1 = small_slot(h, p, kR1);
-    double* R1iT = small_slot(h, p, kR1iT);
-    int* flags = static_cast<int*>(h->flags.p);
-    // G = Zt Zt^T  (ax with A = Zt (NP x N), X^T = Zt)
-    gemm_ax(h, Zt, NP, N, ldz, Zt, ldz, NP, G, NP);
-    h->launched(launch_cholesky(G, NP, s, NP, R1, R1iT, flags + kFlagChol, kCholTol, h->stream),
-                "cholesky");
-    download_flags(h);
-    if (h->read_flag(kFlagChol) == 0) {
-        // Q1^T = R1^-T Zt : atx with A = Zt (K = NP rows, N cols), W = R1^-1 (NP x NP).
-        // W must be R1^-1 itself (row-major): R1iT holds its transpose, so transpose back.
-        double* R1i = small_slot(h, p, kTmp);
-        h->launched(launch_transpose(R1iT, NP, NP, NP, R1i, NP, h->stream), "transpose");
-        gemm_atx(h, Zt, NP, N, ldz, R1i, NP, NP, Qt, ldz, true);
-        gemm_ax(h, Qt, NP, N, ldz, Qt, ldz, NP, G, NP);
-        double* R2 = small_slot(h, p, kR2);
-        double* R2iT = small_slot(h, p, kR2iT);
-        h->launched(launch_cholesky(G, NP, s, NP, R2, R2iT, flags + kFlagChol, kCholTol, h->stream),
-                    "cholesky");
-        download_flags(h);
-        if (h->read_flag(kFlagChol) == 0) {
-            double* R2i = small_slot(h, p, kTmp);
-            h->launched(launch_transpose(R2iT, NP, NP, NP, R2i, NP, h->stream), "transpose");
+// Thin QR of an N x s matrix held transposed, Zt (NP x N, ld ldz) -> Qt (NP x N, ld ldz),
+// R (NP x NP) into slot r_slot. CholeskyQR with `passes` passes (both triangular solves
+// applied: these matrices are only n x s); Householder fallback on the robust path.
+bool wide_qr(const Ctx& c, const double* Zt, long N, long ldz, double* Qt, int r_slot,
+             int passes) {
+    rsvd_b200_handle* h = c.h;
+    const int NP = c.p.NP, s = c.p.s;
+    gemm_ax(h, Zt, NP, N, ldz, Zt, ldz, NP, c.slot(kG), NP);  // G = Zt Zt^T
+    cholesky(c, kG, kR1, kR1iT);
+    if (!chol_broke(c)) {
+        h->launched(launch_transpose(c.slot(kR1iT), NP, NP, NP, c.slot(kTmp), NP, h->stream),
+                    "transpose");
+        gemm_atx(h, Zt, NP, N, ldz, c.slot(kTmp), NP, NP, Qt, ldz, true);  // Q1^T = R1^-T Zt
+        if (passes == 1) {
+            h->launched(launch_copy2d(c.slot(kR1), NP, c.slot(r_slot), NP, NP, NP, h->stream),
+                        "copy2d");
+            return false;
+        }
+        gemm_ax(h, Qt, NP, N, ldz, Qt, ldz, NP, c.slot(kG), NP);
+        cholesky(c, kG, kR2, kR2iT);
+        if (!chol_broke(c)) {
+            h->launched(launch_transpose(c.slot(kR2iT), NP, NP, NP, c.slot(kTmp), NP, h->stream),
+                        "transpose");
             // in place: each atx CTA reads exactly the Qt columns it writes (K = NP rows)
-            gemm_atx(h, Qt, NP, N, ldz, R2i, NP, NP, Qt, ldz, true);
-            h->launched(launch_small_matmul(R2, R1, s, NP, small_slot(h, p, r_slot), false,
+            gemm_atx(h, Qt, NP, N, ldz, c.slot(kTmp), NP, NP, Qt, ldz, true);
+            h->launched(launch_small_matmul(c.slot(kR2), c.slot(kR1), s, NP, c.slot(r_slot), false,
                                             h->stream),
                         "small_matmul");
             return false;
         }
     }
-    // Householder fallback on the row-major n x s copy
     DevBuf zrow, qrow;
     zrow.reserve((size_t)N * NP * sizeof(double));
     qrow.reserve((size_t)N * NP * sizeof(double));
     h->launched(launch_transpose(Zt, NP, N, ldz, zrow.d(), NP, h->stream), "transpose");
     h->hh_work.reserve(householder_work_doubles(N, s) * sizeof(double));
-    h->launched(launch_householder_qr(zrow.d(), N, s, NP, qrow.d(), NP, small_slot(h, p, r_slot),
-                                      NP, h->hh_work.d(), h->stream),
+    h->launched(launch_householder_qr(zrow.d(), N, s, NP, qrow.d(), NP, c.slot(r_slot), NP,
+                                      h->hh_work.d(), h->stream),
                 "householder_qr");
     h->launched(launch_transpose(qrow.d(), N, NP, NP, Qt, ldz, h->stream), "transpose");
-    h->sync();
+    h->sync();  // zrow/qrow lifetime
+    h->fallbacks += 1;
     return true;
+}
+
+// (NP x N) = C^T * in: the deferred R2^-1 of a factored basis Q = Q1 C applied to
+// (A^T Q1)^T or Q1^T A. Returns `in` unchanged when C = I.
+const double* apply_ct(const Ctx& c, const double* in, double* out) {
+    if (c.h->c_identity) return in;
+    gemm_atx(c.h, in, c.p.NP, c.p.n, c.p.ldn, c.slot(kC), c.p.NP, c.p.NP, out, c.p.ldn, true);
+    return out;
 }
 
 Plan make_plan(long m, long n, long lda, long s) {
@@ -404,26 +534,34 @@ Plan make_plan(long m, long n, long lda, long s) {
     return p;
 }
 
-void reserve_workspace(rsvd_b200_handle* h, const Plan& p) {
+Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     const int NP = p.NP;
     h->xt.reserve((size_t)NP * p.ldn * sizeof(double));
     h->y.reserve((size_t)p.m * NP * sizeof(double));
     h->q.reserve((size_t)p.m * NP * sizeof(double));
     h->b.reserve((size_t)NP * p.ldn * sizeof(double));
+    h->b2.reserve((size_t)NP * p.ldn * sizeof(double));
     h->qbt.reserve((size_t)NP * p.ldn * sizeof(double));
     h->vbuf.reserve((size_t)p.n * NP * sizeof(double));
     h->small.reserve((size_t)kNumSmall * NP * NP * sizeof(double));
+    h->part.reserve(partial_doubles(p) * sizeof(double));
+    if (NP <= 96) h->gpart.reserve((size_t)ax_tiles(p.m, NP) * NP * NP * sizeof(double));
+    h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(p.s)) * sizeof(double));
+    h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
     ck(cudaMemsetAsync(h->flags.p, 0, kNumFlags * sizeof(int), h->stream), "memset flags");
+    h->trace = getenv("RSVD_B200_TRACE") ? atoi(getenv("RSVD_B200_TRACE")) : 0;
+    return Ctx{h, p, robust, static_cast<int*>(h->flags.p)};
 }
 
 // ---- sketch (rsvd.cpp:51-59): h->y (m x NP) = A * Omega, Omega from the device
 // generator or the validation-mode host Omega; `check` fuses the NaN/Inf scan of A
 // (validate, rsvd.cpp:144) into this first pass over A.
-void sketch_dev(rsvd_b200_handle* h, const Plan& p, const double* A, uint64_t seed, bool check) {
+void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
+    rsvd_b200_handle* h = c.h;
+    const Plan& p = c.p;
     cudaStream_t st = h->stream;
     const long n = p.n;
     const int s = p.s, NP = p.NP;
-    int* flags = static_cast<int*>(h->flags.p);
     h->mark("omega");
     if (!h->omega_host.empty()) {
         if (h->omega_rows != (size_t)n || h->omega_cols != (size_t)s)
@@ -441,131 +579,142 @@ void sketch_dev(rsvd_b200_handle* h, const Plan& p, const double* A, uint64_t se
         h->launched(launch_omega(seed, n, s, NP, h->xt.d(), p.ldn, st), "omega");
     }
     h->mark("sketch_gemm");
-    gemm_ax(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
-            check ? flags + kFlagNonfinite : nullptr, "gemm_A", 2.0 * p.m * n * s);
-    if (check) {
-        download_flags(h);
-        if (h->read_flag(kFlagNonfinite))
-            fail(RSVD_B200_ARGUMENT_ERROR, "randomized_ksvd input contains NaN or Inf");
-    }
+    h->gram_ready = gemm_ax(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
+                            check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
+                            2.0 * p.m * n * s, c.slot(kG));
 }
 
-// ---- power_iterate (rsvd.cpp:61-73): h->y holds Y0; result W in h->q.
-void power_iterate_dev(rsvd_b200_handle* h, const Plan& p, const double* A, size_t q) {
+// ---- power_iterate (rsvd.cpp:61-73): h->y holds Y0; result W = Q1 C (h->q, slot kC).
+void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize) {
+    rsvd_b200_handle* h = c.h;
+    const Plan& p = c.p;
     if (p.m < p.s)
         fail(RSVD_B200_DIMENSION_ERROR, "householder_qr needs rows >= cols, got %ldx%d", p.m, p.s);
+    if (q > 0 && p.n < p.s)
+        fail(RSVD_B200_DIMENSION_ERROR, "householder_qr needs rows >= cols, got %ldx%d", p.n, p.s);
     h->mark("qr_tall");
-    tall_qr(h, p, h->y.d(), p.m, h->q.d());  // W = QR(Y0).q
+    tall_qr(c, h->y.d(), p.m, h->q.d(), q == 0 ? 2 : 1, materialize && q == 0,
+            h->gram_ready);  // QR(Y0)
     for (size_t round = 0; round < q; ++round) {
-        if (p.n < p.s)
-            fail(RSVD_B200_DIMENSION_ERROR, "householder_qr needs rows >= cols, got %ldx%d", p.n,
-                 p.s);
         h->mark("power_atx");
-        gemm_atx(h, A, p.m, p.n, p.lda, h->q.d(), p.NP, p.NP, h->b.d(), p.ldn, true, "gemm_A",
-                 2.0 * p.m * p.n * p.s);  // (A^T W)^T
+        gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true, "gemm_A",
+                 2.0 * p.m * p.n * p.s);  // (A^T Q1)^T
         h->mark("qr_wide");
-        wide_qr(h, p, h->b.d(), p.n, p.ldn, h->xt.d(), kRB);  // Z = QR(A^T W).q, as Z^T
+        const double* zt = apply_ct(c, h->b.d(), h->b2.d());  // (A^T W)^T, W = Q1 C
+        wide_qr(c, zt, p.n, p.ldn, h->xt.d(), kRB, 1);  // Z = QR(A^T W).q, as Z^T
         h->mark("power_ax");
-        gemm_ax(h, A, p.m, p.n, p.lda, h->xt.d(), p.ldn, p.NP, h->y.d(), p.NP, nullptr, "gemm_A",
-                2.0 * p.m * p.n * p.s);  // Y = A Z
+        h->gram_ready = gemm_ax(h, A, p.m, p.n, p.lda, h->xt.d(), p.ldn, p.NP, h->y.d(), p.NP,
+                                nullptr, "gemm_A", 2.0 * p.m * p.n * p.s, c.slot(kG));  // Y = A Z
         h->mark("qr_tall");
-        tall_qr(h, p, h->y.d(), p.m, h->q.d());  // W = QR(Y).q
+        const bool last = round + 1 == q;
+        tall_qr(c, h->y.d(), p.m, h->q.d(), last ? 2 : 1, materialize && last,
+                h->gram_ready);  // W = QR(Y).q
     }
 }
 
-// ---- project_and_solve (rsvd.cpp:89-109) with basis h->q (m x NP, p.s live columns).
+// ---- project_and_solve (rsvd.cpp:89-109) with basis Q = Q1 C (h->q, slot kC).
 // Outputs (device): sigma (k), v (n x k, ldv) and u (m x k, ldu) unless null.
-void project_and_solve_dev(rsvd_b200_handle* h, const Plan& p, const double* A, long k,
-                           double* u, long ldu, double* sigma, double* v, long ldv) {
+void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, long ldu,
+                           double* sigma, double* v, long ldv) {
+    rsvd_b200_handle* h = c.h;
+    const Plan& p = c.p;
     cudaStream_t st = h->stream;
     const long m = p.m, n = p.n;
     const int s = p.s, NP = p.NP;
-    int* flags = static_cast<int*>(h->flags.p);
     if (n < s)
         fail(RSVD_B200_DIMENSION_ERROR,
              "project_and_solve: basis width %d exceeds the %ld columns of a", s, n);
     h->mark("project_atx");
-    gemm_atx(h, A, m, n, p.lda, h->q.d(), NP, NP, h->b.d(), p.ldn, true, "gemm_A",
-             2.0 * m * n * s);  // B = Q^T A (NP x n)
+    gemm_atx(h, A, m, n, p.lda, h->basis, NP, NP, h->b.d(), p.ldn, true, "gemm_A",
+             2.0 * m * n * s);  // Q1^T A
     h->mark("small_svd");
-    wide_qr(h, p, h->b.d(), n, p.ldn, h->qbt.d(), kRB);  // B^T = Q_B R_B
-    double* UR = small_slot(h, p, kUR);
-    double* WR = small_slot(h, p, kWR);
-    double* sig = small_slot(h, p, kSig);
-    h->launched(launch_jacobi_svd(small_slot(h, p, kRB), s, NP, sig, UR, WR, flags + kFlagJacobi,
-                                  st),
+    const double* bq = apply_ct(c, h->b.d(), h->b2.d());  // B = C^T Q1^T A = Q^T A (NP x n)
+    wide_qr(c, bq, n, p.ldn, h->qbt.d(), kRB, 2);          // B^T = Q_B R_B
+    double* UR = c.slot(kUR);
+    double* WR = c.slot(kWR);
+    double* sig = c.slot(kSig);
+    h->launched(launch_jacobi_svd(c.slot(kRB), s, NP, sig, UR, WR, c.flags + kFlagJacobi,
+                                  h->jscratch.d(), c.flags + kFlagAbort, st),
                 "jacobi_svd");
-    download_flags(h);
-    if (h->read_flag(kFlagJacobi) < 0)
-        fail(RSVD_B200_CONVERGENCE_ERROR,
-             "one-sided Jacobi SVD did not converge within 30 sweeps");
     // V = Q_B U_R (n x NP): atx with A = Q_B^T (K = NP, N = n), W = U_R
     gemm_atx(h, h->qbt.d(), NP, n, p.ldn, UR, NP, NP, h->vbuf.d(), NP, false);
-    // null columns of B's SVD (svd.cpp:221-234) get the reference's canonical completion
-    std::vector<double> sig_host(s);
-    ck(cudaMemcpyAsync(sig_host.data(), sig, s * sizeof(double), cudaMemcpyDeviceToHost, st),
-       "sigma download");
-    h->sync();
-    const double null_thresh = sig_host[0] * (double)std::max<long>(n, s) * 2.220446049250313e-16;
-    int n_valid = s;
-    for (int j = 0; j < s; ++j)
-        if (!(sig_host[j] > null_thresh)) {
-            n_valid = j;
-            break;
-        }
-    if (n_valid < s) {
-        h->hh_work.reserve(complete_basis_work_doubles(n) * sizeof(double));
-        h->launched(launch_complete_basis(h->vbuf.d(), n, NP, n_valid, s, h->hh_work.d(),
-                                          flags + kFlagHH, st),
-                    "complete_basis");
-        download_flags(h);
-        if (h->read_flag(kFlagHH))
-            fail(RSVD_B200_CONVERGENCE_ERROR, "dense_svd could not complete an orthonormal basis");
-    }
+    // null columns of B's SVD (svd.cpp:221-234) get the reference's canonical completion;
+    // the kernel decides on the device whether there are any
+    h->launched(launch_complete_basis(h->vbuf.d(), n, NP, s, sig, std::max<long>(n, s),
+                                      h->cwork.d(), c.flags + kFlagComplete, c.flags + kFlagAbort,
+                                      st),
+                "complete_basis");
     h->launched(launch_sign_fix(h->vbuf.d(), n, NP, s, WR, NP, st), "sign_fix");
 
-    // outputs: sigma[:k], V[:, :k], U = Q U_B[:, :k]
+    // outputs: sigma[:k], V[:, :k], U = Q U_B[:, :k] = Q1 (C U_B)[:, :k]
     ck(cudaMemcpyAsync(sigma, sig, k * sizeof(double), cudaMemcpyDeviceToDevice, st), "sigma");
     if (v) h->launched(launch_copy2d(h->vbuf.d(), NP, v, ldv, n, k, st), "copy2d");
     if (u) {
         h->mark("backproject");
-        const int NPk = pad_np(k);  // Xt for ax = U_B[:, :k]^T, NPk x NP
-        DevBuf ubt_buf;
-        double* ubt = small_slot(h, p, kTmp);
-        if (NPk > NP) {
-            ubt_buf.reserve((size_t)NPk * NP * sizeof(double));
-            ubt = ubt_buf.d();
+        const int NPk = pad_np(k);  // Xt for ax = (C U_B)[:, :k]^T, NPk x NP
+        const double* cu = WR;
+        if (!h->c_identity) {
+            h->launched(launch_small_matmul(c.slot(kC), WR, s, NP, c.slot(kX), false, st),
+                        "small_matmul");
+            cu = c.slot(kX);
         }
-        h->launched(launch_fill(ubt, (long)NPk * NP, 0.0, st), "fill");
-        h->launched(launch_transpose(WR, s, k, NP, ubt, NP, st), "transpose");
+        h->ubt.reserve((size_t)NPk * NP * sizeof(double));
+        h->launched(launch_fill(h->ubt.d(), (long)NPk * NP, 0.0, st), "fill");
+        h->launched(launch_transpose(cu, s, k, NP, h->ubt.d(), NP, st), "transpose");
         const bool direct = (ldu == NPk) && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
         if (direct) {
-            gemm_ax(h, h->q.d(), m, NP, NP, ubt, NP, NPk, u, ldu);
+            gemm_ax(h, h->basis, m, NP, NP, h->ubt.d(), NP, NPk, u, ldu);
         } else {
             // h->y is free at this point (power iteration done)
             h->y.reserve((size_t)m * std::max(NP, NPk) * sizeof(double));
-            gemm_ax(h, h->q.d(), m, NP, NP, ubt, NP, NPk, h->y.d(), NPk);
+            gemm_ax(h, h->basis, m, NP, NP, h->ubt.d(), NP, NPk, h->y.d(), NPk);
             h->launched(launch_copy2d(h->y.d(), NPk, u, ldu, m, k, st), "copy2d");
         }
-        h->sync();  // ubt_buf lifetime
     }
 }
 
-// Tall solve (rsvd.cpp:126-134) on device data. A: m x n (lda), m >= n.
+// Status checks after a run (one synchronisation). Returns false if the optimistic run
+// must be repeated robustly.
+bool finish_run(const Ctx& c, bool checked_nonfinite) {
+    download_flags(c.h);
+    c.h->sync();
+    const int* f = c.h->flags_host;
+    if (checked_nonfinite && f[kFlagNonfinite])
+        fail(RSVD_B200_ARGUMENT_ERROR, "randomized_ksvd input contains NaN or Inf");
+    if (f[kFlagAbort]) return false;
+    c.h->last_sweeps = f[kFlagJacobi];
+    if (f[kFlagJacobi] < 0)
+        fail(RSVD_B200_CONVERGENCE_ERROR,
+             "one-sided Jacobi SVD did not converge within 30 sweeps");
+    if (f[kFlagComplete])
+        fail(RSVD_B200_CONVERGENCE_ERROR, "dense_svd could not complete an orthonormal basis");
+    return true;
+}
+
+// Tall solve (rsvd.cpp:126-134) on device data. A: m x n (lda), m >= n. The optimistic
+// pipeline runs first; a Cholesky breakdown anywhere reruns the whole solve on the robust
+// path (Householder fallbacks), which reproduces the reference's QR semantics.
 void solve_tall(rsvd_b200_handle* h, const double* A, long m, long n, long lda,
                 const rsvd_b200_config& cfg, double* u, long ldu, double* sigma, double* v,
                 long ldv, size_t* sketch_width) {
     const Plan p = make_plan(m, n, lda, (long)rsvd_b200_sketch_width(&cfg, (size_t)m, (size_t)n));
-    reserve_workspace(h, p);
-    sketch_dev(h, p, A, cfg.seed, true);
-    power_iterate_dev(h, p, A, cfg.power_q);
-    // range_basis(W) = W in the pipeline (see the header comment); k <= s always,
-    // so pad_to_rank (rsvd.cpp:117-124) never widens the result here.
+    h->fallbacks = 0;
+    h->reruns = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const Ctx c = begin_run(h, p, /*robust=*/attempt > 0 || h->force_robust);
+        sketch_dev(c, A, cfg.seed, /*check=*/true);
+        power_iterate_dev(c, A, cfg.power_q, false);
+        // range_basis(W) = W in the pipeline (see the header comment); k <= s always,
+        // so pad_to_rank (rsvd.cpp:117-124) never widens the result here.
+        project_and_solve_dev(c, A, (long)cfg.k, u, ldu, sigma, v, ldv);
+        h->mark("end");
+        const bool ok = finish_run(c, true);
+        h->finish_timers();
+        if (ok) break;
+        if (c.robust) fail(RSVD_B200_CUDA_ERROR, "internal: abort flag on the robust path");
+        h->reruns += 1;
+    }
     if (sketch_width) *sketch_width = (size_t)p.s;
-    project_and_solve_dev(h, p, A, (long)cfg.k, u, ldu, sigma, v, ldv);
-    h->mark("end");
-    h->sync();
-    h->finish_timers();
 }
 
 // Device-side entry used by every public solve. Handles orientation (rsvd.cpp:150-156)
@@ -855,10 +1004,9 @@ rsvd_b200_status rsvd_b200_sketch(rsvd_b200_handle* h, const double* a, size_t m
             fail(RSVD_B200_ARGUMENT_ERROR, "sketch width %zu outside [1, %zu] for a %zux%zu input",
                  s, md, m, n);
         const long lda = upload(h, h->a_copy, a, (long)m, (long)n, round_up((long)n, 2));
-        const Plan p = make_plan((long)m, (long)n, lda, (long)s);
-        reserve_workspace(h, p);
-        sketch_dev(h, p, h->a_copy.d(), seed, false);
-        download(h, y0, h->y.d(), (long)m, (long)s, p.NP);
+        const Ctx c = begin_run(h, make_plan((long)m, (long)n, lda, (long)s), true);
+        sketch_dev(c, h->a_copy.d(), seed, false);
+        download(h, y0, h->y.d(), (long)m, (long)s, c.p.NP);
     });
 }
 
@@ -867,12 +1015,13 @@ rsvd_b200_status rsvd_b200_power_iterate(rsvd_b200_handle* h, const double* a, s
     return guarded([&] {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         check_shape((long)m, (long)n, "power_iterate");
+        check_shape((long)m, (long)s, "power_iterate y0");
         const long lda = upload(h, h->a_copy, a, (long)m, (long)n, round_up((long)n, 2));
-        const Plan p = make_plan((long)m, (long)n, lda, (long)s);
-        reserve_workspace(h, p);
-        upload(h, h->y, y0, (long)m, (long)s, p.NP);
-        power_iterate_dev(h, p, h->a_copy.d(), q);
-        download(h, w, h->q.d(), (long)m, (long)s, p.NP);
+        const Ctx c = begin_run(h, make_plan((long)m, (long)n, lda, (long)s), true);
+        upload(h, h->y, y0, (long)m, (long)s, c.p.NP);
+        h->gram_ready = false;
+        power_iterate_dev(c, h->a_copy.d(), q, /*materialize=*/true);
+        download(h, w, h->basis, (long)m, (long)s, c.p.NP);
     });
 }
 
@@ -883,26 +1032,26 @@ rsvd_b200_status rsvd_b200_range_basis(rsvd_b200_handle* h, const double* y, siz
         check_shape((long)m, (long)s, "range_basis");
         if (m < s)
             fail(RSVD_B200_DIMENSION_ERROR, "householder_qr needs rows >= cols, got %zux%zu", m, s);
-        const Plan p = make_plan((long)m, (long)s, (long)s, (long)s);
-        reserve_workspace(h, p);
-        upload(h, h->y, y, (long)m, (long)s, p.NP);
+        const Ctx c = begin_run(h, make_plan((long)m, (long)s, (long)s, (long)s), true);
+        const int NP = c.p.NP;
+        upload(h, h->y, y, (long)m, (long)s, NP);
         // ||y||_F^2 = trace(Y^T Y)
-        double* G = small_slot(h, p, kG);
-        gemm_atx(h, h->y.d(), (long)m, p.NP, p.NP, h->y.d(), p.NP, p.NP, G, p.NP, false);
-        std::vector<double> g((size_t)p.NP * p.NP);
-        download(h, g.data(), G, p.NP, p.NP, p.NP);
+        gemm_atx(h, h->y.d(), (long)m, NP, NP, h->y.d(), NP, NP, c.slot(kG), NP, false);
+        std::vector<double> g((size_t)NP * NP);
+        download(h, g.data(), c.slot(kG), NP, NP, NP);
         double fro2 = 0.0;
-        for (size_t j = 0; j < s; ++j) fro2 += g[j * p.NP + j];
-        const bool fallback = tall_qr(h, p, h->y.d(), (long)m, h->q.d());
+        for (size_t j = 0; j < s; ++j) fro2 += g[j * NP + j];
+        const bool fallback = tall_qr(c, h->y.d(), (long)m, h->q.d(), 2, /*materialize=*/true,
+                                      /*gram_ready=*/false);
         std::vector<double> qh((size_t)m * s);
-        download(h, qh.data(), h->q.d(), (long)m, (long)s, p.NP);
+        download(h, qh.data(), h->q.d(), (long)m, (long)s, NP);
         std::vector<size_t> keep;
         if (fallback) {  // drop rule on the Householder R (rsvd.cpp:77-86)
-            std::vector<double> r((size_t)p.NP * p.NP);
-            download(h, r.data(), small_slot(h, p, kRB), p.NP, p.NP, p.NP);
+            std::vector<double> r((size_t)NP * NP);
+            download(h, r.data(), c.slot(kRB), NP, NP, NP);
             const double drop = 1e-13 * std::sqrt(fro2);
             for (size_t j = 0; j < s; ++j)
-                if (std::fabs(r[j * p.NP + j]) > drop) keep.push_back(j);
+                if (std::fabs(r[j * NP + j]) > drop) keep.push_back(j);
             if (keep.empty()) keep.push_back(0);
         } else {  // CholeskyQR2 succeeded: every |R_jj| >= 1e-6 max||y_j|| > the drop bound
             for (size_t j = 0; j < s; ++j) keep.push_back(j);
@@ -924,19 +1073,31 @@ rsvd_b200_status rsvd_b200_project_and_solve(rsvd_b200_handle* h, const double* 
         if (k < 1 || k > sq)
             fail(RSVD_B200_ARGUMENT_ERROR, "rank k=%zu exceeds the basis width %zu", k, sq);
         const long lda = upload(h, h->a_copy, a, (long)m, (long)n, round_up((long)n, 2));
-        const Plan p = make_plan((long)m, (long)n, lda, (long)sq);
-        reserve_workspace(h, p);
-        upload(h, h->q, qb, (long)m, (long)sq, p.NP);
+        const Ctx c = begin_run(h, make_plan((long)m, (long)n, lda, (long)sq), true);
+        upload(h, h->q, qb, (long)m, (long)sq, c.p.NP);
+        h->c_identity = true;
+        h->basis = h->q.d();
         h->sig_out.reserve(k * sizeof(double));
         h->u_out.reserve((size_t)m * k * sizeof(double));
         h->v_out.reserve((size_t)n * k * sizeof(double));
-        project_and_solve_dev(h, p, h->a_copy.d(), (long)k, h->u_out.d(), (long)k,
-                              h->sig_out.d(), h->v_out.d(), (long)k);
+        project_and_solve_dev(c, h->a_copy.d(), (long)k, h->u_out.d(), (long)k, h->sig_out.d(),
+                              h->v_out.d(), (long)k);
+        finish_run(c, false);
         download(h, sigma, h->sig_out.d(), 1, (long)k, (long)k);
         download(h, u, h->u_out.d(), (long)m, (long)k, (long)k);
         download(h, v, h->v_out.d(), (long)n, (long)k, (long)k);
         if (sketch_width) *sketch_width = sq;
     });
 }
+
+long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
+    if (!strcmp(key, "jacobi_sweeps")) return h->last_sweeps;
+    if (!strcmp(key, "householder_fallbacks")) return h->fallbacks;
+    if (!strcmp(key, "robust_reruns")) return h->reruns;
+    if (!strcmp(key, "launches")) return h->launches;
+    return -1;
+}
+
+void rsvd_b200_set_robust(rsvd_b200_handle* h, int on) { h->force_robust = on != 0; }
 
 }  // extern "C"

@@ -147,6 +147,13 @@ class Solver:
     def reset_stats(self) -> None:
         self.lib.rsvd_b200_reset_stats(self.h)
 
+    def last_info(self, key: str) -> int:
+        return int(self.lib.rsvd_b200_last_info(self.h, key.encode()))
+
+    def set_robust(self, on: bool) -> None:
+        """Force the host-checked robust path (Householder fallback) for every solve."""
+        self.lib.rsvd_b200_set_robust(self.h, int(on))
+
     def last_profile(self) -> dict:
         names = (C.c_char_p * 32)()
         ms = (C.c_double * 32)()

@@ -25,7 +25,7 @@ def cfg_of(c):
                         seed=c["seed"], epsilon=c["epsilon"], epsilon_mode=c["epsilon_mode"])
 
 
-def check_against(res, sigma, u, v, name):
+def check_against(res, sigma, u, v, name, a=None):
     s = res.factors.sigma
     assert s.shape == sigma.shape, name
     floor = 1e-13 * sigma[0]
@@ -36,8 +36,9 @@ def check_against(res, sigma, u, v, name):
     assert np.all(np.diff(s) <= 0), name
     # subspaces are compared on the leading block that ends at a spectral gap (a
     # degenerate cluster, e.g. the identity, has no unique singular subspace)
+    full = sigma if a is None else np.linalg.svd(a, compute_uv=False)
     nl = int(live.sum())
-    while nl > 0 and nl < len(sigma) and sigma[nl - 1] <= sigma[nl] * (1 + 1e-6):
+    while nl > 0 and nl < len(full) and full[nl - 1] <= full[nl] * (1 + 1e-6):
         nl -= 1
     if nl > 0:
         assert principal_angle(res.factors.u[:, :nl], u[:, :nl]) <= ANGLE_TOL, name
@@ -104,7 +105,7 @@ def test_rsvd_golden(solver, golden_cases):
     for c, d in golden_cases:
         res = solver.randomized_ksvd(d["a"], cfg_of(c))
         assert res.sketch_width == int(d["sketch_width"]), c["name"]
-        check_against(res, d["sigma"], d["u"], d["v"], c["name"])
+        check_against(res, d["sigma"], d["u"], d["v"], c["name"], d["a"])
 
 
 def test_rsvd_golden_validation_mode(solver, golden_cases):
@@ -114,7 +115,7 @@ def test_rsvd_golden_validation_mode(solver, golden_cases):
             res = solver.randomized_ksvd(d["a"], cfg_of(c))
         finally:
             solver.set_omega(None)
-        check_against(res, d["sigma"], d["u"], d["v"], c["name"] + "/validation")
+        check_against(res, d["sigma"], d["u"], d["v"], c["name"] + "/validation", d["a"])
 
 
 def test_values_only_bit_identical(solver, golden_cases):
@@ -228,12 +229,27 @@ def test_householder_fallback_ill_conditioned(solver, port):
     sig = 10.0 ** (-np.arange(n) * 12.0 / 29)  # 1e-12 range across the sketch
     a = (uu * sig) @ vv.T
     res = solver.randomized_ksvd(a, P.RsvdConfig(k=k, power_q=0, seed=4))
+    assert solver.last_info("robust_reruns") == 1  # optimistic path aborted, robust rerun
+    assert solver.last_info("householder_fallbacks") >= 1
     ref = port.randomized_ksvd(a, k, power_q=0, seed=4)
     lead = 8  # singular values well above the eps * sigma_1 floor
     rel = np.abs(res.factors.sigma[:lead] - ref.sigma[:lead]) / ref.sigma[:lead]
     assert rel.max() <= SIG_RTOL
     assert principal_angle(res.factors.u[:, :lead], ref.u[:, :lead]) <= ANGLE_TOL
     assert np.abs(res.factors.u.T @ res.factors.u - np.eye(k)).max() <= 1e-10
+
+
+def test_robust_path_matches_fast_path(solver, golden_cases):
+    for c, d in golden_cases[3:6]:
+        fast = solver.randomized_ksvd(d["a"], cfg_of(c))
+        assert solver.last_info("robust_reruns") == 0
+        solver.set_robust(True)
+        try:
+            robust = solver.randomized_ksvd(d["a"], cfg_of(c))
+        finally:
+            solver.set_robust(False)
+        check_against(robust, fast.factors.sigma, fast.factors.u, fast.factors.v, c["name"], d["a"])
+        check_against(robust, d["sigma"], d["u"], d["v"], c["name"] + "/robust", d["a"])
 
 
 def test_lowrank_beyond_rank(solver, port):
