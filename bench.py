@@ -1,20 +1,24 @@
 #!/usr/bin/env python3
-"""Benchmark of the B200 randomized k-SVD on BASELINE.json's headline configuration.
+"""Benchmark of the B200 randomized k-SVD on BASELINE.json's configurations.
 
-Workload (config C2, the metric's 1-GPU case): a CelebA-shaped synthetic FP64 matrix
-A (202599 x 4096) with a controlled, exponentially decaying spectrum, rank k=64,
-oversampling p=10, q=2 power iterations, seed 42. One step = one full
-`randomized_ksvd` (Algorithm 1) with A resident in HBM. A (6.6 GB) is much larger than
-the 126 MB L2, so every step streams it from HBM (no explicit flush needed).
+Default workload (config C2, the metric's 1-GPU case): a CelebA-shaped synthetic FP64
+matrix A (202599 x 4096) with a controlled, exponentially decaying spectrum, rank k=64,
+oversampling p=10, q=2 power iterations, seed 42. One step = one full `randomized_ksvd`
+(Algorithm 1) with A resident in HBM. A (6.6 GB) is much larger than the 126 MB L2, so
+every pass streams it from HBM (no explicit flush needed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c1|c2|c3|c5]
 
-Prints ONE JSON line (rank 0). value = whole-job TFLOP/s with the algorithmic flop
-count F = (2q+2)*2*m*n*s + 2*m*s*k (s = k+p), i.e. the reference's arithmetic, not
-padded tiles; ms_per_step is the wall time of one solve (max over ranks).
---impl reference times the reference's own CPU implementation (oracle/_ref, compiled
-from the unmodified reference sources) on the host cores, on a bounded row sample.
-N > 1 runs independent replicas (one per GPU, no data-path collective), weak scaling.
+Prints ONE JSON line (rank 0). value = whole-job TFLOP/s with the algorithmic flop count
+F = (2q+2)*2*m*n*s + 2*m*s*k (s = k+p), i.e. the reference's arithmetic, not padded
+tiles; ms_per_step is the device time of one solve (CUDA events, max over ranks).
+N > 1 (torchrun): A is row-sharded, each rank holding the config's m rows (weak scaling:
+m_total = N*m), and the solve runs collectively with NCCL all-reduces of the Gram and
+n x s partial sums (rsvd_b200_randomized_ksvd_sharded_device).
+--impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
+the unmodified reference sources; else the C restatement) on the host cores, on a bounded
+row sample of the same workload.
 """
 from __future__ import annotations
 
@@ -32,8 +36,19 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M, N, K_RANK, P_OVER, Q_POW, SEED = 202599, 4096, 64, 10, 2, 42
 METRIC = "rSVD wall ms & TFLOP/s (frac of FP64 TC roofline), 1/2/4/8 B200 vs host CPU"
+SEED = 42
+# BASELINE.json configs (FP64 ones; C4 is the FP32 weak-scaling case)
+CONFIGS = {
+    "c1": dict(m=4096, n=4096, k=64, p=10, q=2, spectrum="exp", cpu_rows=4096,
+               name="C1 rSVD 4096x4096 k=64 p=10 q=2 FP64 (exponential decay)"),
+    "c2": dict(m=202599, n=4096, k=64, p=10, q=2, spectrum="exp", cpu_rows=16384,
+               name="C2 rSVD 202599x4096 k=64 p=10 q=2 FP64 (CelebA-shaped)"),
+    "c3": dict(m=202599, n=16384, k=128, p=20, q=2, spectrum="exp", cpu_rows=2048,
+               name="C3 rSVD 202599x16384 k=128 p=20 q=2 FP64 (CelebA 128x128-shaped)"),
+    "c5": dict(m=65536, n=65536, k=32, p=10, q=6, spectrum="slow", cpu_rows=1024,
+               name="C5 rSVD 65536x65536 k=32 p=10 q=6 FP64 (slow decay 1/i^0.1)"),
+}
 
 
 def flops(m, n, k, p, q):
@@ -46,63 +61,132 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def spectrum(cfg, n, xp):
+    """Controlled decaying spectra: "exp" sigma_i = exp(-i/tau) + 1e-6 with
+    sigma_1/sigma_s = 1e4 over the sketch width; "slow" sigma_i = 1/(i+1)^0.1
+    (synth.cpp:37's slow decay)."""
+    i = xp.arange(n, dtype=xp.float64)
+    if cfg["spectrum"] == "slow":
+        return 1.0 / (i + 1.0) ** 0.1
+    tau = (cfg["k"] + cfg["p"] - 1) / np.log(1e4)
+    return xp.exp(-i / tau) + 1e-6
+
+
+# ----------------------------------------------------------------- synthetic inputs
+def synth_host(cfg, rows):
+    """Host matrix for the CPU legs: the first `rows` rows of a tall G diag(sigma) V^T
+    with the config's n and spectrum (G Gaussian / sqrt(m), V Haar)."""
+    n = cfg["n"]
+    rng = np.random.default_rng(SEED)
+    sig = spectrum(cfg, n, np)
+    if not (cfg["m"] == n and (n & (n - 1)) == 0):
+        g = rng.standard_normal((rows, n)) / np.sqrt(cfg["m"])
+        if n > 8192:  # V = (H D)^T: a Haar QR of n x n is too slow on the host here
+            return np.ascontiguousarray(_fwht(g * sig, np) * rng.choice([-1.0, 1.0], size=n))
+        v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        return np.ascontiguousarray((g * sig) @ v.T)
+    # rows of the square Hadamard-conjugated matrix (see synth_device)
+    return np.ascontiguousarray(_hadamard_rows(cfg, 0, rows, np))
+
+
+def _fwht(x, xp):
+    """Normalised fast Walsh-Hadamard transform along the last axis (length 2^j)."""
+    n = x.shape[-1]
+    h = 1
+    y = x.copy()
+    while h < n:
+        y = y.reshape(*y.shape[:-1], n // (2 * h), 2, h)
+        a, b = y[..., 0, :].copy(), y[..., 1, :].copy()
+        y[..., 0, :] = a + b
+        y[..., 1, :] = a - b
+        y = y.reshape(*y.shape[:-3], n)
+        h *= 2
+    return y / np.sqrt(n)
+
+
+def _hadamard_rows(cfg, r0, r1, xp, device=None):
+    """Rows [r0, r1) of A = D1 H diag(sigma) H D2 P (n = 2^j square): H the normalised
+    Walsh-Hadamard matrix, D1/D2 random signs, P a random column permutation. H diag(s) H
+    is the dyadic convolution A0[i, j] = f(i xor j), f = H (sigma / sqrt(n)) ... so
+    A[i, j] = d1_i d2_j f(i xor pi(j)) is generated elementwise with singular values
+    exactly sigma (to rounding)."""
+    n = cfg["n"]
+    rng = np.random.default_rng(SEED + 7)
+    d1 = rng.choice([-1.0, 1.0], size=n)
+    d2 = rng.choice([-1.0, 1.0], size=n)
+    perm = rng.permutation(n)
+    sig = spectrum(cfg, n, np)
+    f = _fwht(sig[None, :], np)[0] / np.sqrt(n)  # f(t) = (1/n) sum_l sigma_l (-1)^{<l,t>}
+    if xp is np:
+        i = np.arange(r0, r1)[:, None]
+        return d1[r0:r1, None] * d2[None, :] * f[np.bitwise_xor(i, perm[None, :])]
+    t = xp
+    ft = t.from_numpy(f).to(device)
+    i = t.arange(r0, r1, device=device)[:, None]
+    pj = t.from_numpy(perm).to(device)[None, :]
+    return (t.from_numpy(d1[r0:r1]).to(device)[:, None] * t.from_numpy(d2).to(device)[None, :]
+            * ft[t.bitwise_xor(i, pj)])
+
+
+def synth_device(torch, cfg, m, rank, device):
+    """A on the device. Tall configs: A = G diag(sigma) V^T / sqrt(m), G Gaussian (per-rank
+    stream under sharding), V Haar (shared by all ranks), near-isometric columns so the
+    spectrum is sigma up to (1 +- sqrt(n/m)). Square power-of-two configs: the exact
+    Hadamard-conjugated construction of _hadamard_rows."""
+    n = cfg["n"]
+    if m == n and (n & (n - 1)) == 0:
+        a = torch.empty(m, n, dtype=torch.float64, device=device)
+        step = max(1, (1 << 28) // n)
+        for r0 in range(0, m, step):
+            r1 = min(m, r0 + step)
+            a[r0:r1] = _hadamard_rows(cfg, r0, r1, torch, device)
+        return a
+    sig = spectrum(cfg, n, torch).to(device)
+    gv = torch.Generator(device=device).manual_seed(SEED)
+    v = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device=device, generator=gv))[0]
+    gg = torch.Generator(device=device).manual_seed(SEED + 1 + rank)
+    a = torch.empty(m, n, dtype=torch.float64, device=device)
+    step = max(1, (1 << 26) // n)
+    scale = sig / np.sqrt(cfg["m"])
+    for r0 in range(0, m, step):
+        r1 = min(m, r0 + step)
+        g = torch.randn(r1 - r0, n, dtype=torch.float64, device=device, generator=gg)
+        a[r0:r1] = (g * scale) @ v.T
+    del v
+    return a
+
+
 # ----------------------------------------------------------------- CPU reference
-def cpu_reference_run(rows: int, threads: int, reps: int = 1):
+def cpu_reference_run(cfg, rows, threads, reps=1):
     """Time randsvd::randomized_ksvd (the unmodified reference library) on the first
-    `rows` rows of the synthetic C2 matrix (same n, k, p, q, seed), all host threads."""
+    `rows` rows of the config's synthetic matrix (same n, k, p, q, seed), all host threads."""
     from oracle.oracle import Oracle, available
     kind = "reference" if available("reference") else "port"
     orc = Oracle(kind)
-    a = synth_host(rows, N, SEED)
+    a = synth_host(cfg, rows)
+    k, p, q = cfg["k"], cfg["p"], cfg["q"]
     if kind == "reference":
         orc.set_max_threads(threads)
-        times, _ = orc.timed_solve(a, K_RANK, P_OVER, Q_POW, SEED, reps=reps)
+        times, _ = orc.timed_solve(a, k, p, q, SEED, reps=reps)
         cores = threads
     else:
         times = []
         for _ in range(reps):
             t0 = time.perf_counter()
-            orc.randomized_ksvd(a, K_RANK, P_OVER, Q_POW, SEED, values_only=False)
+            orc.randomized_ksvd(a, k, p, q, SEED, values_only=False)
             times.append(time.perf_counter() - t0)
         cores = 1
     t = min(times)
-    f = flops(rows, N, K_RANK, P_OVER, Q_POW)
+    f = flops(rows, cfg["n"], k, p, q)
     return {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
-            "sample": f"{rows}x{N} row block of the C2 synthetic matrix, k={K_RANK} p={P_OVER} "
-                      f"q={Q_POW}; {t:.2f} s per solve ({reps} run)",
+            "sample": f"{rows}x{cfg['n']} row block of the {cfg['name'].split()[0]} synthetic "
+                      f"matrix, k={k} p={p} q={q}; {t:.2f} s per solve ({reps} run)",
             "seconds": t}
 
 
-def synth_host(rows, cols, seed):
-    """Host copy of the first rows of the synthetic matrix (same law as synth_device)."""
-    rng = np.random.default_rng(seed)
-    tau = (K_RANK + P_OVER - 1) / np.log(1e4)
-    sig = np.exp(-np.arange(cols) / tau) + 1e-6
-    v, _ = np.linalg.qr(rng.standard_normal((cols, cols)))
-    g = rng.standard_normal((rows, cols)) / np.sqrt(M)
-    return np.ascontiguousarray((g * sig) @ v.T)
-
-
 # ----------------------------------------------------------------- GPU helpers
-def synth_device(torch, m, n, seed, device):
-    """A = G diag(sigma) V^T: G Gaussian / sqrt(m) (near-isometric columns), V a random
-    orthogonal n x n, sigma_i = exp(-i/tau) + 1e-6 with sigma_1/sigma_s = 1e4 over the
-    sketch width (a controlled, decaying spectrum)."""
-    gen = torch.Generator(device=device).manual_seed(seed)
-    tau = (K_RANK + P_OVER - 1) / np.log(1e4)
-    sig = torch.exp(-torch.arange(n, dtype=torch.float64, device=device) / tau) + 1e-6
-    v = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device=device, generator=gen))[0]
-    a = torch.empty(m, n, dtype=torch.float64, device=device)
-    step = 16384
-    for r0 in range(0, m, step):
-        r1 = min(m, r0 + step)
-        g = torch.randn(r1 - r0, n, dtype=torch.float64, device=device, generator=gen)
-        a[r0:r1] = (g * (sig / np.sqrt(m))) @ v.T
-    return a
-
-
-def fp64_peak(torch, device):
-    """Measured FP64 tensor-core peak for the roofline: cuBLAS DGEMM 8192^3, best of 3."""
+def cublas_dgemm_peak(torch, device):
+    """cuBLAS DGEMM 8192^3, best of 3 (library reference point for the FP64 roofline)."""
     a = torch.randn(8192, 8192, dtype=torch.float64, device=device)
     b = torch.randn(8192, 8192, dtype=torch.float64, device=device)
     c = a @ b
@@ -176,11 +260,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def load_traffic():
+def load_traffic(config):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(path):
         with open(path) as f:
-            return json.load(f)
+            t = json.load(f)
+        if t.get("config", "c2") == config:
+            return t
     return None
 
 
@@ -189,25 +275,24 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    cfg = CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    rows = args.cpu_rows
+    rows = args.cpu_rows or cfg["cpu_rows"]
     for _ in range(args.warmup):  # untimed warm-up on a quarter-size sample (bounded time)
-        cpu_reference_run(max(1024, rows // 4), threads)
-    samples = []
-    for _ in range(args.steps):
-        r = cpu_reference_run(rows, threads)
-        samples.append(r)
+        cpu_reference_run(cfg, max(256, rows // 4), threads)
+    samples = [cpu_reference_run(cfg, rows, threads) for _ in range(args.steps)]
     secs = [r["seconds"] for r in samples]
     value = statistics.median([r["value"] for r in samples])
     base = samples[0]
     out = {
         "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 3),
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * statistics.median(secs), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (G diag(sigma) V^T, exponential decay, seed 42)",
-        "config": {"workload": f"C2 rSVD {M}x{N} k={K_RANK} p={P_OVER} q={Q_POW} FP64, "
-                               f"CPU sample {rows}x{N}", "m": M, "n": N, "k": K_RANK,
-                   "p": P_OVER, "q": Q_POW, "parallelism": "host threads"},
+        "data": "synthetic (controlled decaying spectrum, seed 42)",
+        "config": {"workload": f"{cfg['name']}, CPU sample {rows}x{cfg['n']}", "m": cfg["m"],
+                   "n": cfg["n"], "k": cfg["k"], "p": cfg["p"], "q": cfg["q"],
+                   "parallelism": "host threads"},
         "impl": "reference",
         "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": base["cores"],
                          "kind": base["kind"], "sample": base["sample"]},
@@ -222,20 +307,33 @@ def run_ours(args):
     import paper_2110_03423_b200 as P
 
     rank, world, local_rank = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-
-    m, n, k, p, q = args.m, args.n, K_RANK, P_OVER, Q_POW
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfgd = CONFIGS[args.config]
+    m, n, k, p, q = cfgd["m"], cfgd["n"], cfgd["k"], cfgd["p"], cfgd["q"]
+    m_total = m * world
     cfg = P.RsvdConfig(k=k, oversample=p, power_q=q, seed=SEED)
-    F = flops(m, n, k, p, q)
+    F = flops(m_total, n, k, p, q)
     solver = P.Solver(local_rank)
-    a = synth_device(torch, m, n, SEED + rank, dev)
-    peak = fp64_peak(torch, dev)
-    torch.cuda.synchronize()
+    if world > 1:
+        P.attach_process_group(solver)
 
+    def solve_dev(a):
+        if world > 1:
+            return solver.randomized_ksvd_sharded_device(a, m_total, cfg)
+        return solver.randomized_ksvd_device(a, cfg)
+
+    def solve_host(a_host):
+        if world > 1:
+            return solver.randomized_ksvd_sharded(a_host, m_total, cfg)
+        return solver.randomized_ksvd(a_host, cfg)
+
+    a = synth_device(torch, cfgd, m, rank, dev)
+    peak_cublas = cublas_dgemm_peak(torch, dev)
+    torch.cuda.synchronize()
     lib_stream = torch.cuda.ExternalStream(solver.stream, device=dev)
 
     def barrier():
@@ -246,7 +344,7 @@ def run_ours(args):
 
     # ---- warm-up (also allocates the workspace)
     for _ in range(args.warmup):
-        u, s, v, sw = solver.randomized_ksvd_device(a, cfg)
+        u, s, v, sw = solve_dev(a)
     launches_per_step = solver.last_launch_count()
 
     # ---- timed region: K device-resident solves
@@ -259,7 +357,7 @@ def run_ours(args):
         e0.record(lib_stream)
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            u, s, v, sw = solver.randomized_ksvd_device(a, cfg)
+            u, s, v, sw = solve_dev(a)
         e1.record(lib_stream)
         e1.synchronize()
         wall = time.perf_counter() - t0
@@ -272,70 +370,79 @@ def run_ours(args):
         t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         step_ms = float(t.item())
-    value = world * F / (step_ms * 1e-3) / 1e12
+    value = F / (step_ms * 1e-3) / 1e12
+    sigma1 = float(s[0].item())
 
     # ---- e2e: the public host-buffer API (pinned A in, U, sigma, V out), same config
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     a_host_t = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
     a_host_t.copy_(a)
     a_host = a_host_t.numpy()
-    del a
+    del a, u, v
     torch.cuda.empty_cache()
-    res = solver.randomized_ksvd(a_host, cfg)  # warm the host path
+    res = solve_host(a_host)  # warm the host path
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res = solver.randomized_ksvd(a_host, cfg)
+        res = solve_host(a_host)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * F / e2e_s / 1e12
-    sigma_check = float(res.factors.sigma[0])
+    e2e_value = F / e2e_s / 1e12
 
     # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded row sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_reference_run(args.cpu_rows, os.cpu_count() or 1)
+        cpu = cpu_reference_run(cfgd, args.cpu_rows or cfgd["cpu_rows"], os.cpu_count() or 1)
         cpu.pop("seconds", None)
 
     if rank == 0:
+        peak_dmma = solver.dmma_peak_tflops()
+        peak = max(peak_dmma, peak_cublas)
         per_launch_ms = stats["ms"] / max(1, stats["count"])
         per_launch_flops = stats["flops"] / max(1, stats["count"])
         achieved = per_launch_flops / (per_launch_ms * 1e-3) / 1e12 if stats["count"] else None
-        traffic = load_traffic()
+        traffic = load_traffic(args.config)
         roof = {"bound": "tensor", "kernel": "gemm_A (FP64 DMMA passes over A: ax + atx)",
                 "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 3),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
                 "traffic": traffic.get("gemm_A_bytes_per_launch") if traffic else None,
-                "peak_source": "cuBLAS DGEMM 8192^3 best-of-3 measured in this run "
-                               "(MEASURED_PEAKS.json has no FP64 entry)",
+                "traffic_algorithmic": m * n * 8,
+                "peak_source": ("max of the DMMA m16n8k16 issue-rate probe (rsvd_b200_dmma_peak, "
+                                f"{peak_dmma:.2f}) and cuBLAS DGEMM 8192^3 ({peak_cublas:.2f}), "
+                                "both measured in this run; MEASURED_PEAKS.json has no FP64 entry"),
                 "launches_timed": stats["count"], "ms_per_launch": round(per_launch_ms, 4),
                 "share_of_step": round(stats["ms"] / dev_ms, 4) if dev_ms else None,
-                "algorithmic_flops_per_launch": per_launch_flops}
+                "algorithmic_flops_per_launch": per_launch_flops,
+                "step_frac": round(value / world / peak, 4)}
         out = {
             "metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (G diag(sigma) V^T, exponential decay sigma_1/sigma_s=1e4, seed 42)",
-            "config": {"workload": f"C2 rSVD {m}x{n} k={k} p={p} q={q} FP64 (CelebA-shaped)",
-                       "m": m, "n": n, "k": k, "p": p, "q": q, "sketch_width": sw,
-                       "parallelism": "replicas" if world > 1 else "single GPU",
-                       "l2": "A (6.6 GB) >> L2 (126 MB): every pass streams HBM, no flush"},
+            "data": f"synthetic ({cfgd['spectrum']} spectrum, seed 42)",
+            "config": {"workload": cfgd["name"], "m": m_total, "m_per_gpu": m, "n": n, "k": k,
+                       "p": p, "q": q, "sketch_width": sw,
+                       "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "single GPU",
+                       "l2": f"A ({m * n * 8 / 1e9:.1f} GB per GPU) >> L2 (126 MB): every pass "
+                             "streams HBM, no flush"},
             "clocks": clocks.summary(),
-            "e2e": {"value": round(e2e_value, 4), "unit": "TFLOP/s", "ms_per_step": round(1e3 * e2e_s, 2),
+            "e2e": {"value": round(e2e_value, 4), "unit": "TFLOP/s",
+                    "ms_per_step": round(1e3 * e2e_s, 2),
                     "h2d_bytes_per_step": m * n * 8,
                     "d2h_bytes_per_step": (m * k + n * k + k) * 8,
-                    "api": "rsvd_b200_randomized_ksvd (host buffers, pinned A)"},
+                    "api": ("rsvd_b200_randomized_ksvd_sharded" if world > 1
+                            else "rsvd_b200_randomized_ksvd") + " (host buffers, pinned A)"},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
             "cpu_baseline": cpu,
             "wall_s_timed": round(wall, 3),
-            "sigma1": sigma_check,
+            "sigma1": sigma1,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
+        solver.detach()
         torch.distributed.destroy_process_group()
 
 
@@ -345,9 +452,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--m", type=int, default=M)
-    ap.add_argument("--n", type=int, default=N)
-    ap.add_argument("--cpu-rows", type=int, default=16384)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

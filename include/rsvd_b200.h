@@ -100,6 +100,46 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_device(rsvd_b200_handle* h, const dou
                                                   size_t* sketch_width);
 
 /* ---------------------------------------------------------------------------
+ * Row-sharded solves across GPUs (no reference counterpart: the reference is one
+ * host process; this is §8e's data-parallel split of the same
+ * randomized_ksvd, rsvd.hpp:58). Rank g holds a contiguous row block A_g of the
+ * m_total x n input (m_total >= n); every rank calls the solve collectively with the
+ * same n, m_total and config. Only sums over rows cross ranks (the s x s Gram of each
+ * CholeskyQR pass, the n x s partials of A^T Q and Q^T A, the TSQR R stack of the
+ * Householder fallback, the status flags), as in-place FP64 sum all-reduces on the
+ * handle's stream. sigma and V are returned replicated, U sharded like A
+ * (m_local x k). Results agree with the single-device solve to rounding.
+ * ------------------------------------------------------------------------- */
+/* 128-byte NCCL unique id, created on rank 0 and distributed out of band. */
+rsvd_b200_status rsvd_b200_nccl_unique_id(unsigned char* id128);
+/* Attach an NCCL communicator (the process's libnccl.so.2) to the handle's device. */
+rsvd_b200_status rsvd_b200_comm_init_nccl(rsvd_b200_handle* h, const unsigned char* id128,
+                                          int rank, int world);
+/* In-process group of handles (one host thread per rank; buffers on one device or
+ * P2P-reachable devices): reductions are fixed-order device sums. For testing the
+ * sharded pipeline on one GPU. */
+typedef struct rsvd_b200_local_group rsvd_b200_local_group;
+rsvd_b200_status rsvd_b200_local_group_create(int world, rsvd_b200_local_group** out);
+void rsvd_b200_local_group_destroy(rsvd_b200_local_group* g);
+rsvd_b200_status rsvd_b200_comm_init_local(rsvd_b200_handle* h, rsvd_b200_local_group* g,
+                                           int rank);
+/* rank / world of the attached communicator (0 / 1 without one). */
+rsvd_b200_status rsvd_b200_comm_info(rsvd_b200_handle* h, int* rank, int* world);
+/* Detach and destroy the handle's communicator. */
+void rsvd_b200_comm_free(rsvd_b200_handle* h);
+/* Host buffers: a (m_local x n) in, u (m_local x k), sigma (k), v (n x k) out. */
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded(rsvd_b200_handle* h, const double* a,
+                                                   size_t m_local, size_t m_total, size_t n,
+                                                   const rsvd_b200_config* cfg, double* u,
+                                                   double* sigma, double* v,
+                                                   size_t* sketch_width);
+/* Device buffers (A shard resident in HBM, same layout rules as the _device solve). */
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_device(
+    rsvd_b200_handle* h, const double* a_dev, size_t m_local, size_t m_total, size_t n,
+    size_t lda, const rsvd_b200_config* cfg, double* u_dev, double* sigma_dev, double* v_dev,
+    size_t* sketch_width);
+
+/* ---------------------------------------------------------------------------
  * Step functions (rsvd.hpp:36-53), host buffers, for the reference's step-level
  * tests.  range_basis writes the kept width to *cols_out (q must hold m x s).
  * ------------------------------------------------------------------------- */
@@ -149,6 +189,10 @@ long rsvd_b200_last_launch_count(rsvd_b200_handle* h);
 long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key);
 /* Force the robust path (host-checked Cholesky, Householder fallback) for every solve. */
 void rsvd_b200_set_robust(rsvd_b200_handle* h, int on);
+
+/* Measured FP64 tensor-core peak of the handle's GPU (TFLOP/s): an issue-bound
+ * mma.sync m16n8k16 f64 loop on every SM — the roofline denominator of the GEMMs. */
+rsvd_b200_status rsvd_b200_dmma_peak(rsvd_b200_handle* h, double* tflops);
 
 /* Library build identification (sm_100a). */
 const char* rsvd_b200_version(void);

@@ -19,7 +19,10 @@ EXPORTS = [
     "rsvd_b200_splitmix_words", "rsvd_b200_uniforms", "rsvd_b200_last_profile",
     "rsvd_b200_set_profiling", "rsvd_b200_last_launch_count", "rsvd_b200_version",
     "rsvd_b200_kernel_stats", "rsvd_b200_reset_stats", "rsvd_b200_last_info",
-    "rsvd_b200_set_robust",
+    "rsvd_b200_set_robust", "rsvd_b200_nccl_unique_id", "rsvd_b200_comm_init_nccl",
+    "rsvd_b200_local_group_create", "rsvd_b200_local_group_destroy", "rsvd_b200_comm_init_local",
+    "rsvd_b200_comm_info", "rsvd_b200_comm_free", "rsvd_b200_randomized_ksvd_sharded",
+    "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak",
 ]
 
 
@@ -74,6 +77,19 @@ def load() -> C.CDLL:
         "rsvd_b200_reset_stats": (None, [_vp]),
         "rsvd_b200_last_info": (C.c_long, [_vp, C.c_char_p]),
         "rsvd_b200_set_robust": (None, [_vp, C.c_int]),
+        "rsvd_b200_nccl_unique_id": (C.c_int, [C.c_char_p]),
+        "rsvd_b200_dmma_peak": (C.c_int, [_vp, _dp]),
+        "rsvd_b200_comm_init_nccl": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
+        "rsvd_b200_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+        "rsvd_b200_local_group_destroy": (None, [_vp]),
+        "rsvd_b200_comm_init_local": (C.c_int, [_vp, _vp, C.c_int]),
+        "rsvd_b200_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "rsvd_b200_comm_free": (None, [_vp]),
+        "rsvd_b200_randomized_ksvd_sharded": (C.c_int, [_vp, _dp, _sz, _sz, _sz, cfgp, _dp, _dp,
+                                                        _dp, C.POINTER(_sz)]),
+        "rsvd_b200_randomized_ksvd_sharded_device": (C.c_int, [_vp, _dp, _sz, _sz, _sz, _sz,
+                                                               cfgp, _dp, _dp, _dp,
+                                                               C.POINTER(_sz)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -565,3 +565,62 @@ cudaError_t launch_reduce_partials(const double* part, long stride, int splits, 
 }
 
 }  // namespace rsvdb200
+
+// ===================================================================== peak probe
+namespace rsvdb200 {
+
+// FP64 tensor-pipe issue rate: every warp runs independent m16n8k16 DMMA chains on
+// register operands (no memory traffic), 2 CTAs x 8 warps per SM. The roofline
+// denominator for the passes over A (MEASURED_PEAKS.json has no FP64 entry).
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+    double acc[4][4];
+    double a[8], b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[t][r] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = (threadIdx.x + i) * 1e-3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = (threadIdx.x - i) * 1e-3;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma_16x8x16(acc[t], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s += acc[t][r];
+    if (s == 1234.5) out[0] = s;  // keep the chains alive
+}
+
+cudaError_t measure_dmma_peak(cudaStream_t st, double* tflops) {
+    double* out = nullptr;
+    cudaError_t e = cudaMalloc(&out, sizeof(double));
+    if (e != cudaSuccess) return e;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = 148 * 2, iters = 4096;
+    dmma_peak_kernel<<<grid, 256, 0, st>>>(out, iters);  // warm-up (clocks up)
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0, st);
+        dmma_peak_kernel<<<grid, 256, 0, st>>>(out, iters);
+        cudaEventRecord(e1, st);
+        e = cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flop = 2.0 * 16 * 8 * 16 * 4.0 * iters * grid * (256 / 32);
+    *tflops = flop / (best * 1e-3) / 1e12;
+    return e;
+}
+
+}  // namespace rsvdb200

@@ -46,6 +46,9 @@ cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);
 cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
                                    long count, cudaStream_t st);
 
+// FP64 tensor-core (DMMA m16n8k16) issue-rate probe on the whole GPU, TFLOP/s.
+cudaError_t measure_dmma_peak(cudaStream_t st, double* tflops);
+
 // Omega^T (NP x n, ld) for the reference's SplitMix64 + Box-Muller stream:
 // Omega(r, c) = normal #(r*s + c) of GaussianSampler(seed); rows c >= s of
 // Omega^T are zero.

@@ -34,10 +34,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/rsvd_b200.h"
+#include "comm.h"
 #include "kernels.h"
 
 using namespace rsvdb200;
@@ -139,6 +141,8 @@ struct rsvd_b200_handle {
     // workspace
     DevBuf a_copy, a_t, xt, y, q, part, b, b2, qbt, vbuf, small, flags, u_out, v_out, sig_out,
         hh_work, omega_host_dev, jscratch, cwork, ubt;
+    std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
+    DevBuf red_scratch;          // TSQR R stack / flag reduction
     long fallbacks = 0, reruns = 0;
     int last_sweeps = 0;
     bool force_robust = false;
@@ -261,10 +265,11 @@ enum { kG = 0, kR1 = 1, kR1iT = 2, kR2 = 3, kR2iT = 4, kRB = 5, kUR = 6, kWR = 7
        kSig = 9, kC = 10, kX = 11, kNumSmall = 12 };
 
 struct Plan {
-    long m, n;   // tall problem: m >= n
+    long m, n;   // tall problem: m >= n (m = this rank's rows when sharded)
     long lda;    // leading dimension of A on device
     int s, NP;   // sketch width and padded width
     long ldn;    // leading dimension of n-length rows (Xt, B, Q_B^T): round_up(n, 2)
+    bool sharded = false;  // A row-sharded over h->comm: sums over m are all-reduced
 };
 
 // One pipeline run. `robust`: synchronise after every Cholesky and take the
@@ -278,6 +283,14 @@ struct Ctx {
     bool robust;
     int* flags;
     double* slot(int i) const { return h->small.d() + (size_t)i * p.NP * p.NP; }
+    // Sum over the row shards (no-op on a single device): the Gram of a tall QR and the
+    // n x s partials of A^T Q / Q^T A are the only cross-rank data of Algorithm 1.
+    void allreduce(double* buf, size_t count) const {
+        if (!p.sharded) return;
+        const std::string err = h->comm->allreduce_sum(buf, count, h->stream);
+        if (!err.empty()) fail(RSVD_B200_NCCL_ERROR, "%s", err.c_str());
+        h->launches += 1;
+    }
 };
 
 double* small_slot(rsvd_b200_handle* h, const Plan& p, int slot) {
@@ -405,6 +418,40 @@ void set_identity(const Ctx& c, int slot) {
     c.h->sync();  // eye is a stack temporary
 }
 
+// Householder fallback of a row-sharded tall QR (TSQR): Y_g = Q_g R_g locally, the
+// ranks' R_g (NP x NP blocks, zero padded) are stacked by a sum all-reduce of a
+// world*NP x NP buffer in which each rank fills its own block, the stack is factored
+// again (replicated, identical on every rank) as Q_s R, and Q_g <- Q_g Q_s[block g].
+// R keeps diag >= 0 (the reference's sign fix, qr.cpp:86-93), so for a full-rank Y the
+// result is the unique thin QR the unsharded Householder QR produces.
+void tsqr(const Ctx& c, double* Y, long M, double* Qout) {
+    rsvd_b200_handle* h = c.h;
+    const int NP = c.p.NP, s = c.p.s;
+    const int world = h->comm->world, rank = h->comm->rank;
+    if (M < s)
+        fail(RSVD_B200_DIMENSION_ERROR,
+             "TSQR fallback needs at least s=%d rows per shard, rank %d has %ld", s, rank, M);
+    const long stack_rows = (long)world * NP;
+    const size_t stack = (size_t)stack_rows * NP;
+    h->red_scratch.reserve((stack * 2 + (size_t)NP * NP) * sizeof(double));
+    double* R = h->red_scratch.d();
+    double* Qs = R + stack;
+    double* Xt = Qs + stack;
+    h->hh_work.reserve(householder_work_doubles(std::max(M, stack_rows), s) * sizeof(double));
+    h->launched(launch_fill(R, (long)stack, 0.0, h->stream), "fill");
+    h->launched(launch_householder_qr(Y, M, s, NP, Qout, NP, R + (size_t)rank * NP * NP, NP,
+                                      h->hh_work.d(), h->stream),
+                "householder_qr");
+    c.allreduce(R, stack);
+    h->launched(launch_householder_qr(R, stack_rows, s, NP, Qs, NP, c.slot(kRB), NP,
+                                      h->hh_work.d(), h->stream),
+                "householder_qr");
+    // Q_g (M x NP) <- Q_g * Q_s[rank block] (NP x NP); ax takes the transposed block
+    h->launched(launch_transpose(Qs + (size_t)rank * NP * NP, NP, NP, NP, Xt, NP, h->stream),
+                "transpose");
+    gemm_ax(h, Qout, M, NP, NP, Xt, NP, NP, Qout, NP);  // in place: K = NP, one k-pass per CTA
+}
+
 // ---------------------------------------------------------------- tall QR
 // Thin QR of Y (M x NP, ld NP, columns >= s zero) by CholeskyQR, returned in factored
 // form Q = Q1 * C with Q1 at h->basis and C in slot kC (h->c_identity when C = I):
@@ -425,6 +472,7 @@ bool tall_qr(const Ctx& c, double* Y, long M, double* Q1out, int passes, bool ma
     h->c_identity = true;
     h->basis = Q1out;
     if (!gram_ready) gemm_atx(h, Y, M, NP, NP, Y, NP, NP, c.slot(kG), NP, false);  // G1 = Y^T Y
+    c.allreduce(c.slot(kG), (size_t)NP * NP);  // sharded: G1 = sum_g Y_g^T Y_g
     cholesky(c, kG, kR1, kR1iT);
     if (!chol_broke(c)) {
         if (passes == 1 && !materialize) {
@@ -445,6 +493,7 @@ bool tall_qr(const Ctx& c, double* Y, long M, double* Q1out, int passes, bool ma
             return false;
         }
         if (!g2) gemm_atx(h, Q1out, M, NP, NP, Q1out, NP, NP, c.slot(kG), NP, false);
+        c.allreduce(c.slot(kG), (size_t)NP * NP);
         cholesky(c, kG, kR2, kR2iT);
         if (!chol_broke(c)) {
             if (materialize) {  // in place: each ax CTA reads exactly the rows it writes
@@ -459,6 +508,13 @@ bool tall_qr(const Ctx& c, double* Y, long M, double* Q1out, int passes, bool ma
                         "small_matmul");  // R = R2 R1
             return false;
         }
+    }
+    if (c.p.sharded) {
+        tsqr(c, Y, M, Q1out);
+        h->basis = Q1out;
+        h->c_identity = true;
+        h->fallbacks += 1;
+        return true;
     }
     h->hh_work.reserve(householder_work_doubles(M, s) * sizeof(double));
     h->launched(launch_householder_qr(Y, M, s, NP, Q1out, NP, c.slot(kRB), NP, h->hh_work.d(),
@@ -599,6 +655,7 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
         h->mark("power_atx");
         gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true, "gemm_A",
                  2.0 * p.m * p.n * p.s);  // (A^T Q1)^T
+        c.allreduce(h->b.d(), (size_t)p.NP * p.ldn);  // sharded: sum_g (A_g^T Q1_g)^T
         h->mark("qr_wide");
         const double* zt = apply_ct(c, h->b.d(), h->b2.d());  // (A^T W)^T, W = Q1 C
         wide_qr(c, zt, p.n, p.ldn, h->xt.d(), kRB, 1);  // Z = QR(A^T W).q, as Z^T
@@ -627,6 +684,7 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
     h->mark("project_atx");
     gemm_atx(h, A, m, n, p.lda, h->basis, NP, NP, h->b.d(), p.ldn, true, "gemm_A",
              2.0 * m * n * s);  // Q1^T A
+    c.allreduce(h->b.d(), (size_t)NP * p.ldn);  // sharded: B = sum_g Q1_g^T A_g
     h->mark("small_svd");
     const double* bq = apply_ct(c, h->b.d(), h->b2.d());  // B = C^T Q1^T A = Q^T A (NP x n)
     wide_qr(c, bq, n, p.ldn, h->qbt.d(), kRB, 2);          // B^T = Q_B R_B
@@ -678,7 +736,21 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
 bool finish_run(const Ctx& c, bool checked_nonfinite) {
     download_flags(c.h);
     c.h->sync();
-    const int* f = c.h->flags_host;
+    int* f = c.h->flags_host;
+    if (c.p.sharded) {  // NaN/Inf in any shard, abort on any rank (replicated: all agree)
+        double fl[2] = {(double)f[kFlagNonfinite], (double)f[kFlagAbort]};
+        c.h->red_scratch.reserve(2 * sizeof(double));
+        ck(cudaMemcpyAsync(c.h->red_scratch.p, fl, sizeof fl, cudaMemcpyHostToDevice,
+                           c.h->stream),
+           "flag upload");
+        c.allreduce(c.h->red_scratch.d(), 2);
+        ck(cudaMemcpyAsync(fl, c.h->red_scratch.p, sizeof fl, cudaMemcpyDeviceToHost,
+                           c.h->stream),
+           "flag download");
+        c.h->sync();
+        f[kFlagNonfinite] = fl[0] != 0.0;
+        f[kFlagAbort] = fl[1] != 0.0;
+    }
     if (checked_nonfinite && f[kFlagNonfinite])
         fail(RSVD_B200_ARGUMENT_ERROR, "randomized_ksvd input contains NaN or Inf");
     if (f[kFlagAbort]) return false;
@@ -694,10 +766,8 @@ bool finish_run(const Ctx& c, bool checked_nonfinite) {
 // Tall solve (rsvd.cpp:126-134) on device data. A: m x n (lda), m >= n. The optimistic
 // pipeline runs first; a Cholesky breakdown anywhere reruns the whole solve on the robust
 // path (Householder fallbacks), which reproduces the reference's QR semantics.
-void solve_tall(rsvd_b200_handle* h, const double* A, long m, long n, long lda,
-                const rsvd_b200_config& cfg, double* u, long ldu, double* sigma, double* v,
-                long ldv, size_t* sketch_width) {
-    const Plan p = make_plan(m, n, lda, (long)rsvd_b200_sketch_width(&cfg, (size_t)m, (size_t)n));
+void solve_tall(rsvd_b200_handle* h, const double* A, const Plan& p, const rsvd_b200_config& cfg,
+                double* u, long ldu, double* sigma, double* v, long ldv, size_t* sketch_width) {
     h->fallbacks = 0;
     h->reruns = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -738,14 +808,69 @@ void solve_device(rsvd_b200_handle* h, const double* A, long m, long n, long lda
             h->launched(launch_copy2d(A, lda, h->a_copy.d(), la, m, n, h->stream), "copy2d");
             a = h->a_copy.d();
         }
-        solve_tall(h, a, m, n, la, cfg, u, k, sigma, v, k, sketch_width);
+        const Plan p =
+            make_plan(m, n, la, (long)rsvd_b200_sketch_width(&cfg, (size_t)m, (size_t)n));
+        solve_tall(h, a, p, cfg, u, k, sigma, v, k, sketch_width);
         return;
     }
     // wide: solve on the materialised transpose, U and V swap roles
     const long lt = round_up(m, 2);
     h->a_t.reserve((size_t)n * lt * sizeof(double));
     h->launched(launch_transpose(A, m, n, lda, h->a_t.d(), lt, h->stream), "transpose");
-    solve_tall(h, h->a_t.d(), n, m, lt, cfg, v, k, sigma, u, k, sketch_width);
+    const Plan p = make_plan(n, m, lt, (long)rsvd_b200_sketch_width(&cfg, (size_t)n, (size_t)m));
+    solve_tall(h, h->a_t.d(), p, cfg, v, k, sigma, u, k, sketch_width);
+}
+
+// Row-sharded solve: this rank holds rows [r0, r0 + m_local) of the m_total x n input
+// (m_total >= n). Every rank calls it collectively with the same n, m_total and config;
+// sigma and V come back replicated, U sharded like A. The shard layout is checked
+// collectively first (one tiny all-reduce), so a bad shard fails on every rank alike.
+void solve_sharded(rsvd_b200_handle* h, const double* A, long m_local, long m_total, long n,
+                   long lda, const rsvd_b200_config& cfg, double* u, double* sigma, double* v,
+                   size_t* sketch_width) {
+    if (!h->comm) fail(RSVD_B200_ARGUMENT_ERROR, "sharded solve needs a communicator "
+                                                 "(rsvd_b200_comm_init_nccl / _local)");
+    if (m_total < n)
+        fail(RSVD_B200_DIMENSION_ERROR,
+             "the row-sharded solve needs a tall input (m_total >= n), got %ldx%ld", m_total, n);
+    const long md = std::min(m_total, n);
+    if (cfg.k < 1 || (long)cfg.k > md)
+        fail(RSVD_B200_ARGUMENT_ERROR, "target rank k=%zu outside [1, %ld] for a %ldx%ld input",
+             cfg.k, md, m_total, n);
+    if (!(cfg.epsilon > 0.0 && cfg.epsilon < 1.0))
+        fail(RSVD_B200_ARGUMENT_ERROR, "epsilon must lie in (0, 1)");
+    const long s = (long)rsvd_b200_sketch_width(&cfg, (size_t)m_total, (size_t)n);
+    // collective shard check: sum of m_local, count of shards thinner than s
+    {
+        double chk[2] = {(double)m_local, m_local < s ? 1.0 : 0.0};
+        h->red_scratch.reserve(2 * sizeof(double));
+        ck(cudaMemcpyAsync(h->red_scratch.p, chk, sizeof chk, cudaMemcpyHostToDevice, h->stream),
+           "shard check upload");
+        const std::string err = h->comm->allreduce_sum(h->red_scratch.d(), 2, h->stream);
+        if (!err.empty()) fail(RSVD_B200_NCCL_ERROR, "%s", err.c_str());
+        ck(cudaMemcpyAsync(chk, h->red_scratch.p, sizeof chk, cudaMemcpyDeviceToHost, h->stream),
+           "shard check download");
+        h->sync();
+        if ((long)chk[0] != m_total)
+            fail(RSVD_B200_DIMENSION_ERROR, "shard rows sum to %ld, m_total is %ld",
+                 (long)chk[0], m_total);
+        if (chk[1] != 0.0)
+            fail(RSVD_B200_DIMENSION_ERROR,
+                 "every shard needs at least s=%ld rows (%d shard(s) are thinner)", s,
+                 (int)chk[1]);
+    }
+    const double* a = A;
+    long la = lda;
+    if ((lda % 2) || (reinterpret_cast<uintptr_t>(A) & 15)) {  // TMA needs 16-byte rows
+        la = round_up(n, 2);
+        h->a_copy.reserve((size_t)m_local * la * sizeof(double));
+        h->launched(launch_copy2d(A, lda, h->a_copy.d(), la, m_local, n, h->stream), "copy2d");
+        a = h->a_copy.d();
+    }
+    Plan p = make_plan(m_local, n, la, s);
+    p.sharded = true;
+    const long k = (long)cfg.k;
+    solve_tall(h, a, p, cfg, u, k, sigma, v, k, sketch_width);
 }
 
 }  // namespace
@@ -903,6 +1028,110 @@ static void solve_host(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                            h->stream),
            "D2H v");
     h->sync();
+}
+
+// ------------------------------------------------------------ row-sharded solves
+struct rsvd_b200_local_group {
+    explicit rsvd_b200_local_group(int w) : g(w) {}
+    LocalGroup g;
+};
+
+rsvd_b200_status rsvd_b200_nccl_unique_id(unsigned char* out) {
+    return guarded([&] {
+        const std::string err = nccl_unique_id(out);
+        if (!err.empty()) fail(RSVD_B200_NCCL_ERROR, "%s", err.c_str());
+    });
+}
+
+rsvd_b200_status rsvd_b200_comm_init_nccl(rsvd_b200_handle* h, const unsigned char* id, int rank,
+                                          int world) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world)
+            fail(RSVD_B200_ARGUMENT_ERROR, "rank %d outside [0, %d)", rank, world);
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        std::unique_ptr<Comm> c;
+        const std::string err = make_nccl_comm(id, rank, world, &c);
+        if (!err.empty()) fail(RSVD_B200_NCCL_ERROR, "%s", err.c_str());
+        h->comm = std::move(c);
+    });
+}
+
+rsvd_b200_status rsvd_b200_local_group_create(int world, rsvd_b200_local_group** out) {
+    return guarded([&] {
+        if (world < 1 || world > 16)
+            fail(RSVD_B200_ARGUMENT_ERROR, "local group size %d outside [1, 16]", world);
+        *out = new rsvd_b200_local_group(world);
+    });
+}
+
+void rsvd_b200_local_group_destroy(rsvd_b200_local_group* g) { delete g; }
+
+rsvd_b200_status rsvd_b200_comm_init_local(rsvd_b200_handle* h, rsvd_b200_local_group* g,
+                                           int rank) {
+    return guarded([&] {
+        if (!g || rank < 0 || rank >= g->g.world)
+            fail(RSVD_B200_ARGUMENT_ERROR, "rank %d outside the local group", rank);
+        h->comm = make_local_comm(&g->g, rank);
+    });
+}
+
+rsvd_b200_status rsvd_b200_comm_info(rsvd_b200_handle* h, int* rank, int* world) {
+    *rank = h->comm ? h->comm->rank : 0;
+    *world = h->comm ? h->comm->world : 1;
+    return RSVD_B200_OK;
+}
+
+void rsvd_b200_comm_free(rsvd_b200_handle* h) {
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    h->comm.reset();
+}
+
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_device(
+    rsvd_b200_handle* h, const double* a_dev, size_t m_local, size_t m_total, size_t n,
+    size_t lda, const rsvd_b200_config* cfg, double* u_dev, double* sigma_dev, double* v_dev,
+    size_t* sketch_width) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        h->launches = 0;
+        solve_sharded(h, a_dev, (long)m_local, (long)m_total, (long)n, (long)lda, *cfg, u_dev,
+                      sigma_dev, v_dev, sketch_width);
+    });
+}
+
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded(rsvd_b200_handle* h, const double* a,
+                                                   size_t m_local, size_t m_total, size_t n,
+                                                   const rsvd_b200_config* cfg, double* u,
+                                                   double* sigma, double* v,
+                                                   size_t* sketch_width) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        h->launches = 0;
+        const long lda = round_up((long)n, 2);
+        h->a_copy.reserve(std::max<size_t>(1, m_local * lda) * sizeof(double));
+        ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(double), a, n * sizeof(double),
+                             n * sizeof(double), m_local, cudaMemcpyHostToDevice, h->stream),
+           "H2D of A shard");
+        const size_t k = cfg->k;
+        h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
+        if (u) h->u_out.reserve(std::max<size_t>(m_local * k, 1) * sizeof(double));
+        if (v) h->v_out.reserve(std::max<size_t>(n * k, 1) * sizeof(double));
+        solve_sharded(h, h->a_copy.d(), (long)m_local, (long)m_total, (long)n, lda, *cfg,
+                      u ? h->u_out.d() : nullptr, h->sig_out.d(), v ? h->v_out.d() : nullptr,
+                      sketch_width);
+        ck(cudaMemcpyAsync(sigma, h->sig_out.p, k * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream),
+           "D2H sigma");
+        if (u)
+            ck(cudaMemcpyAsync(u, h->u_out.p, m_local * k * sizeof(double),
+                               cudaMemcpyDeviceToHost, h->stream),
+               "D2H u");
+        if (v)
+            ck(cudaMemcpyAsync(v, h->v_out.p, n * k * sizeof(double), cudaMemcpyDeviceToHost,
+                               h->stream),
+               "D2H v");
+        h->sync();
+    });
 }
 
 rsvd_b200_status rsvd_b200_randomized_ksvd(rsvd_b200_handle* h, const double* a, size_t m,
@@ -1099,5 +1328,12 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
 }
 
 void rsvd_b200_set_robust(rsvd_b200_handle* h, int on) { h->force_robust = on != 0; }
+
+rsvd_b200_status rsvd_b200_dmma_peak(rsvd_b200_handle* h, double* tflops) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        ck(measure_dmma_peak(h->stream, tflops), "DMMA peak probe");
+    });
+}
 
 }  // extern "C"

@@ -160,6 +160,12 @@ class Solver:
         n = self.lib.rsvd_b200_last_profile(self.h, names, ms, 32)
         return {names[i].decode(): ms[i] for i in range(n)}
 
+    def dmma_peak_tflops(self) -> float:
+        """Measured FP64 tensor-core peak of this GPU (rsvd_b200_dmma_peak)."""
+        t = C.c_double(0)
+        _check(self.lib, self.lib.rsvd_b200_dmma_peak(self.h, C.byref(t)))
+        return t.value
+
     def last_launch_count(self) -> int:
         return int(self.lib.rsvd_b200_last_launch_count(self.h))
 
@@ -207,6 +213,59 @@ class Solver:
         _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_device(
             self.h, dptr(a), m, n, a.stride(0), C.byref(c), dptr(u), dptr(sig), dptr(v),
             C.byref(sw)))
+        return u, sig[:k], v, sw.value
+
+    # ------------------------------------------------------- row-sharded solves
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
+        """Attach an NCCL communicator (rank 0 made `unique_id` with nccl_unique_id())."""
+        if len(unique_id) != 128:
+            raise ArgumentError("NCCL unique id must be 128 bytes")
+        _check(self.lib, self.lib.rsvd_b200_comm_init_nccl(self.h, unique_id, rank, world))
+
+    def attach_local(self, group: "LocalGroup", rank: int) -> None:
+        """Join an in-process group (one thread per rank, buffers mutually addressable)."""
+        _check(self.lib, self.lib.rsvd_b200_comm_init_local(self.h, group.g, rank))
+
+    def detach(self) -> None:
+        self.lib.rsvd_b200_comm_free(self.h)
+
+    def comm_info(self) -> tuple[int, int]:
+        r, w = C.c_int(0), C.c_int(1)
+        self.lib.rsvd_b200_comm_info(self.h, C.byref(r), C.byref(w))
+        return r.value, w.value
+
+    def randomized_ksvd_sharded(self, a_local, m_total: int, cfg: RsvdConfig) -> RsvdResult:
+        """Collective row-sharded solve from host buffers: this rank's rows of A in, its
+        rows of U and the replicated sigma, V out."""
+        a = _arr(a_local)
+        ml, n = a.shape
+        k = max(int(cfg.k), 1)
+        u, v, s = np.empty((ml, k)), np.empty((n, k)), np.empty(k)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_sharded(
+            self.h, _dp(a), ml, m_total, n, C.byref(c), _dp(u), _dp(s), _dp(v), C.byref(sw)))
+        return RsvdResult(SvdFactors(u, s, v), sw.value)
+
+    def randomized_ksvd_sharded_device(self, a_local, m_total: int, cfg: RsvdConfig,
+                                       values_only: bool = False):
+        """Collective row-sharded solve with this rank's rows resident in HBM (CUDA float64
+        tensor). Returns (u_local, sigma, v, sketch_width) as CUDA tensors."""
+        import torch
+        a = a_local
+        assert a.is_cuda and a.dtype == torch.float64 and a.dim() == 2 and a.stride(1) == 1
+        ml, n = a.shape
+        k = int(cfg.k)
+        dev = a.device
+        sig = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+        u = None if values_only else torch.empty((ml, max(k, 1)), dtype=torch.float64, device=dev)
+        v = None if values_only else torch.empty((n, max(k, 1)), dtype=torch.float64, device=dev)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        dptr = lambda t: None if t is None else C.cast(t.data_ptr(), C.POINTER(C.c_double))
+        _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_sharded_device(
+            self.h, dptr(a), ml, m_total, n, a.stride(0), C.byref(c), dptr(u), dptr(sig),
+            dptr(v), C.byref(sw)))
         return u, sig[:k], v, sw.value
 
     # ---------------------------------------------------------- step functions
@@ -262,6 +321,34 @@ class Solver:
         _check(self.lib, self.lib.rsvd_b200_project_and_solve(
             self.h, _dp(a), m, n, _dp(qb), qb.shape[1], k, _dp(u), _dp(s), _dp(v), C.byref(sw)))
         return RsvdResult(SvdFactors(u, s, v), sw.value)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0), to broadcast to the other ranks."""
+    lib = _lib.load()
+    buf = C.create_string_buffer(128)
+    _check(lib, lib.rsvd_b200_nccl_unique_id(buf))
+    return buf.raw
+
+
+class LocalGroup:
+    """In-process communicator group (rsvd_b200_local_group): `world` handles driven from
+    `world` host threads reduce through fixed-order device sums."""
+
+    def __init__(self, world: int):
+        self.lib = _lib.load()
+        g = C.c_void_p()
+        _check(self.lib, self.lib.rsvd_b200_local_group_create(world, C.byref(g)))
+        self.g = g
+        self.world = world
+
+    def __del__(self):
+        try:
+            if self.g:
+                self.lib.rsvd_b200_local_group_destroy(self.g)
+                self.g = None
+        except Exception:
+            pass
 
 
 _default: Solver | None = None
