@@ -187,8 +187,16 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
                 const int k = (kt0 + it) * kBK;
                 tma_load_2d(st, &mapA, &full[s], k, m0);
                 tma_load_2d(st + kABox, &mapA, &full[s], k + 16, m0);
-                tma_load_2d(st + 2 * kABox, &mapX, &full[s], k, 0);
-                tma_load_2d(st + 2 * kABox + kXBox, &mapX, &full[s], k + 16, 0);
+                // TMA boxes hold at most 256 rows: wide sketches load Xt in two halves
+                // (NP/2 is a multiple of 8 rows, so the 128B swizzle atoms line up)
+                constexpr int kXParts = NP > 256 ? 2 : 1;
+#pragma unroll
+                for (int part = 0; part < kXParts; ++part) {
+                    const uint32_t off = part * (kXBox / kXParts);
+                    const int r0 = part * (NP / kXParts);
+                    tma_load_2d(st + 2 * kABox + off, &mapX, &full[s], k, r0);
+                    tma_load_2d(st + 2 * kABox + kXBox + off, &mapX, &full[s], k + 16, r0);
+                }
             }
         }
         return;
@@ -467,7 +475,8 @@ cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mA, mX;
-    if (make_map(&mA, p.A, p.M, p.K, p.lda, BM) || make_map(&mX, p.Xt, NP, p.K, p.ldx, NP))
+    if (make_map(&mA, p.A, p.M, p.K, p.lda, BM) ||
+        make_map(&mX, p.Xt, NP, p.K, p.ldx, NP > 256 ? NP / 2 : NP))
         return cudaErrorInvalidValue;
     const int k_tiles = (int)((p.K + kBK - 1) / kBK);
     const int splits = p.splits < 1 ? 1 : p.splits;
@@ -508,6 +517,9 @@ cudaError_t dispatch_ax(const GemmAx& p, cudaStream_t st) {
     if constexpr (NT <= 12) {
         return p.flag ? launch_ax_t<128, NT, 4, 2, 4, true>(p, st)
                       : launch_ax_t<128, NT, 4, 2, 4, false>(p, st);
+    } else if constexpr (NT > 24) {  // sketches wider than 192: 2 stages fit in smem
+        return p.flag ? launch_ax_t<64, NT, 4, 4, 2, true>(p, st)
+                      : launch_ax_t<64, NT, 4, 4, 2, false>(p, st);
     } else {
         return p.flag ? launch_ax_t<64, NT, 2, 4, 3, true>(p, st)
                       : launch_ax_t<64, NT, 2, 4, 3, false>(p, st);
@@ -519,6 +531,9 @@ cudaError_t dispatch_atx(const GemmAtx& p, cudaStream_t st) {
     if constexpr (NT <= 12) {
         return p.out_transposed ? launch_atx_t<128, NT, 4, 2, 4, true>(p, st)
                                 : launch_atx_t<128, NT, 4, 2, 4, false>(p, st);
+    } else if constexpr (NT > 24) {
+        return p.out_transposed ? launch_atx_t<64, NT, 4, 4, 2, true>(p, st)
+                                : launch_atx_t<64, NT, 4, 4, 2, false>(p, st);
     } else {
         return p.out_transposed ? launch_atx_t<64, NT, 2, 4, 3, true>(p, st)
                                 : launch_atx_t<64, NT, 2, 4, 3, false>(p, st);
@@ -536,6 +551,9 @@ cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st) {
         case 16: return dispatch_ax<16>(p, st);
         case 20: return dispatch_ax<20>(p, st);
         case 24: return dispatch_ax<24>(p, st);
+        case 28: return dispatch_ax<28>(p, st);
+        case 32: return dispatch_ax<32>(p, st);
+        case 36: return dispatch_ax<36>(p, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -551,6 +569,9 @@ cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st) {
         case 16: return dispatch_atx<16>(p, st);
         case 20: return dispatch_atx<20>(p, st);
         case 24: return dispatch_atx<24>(p, st);
+        case 28: return dispatch_atx<28>(p, st);
+        case 32: return dispatch_atx<32>(p, st);
+        case 36: return dispatch_atx<36>(p, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -22,14 +22,15 @@ namespace rsvdb200 {
 
 constexpr int kHHThreads = 256;
 constexpr int kHHWarps = kHHThreads / 32;
-constexpr int kMaxCh = 6;  // up to 192 columns, 32 per lane-chunk
+constexpr int kMaxCh = 9;  // up to 288 columns, 32 per lane-chunk
+constexpr int kMaxCols = 32 * kMaxCh;
 
 // Block-wide partial sums of sum_{rows i in [lo,hi)} x_i * w[i][j] for j in [j0, s),
 // x_i given by a functor; written to out[j].
 template <typename XF>
 __device__ void block_col_dots(const double* __restrict__ w, long ld, long lo, long hi, int j0,
                                int s, XF xval, double* __restrict__ out /* [s] */,
-                               double* __restrict__ red /* smem kHHWarps x 192 */) {
+                               double* __restrict__ red /* smem kHHWarps x kMaxCols */) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double acc[kMaxCh];
 #pragma unroll
@@ -46,12 +47,12 @@ __device__ void block_col_dots(const double* __restrict__ w, long ld, long lo, l
 #pragma unroll
     for (int c = 0; c < kMaxCh; ++c) {
         const int j = j0 + lane + 32 * c;
-        if (j < s) red[warp * 192 + j] = acc[c];
+        if (j < s) red[warp * kMaxCols + j] = acc[c];
     }
     __syncthreads();
     for (int j = j0 + threadIdx.x; j < s; j += blockDim.x) {
         double t = 0.0;
-        for (int q = 0; q < kHHWarps; ++q) t += red[q * 192 + j];
+        for (int q = 0; q < kHHWarps; ++q) t += red[q * kMaxCols + j];
         out[j] = t;
     }
     __syncthreads();
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kHHThreads) hh_init_kernel(HH h) {
 
 // column k, phase A: reflector v_k (qr.cpp:44-58) and partial dots v_k . w_j, j > k
 __global__ void __launch_bounds__(kHHThreads) hh_col_a_kernel(HH h, int k) {
-    __shared__ double red[kHHWarps * 192];
+    __shared__ double red[kHHWarps * kMaxCols];
     long lo, hi;
     hh_rows(h, lo, hi);
     const int NP = h.NP;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kHHThreads) hh_col_a_kernel(HH h, int k) {
 
 // column k, phase B: w_j -= 2 (v.w_j) v for j > k, r_kk, tail norm of column k + 1
 __global__ void __launch_bounds__(kHHThreads) hh_col_b_kernel(HH h, int k) {
-    __shared__ double dj[192];
+    __shared__ double dj[kMaxCols];
     __shared__ double red[kHHWarps];
     long lo, hi;
     hh_rows(h, lo, hi);
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kHHThreads) hh_q_init_kernel(HH h) {
 
 // backward accumulation (qr.cpp:71-84), reflector kk: partial dots, then the update
 __global__ void __launch_bounds__(kHHThreads) hh_q_a_kernel(HH h, int kk) {
-    __shared__ double red[kHHWarps * 192];
+    __shared__ double red[kHHWarps * kMaxCols];
     if (!h.act[kk]) return;
     long lo, hi;
     hh_rows(h, lo, hi);
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kHHThreads) hh_q_a_kernel(HH h, int kk) {
 }
 
 __global__ void __launch_bounds__(kHHThreads) hh_q_b_kernel(HH h, int kk) {
-    __shared__ double dj[192];
+    __shared__ double dj[kMaxCols];
     if (!h.act[kk]) return;
     long lo, hi;
     hh_rows(h, lo, hi);
@@ -226,14 +227,14 @@ __global__ void __launch_bounds__(kHHThreads) hh_finish_kernel(HH h) {
 }
 
 size_t householder_work_doubles(long M, int s) {
-    const int NP = 192;
+    const int NP = kMaxCols;
     (void)s;
     return 2 * (size_t)M * NP + 2 * 296 * (size_t)(NP + 2) + NP + 64;
 }
 
 cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, double* Qout, long ldq,
                                   double* R, int NP, double* work, cudaStream_t st) {
-    if (s > 192 || NP > 192) return cudaErrorInvalidValue;
+    if (s > kMaxCols || NP > kMaxCols) return cudaErrorInvalidValue;
     const unsigned nb = (unsigned)std::max(1L, std::min(296L, M));
     HH h;
     h.Y = Y;

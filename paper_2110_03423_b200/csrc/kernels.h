@@ -66,8 +66,26 @@ cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double
 // Cholesky of the s x s Gram G (ld ldg): writes R (upper, NP x NP, ld NP, zero padded)
 // and Rinv^T (NP x NP, ld NP, zero padded: usable directly as the Xt operand of ax).
 // status[0] = 0 ok, 1 breakdown (min pivot below tol * max diag); status is int[4].
+// Gref/ldref/sref (optional): the breakdown threshold is tol * max diag of Gref's leading
+// sref x sref block instead of G's (blocked Cholesky: the Schur complement is judged
+// against the whole Gram). accumulate: status[0] is only ever set to 1 (OR semantics),
+// never cleared. Widths up to cholesky_max_width() (shared memory).
 cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
-                            int* status, int* abort_flag, double tol, cudaStream_t st);
+                            int* status, int* abort_flag, double tol, cudaStream_t st,
+                            const double* Gref = nullptr, long ldref = 0, int sref = 0,
+                            bool accumulate = false);
+int cholesky_max_width();
+// C (M x N, ldc) = alpha op(A) op(B) + beta Cin; ta/tb: operand stored transposed.
+// Cin == nullptr means Cin = C.
+cudaError_t launch_small_gemm(int M, int N, int K, double alpha, const double* A, long lda,
+                              bool ta, const double* B, long ldb, bool tb, double beta,
+                              const double* Cin, long ldcin, double* C, long ldc,
+                              cudaStream_t st);
+// Block one-sided Jacobi for s > 160 (cooperative launch, global scratch).
+cudaError_t launch_block_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U,
+                                    double* W, int* status, double* scratch,
+                                    const int* abort_flag, cudaStream_t st);
+size_t block_jacobi_scratch_doubles(int s);
 // out (NP x NP) = X (NP x NP) * Y (NP x NP), row-major, s-leading block only (rest zero).
 cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP, double* out,
                                 bool transpose_out, cudaStream_t st);

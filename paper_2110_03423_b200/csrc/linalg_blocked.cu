@@ -1,0 +1,303 @@
+// Small dense linear algebra for wide sketches (s > ~140), where an s x s FP64 matrix
+// no longer fits one CTA's shared memory (s = 272 is 592 KB):
+//   * small_gemm_kernel — generic C = alpha op(A) op(B) + beta Cin on s-sized
+//     operands (tiles of 32 x 32 per CTA), the building block of the blocked Cholesky
+//     that rsvd_b200.cpp assembles from two in-smem Cholesky factorisations;
+//   * block_jacobi_kernel — one-sided block Jacobi SVD of the s x s triangular factor
+//     R_B, the wide-sketch twin of jacobi_kernel (linalg_small.cu). Columns live in
+//     global memory (L2 resident); the s/16 column blocks are paired in round-robin
+//     (tournament) order, each block pair is one CTA that loads its 32 columns into
+//     shared memory and runs an inner one-sided Jacobi sweep over them with the
+//     reference's rotation rule and skip thresholds (svd.cpp:35-36, 60-90); a grid-wide
+//     barrier (cooperative launch) separates rounds. A sweep without any rotation ends
+//     the iteration, more than 30 sweeps is a convergence failure (svd.hpp:20), and the
+//     final sort / U / W extraction matches jacobi_kernel.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace rsvdb200 {
+
+// ============================================================== small GEMM
+// C (M x N, ldc) = alpha * op(A) op(B) + beta * Cin (ldcin); op(A) is M x K,
+// op(B) K x N; ta / tb: the operand is stored transposed (row-major K x M / N x K).
+// Cin may alias C (each element is read before it is written by the same thread).
+__global__ void __launch_bounds__(256) small_gemm_kernel(int M, int N, int K, double alpha,
+                                                         const double* __restrict__ A, long lda,
+                                                         bool ta, const double* __restrict__ B,
+                                                         long ldb, bool tb, double beta,
+                                                         const double* Cin, long ldcin,
+                                                         double* C, long ldc) {
+    __shared__ double As[32][33], Bs[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        for (int r = ty; r < 32; r += 8) {
+            const int i = i0 + r, k = k0 + tx;  // As[r][tx] = op(A)[i][k]
+            As[r][tx] = (i < M && k < K) ? (ta ? A[(long)k * lda + i] : A[(long)i * lda + k]) : 0.0;
+            const int kk = k0 + r, j = j0 + tx;  // Bs[r][tx] = op(B)[kk][j]
+            Bs[r][tx] = (kk < K && j < N) ? (tb ? B[(long)j * ldb + kk] : B[(long)kk * ldb + j]) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            const double b = Bs[kk][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][kk], b, acc[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ty + 8 * q, j = j0 + tx;
+        if (i < M && j < N) {
+            double v = alpha * acc[q];
+            if (beta != 0.0) v += beta * Cin[(long)i * ldcin + j];
+            C[(long)i * ldc + j] = v;
+        }
+    }
+}
+
+cudaError_t launch_small_gemm(int M, int N, int K, double alpha, const double* A, long lda,
+                              bool ta, const double* B, long ldb, bool tb, double beta,
+                              const double* Cin, long ldcin, double* C, long ldc,
+                              cudaStream_t st) {
+    if (M <= 0 || N <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+    small_gemm_kernel<<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta,
+                                            Cin ? Cin : C, Cin ? ldcin : ldc, C, ldc);
+    return cudaGetLastError();
+}
+
+// ========================================================= block Jacobi SVD
+constexpr int kBJW = 16;          // columns per block
+constexpr int kBJThreads = 512;   // 16 warps: one per column pair of an inner round
+constexpr int kBJMaxSweeps = 30;
+
+__device__ __forceinline__ int bj_rr(int slot, int round, int sp) {
+    return slot == 0 ? 0 : 1 + (slot - 1 + round) % (sp - 1);
+}
+
+// scratch: Rc (s*s, column c at Rc + c*s), J (s*s), sweep flags (32 ints), norms (s)
+__global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
+    const double* __restrict__ Rin, int s, int NP, double* __restrict__ sigma_out,
+    double* __restrict__ Uout, double* __restrict__ Wout, int* __restrict__ status,
+    double* __restrict__ scratch, const int* __restrict__ abort_flag) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sh[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nb = (s + kBJW - 1) / kBJW;
+    const int sp = (nb + 1) & ~1;
+    double* Rc = scratch;
+    double* J = Rc + (size_t)s * s;
+    int* sweep_flag = reinterpret_cast<int*>(J + (size_t)s * s);
+    double* norms = J + (size_t)s * s + 16;
+    __shared__ double red[32];
+    __shared__ double scale_sh, athr_sh;
+    __shared__ int order_sh[320];
+    if (abort_flag && *abort_flag) {  // uniform over the grid
+        if (blockIdx.x == 0 && tid == 0) status[0] = 0;
+        return;
+    }
+    // power-of-two scale and the absolute threshold, computed redundantly per CTA (same
+    // order everywhere, so every CTA holds identical values)
+    {
+        double mx = 0.0;
+        for (int e = tid; e < s * s; e += kBJThreads) mx = fmax(mx, fabs(Rin[(e / s) * NP + e % s]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) red[warp] = mx;
+        __syncthreads();
+        if (tid == 0) {
+            double m = 0.0;
+            for (int w = 0; w < kBJThreads / 32; ++w) m = fmax(m, red[w]);
+            int ex = 0;
+            frexp(m, &ex);
+            scale_sh = m > 0.0 ? ldexp(1.0, -ex) : 1.0;
+        }
+        __syncthreads();
+        const double sc = scale_sh;
+        double acc = 0.0;
+        for (int e = tid; e < s * s; e += kBJThreads) {
+            const double x = Rin[(e / s) * NP + e % s] * sc;
+            acc = fma(x, x, acc);
+        }
+        acc = warp_sum(acc);
+        __syncthreads();
+        if (lane == 0) red[warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kBJThreads / 32; ++w) t += red[w];
+            athr_sh = 1e-14 * t;
+        }
+        __syncthreads();
+    }
+    const double scale = scale_sh, athr = athr_sh;
+    for (long e = blockIdx.x * (long)kBJThreads + tid; e < (long)s * s;
+         e += (long)gridDim.x * kBJThreads) {
+        const int c = (int)(e / s), r = (int)(e % s);
+        Rc[e] = Rin[(long)r * NP + c] * scale;
+        J[e] = (r == c) ? 1.0 : 0.0;
+    }
+    if (blockIdx.x == 0 && tid < 32) sweep_flag[tid] = 0;
+    grid.sync();
+
+    double* C = sh;                      // 2*kBJW columns of length s
+    double* Jl = sh + 2 * kBJW * s;      // their rotation accumulators
+    __shared__ int cols[2 * kBJW];
+    int sweeps = 0;
+    bool converged = false;
+    while (sweeps < kBJMaxSweeps) {
+        ++sweeps;
+        for (int round = 0; round < sp - 1; ++round) {
+            const int k = blockIdx.x;
+            int bi = bj_rr(k, round, sp), bj = bj_rr(sp - 1 - k, round, sp);
+            if (bi > bj) { const int t = bi; bi = bj; bj = t; }
+            int cnt = 0;
+            if (k < sp / 2 && bj < nb) {
+                const int e0 = min(s, (bi + 1) * kBJW), e1 = min(s, (bj + 1) * kBJW);
+                cnt = (e0 - bi * kBJW) + (e1 - bj * kBJW);
+                if (tid < cnt) {
+                    const int n0 = e0 - bi * kBJW;
+                    cols[tid] = tid < n0 ? bi * kBJW + tid : bj * kBJW + (tid - n0);
+                }
+            }
+            __syncthreads();
+            int rotated = 0;
+            if (cnt > 0) {
+                for (int e = tid; e < cnt * s; e += kBJThreads) {
+                    const int l = e / s, r = e % s;
+                    C[e] = Rc[(long)cols[l] * s + r];
+                    Jl[e] = J[(long)cols[l] * s + r];
+                }
+                __syncthreads();
+                const int spl = (cnt + 1) & ~1;
+                for (int ir = 0; ir < spl - 1; ++ir) {
+                    const int pk = warp;
+                    bool live = pk < spl / 2;
+                    int i = 0, j = 0;
+                    if (live) {
+                        i = bj_rr(pk, ir, spl);
+                        j = bj_rr(spl - 1 - pk, ir, spl);
+                        if (i > j) { const int t = i; i = j; j = t; }
+                        live = j < cnt;
+                    }
+                    if (live) {
+                        double* ci = C + i * s;
+                        double* cj = C + j * s;
+                        double aii = 0.0, ajj = 0.0, d = 0.0;
+                        for (int r = lane; r < s; r += 32) {
+                            const double x = ci[r], y = cj[r];
+                            aii = fma(x, x, aii);
+                            ajj = fma(y, y, ajj);
+                            d = fma(x, y, d);
+                        }
+                        aii = warp_sum(aii);
+                        ajj = warp_sum(ajj);
+                        d = warp_sum(d);
+                        if (!(fabs(d) <= athr && d * d <= (1e-13 * 1e-13) * aii * ajj)) {
+                            const double diff = ajj - aii;
+                            const double sgn =
+                                ((diff >= 0.0) == (d >= 0.0)) || diff == 0.0 ? 1.0 : -1.0;
+                            const double t = sgn * 2.0 * fabs(d) /
+                                             (fabs(diff) + sqrt(fma(diff, diff, 4.0 * d * d)));
+                            const double c = rsqrt(fma(t, t, 1.0));
+                            const double sn = c * t;
+                            for (int r = lane; r < s; r += 32) {
+                                const double x = ci[r], y = cj[r];
+                                ci[r] = c * x - sn * y;
+                                cj[r] = sn * x + c * y;
+                            }
+                            double* ji = Jl + i * s;
+                            double* jj = Jl + j * s;
+                            for (int r = lane; r < s; r += 32) {
+                                const double x = ji[r], y = jj[r];
+                                ji[r] = c * x - sn * y;
+                                jj[r] = sn * x + c * y;
+                            }
+                            rotated = 1;
+                        }
+                    }
+                    __syncthreads();
+                }
+                for (int e = tid; e < cnt * s; e += kBJThreads) {
+                    const int l = e / s, r = e % s;
+                    Rc[(long)cols[l] * s + r] = C[e];
+                    J[(long)cols[l] * s + r] = Jl[e];
+                }
+            }
+            if (__syncthreads_or(rotated) && tid == 0) atomicOr(&sweep_flag[sweeps - 1], 1);
+            grid.sync();
+        }
+        if (*((volatile int*)&sweep_flag[sweeps - 1]) == 0) {
+            converged = true;
+            break;
+        }
+    }
+    if (!converged) {
+        if (blockIdx.x == 0 && tid == 0) status[0] = -1;
+        return;
+    }
+    // column norms (grid-stride), then every CTA derives the same stable descending order
+    for (int c = blockIdx.x * (kBJThreads / 32) + warp; c < s; c += gridDim.x * (kBJThreads / 32)) {
+        double acc = 0.0;
+        for (int r = lane; r < s; r += 32) acc = fma(Rc[(long)c * s + r], Rc[(long)c * s + r], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) norms[c] = sqrt(acc);
+    }
+    grid.sync();
+    for (int c = tid; c < s; c += kBJThreads) {
+        const double nc = norms[c];
+        int rank = 0;
+        for (int o = 0; o < s; ++o) {
+            const double no = norms[o];
+            rank += (no > nc) || (no == nc && o < c);
+        }
+        order_sh[rank] = c;
+    }
+    __syncthreads();
+    for (long e = blockIdx.x * (long)kBJThreads + tid; e < (long)NP * NP;
+         e += (long)gridDim.x * kBJThreads) {
+        const int r = (int)(e / NP), cc = (int)(e % NP);
+        double u = 0.0, w = 0.0;
+        if (r < s && cc < s) {
+            const int src = order_sh[cc];
+            const double sg = norms[src];
+            u = sg > 0.0 ? Rc[(long)src * s + r] / sg : 0.0;
+            w = J[(long)src * s + r];
+        }
+        Uout[e] = u;
+        Wout[e] = w;
+    }
+    if (blockIdx.x == 0) {
+        for (int c = tid; c < NP; c += kBJThreads)
+            sigma_out[c] = c < s ? norms[order_sh[c]] / scale : 0.0;
+        if (tid == 0) status[0] = sweeps;
+    }
+}
+
+size_t block_jacobi_scratch_doubles(int s) { return 2 * (size_t)s * s + 16 + (size_t)s + 16; }
+
+cudaError_t launch_block_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U,
+                                    double* W, int* status, double* scratch,
+                                    const int* abort_flag, cudaStream_t st) {
+    if (s > 320) return cudaErrorInvalidValue;
+    const size_t smem = 2 * (size_t)(2 * kBJW) * s * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(block_jacobi_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int nb = (s + kBJW - 1) / kBJW;
+    const int sp = (nb + 1) & ~1;
+    void* args[] = {(void*)&R, (void*)&s, (void*)&NP, (void*)&sigma, (void*)&U, (void*)&W,
+                    (void*)&status, (void*)&scratch, (void*)&abort_flag};
+    e = cudaLaunchCooperativeKernel((void*)block_jacobi_kernel, dim3(sp / 2), dim3(kBJThreads),
+                                    args, smem, st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+}  // namespace rsvdb200

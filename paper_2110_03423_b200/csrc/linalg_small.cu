@@ -7,6 +7,9 @@
 //   * the reference's sign convention (svd.cpp:237-254),
 // plus the elementwise helpers (transpose, copies, NaN/Inf scan).
 #include <float.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -29,7 +32,7 @@ constexpr int kCholThreads = 1024;
 __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
     const double* __restrict__ G, long ldg, int s, int NP, double* __restrict__ R,
     double* __restrict__ RinvT, int* __restrict__ status, int* __restrict__ abort_flag,
-    double tol) {
+    double tol, const double* __restrict__ Gref, long ldref, int sref, bool accumulate) {
     extern __shared__ double S[];
     const int ld = s | 1;
     double* dinv = S + (size_t)s * ld;
@@ -46,9 +49,9 @@ __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
     __syncthreads();
     for (int r = warp; r < s; r += nw)
         for (int c = r + lane; c < s; c += 32) tab[rstart[r] + (c - r)] = ((uint32_t)r << 16) | c;
-    if (warp == 0) {
+    if (warp == 0) {  // breakdown threshold relative to the largest diagonal of Gref
         double m = 0.0;
-        for (int i = lane; i < s; i += 32) m = fmax(m, G[i * ldg + i]);
+        for (int i = lane; i < sref; i += 32) m = fmax(m, Gref[i * ldref + i]);
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) gmax = m;
     }
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
     }
     if (broke) {
         if (tid == 0) {
-            status[0] = 1;
+            status[0] = 1;  // (accumulate: OR into a status a previous block may have set)
             if (abort_flag) atomicOr(abort_flag, 1);
         }
         return;
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
         R[e] = rv;
         RinvT[e] = xv;
     }
-    if (tid == 0) status[0] = 0;
+    if (tid == 0 && !accumulate) status[0] = 0;
 }
 
 size_t cholesky_smem(int s) {
@@ -118,14 +121,27 @@ size_t cholesky_smem(int s) {
            ((size_t)s * (s + 1) / 2 + s + 1) * sizeof(uint32_t);
 }
 
+int cholesky_max_width() {
+    int s = 1;
+    while (cholesky_smem(s + 1) <= 225 * 1024) ++s;
+    return s;
+}
+
 cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
-                            int* status, int* abort_flag, double tol, cudaStream_t st) {
+                            int* status, int* abort_flag, double tol, cudaStream_t st,
+                            const double* Gref, long ldref, int sref, bool accumulate) {
+    if (!Gref) {
+        Gref = G;
+        ldref = ldg;
+        sref = s;
+    }
     const size_t smem = cholesky_smem(s);
     if (smem > 225 * 1024) return cudaErrorInvalidValue;
     cudaError_t e =
         cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cholesky_kernel<<<1, kCholThreads, smem, st>>>(G, ldg, s, NP, R, RinvT, status, abort_flag, tol);
+    cholesky_kernel<<<1, kCholThreads, smem, st>>>(G, ldg, s, NP, R, RinvT, status, abort_flag, tol,
+                                                   Gref, ldref, sref, accumulate);
     return cudaGetLastError();
 }
 
@@ -158,6 +174,7 @@ cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP,
 // Columns are stored contiguously in shared memory; the rotation accumulator J lives
 // in shared memory when both fit, else in global scratch (L2 resident).
 constexpr int kJacobiThreads = 1024;
+constexpr int kJacobiSmemMax = 160;  // widths beyond run the block Jacobi (linalg_blocked.cu)
 constexpr int kMaxSweeps = 30;
 
 __device__ __forceinline__ int rr_index(int slot, int round, int sp) {
@@ -172,8 +189,8 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
     double* Rc = sh;                             // s columns of length s
     double* J = Jglobal ? Jglobal : sh + s * s;  // s columns of length s
     __shared__ double abs_thresh;
-    __shared__ double norms[256];
-    __shared__ int order[256];
+    __shared__ double norms[kJacobiSmemMax];
+    __shared__ int order[kJacobiSmemMax];
     const int tid = threadIdx.x, nth = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
     if (abort_flag && *abort_flag) {  // an earlier stage failed; the host reruns robustly
@@ -307,16 +324,21 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
     if (tid == 0) status[0] = sweeps;
 }
 
-size_t jacobi_max_width() { return 256; }
+size_t jacobi_max_width() { return 320; }
 
 size_t jacobi_global_scratch_doubles(int s) {
-    return 2 * (size_t)s * s * sizeof(double) > 200 * 1024 ? (size_t)s * s : 0;
+    return block_jacobi_scratch_doubles(s);  // covers both kernels' needs
 }
 
 cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U, double* W,
                               int* status, double* scratch, const int* abort_flag,
                               cudaStream_t st) {
     if (s > (int)jacobi_max_width()) return cudaErrorInvalidValue;
+    static const int smem_max = getenv("RSVD_B200_JACOBI_SMEM_MAX")
+                                    ? atoi(getenv("RSVD_B200_JACOBI_SMEM_MAX"))
+                                    : kJacobiSmemMax;
+    if (s > std::min(smem_max, kJacobiSmemMax))
+        return launch_block_jacobi_svd(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
     const size_t one = (size_t)s * s * sizeof(double);
     const bool global_j = jacobi_global_scratch_doubles(s) > 0;
     const size_t smem = global_j ? one : 2 * one;

@@ -83,11 +83,11 @@ rsvd_b200_status guarded(F&& f) {
 long round_up(long x, long m) { return (x + m - 1) / m * m; }
 
 // Padded sketch width: multiples of 16 up to 96 (128-row tiles, 4x2 warps),
-// multiples of 32 up to 192 (64-row tiles, 2x4 warps).
+// multiples of 32 up to 288 (64-row tiles, 2x4 warps).
 int pad_np(long s) {
     if (s <= 96) return (int)round_up(std::max(1L, s), 16);
-    if (s <= 192) return (int)round_up(s, 32);
-    fail(RSVD_B200_ARGUMENT_ERROR, "sketch width %ld exceeds the supported maximum of 192", s);
+    if (s <= 288) return (int)round_up(s, 32);
+    fail(RSVD_B200_ARGUMENT_ERROR, "sketch width %ld exceeds the supported maximum of 288", s);
 }
 
 // Split-K count so that tiles * splits fills whole waves of 148 SMs, with at least two
@@ -262,7 +262,8 @@ enum {
 
 // Small s-by-s scratch layout inside h->small (each NP x NP doubles).
 enum { kG = 0, kR1 = 1, kR1iT = 2, kR2 = 3, kR2iT = 4, kRB = 5, kUR = 6, kWR = 7, kTmp = 8,
-       kSig = 9, kC = 10, kX = 11, kNumSmall = 12 };
+       kSig = 9, kC = 10, kX = 11, kB1 = 12, kB2 = 13, kB3 = 14, kB4 = 15, kB5 = 16,
+       kNumSmall = 17 };
 
 struct Plan {
     long m, n;   // tall problem: m >= n (m = this rank's rows when sharded)
@@ -395,12 +396,58 @@ size_t partial_doubles(const Plan& p) {
 
 constexpr double kCholTol = 1e-12;  // pivot / max diag: beyond cond ~1e6 use Householder
 
+// G = R^T R (R upper, diag > 0) and R^-T of the s x s Gram in slot g_slot. Widths that
+// fit one CTA's shared memory run cholesky_kernel directly; wider ones (s > ~150, e.g.
+// s = 272) are factored as a 2 x 2 block Cholesky from two in-smem factorisations:
+//   R11 = chol(G11), R12 = R11^-T G12, S = G22 - R12^T R12, R22 = chol(S),
+//   R^-T = [[R11^-T, 0], [-R22^-T R12^T R11^-T, R22^-T]],
+// with both pivot tests judged against the largest diagonal of the whole G.
 void cholesky(const Ctx& c, int g_slot, int r_slot, int rit_slot) {
     rsvd_b200_handle* h = c.h;
-    h->launched(launch_cholesky(c.slot(g_slot), c.p.NP, c.p.s, c.p.NP, c.slot(r_slot),
-                                c.slot(rit_slot), c.flags + (c.robust ? kFlagChol : kFlagCholScratch),
-                                c.robust ? nullptr : c.flags + kFlagAbort, kCholTol, h->stream),
+    cudaStream_t st = h->stream;
+    const int NP = c.p.NP, s = c.p.s;
+    int* status = c.flags + (c.robust ? kFlagChol : kFlagCholScratch);
+    int* abort = c.robust ? nullptr : c.flags + kFlagAbort;
+    const double* G = c.slot(g_slot);
+    double* R = c.slot(r_slot);
+    double* RiT = c.slot(rit_slot);
+    static const int chol_max = getenv("RSVD_B200_CHOL_MAX") ? atoi(getenv("RSVD_B200_CHOL_MAX"))
+                                                             : cholesky_max_width();
+    if (s <= std::min(chol_max, cholesky_max_width())) {
+        h->launched(launch_cholesky(G, NP, s, NP, R, RiT, status, abort, kCholTol, st),
+                    "cholesky");
+        return;
+    }
+    const int s1 = (s + 1) / 2, s2 = s - s1;
+    double *R11 = c.slot(kB1), *R11iT = c.slot(kB2), *S = c.slot(kB3), *R22 = c.slot(kB4),
+           *R22iT = c.slot(kB5);
+    h->launched(launch_fill(R, (long)NP * NP, 0.0, st), "fill");
+    h->launched(launch_fill(RiT, (long)NP * NP, 0.0, st), "fill");
+    h->launched(launch_cholesky(G, NP, s1, NP, R11, R11iT, status, abort, kCholTol, st, G, NP, s,
+                                false),
                 "cholesky");
+    // R12 = R11^-T G12 -> R[0:s1, s1:s]
+    h->launched(launch_small_gemm(s1, s2, s1, 1.0, R11iT, NP, false, G + s1, NP, false, 0.0,
+                                  nullptr, 0, R + s1, NP, st),
+                "small_gemm");
+    // S = G22 - R12^T R12
+    h->launched(launch_small_gemm(s2, s2, s1, -1.0, R + s1, NP, true, R + s1, NP, false, 1.0,
+                                  G + (size_t)s1 * NP + s1, NP, S, NP, st),
+                "small_gemm");
+    h->launched(launch_cholesky(S, NP, s2, NP, R22, R22iT, status, abort, kCholTol, st, G, NP, s,
+                                true),
+                "cholesky");
+    h->launched(launch_copy2d(R11, NP, R, NP, s1, s1, st), "copy2d");
+    h->launched(launch_copy2d(R22, NP, R + (size_t)s1 * NP + s1, NP, s2, s2, st), "copy2d");
+    h->launched(launch_copy2d(R11iT, NP, RiT, NP, s1, s1, st), "copy2d");
+    h->launched(launch_copy2d(R22iT, NP, RiT + (size_t)s1 * NP + s1, NP, s2, s2, st), "copy2d");
+    // T = R12^T R11^-T (s2 x s1) into S; RiT[s1:, 0:s1] = -R22^-T T
+    h->launched(launch_small_gemm(s2, s1, s1, 1.0, R + s1, NP, true, R11iT, NP, false, 0.0,
+                                  nullptr, 0, S, NP, st),
+                "small_gemm");
+    h->launched(launch_small_gemm(s2, s1, s2, -1.0, R22iT, NP, false, S, NP, false, 0.0, nullptr,
+                                  0, RiT + (size_t)s1 * NP, NP, st),
+                "small_gemm");
 }
 
 bool chol_broke(const Ctx& c) {
