@@ -100,6 +100,23 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_device(rsvd_b200_handle* h, const dou
                                                   size_t* sketch_width);
 
 /* ---------------------------------------------------------------------------
+ * FP32 input (BASELINE config C4). Same solve for an FP32 A: every product with an
+ * m-dimension runs on the 5th-generation tensor cores (tcgen05.mma kind::tf32) as
+ * 3xTF32 split products (FP32-class accuracy), the (k+p)-sized side in FP64; outputs
+ * are FP64. Tolerance bar (BASELINE.json): sigma 1e-4 relative, angles 1e-3. No
+ * reference counterpart (the reference is FP64-only); rsvd.hpp:58 semantics otherwise.
+ * Device A: lda a multiple of 4 floats and 16-byte aligned base (else copied).
+ * ------------------------------------------------------------------------- */
+rsvd_b200_status rsvd_b200_randomized_ksvd_f32(rsvd_b200_handle* h, const float* a, size_t m,
+                                               size_t n, const rsvd_b200_config* cfg, double* u,
+                                               double* sigma, double* v, size_t* sketch_width);
+rsvd_b200_status rsvd_b200_randomized_ksvd_f32_device(rsvd_b200_handle* h, const float* a_dev,
+                                                      size_t m, size_t n, size_t lda,
+                                                      const rsvd_b200_config* cfg, double* u_dev,
+                                                      double* sigma_dev, double* v_dev,
+                                                      size_t* sketch_width);
+
+/* ---------------------------------------------------------------------------
  * Row-sharded solves across GPUs (no reference counterpart: the reference is one
  * host process; this is §8e's data-parallel split of the same
  * randomized_ksvd, rsvd.hpp:58). Rank g holds a contiguous row block A_g of the
@@ -136,6 +153,17 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_sharded(rsvd_b200_handle* h, const do
 /* Device buffers (A shard resident in HBM, same layout rules as the _device solve). */
 rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_device(
     rsvd_b200_handle* h, const double* a_dev, size_t m_local, size_t m_total, size_t n,
+    size_t lda, const rsvd_b200_config* cfg, double* u_dev, double* sigma_dev, double* v_dev,
+    size_t* sketch_width);
+
+/* FP32 row-sharded solves (host / device buffers). */
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_f32(rsvd_b200_handle* h, const float* a,
+                                                       size_t m_local, size_t m_total, size_t n,
+                                                       const rsvd_b200_config* cfg, double* u,
+                                                       double* sigma, double* v,
+                                                       size_t* sketch_width);
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_f32_device(
+    rsvd_b200_handle* h, const float* a_dev, size_t m_local, size_t m_total, size_t n,
     size_t lda, const rsvd_b200_config* cfg, double* u_dev, double* sigma_dev, double* v_dev,
     size_t* sketch_width);
 
@@ -193,6 +221,14 @@ void rsvd_b200_set_robust(rsvd_b200_handle* h, int on);
 /* Measured FP64 tensor-core peak of the handle's GPU (TFLOP/s): an issue-bound
  * mma.sync m16n8k16 f64 loop on every SM — the roofline denominator of the GEMMs. */
 rsvd_b200_status rsvd_b200_dmma_peak(rsvd_b200_handle* h, double* tflops);
+
+/* Test hook for the FP32-input 3xTF32 tcgen05 GEMM (device pointers; see csrc/kernels.h
+ * GemmTf32): mn = 0: out = A (M x K) * Bt^T, Bt NP x K; mn = 1: out = A^T W, A K x M,
+ * W K x NP. out FP64 (out64) or FP32, row-major or transposed (out_t); splits > 1 = split-K
+ * with a fixed-order reduce (FP64 only). Synchronous. */
+rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const float* A, long M,
+                                          long K, long lda, const float* B, long ldb, int NP,
+                                          void* out, long ldo, int out64, int out_t, int splits);
 
 /* Library build identification (sm_100a). */
 const char* rsvd_b200_version(void);

@@ -23,6 +23,9 @@ EXPORTS = [
     "rsvd_b200_local_group_create", "rsvd_b200_local_group_destroy", "rsvd_b200_comm_init_local",
     "rsvd_b200_comm_info", "rsvd_b200_comm_free", "rsvd_b200_randomized_ksvd_sharded",
     "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak",
+    "rsvd_b200_debug_gemm_tf32", "rsvd_b200_randomized_ksvd_f32",
+    "rsvd_b200_randomized_ksvd_f32_device", "rsvd_b200_randomized_ksvd_sharded_f32",
+    "rsvd_b200_randomized_ksvd_sharded_f32_device",
 ]
 
 
@@ -33,6 +36,7 @@ class Config(C.Structure):
 
 
 _dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
 _sz = C.c_size_t
 _vp = C.c_void_p
 _LIB = None
@@ -79,6 +83,18 @@ def load() -> C.CDLL:
         "rsvd_b200_set_robust": (None, [_vp, C.c_int]),
         "rsvd_b200_nccl_unique_id": (C.c_int, [C.c_char_p]),
         "rsvd_b200_dmma_peak": (C.c_int, [_vp, _dp]),
+        "rsvd_b200_randomized_ksvd_f32": (C.c_int, [_vp, _fp, _sz, _sz, cfgp, _dp, _dp, _dp,
+                                                    C.POINTER(_sz)]),
+        "rsvd_b200_randomized_ksvd_f32_device": (C.c_int, [_vp, _fp, _sz, _sz, _sz, cfgp, _dp,
+                                                           _dp, _dp, C.POINTER(_sz)]),
+        "rsvd_b200_randomized_ksvd_sharded_f32": (C.c_int, [_vp, _fp, _sz, _sz, _sz, cfgp, _dp,
+                                                            _dp, _dp, C.POINTER(_sz)]),
+        "rsvd_b200_randomized_ksvd_sharded_f32_device": (C.c_int, [_vp, _fp, _sz, _sz, _sz, _sz,
+                                                                   cfgp, _dp, _dp, _dp,
+                                                                   C.POINTER(_sz)]),
+        "rsvd_b200_debug_gemm_tf32": (C.c_int, [_vp, C.c_int, _vp, C.c_long, C.c_long, C.c_long,
+                                                _vp, C.c_long, C.c_int, _vp, C.c_long, C.c_int,
+                                                C.c_int, C.c_int]),
         "rsvd_b200_comm_init_nccl": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
         "rsvd_b200_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
         "rsvd_b200_local_group_destroy": (None, [_vp]),

@@ -1,0 +1,463 @@
+// FP32-input GEMMs of the rSVD on the 5th-generation tensor cores (tcgen05, sm_100a):
+// 3xTF32 split products accumulated in TMEM, operands staged by TMA.
+//
+// The FP32 path (BASELINE config C4: A stored in FP32) runs every product with an
+// m-dimension on tcgen05.mma.kind::tf32. TF32 keeps 10 mantissa bits, so each operand
+// x is split in shared memory into hi = rna_tf32(x) and lo = rna_tf32(x - hi) and the
+// product is accumulated as a_hi b_hi + a_hi b_lo + a_lo b_hi (the lo*lo term is below
+// FP32 rounding): ~2^-21 relative error per product, i.e. FP32-class accuracy at a third
+// of the TF32 tensor rate, well above the FP32 SIMT rate.
+//
+// Two operand shapes, the same two the FP64 path has (gemm_f64.cu):
+//   ax  (K-major A and B): D[M x NP] = A (M x K row-major) * B, B given as Bt (NP x K
+//       row-major). Y = A*Omega, Y = A*Z, Q = Y*R^-1, U = Q*U_B.
+//   atx (MN-major A and B): D[M x NP] = A^T W, A (K x M row-major) read in place,
+//       W (K x NP row-major). (A^T Q)^T, Q^T A, the tall Gram Y^T Y. Split-K over K.
+//
+// CTA = 6 warps: warp 0 issues TMA (128B-swizzled boxes of 32 fp32), warp 1 owns the
+// TMEM allocation and one elected lane issues the MMAs (M = 128, N = NP in chunks of at
+// most 256), warps 2-5 split the freshly landed tiles into hi/lo (and scan A for
+// NaN/Inf when asked), then drain the accumulator (tcgen05.ld 32x32b) in the epilogue.
+// Two pipeline stages; mbarriers: full (TMA tx) -> conv (128 converter threads) ->
+// MMA -> empty (tcgen05.commit) -> producer.
+//
+// UMMA shared-memory descriptors (SWIZZLE_128B, version 1):
+//   K-major : rows of 128 B (32 fp32 along K), 8-row atoms of 1024 B: SBO = 1024,
+//             LBO unused; the k-th 8-wide K step starts 32*k bytes into the row.
+//   MN-major: 32-bit MN-major operands only exist in the SWIZZLE_128B_BASE32B layout
+//             (layout type 1, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B: 32-byte chunks of a
+//             128-byte row XORed with row % 4): rows of 128 B (32 fp32 along M/N) indexed
+//             by K, 4-row atoms along K (SBO = 512) and 32-wide M/N chunks one TMA box
+//             apart (LBO = box bytes); the k-th K step starts 1024*k bytes in.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvdb200 {
+namespace tf32 {
+
+constexpr int BM = 128;
+constexpr int BK = 32;
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+constexpr uint32_t kABytes = BM * BK * 4;  // 16 KB per A tile (hi or lo)
+
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// layout: 2 = SWIZZLE_128B (K-major), 1 = SWIZZLE_128B_BASE32B (MN-major 32-bit)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                          uint64_t layout) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (layout << 61);
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128, N, operand majors.
+__device__ __forceinline__ uint32_t idesc(int N, bool mn) {
+    const uint32_t maj = mn ? 1u : 0u;
+    return (1u << 4) | (2u << 7) | (2u << 10) | (maj << 15) | (maj << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Bytes of one B tile (hi or lo): K-major NP rows of 128 B; MN-major ceil(NP/32) boxes
+// of 32 K-rows x 128 B.
+__host__ __device__ __forceinline__ uint32_t b_bytes(int NP, bool mn) {
+    return mn ? (uint32_t)((NP + 31) / 32) * 4096u : (uint32_t)NP * 128u;
+}
+__host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
+    return 2 * kABytes + 2 * b_bytes(NP, mn);
+}
+
+template <bool MN, bool OUT64, bool OUT_T>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, void* __restrict__ out, long ldo,
+                     long split_stride, int M, int NP, int k_tiles, int k_tiles_per_split,
+                     int* __restrict__ flag) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                         ~uintptr_t(1023));
+    const uint32_t bB = b_bytes(NP, MN);
+    const uint32_t kStage = 2 * kABytes + 2 * bB;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
+    uint64_t* conv = full + kStages;
+    uint64_t* empty = conv + kStages;
+    uint64_t* accum = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM;
+    const int kt0 = blockIdx.y * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int n_iter = max(0, kt1 - kt0);
+    const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 4);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&mapA);
+            tma_prefetch_desc(&mapB);
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages;
+                if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+                char* st = smem + s * kStage;
+                char* sb = st + 2 * kABytes;
+                const int k = (kt0 + it) * BK;
+                if constexpr (!MN) {
+                    const int parts = NP > 256 ? 2 : 1;
+                    mbar_arrive_expect_tx(&full[s], kABytes + (uint32_t)NP * 128u);
+                    tma_load_2d(st, &mapA, &full[s], k, m0);
+                    for (int p = 0; p < parts; ++p)
+                        tma_load_2d(sb + p * (NP / parts) * 128, &mapB, &full[s], k,
+                                    p * (NP / parts));
+                } else {
+                    const int nb = (NP + 31) / 32;
+                    mbar_arrive_expect_tx(&full[s], kABytes + (uint32_t)nb * 4096u);
+#pragma unroll
+                    for (int i = 0; i < BM / 32; ++i)
+                        tma_load_2d(st + i * 4096, &mapA, &full[s], m0 + 32 * i, k);
+                    for (int j = 0; j < nb; ++j) tma_load_2d(sb + j * 4096, &mapB, &full[s], 32 * j, k);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t lbo = MN ? 4096u : 16u, sbo = MN ? 512u : 1024u;
+            const uint64_t lay = MN ? 1u : 2u;
+            const int n1 = NP > 256 ? 256 : NP, n2 = NP - n1;
+            const uint32_t id1 = idesc(n1, MN), id2 = n2 > 0 ? idesc(n2, MN) : 0u;
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages;
+                mbar_wait(&full[s], (it / kStages) & 1);
+                mbar_wait(&conv[s], (it / kStages) & 1);
+                fence_after();
+                const uint32_t st = smem_u32(smem + s * kStage);
+                const uint32_t a_hi = st, a_lo = st + kABytes;
+                const uint32_t b_hi = st + 2 * kABytes, b_lo = b_hi + bB;
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ++ks) {
+                    const uint32_t ko = MN ? ks * 1024u : ks * 32u;
+                    const uint64_t ah = sdesc(a_hi + ko, lbo, sbo, lay),
+                                   al = sdesc(a_lo + ko, lbo, sbo, lay);
+                    const uint32_t acc0 = (it > 0 || ks > 0) ? 1u : 0u;
+                    {
+                        const uint64_t bh = sdesc(b_hi + ko, lbo, sbo, lay),
+                                       bl = sdesc(b_lo + ko, lbo, sbo, lay);
+                        mma(tmem, ah, bh, id1, acc0);
+                        mma(tmem, ah, bl, id1, 1u);
+                        mma(tmem, al, bh, id1, 1u);
+                    }
+                    if (n2 > 0) {  // columns 256.. (K-major: row 256; MN-major: box 8)
+                        const uint32_t co = 256u * 128u;
+                        const uint64_t bh = sdesc(b_hi + co + ko, lbo, sbo, lay),
+                                       bl = sdesc(b_lo + co + ko, lbo, sbo, lay);
+                        mma(tmem + 256, ah, bh, id2, acc0);
+                        mma(tmem + 256, ah, bl, id2, 1u);
+                        mma(tmem + 256, al, bh, id2, 1u);
+                    }
+                }
+                commit(&empty[s]);
+            }
+            if (n_iter > 0) commit(accum);
+        }
+    } else {
+        // --------------------------------------------------- hi/lo split (warps 2-5)
+        const int ct = threadIdx.x - 64;
+        bool bad = false;
+        for (int it = 0; it < n_iter; ++it) {
+            const int s = it % kStages;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            char* st = smem + s * kStage;
+            float4* ah = reinterpret_cast<float4*>(st);
+            float4* al = reinterpret_cast<float4*>(st + kABytes);
+            for (int i = ct; i < (int)(kABytes / 16); i += 128) {
+                const float4 v = ah[i];
+                if (flag) {
+                    const uint32_t e = 0x7f800000u;
+                    bad |= ((__float_as_uint(v.x) & e) == e) | ((__float_as_uint(v.y) & e) == e) |
+                           ((__float_as_uint(v.z) & e) == e) | ((__float_as_uint(v.w) & e) == e);
+                }
+                float4 h, l;
+                h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
+                h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
+                h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
+                h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
+                ah[i] = h;
+                al[i] = l;
+            }
+            float4* bh = reinterpret_cast<float4*>(st + 2 * kABytes);
+            float4* bl = reinterpret_cast<float4*>(st + 2 * kABytes + bB);
+            for (int i = ct; i < (int)(bB / 16); i += 128) {
+                const float4 v = bh[i];
+                float4 h, l;
+                h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
+                h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
+                h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
+                h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
+                bh[i] = h;
+                bl[i] = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[s]);
+        }
+        if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = m0 + 32 * q + lane;
+        const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+        if (n_iter > 0) {
+            mbar_wait(accum, 0);
+            fence_after();
+        }
+        char* ob = reinterpret_cast<char*>(out) + (size_t)blockIdx.y * split_stride * (OUT64 ? 8 : 4);
+        for (int c0 = 0; c0 < NP; c0 += 16) {
+            float v[16];
+            if (n_iter > 0) {
+                tmem_ld16(trow + c0, v);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            if (row < M) {
+                if constexpr (OUT_T) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const size_t o = (size_t)(c0 + i) * ldo + row;
+                        if constexpr (OUT64)
+                            reinterpret_cast<double*>(ob)[o] = (double)v[i];
+                        else
+                            reinterpret_cast<float*>(ob)[o] = v[i];
+                    }
+                } else if constexpr (OUT64) {
+                    double2* d = reinterpret_cast<double2*>(reinterpret_cast<double*>(ob) +
+                                                            (size_t)row * ldo + c0);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) d[i] = make_double2(v[2 * i], v[2 * i + 1]);
+                } else {
+                    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(ob) +
+                                                          (size_t)row * ldo + c0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(tmem_cols));
+    }
+}
+
+}  // namespace tf32
+
+// ================================================================ host side
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// Row-major FP32 (rows x cols, ld elements), box {32 cols, box_rows rows}, 128B swizzle.
+int map_f32(CUtensorMap* map, const float* base, long rows, long cols, long ld, int box_rows,
+            bool atom32 = false) {
+    auto encode = encode_fn();
+    if (!encode) return -1;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 4) & 15)) return -2;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -3;
+}
+
+template <bool MN, bool OUT64, bool OUT_T>
+cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
+                     cudaStream_t st) {
+    const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN) + 8 * 8 + 16 + 1024;
+    auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int k_tiles = (int)((p.K + tf32::BK - 1) / tf32::BK);
+    const int splits = p.splits < 1 ? 1 : p.splits;
+    const int per = (k_tiles + splits - 1) / splits;
+    dim3 grid((unsigned)((p.M + tf32::BM - 1) / tf32::BM), (unsigned)splits);
+    kern<<<grid, tf32::kThreads, smem, st>>>(mA, mB, p.out, p.ldo, p.split_stride, (int)p.M,
+                                             p.NP, k_tiles, per, p.flag);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
+    if (p.NP < 16 || p.NP > 288 || (p.NP % 16) != 0) return cudaErrorInvalidValue;
+    if (!p.out64 && p.splits > 1) return cudaErrorInvalidValue;
+    CUtensorMap mA, mB;
+    if (!p.mn) {  // A: M x K (lda), Bt: NP x K (ldb)
+        const int brows = p.NP > 256 ? p.NP / 2 : p.NP;
+        if (map_f32(&mA, p.A, p.M, p.K, p.lda, tf32::BM) ||
+            map_f32(&mB, p.B, p.NP, p.K, p.ldb, brows))
+            return cudaErrorInvalidValue;
+    } else {  // A: K x M (lda), W: K x NP (ldb)
+        if (map_f32(&mA, p.A, p.K, p.M, p.lda, 32, true) ||
+            map_f32(&mB, p.B, p.K, p.NP, p.ldb, 32, true))
+            return cudaErrorInvalidValue;
+    }
+    if (!p.mn) {
+        if (p.out64) return p.out_t ? launch_t<false, true, true>(p, mA, mB, st)
+                                    : launch_t<false, true, false>(p, mA, mB, st);
+        return p.out_t ? launch_t<false, false, true>(p, mA, mB, st)
+                       : launch_t<false, false, false>(p, mA, mB, st);
+    }
+    if (p.out64) return p.out_t ? launch_t<true, true, true>(p, mA, mB, st)
+                                : launch_t<true, true, false>(p, mA, mB, st);
+    return p.out_t ? launch_t<true, false, true>(p, mA, mB, st)
+                   : launch_t<true, false, false>(p, mA, mB, st);
+}
+
+// ------------------------------------------------------------ conversions
+__global__ void cvt_f64_f32_kernel(const double* __restrict__ in, long ldi, long rows, long cols,
+                                   long rows_valid, long cols_valid, float* __restrict__ out,
+                                   long ldo) {
+    const long total = rows * cols;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long r = e / cols, c = e % cols;
+        out[r * ldo + c] = (r < rows_valid && c < cols_valid) ? (float)in[r * ldi + c] : 0.f;
+    }
+}
+
+__global__ void cvt_f32_f64_kernel(const float* __restrict__ in, long ldi, long rows, long cols,
+                                   double* __restrict__ out, long ldo) {
+    const long total = rows * cols;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long r = e / cols, c = e % cols;
+        out[r * ldo + c] = (double)in[r * ldi + c];
+    }
+}
+
+__global__ void transpose_f32_kernel(const float* __restrict__ in, long rows, long cols, long ldi,
+                                     float* __restrict__ out, long ldo) {
+    __shared__ float tile[32][33];
+    const long r0 = (long)blockIdx.y * 32, c0 = (long)blockIdx.x * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const long r = r0 + y, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[y][threadIdx.x] = in[r * ldi + c];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const long c = c0 + y, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][y];
+    }
+}
+
+cudaError_t launch_transpose_f32(const float* in, long rows, long cols, long ldi, float* out,
+                                 long ldo, cudaStream_t st) {
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_f32_kernel<<<grid, dim3(32, 8), 0, st>>>(in, rows, cols, ldi, out, ldo);
+    return cudaGetLastError();
+}
+
+static unsigned cvt_grid(long work) {
+    long b = (work + 255) / 256;
+    if (b > 148L * 32) b = 148L * 32;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_cvt_f64_f32(const double* in, long ldi, long rows, long cols, long rows_valid,
+                               long cols_valid, float* out, long ldo, cudaStream_t st) {
+    cvt_f64_f32_kernel<<<cvt_grid(rows * cols), 256, 0, st>>>(in, ldi, rows, cols, rows_valid,
+                                                              cols_valid, out, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cvt_f32_f64(const float* in, long ldi, long rows, long cols, double* out,
+                               long ldo, cudaStream_t st) {
+    cvt_f32_f64_kernel<<<cvt_grid(rows * cols), 256, 0, st>>>(in, ldi, rows, cols, out, ldo);
+    return cudaGetLastError();
+}
+
+}  // namespace rsvdb200

@@ -41,6 +41,34 @@ struct GemmAtx {
     long split_stride = 0;
 };
 
+// FP32-input 3xTF32 tensor-core GEMM (tcgen05, gemm_tf32.cu), D = op(A) * B (M x NP):
+//   mn = false (ax):  A M x K row-major (lda), B given as Bt NP x K row-major (ldb);
+//   mn = true  (atx): A K x M row-major (lda) read in place, B = W K x NP row-major (ldb).
+// out: FP64 (out64) or FP32, row-major M x NP (ldo) or transposed NP x M (out_t); split-K
+// writes slab s at out + s*split_stride (FP64 only). NP multiple of 16, <= 288.
+// flag != nullptr ORs 1 into *flag if A holds a NaN/Inf.
+struct GemmTf32 {
+    const float* A;
+    long M, K, lda;
+    const float* B;
+    long ldb;
+    int NP;
+    void* out;
+    long ldo;
+    bool mn = false, out64 = true, out_t = false;
+    int splits = 1;
+    long split_stride = 0;
+    int* flag = nullptr;
+};
+cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st);
+// out (rows x cols, FP32, ldo) = in (FP64, ldi) for r < rows_valid and c < cols_valid, else 0.
+cudaError_t launch_cvt_f64_f32(const double* in, long ldi, long rows, long cols, long rows_valid,
+                               long cols_valid, float* out, long ldo, cudaStream_t st);
+cudaError_t launch_cvt_f32_f64(const float* in, long ldi, long rows, long cols, double* out,
+                               long ldo, cudaStream_t st);
+cudaError_t launch_transpose_f32(const float* in, long rows, long cols, long ldi, float* out,
+                                 long ldo, cudaStream_t st);
+
 cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
 cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);
 cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,

@@ -143,6 +143,9 @@ struct rsvd_b200_handle {
         hh_work, omega_host_dev, jscratch, cwork, ubt;
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
     DevBuf red_scratch;          // TSQR R stack / flag reduction
+    // FP32 path (A stored in FP32, 3xTF32 tensor-core products): tall FP32 buffers
+    DevBuf yf, qf, xtf, rtf, ubtf, af_copy;
+    float* basis_f = nullptr;  // Q1 of the current basis in the FP32 path (yf or qf)
     long fallbacks = 0, reruns = 0;
     int last_sweeps = 0;
     bool force_robust = false;
@@ -271,6 +274,13 @@ struct Plan {
     int s, NP;   // sketch width and padded width
     long ldn;    // leading dimension of n-length rows (Xt, B, Q_B^T): round_up(n, 2)
     bool sharded = false;  // A row-sharded over h->comm: sums over m are all-reduced
+    // FP32 path: A (af, lda floats) in FP32; every product with an m-dimension runs on the
+    // tcgen05 3xTF32 kernels with tall operands m x NPf in FP32 (NPf = s rounded up to 16);
+    // the s x s and n x s side stays FP64 at width NP.
+    bool f32 = false;
+    const float* af = nullptr;
+    int NPf = 0;
+    long ldnf = 0;  // leading dimension of FP32 n-length rows (16-byte multiple)
 };
 
 // One pipeline run. `robust`: synchronise after every Cholesky and take the
@@ -372,6 +382,32 @@ void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, co
                 "reduce_partials");
 }
 
+// 3xTF32 tensor-core product (gemm_tf32.cu) with split-K over K for FP64 outputs when the
+// output tiles alone would not fill the GPU (1 CTA per SM); slabs reduced in fixed order.
+// Slab: the out_t rows NP x ldo, else M x ldo.
+void gemm_tf32(rsvd_b200_handle* h, GemmTf32 g, const char* tag = nullptr, double flops = 0.0) {
+    const long tiles = (g.M + 127) / 128;
+    const int splits = g.out64 ? choose_splits(tiles, (g.K + 31) / 32) : 1;
+    if (splits == 1) {
+        h->kernel_begin(tag, flops);
+        h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32");
+        h->kernel_end(tag);
+        return;
+    }
+    const long slab = g.out_t ? (long)g.NP * g.ldo : g.M * g.ldo;
+    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
+    double* out = static_cast<double*>(g.out);
+    g.out = h->part.p;
+    g.splits = splits;
+    g.split_stride = slab;
+    h->kernel_begin(tag, flops);
+    h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32(split)");
+    h->kernel_end(tag);
+    h->launched(launch_reduce_partials(h->part.d(), slab, splits, out, slab, h->stream),
+                "reduce_partials");
+}
+
 // Largest split-K slab set any GEMM of a plan needs.
 size_t partial_doubles(const Plan& p) {
     const long NP = p.NP;
@@ -391,10 +427,19 @@ size_t partial_doubles(const Plan& p) {
     ax(p.m, p.n, NP);            // A-pass A Z
     ax(p.m, NP, NP);             // tall TRSM, back-projection
     ax(NP, p.n, NP);             // wide Gram
+    if (p.f32) {  // 3xTF32: A-pass (A^T Q)^T (NPf x ldn slabs) and the tall Gram (NPf x NP)
+        const int sp1 = choose_splits((p.n + 127) / 128, (p.m + 31) / 32);
+        if (sp1 > 1) need = std::max(need, (size_t)sp1 * p.NPf * p.ldn);
+        const int sp2 = choose_splits((p.NPf + 127) / 128, (p.m + 31) / 32);
+        if (sp2 > 1) need = std::max(need, (size_t)sp2 * p.NPf * NP);
+    }
     return std::max<size_t>(need, 1);
 }
 
 constexpr double kCholTol = 1e-12;  // pivot / max diag: beyond cond ~1e6 use Householder
+// FP32 path: Grams carry ~1e-5 relative error (TF32 tensor-core accumulation), so
+// CholeskyQR is only trusted up to cond(Y) ~ 300; beyond, the FP64 Householder fallback.
+constexpr double kCholTolF32 = 1e-5;
 
 // G = R^T R (R upper, diag > 0) and R^-T of the s x s Gram in slot g_slot. Widths that
 // fit one CTA's shared memory run cholesky_kernel directly; wider ones (s > ~150, e.g.
@@ -413,9 +458,9 @@ void cholesky(const Ctx& c, int g_slot, int r_slot, int rit_slot) {
     double* RiT = c.slot(rit_slot);
     static const int chol_max = getenv("RSVD_B200_CHOL_MAX") ? atoi(getenv("RSVD_B200_CHOL_MAX"))
                                                              : cholesky_max_width();
+    const double tol = c.p.f32 ? kCholTolF32 : kCholTol;
     if (s <= std::min(chol_max, cholesky_max_width())) {
-        h->launched(launch_cholesky(G, NP, s, NP, R, RiT, status, abort, kCholTol, st),
-                    "cholesky");
+        h->launched(launch_cholesky(G, NP, s, NP, R, RiT, status, abort, tol, st), "cholesky");
         return;
     }
     const int s1 = (s + 1) / 2, s2 = s - s1;
@@ -423,7 +468,7 @@ void cholesky(const Ctx& c, int g_slot, int r_slot, int rit_slot) {
            *R22iT = c.slot(kB5);
     h->launched(launch_fill(R, (long)NP * NP, 0.0, st), "fill");
     h->launched(launch_fill(RiT, (long)NP * NP, 0.0, st), "fill");
-    h->launched(launch_cholesky(G, NP, s1, NP, R11, R11iT, status, abort, kCholTol, st, G, NP, s,
+    h->launched(launch_cholesky(G, NP, s1, NP, R11, R11iT, status, abort, tol, st, G, NP, s,
                                 false),
                 "cholesky");
     // R12 = R11^-T G12 -> R[0:s1, s1:s]
@@ -434,7 +479,7 @@ void cholesky(const Ctx& c, int g_slot, int r_slot, int rit_slot) {
     h->launched(launch_small_gemm(s2, s2, s1, -1.0, R + s1, NP, true, R + s1, NP, false, 1.0,
                                   G + (size_t)s1 * NP + s1, NP, S, NP, st),
                 "small_gemm");
-    h->launched(launch_cholesky(S, NP, s2, NP, R22, R22iT, status, abort, kCholTol, st, G, NP, s,
+    h->launched(launch_cholesky(S, NP, s2, NP, R22, R22iT, status, abort, tol, st, G, NP, s,
                                 true),
                 "cholesky");
     h->launched(launch_copy2d(R11, NP, R, NP, s1, s1, st), "copy2d");
@@ -573,6 +618,74 @@ bool tall_qr(const Ctx& c, double* Y, long M, double* Q1out, int passes, bool ma
     return true;
 }
 
+// Tall QR of the FP32 path: Y = h->yf (M x NPf, FP32), same factored-basis contract as
+// tall_qr (basis h->basis_f = Q1, C in slot kC). Grams G = Y^T Y by the MN-major 3xTF32
+// kernel (FP64 out), Q1 = Y R1^-1 by the K-major one. The Householder fallback (and TSQR
+// when sharded) runs in FP64 on a converted copy of Y.
+bool tall_qr_f32(const Ctx& c, long M, int passes) {
+    rsvd_b200_handle* h = c.h;
+    cudaStream_t st = h->stream;
+    const int NP = c.p.NP, NPf = c.p.NPf, s = c.p.s;
+    float* Y = static_cast<float*>(h->yf.p);
+    float* Q1 = static_cast<float*>(h->qf.p);
+    auto gram = [&](const float* X) {
+        GemmTf32 g{X, (long)NPf, M, (long)NPf, X, (long)NPf, NPf, c.slot(kG), (long)NP};
+        g.mn = true;
+        gemm_tf32(h, g);
+        c.allreduce(c.slot(kG), (size_t)NP * NP);
+    };
+    h->c_identity = true;
+    h->basis_f = Y;
+    gram(Y);
+    cholesky(c, kG, kR1, kR1iT);
+    if (!chol_broke(c)) {
+        if (passes == 1) {
+            h->launched(launch_transpose(c.slot(kR1iT), NP, NP, NP, c.slot(kC), NP, st),
+                        "transpose");  // C = R1^-1
+            h->c_identity = false;
+            h->launched(launch_copy2d(c.slot(kR1), NP, c.slot(kRB), NP, NP, NP, st), "copy2d");
+            return false;
+        }
+        // Q1 = Y R1^-1 (K-major 3xTF32 with Bt = R1^-T in FP32), then its Gram
+        h->launched(launch_cvt_f64_f32(c.slot(kR1iT), NP, NPf, NPf, s, s,
+                                       static_cast<float*>(h->rtf.p), NPf, st),
+                    "cvt");
+        GemmTf32 t{Y, M, (long)NPf, (long)NPf, static_cast<float*>(h->rtf.p), (long)NPf, NPf,
+                   Q1, (long)NPf};
+        t.out64 = false;
+        gemm_tf32(h, t);
+        gram(Q1);
+        cholesky(c, kG, kR2, kR2iT);
+        if (!chol_broke(c)) {
+            h->launched(launch_transpose(c.slot(kR2iT), NP, NP, NP, c.slot(kC), NP, st),
+                        "transpose");  // C = R2^-1
+            h->c_identity = false;
+            h->basis_f = Q1;
+            h->launched(launch_small_matmul(c.slot(kR2), c.slot(kR1), s, NP, c.slot(kRB), false, st),
+                        "small_matmul");  // R = R2 R1
+            return false;
+        }
+    }
+    // FP64 fallback on a converted copy of Y
+    h->y.reserve((size_t)M * NP * sizeof(double));
+    h->q.reserve((size_t)M * NP * sizeof(double));
+    h->launched(launch_fill(h->y.d(), M * NP, 0.0, st), "fill");
+    h->launched(launch_cvt_f32_f64(Y, NPf, M, NPf, h->y.d(), NP, st), "cvt");
+    if (c.p.sharded) {
+        tsqr(c, h->y.d(), M, h->q.d());
+    } else {
+        h->hh_work.reserve(householder_work_doubles(M, s) * sizeof(double));
+        h->launched(launch_householder_qr(h->y.d(), M, s, NP, h->q.d(), NP, c.slot(kRB), NP,
+                                          h->hh_work.d(), st),
+                    "householder_qr");
+    }
+    h->launched(launch_cvt_f64_f32(h->q.d(), NP, M, NPf, M, s, Q1, NPf, st), "cvt");
+    h->basis_f = Q1;
+    h->c_identity = true;
+    h->fallbacks += 1;
+    return true;
+}
+
 // Thin QR of an N x s matrix held transposed, Zt (NP x N, ld ldz) -> Qt (NP x N, ld ldz),
 // R (NP x NP) into slot r_slot. CholeskyQR with `passes` passes (both triangular solves
 // applied: these matrices are only n x s); Householder fallback on the robust path.
@@ -640,20 +753,46 @@ Plan make_plan(long m, long n, long lda, long s) {
 Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     const int NP = p.NP;
     h->xt.reserve((size_t)NP * p.ldn * sizeof(double));
-    h->y.reserve((size_t)p.m * NP * sizeof(double));
-    h->q.reserve((size_t)p.m * NP * sizeof(double));
+    if (p.f32) {
+        h->yf.reserve((size_t)p.m * p.NPf * sizeof(float));
+        h->qf.reserve((size_t)p.m * p.NPf * sizeof(float));
+        h->xtf.reserve((size_t)p.NPf * p.ldnf * sizeof(float));
+        h->rtf.reserve((size_t)p.NPf * p.NPf * sizeof(float));
+    } else {
+        h->y.reserve((size_t)p.m * NP * sizeof(double));
+        h->q.reserve((size_t)p.m * NP * sizeof(double));
+    }
     h->b.reserve((size_t)NP * p.ldn * sizeof(double));
     h->b2.reserve((size_t)NP * p.ldn * sizeof(double));
     h->qbt.reserve((size_t)NP * p.ldn * sizeof(double));
     h->vbuf.reserve((size_t)p.n * NP * sizeof(double));
     h->small.reserve((size_t)kNumSmall * NP * NP * sizeof(double));
     h->part.reserve(partial_doubles(p) * sizeof(double));
-    if (NP <= 96) h->gpart.reserve((size_t)ax_tiles(p.m, NP) * NP * NP * sizeof(double));
+    if (NP <= 96 && !p.f32) h->gpart.reserve((size_t)ax_tiles(p.m, NP) * NP * NP * sizeof(double));
     h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(p.s)) * sizeof(double));
     h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
     ck(cudaMemsetAsync(h->flags.p, 0, kNumFlags * sizeof(int), h->stream), "memset flags");
+    if (p.f32)  // the 3xTF32 A-pass writes rows < NPf of (A^T Q)^T / Q^T A; pad rows stay 0
+        ck(cudaMemsetAsync(h->b.p, 0, (size_t)NP * p.ldn * sizeof(double), h->stream), "memset b");
     h->trace = getenv("RSVD_B200_TRACE") ? atoi(getenv("RSVD_B200_TRACE")) : 0;
     return Ctx{h, p, robust, static_cast<int*>(h->flags.p)};
+}
+
+// FP32 path: the n-side operand of the next A-pass, Xt (NP x ldn, FP64) -> xtf (NPf x ldnf)
+void xt_to_f32(const Ctx& c) {
+    const Plan& p = c.p;
+    c.h->launched(launch_cvt_f64_f32(c.h->xt.d(), p.ldn, p.NPf, p.n, p.s, p.n,
+                                     static_cast<float*>(c.h->xtf.p), p.ldnf, c.h->stream),
+                  "cvt");
+}
+
+// FP32 path A-pass (A^T Q1)^T / Q1^T A into h->b (rows < NPf, FP64).
+void atx_a_f32(const Ctx& c) {
+    const Plan& p = c.p;
+    GemmTf32 g{p.af, p.n, p.m, p.lda, c.h->basis_f, (long)p.NPf, p.NPf, c.h->b.p, p.ldn};
+    g.mn = true;
+    g.out_t = true;
+    gemm_tf32(c.h, g, "gemm_A", 2.0 * p.m * p.n * p.s);
 }
 
 // ---- sketch (rsvd.cpp:51-59): h->y (m x NP) = A * Omega, Omega from the device
@@ -682,6 +821,16 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
         h->launched(launch_omega(seed, n, s, NP, h->xt.d(), p.ldn, st), "omega");
     }
     h->mark("sketch_gemm");
+    if (p.f32) {
+        xt_to_f32(c);
+        GemmTf32 g{p.af, p.m, n, p.lda, static_cast<float*>(h->xtf.p), p.ldnf, p.NPf, h->yf.p,
+                   (long)p.NPf};
+        g.out64 = false;
+        g.flag = check ? c.flags + kFlagNonfinite : nullptr;
+        gemm_tf32(h, g, "gemm_A", 2.0 * p.m * n * s);
+        h->gram_ready = false;
+        return;
+    }
     h->gram_ready = gemm_ax(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                             check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
                             2.0 * p.m * n * s, c.slot(kG));
@@ -696,6 +845,26 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
     if (q > 0 && p.n < p.s)
         fail(RSVD_B200_DIMENSION_ERROR, "householder_qr needs rows >= cols, got %ldx%d", p.n, p.s);
     h->mark("qr_tall");
+    if (p.f32) {
+        tall_qr_f32(c, p.m, q == 0 ? 2 : 1);  // QR(Y0)
+        for (size_t round = 0; round < q; ++round) {
+            h->mark("power_atx");
+            atx_a_f32(c);  // (A^T Q1)^T
+            c.allreduce(h->b.d(), (size_t)p.NP * p.ldn);
+            h->mark("qr_wide");
+            const double* zt = apply_ct(c, h->b.d(), h->b2.d());
+            wide_qr(c, zt, p.n, p.ldn, h->xt.d(), kRB, 1);  // Z^T (FP64)
+            h->mark("power_ax");
+            xt_to_f32(c);
+            GemmTf32 g{p.af, p.m, p.n, p.lda, static_cast<float*>(h->xtf.p), p.ldnf, p.NPf,
+                       h->yf.p, (long)p.NPf};
+            g.out64 = false;
+            gemm_tf32(h, g, "gemm_A", 2.0 * p.m * p.n * p.s);  // Y = A Z
+            h->mark("qr_tall");
+            tall_qr_f32(c, p.m, round + 1 == q ? 2 : 1);
+        }
+        return;
+    }
     tall_qr(c, h->y.d(), p.m, h->q.d(), q == 0 ? 2 : 1, materialize && q == 0,
             h->gram_ready);  // QR(Y0)
     for (size_t round = 0; round < q; ++round) {
@@ -729,8 +898,11 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
         fail(RSVD_B200_DIMENSION_ERROR,
              "project_and_solve: basis width %d exceeds the %ld columns of a", s, n);
     h->mark("project_atx");
-    gemm_atx(h, A, m, n, p.lda, h->basis, NP, NP, h->b.d(), p.ldn, true, "gemm_A",
-             2.0 * m * n * s);  // Q1^T A
+    if (p.f32)
+        atx_a_f32(c);  // Q1^T A
+    else
+        gemm_atx(h, A, m, n, p.lda, h->basis, NP, NP, h->b.d(), p.ldn, true, "gemm_A",
+                 2.0 * m * n * s);  // Q1^T A
     c.allreduce(h->b.d(), (size_t)NP * p.ldn);  // sharded: B = sum_g Q1_g^T A_g
     h->mark("small_svd");
     const double* bq = apply_ct(c, h->b.d(), h->b2.d());  // B = C^T Q1^T A = Q^T A (NP x n)
@@ -766,6 +938,20 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
         h->ubt.reserve((size_t)NPk * NP * sizeof(double));
         h->launched(launch_fill(h->ubt.d(), (long)NPk * NP, 0.0, st), "fill");
         h->launched(launch_transpose(cu, s, k, NP, h->ubt.d(), NP, st), "transpose");
+        if (p.f32) {  // U = Q1 (C U_B)[:, :k] with the K-major 3xTF32 kernel, FP64 out
+            const int NPkf = (int)round_up(k, 16);
+            h->ubtf.reserve((size_t)NPkf * p.NPf * sizeof(float));
+            h->launched(launch_cvt_f64_f32(h->ubt.d(), NP, NPkf, p.NPf, k, s,
+                                           static_cast<float*>(h->ubtf.p), p.NPf, st),
+                        "cvt");
+            const bool direct = (ldu == NPkf) && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
+            if (!direct) h->y.reserve((size_t)m * NPkf * sizeof(double));
+            GemmTf32 g{h->basis_f, m, (long)p.NPf, (long)p.NPf, static_cast<float*>(h->ubtf.p),
+                       (long)p.NPf, NPkf, direct ? (void*)u : h->y.p, direct ? ldu : (long)NPkf};
+            gemm_tf32(h, g);
+            if (!direct) h->launched(launch_copy2d(h->y.d(), NPkf, u, ldu, m, k, st), "copy2d");
+            return;
+        }
         const bool direct = (ldu == NPk) && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
         if (direct) {
             gemm_ax(h, h->basis, m, NP, NP, h->ubt.d(), NP, NPk, u, ldu);
@@ -868,13 +1054,58 @@ void solve_device(rsvd_b200_handle* h, const double* A, long m, long n, long lda
     solve_tall(h, h->a_t.d(), p, cfg, v, k, sigma, u, k, sketch_width);
 }
 
+void make_f32(Plan& p, const float* af) {
+    p.f32 = true;
+    p.af = af;
+    p.NPf = (int)round_up(p.s, 16);
+    p.ldnf = round_up(p.n, 4);
+}
+
+// FP32 input (BASELINE config C4): A m x n FP32 (lda floats); outputs FP64 like every
+// other entry point. Orientation handling as solve_device.
+void solve_device_f32(rsvd_b200_handle* h, const float* A, long m, long n, long lda,
+                      const rsvd_b200_config& cfg, double* u, double* sigma, double* v,
+                      size_t* sketch_width) {
+    const long md = std::min(m, n);
+    if (cfg.k < 1 || (long)cfg.k > md)
+        fail(RSVD_B200_ARGUMENT_ERROR, "target rank k=%zu outside [1, %ld] for a %ldx%ld input",
+             cfg.k, md, m, n);
+    if (!(cfg.epsilon > 0.0 && cfg.epsilon < 1.0))
+        fail(RSVD_B200_ARGUMENT_ERROR, "epsilon must lie in (0, 1)");
+    const long k = (long)cfg.k;
+    if (m >= n) {
+        const float* a = A;
+        long la = lda;
+        if ((lda % 4) || (reinterpret_cast<uintptr_t>(A) & 15)) {  // 16-byte TMA rows
+            la = round_up(n, 4);
+            h->af_copy.reserve((size_t)m * la * sizeof(float));
+            ck(cudaMemcpy2DAsync(h->af_copy.p, la * 4, A, lda * 4, n * 4, m,
+                                 cudaMemcpyDeviceToDevice, h->stream),
+               "A copy");
+            a = static_cast<float*>(h->af_copy.p);
+        }
+        Plan p = make_plan(m, n, la, (long)rsvd_b200_sketch_width(&cfg, (size_t)m, (size_t)n));
+        make_f32(p, a);
+        solve_tall(h, nullptr, p, cfg, u, k, sigma, v, k, sketch_width);
+        return;
+    }
+    const long lt = round_up(m, 4);
+    h->af_copy.reserve((size_t)n * lt * sizeof(float));
+    h->launched(launch_transpose_f32(A, m, n, lda, static_cast<float*>(h->af_copy.p), lt,
+                                     h->stream),
+                "transpose_f32");
+    Plan p = make_plan(n, m, lt, (long)rsvd_b200_sketch_width(&cfg, (size_t)n, (size_t)m));
+    make_f32(p, static_cast<float*>(h->af_copy.p));
+    solve_tall(h, nullptr, p, cfg, v, k, sigma, u, k, sketch_width);
+}
+
 // Row-sharded solve: this rank holds rows [r0, r0 + m_local) of the m_total x n input
 // (m_total >= n). Every rank calls it collectively with the same n, m_total and config;
 // sigma and V come back replicated, U sharded like A. The shard layout is checked
 // collectively first (one tiny all-reduce), so a bad shard fails on every rank alike.
-void solve_sharded(rsvd_b200_handle* h, const double* A, long m_local, long m_total, long n,
-                   long lda, const rsvd_b200_config& cfg, double* u, double* sigma, double* v,
-                   size_t* sketch_width) {
+void solve_sharded(rsvd_b200_handle* h, const void* Av, bool f32, long m_local, long m_total,
+                   long n, long lda, const rsvd_b200_config& cfg, double* u, double* sigma,
+                   double* v, size_t* sketch_width) {
     if (!h->comm) fail(RSVD_B200_ARGUMENT_ERROR, "sharded solve needs a communicator "
                                                  "(rsvd_b200_comm_init_nccl / _local)");
     if (m_total < n)
@@ -906,6 +1137,25 @@ void solve_sharded(rsvd_b200_handle* h, const double* A, long m_local, long m_to
                  "every shard needs at least s=%ld rows (%d shard(s) are thinner)", s,
                  (int)chk[1]);
     }
+    const long k = (long)cfg.k;
+    if (f32) {
+        const float* a = static_cast<const float*>(Av);
+        long la = lda;
+        if ((lda % 4) || (reinterpret_cast<uintptr_t>(a) & 15)) {
+            la = round_up(n, 4);
+            h->af_copy.reserve((size_t)m_local * la * sizeof(float));
+            ck(cudaMemcpy2DAsync(h->af_copy.p, la * 4, a, lda * 4, n * 4, m_local,
+                                 cudaMemcpyDeviceToDevice, h->stream),
+               "A copy");
+            a = static_cast<float*>(h->af_copy.p);
+        }
+        Plan p = make_plan(m_local, n, la, s);
+        p.sharded = true;
+        make_f32(p, a);
+        solve_tall(h, nullptr, p, cfg, u, k, sigma, v, k, sketch_width);
+        return;
+    }
+    const double* A = static_cast<const double*>(Av);
     const double* a = A;
     long la = lda;
     if ((lda % 2) || (reinterpret_cast<uintptr_t>(A) & 15)) {  // TMA needs 16-byte rows
@@ -916,7 +1166,6 @@ void solve_sharded(rsvd_b200_handle* h, const double* A, long m_local, long m_to
     }
     Plan p = make_plan(m_local, n, la, s);
     p.sharded = true;
-    const long k = (long)cfg.k;
     solve_tall(h, a, p, cfg, u, k, sigma, v, k, sketch_width);
 }
 
@@ -1141,8 +1390,8 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_device(
     return guarded([&] {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         h->launches = 0;
-        solve_sharded(h, a_dev, (long)m_local, (long)m_total, (long)n, (long)lda, *cfg, u_dev,
-                      sigma_dev, v_dev, sketch_width);
+        solve_sharded(h, a_dev, false, (long)m_local, (long)m_total, (long)n, (long)lda, *cfg,
+                      u_dev, sigma_dev, v_dev, sketch_width);
     });
 }
 
@@ -1163,7 +1412,7 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_sharded(rsvd_b200_handle* h, const do
         h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
         if (u) h->u_out.reserve(std::max<size_t>(m_local * k, 1) * sizeof(double));
         if (v) h->v_out.reserve(std::max<size_t>(n * k, 1) * sizeof(double));
-        solve_sharded(h, h->a_copy.d(), (long)m_local, (long)m_total, (long)n, lda, *cfg,
+        solve_sharded(h, h->a_copy.d(), false, (long)m_local, (long)m_total, (long)n, lda, *cfg,
                       u ? h->u_out.d() : nullptr, h->sig_out.d(), v ? h->v_out.d() : nullptr,
                       sketch_width);
         ck(cudaMemcpyAsync(sigma, h->sig_out.p, k * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1191,6 +1440,85 @@ rsvd_b200_status rsvd_b200_singular_values_only(rsvd_b200_handle* h, const doubl
                                                 size_t n, const rsvd_b200_config* cfg,
                                                 double* sigma) {
     return guarded([&] { solve_host(h, a, m, n, cfg, nullptr, sigma, nullptr, nullptr); });
+}
+
+// ---------------------------------------------------------------- FP32 input
+rsvd_b200_status rsvd_b200_randomized_ksvd_f32_device(rsvd_b200_handle* h, const float* a_dev,
+                                                      size_t m, size_t n, size_t lda,
+                                                      const rsvd_b200_config* cfg, double* u_dev,
+                                                      double* sigma_dev, double* v_dev,
+                                                      size_t* sketch_width) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        h->launches = 0;
+        solve_device_f32(h, a_dev, (long)m, (long)n, (long)lda, *cfg, u_dev, sigma_dev, v_dev,
+                         sketch_width);
+    });
+}
+
+// Host-buffer FP32 solve (and, with world > 1 communicators, the sharded one): A goes to
+// h->a_copy (raw bytes), outputs come back from the handle's FP64 output buffers.
+static void solve_host_f32(rsvd_b200_handle* h, const float* a, size_t m_local, size_t m_total,
+                           size_t n, bool sharded, const rsvd_b200_config* cfg, double* u,
+                           double* sigma, double* v, size_t* sketch_width) {
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    h->launches = 0;
+    const long lda = round_up((long)n, 4);
+    h->a_copy.reserve(std::max<size_t>(1, m_local * lda) * sizeof(float));
+    ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(float), a, n * sizeof(float),
+                         n * sizeof(float), m_local, cudaMemcpyHostToDevice, h->stream),
+       "H2D of A (FP32)");
+    const size_t k = cfg->k;
+    h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
+    if (u) h->u_out.reserve(std::max<size_t>(m_local * k, 1) * sizeof(double));
+    if (v) h->v_out.reserve(std::max<size_t>(n * k, 1) * sizeof(double));
+    const float* ad = static_cast<const float*>(h->a_copy.p);
+    if (sharded)
+        solve_sharded(h, ad, true, (long)m_local, (long)m_total, (long)n, lda, *cfg,
+                      u ? h->u_out.d() : nullptr, h->sig_out.d(), v ? h->v_out.d() : nullptr,
+                      sketch_width);
+    else
+        solve_device_f32(h, ad, (long)m_local, (long)n, lda, *cfg, u ? h->u_out.d() : nullptr,
+                         h->sig_out.d(), v ? h->v_out.d() : nullptr, sketch_width);
+    ck(cudaMemcpyAsync(sigma, h->sig_out.p, k * sizeof(double), cudaMemcpyDeviceToHost, h->stream),
+       "D2H sigma");
+    const size_t urows = sharded || m_local >= n ? m_local : m_local;
+    if (u)
+        ck(cudaMemcpyAsync(u, h->u_out.p, urows * k * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream),
+           "D2H u");
+    if (v)
+        ck(cudaMemcpyAsync(v, h->v_out.p, n * k * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream),
+           "D2H v");
+    h->sync();
+}
+
+rsvd_b200_status rsvd_b200_randomized_ksvd_f32(rsvd_b200_handle* h, const float* a, size_t m,
+                                               size_t n, const rsvd_b200_config* cfg, double* u,
+                                               double* sigma, double* v, size_t* sketch_width) {
+    return guarded([&] { solve_host_f32(h, a, m, m, n, false, cfg, u, sigma, v, sketch_width); });
+}
+
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_f32(rsvd_b200_handle* h, const float* a,
+                                                       size_t m_local, size_t m_total, size_t n,
+                                                       const rsvd_b200_config* cfg, double* u,
+                                                       double* sigma, double* v,
+                                                       size_t* sketch_width) {
+    return guarded(
+        [&] { solve_host_f32(h, a, m_local, m_total, n, true, cfg, u, sigma, v, sketch_width); });
+}
+
+rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_f32_device(
+    rsvd_b200_handle* h, const float* a_dev, size_t m_local, size_t m_total, size_t n,
+    size_t lda, const rsvd_b200_config* cfg, double* u_dev, double* sigma_dev, double* v_dev,
+    size_t* sketch_width) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        h->launches = 0;
+        solve_sharded(h, a_dev, true, (long)m_local, (long)m_total, (long)n, (long)lda, *cfg,
+                      u_dev, sigma_dev, v_dev, sketch_width);
+    });
 }
 
 rsvd_b200_status rsvd_b200_gaussian_matrix(rsvd_b200_handle* h, uint64_t seed, size_t rows,
@@ -1375,6 +1703,32 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
 }
 
 void rsvd_b200_set_robust(rsvd_b200_handle* h, int on) { h->force_robust = on != 0; }
+
+rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const float* A, long M,
+                                          long K, long lda, const float* B, long ldb, int NP,
+                                          void* out, long ldo, int out64, int out_t, int splits) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        GemmTf32 g{A, M, K, lda, B, ldb, NP, out, ldo};
+        g.mn = mn != 0;
+        g.out64 = out64 != 0;
+        g.out_t = out_t != 0;
+        if (splits > 1) {
+            const long slab = out_t ? (long)NP * ldo : M * ldo;
+            h->part.reserve((size_t)splits * slab * sizeof(double));
+            g.out = h->part.p;
+            g.splits = splits;
+            g.split_stride = slab;
+            h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32(split)");
+            h->launched(launch_reduce_partials(h->part.d(), slab, splits, (double*)out, slab,
+                                               h->stream),
+                        "reduce_partials");
+        } else {
+            h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32");
+        }
+        h->sync();
+    });
+}
 
 rsvd_b200_status rsvd_b200_dmma_peak(rsvd_b200_handle* h, double* tflops) {
     return guarded([&] {

@@ -215,6 +215,62 @@ class Solver:
             C.byref(sw)))
         return u, sig[:k], v, sw.value
 
+    # ------------------------------------------------------------- FP32 input
+    def randomized_ksvd_f32(self, a, cfg: RsvdConfig) -> RsvdResult:
+        """FP32 A (host): 3xTF32 tensor-core products, FP64 outputs (BASELINE config C4)."""
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+            raise DimensionError(f"DenseMatrix requires rows >= 1 and cols >= 1, got {a.shape}")
+        m, n = a.shape
+        k = max(int(cfg.k), 1)
+        u, v, s = np.empty((m, k)), np.empty((n, k)), np.empty(k)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        fp = a.ctypes.data_as(C.POINTER(C.c_float))
+        _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_f32(self.h, fp, m, n, C.byref(c),
+                                                                _dp(u), _dp(s), _dp(v),
+                                                                C.byref(sw)))
+        return RsvdResult(SvdFactors(u, s, v), sw.value)
+
+    def _device_f32(self, fn, a, extra, cfg, values_only):
+        import torch
+        assert a.is_cuda and a.dtype == torch.float32 and a.dim() == 2 and a.stride(1) == 1
+        ml, n = a.shape
+        k = int(cfg.k)
+        dev = a.device
+        sig = torch.empty(max(k, 1), dtype=torch.float64, device=dev)
+        u = None if values_only else torch.empty((ml, max(k, 1)), dtype=torch.float64, device=dev)
+        v = None if values_only else torch.empty((n, max(k, 1)), dtype=torch.float64, device=dev)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        dptr = lambda t: None if t is None else C.cast(t.data_ptr(), C.POINTER(C.c_double))
+        fptr = C.cast(a.data_ptr(), C.POINTER(C.c_float))
+        _check(self.lib, fn(self.h, fptr, ml, *extra, n, a.stride(0), C.byref(c), dptr(u),
+                            dptr(sig), dptr(v), C.byref(sw)))
+        return u, sig[:k], v, sw.value
+
+    def randomized_ksvd_f32_device(self, a, cfg: RsvdConfig, values_only: bool = False):
+        """FP32 A resident in HBM (CUDA float32 tensor); returns FP64 (u, sigma, v, s)."""
+        return self._device_f32(self.lib.rsvd_b200_randomized_ksvd_f32_device, a, (), cfg,
+                                values_only)
+
+    def randomized_ksvd_sharded_f32_device(self, a_local, m_total: int, cfg: RsvdConfig,
+                                           values_only: bool = False):
+        return self._device_f32(self.lib.rsvd_b200_randomized_ksvd_sharded_f32_device, a_local,
+                                (m_total,), cfg, values_only)
+
+    def randomized_ksvd_sharded_f32(self, a_local, m_total: int, cfg: RsvdConfig) -> RsvdResult:
+        a = np.ascontiguousarray(a_local, dtype=np.float32)
+        ml, n = a.shape
+        k = max(int(cfg.k), 1)
+        u, v, s = np.empty((ml, k)), np.empty((n, k)), np.empty(k)
+        sw = C.c_size_t(0)
+        c = cfg._c()
+        fp = a.ctypes.data_as(C.POINTER(C.c_float))
+        _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_sharded_f32(
+            self.h, fp, ml, m_total, n, C.byref(c), _dp(u), _dp(s), _dp(v), C.byref(sw)))
+        return RsvdResult(SvdFactors(u, s, v), sw.value)
+
     # ------------------------------------------------------- row-sharded solves
     def attach_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
         """Attach an NCCL communicator (rank 0 made `unique_id` with nccl_unique_id())."""
