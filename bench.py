@@ -48,6 +48,10 @@ CONFIGS = {
                name="C3 rSVD 202599x16384 k=128 p=20 q=2 FP64 (CelebA 128x128-shaped)"),
     "c5": dict(m=65536, n=65536, k=32, p=10, q=6, spectrum="slow", cpu_rows=1024,
                name="C5 rSVD 65536x65536 k=32 p=10 q=6 FP64 (slow decay 1/i^0.1)"),
+    # FP32 A, 3xTF32 tensor cores; m is per GPU (weak scaling up to 1.6M x 4096 at 8 GPUs).
+    # sigma_1/sigma_s = 1e2 keeps the FP32 bar (1e-4 on sigma) meaningful.
+    "c4": dict(m=200000, n=4096, k=256, p=16, q=4, spectrum="exp", ratio=1e2, cpu_rows=2048,
+               f32=True, name="C4 rSVD 200000x4096 per GPU k=256 p=16 q=4 FP32 (3xTF32)"),
 }
 
 
@@ -68,7 +72,7 @@ def spectrum(cfg, n, xp):
     i = xp.arange(n, dtype=xp.float64)
     if cfg["spectrum"] == "slow":
         return 1.0 / (i + 1.0) ** 0.1
-    tau = (cfg["k"] + cfg["p"] - 1) / np.log(1e4)
+    tau = (cfg["k"] + cfg["p"] - 1) / np.log(cfg.get("ratio", 1e4))
     return xp.exp(-i / tau) + 1e-6
 
 
@@ -164,6 +168,10 @@ def cpu_reference_run(cfg, rows, threads, reps=1):
     kind = "reference" if available("reference") else "port"
     orc = Oracle(kind)
     a = synth_host(cfg, rows)
+    note = ""
+    if cfg.get("f32"):  # the reference is FP64-only: it runs on the FP32-rounded sample
+        a = a.astype(np.float32).astype(np.float64)
+        note = " (FP64 reference on the FP32-rounded sample; it has no FP32 path)"
     k, p, q = cfg["k"], cfg["p"], cfg["q"]
     if kind == "reference":
         orc.set_max_threads(threads)
@@ -180,11 +188,36 @@ def cpu_reference_run(cfg, rows, threads, reps=1):
     f = flops(rows, cfg["n"], k, p, q)
     return {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
             "sample": f"{rows}x{cfg['n']} row block of the {cfg['name'].split()[0]} synthetic "
-                      f"matrix, k={k} p={p} q={q}; {t:.2f} s per solve ({reps} run)",
+                      f"matrix, k={k} p={p} q={q}; {t:.2f} s per solve ({reps} run){note}",
             "seconds": t}
 
 
 # ----------------------------------------------------------------- GPU helpers
+def tf32x3_peak(torch, device):
+    """TF32 dense tensor peak / 3 (three TF32 products per FP32 product). The TF32 rate is
+    half the bf16 rate on Blackwell; the bf16 rate is MEASURED_PEAKS.json's (driver-measured
+    cuBLAS bf16), falling back to a bf16 8192^3 matmul measured here."""
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    bf16 = None
+    if os.path.exists(path):
+        with open(path) as f:
+            bf16 = json.load(f).get("bf16_tflops")
+    src = "MEASURED_PEAKS.json bf16_tflops"
+    if not bf16:
+        a = torch.randn(8192, 8192, dtype=torch.bfloat16, device=device)
+        c = a @ a
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = a @ a
+        e1.record()
+        torch.cuda.synchronize()
+        bf16 = 2 * 8192**3 / (e0.elapsed_time(e1) * 1e-3) / 1e12
+        src = "bf16 8192^3 matmul measured here"
+        del a, c
+    return bf16 / 2 / 3, f"bf16 {bf16:.0f} TF ({src}) / 2 (TF32) / 3 (3xTF32 products)"
+
+
 def cublas_dgemm_peak(torch, device):
     """cuBLAS DGEMM 8192^3, best of 3 (library reference point for the FP64 roofline)."""
     a = torch.randn(8192, 8192, dtype=torch.float64, device=device)
@@ -314,6 +347,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     cfgd = CONFIGS[args.config]
     m, n, k, p, q = cfgd["m"], cfgd["n"], cfgd["k"], cfgd["p"], cfgd["q"]
+    f32 = cfgd.get("f32", False)
     m_total = m * world
     cfg = P.RsvdConfig(k=k, oversample=p, power_q=q, seed=SEED)
     F = flops(m_total, n, k, p, q)
@@ -322,17 +356,28 @@ def run_ours(args):
         P.attach_process_group(solver)
 
     def solve_dev(a):
+        if f32:
+            if world > 1:
+                return solver.randomized_ksvd_sharded_f32_device(a, m_total, cfg)
+            return solver.randomized_ksvd_f32_device(a, cfg)
         if world > 1:
             return solver.randomized_ksvd_sharded_device(a, m_total, cfg)
         return solver.randomized_ksvd_device(a, cfg)
 
     def solve_host(a_host):
+        if f32:
+            if world > 1:
+                return solver.randomized_ksvd_sharded_f32(a_host, m_total, cfg)
+            return solver.randomized_ksvd_f32(a_host, cfg)
         if world > 1:
             return solver.randomized_ksvd_sharded(a_host, m_total, cfg)
         return solver.randomized_ksvd(a_host, cfg)
 
     a = synth_device(torch, cfgd, m, rank, dev)
-    peak_cublas = cublas_dgemm_peak(torch, dev)
+    if f32:
+        a = a.float()
+        torch.cuda.empty_cache()
+    peak_cublas = cublas_dgemm_peak(torch, dev) if not f32 else None
     torch.cuda.synchronize()
     lib_stream = torch.cuda.ExternalStream(solver.stream, device=dev)
 
@@ -375,7 +420,7 @@ def run_ours(args):
 
     # ---- e2e: the public host-buffer API (pinned A in, U, sigma, V out), same config
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    a_host_t = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+    a_host_t = torch.empty((m, n), dtype=a.dtype, pin_memory=True)
     a_host_t.copy_(a)
     a_host = a_host_t.numpy()
     del a, u, v
@@ -399,20 +444,26 @@ def run_ours(args):
         cpu.pop("seconds", None)
 
     if rank == 0:
-        peak_dmma = solver.dmma_peak_tflops()
-        peak = max(peak_dmma, peak_cublas)
+        if f32:
+            peak, peak_src = tf32x3_peak(torch, dev)
+            kernel = "gemm_A (3xTF32 tcgen05 passes over A: ax + atx)"
+        else:
+            peak_dmma = solver.dmma_peak_tflops()
+            peak = max(peak_dmma, peak_cublas)
+            peak_src = ("max of the DMMA m16n8k16 issue-rate probe (rsvd_b200_dmma_peak, "
+                        f"{peak_dmma:.2f}) and cuBLAS DGEMM 8192^3 ({peak_cublas:.2f}), both "
+                        "measured in this run; MEASURED_PEAKS.json has no FP64 entry")
+            kernel = "gemm_A (FP64 DMMA passes over A: ax + atx)"
         per_launch_ms = stats["ms"] / max(1, stats["count"])
         per_launch_flops = stats["flops"] / max(1, stats["count"])
         achieved = per_launch_flops / (per_launch_ms * 1e-3) / 1e12 if stats["count"] else None
         traffic = load_traffic(args.config)
-        roof = {"bound": "tensor", "kernel": "gemm_A (FP64 DMMA passes over A: ax + atx)",
+        roof = {"bound": "tensor", "kernel": kernel,
                 "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 3),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if achieved else None,
                 "traffic": traffic.get("gemm_A_bytes_per_launch") if traffic else None,
-                "traffic_algorithmic": m * n * 8,
-                "peak_source": ("max of the DMMA m16n8k16 issue-rate probe (rsvd_b200_dmma_peak, "
-                                f"{peak_dmma:.2f}) and cuBLAS DGEMM 8192^3 ({peak_cublas:.2f}), "
-                                "both measured in this run; MEASURED_PEAKS.json has no FP64 entry"),
+                "traffic_algorithmic": m * n * (4 if f32 else 8),
+                "peak_source": peak_src,
                 "launches_timed": stats["count"], "ms_per_launch": round(per_launch_ms, 4),
                 "share_of_step": round(stats["ms"] / dev_ms, 4) if dev_ms else None,
                 "algorithmic_flops_per_launch": per_launch_flops,
@@ -420,20 +471,21 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (A; 3xTF32 tensor cores, f64 small side)" if f32 else "f64",
             "data": f"synthetic ({cfgd['spectrum']} spectrum, seed 42)",
             "config": {"workload": cfgd["name"], "m": m_total, "m_per_gpu": m, "n": n, "k": k,
                        "p": p, "q": q, "sketch_width": sw,
                        "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "single GPU",
-                       "l2": f"A ({m * n * 8 / 1e9:.1f} GB per GPU) >> L2 (126 MB): every pass "
+                       "l2": f"A ({m * n * (4 if f32 else 8) / 1e9:.1f} GB per GPU) >> L2 (126 MB): every pass "
                              "streams HBM, no flush"},
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_value, 4), "unit": "TFLOP/s",
                     "ms_per_step": round(1e3 * e2e_s, 2),
-                    "h2d_bytes_per_step": m * n * 8,
+                    "h2d_bytes_per_step": m * n * (4 if f32 else 8),
                     "d2h_bytes_per_step": (m * k + n * k + k) * 8,
-                    "api": ("rsvd_b200_randomized_ksvd_sharded" if world > 1
-                            else "rsvd_b200_randomized_ksvd") + " (host buffers, pinned A)"},
+                    "api": ("rsvd_b200_randomized_ksvd" + ("_sharded" if world > 1 else "")
+                            + ("_f32" if f32 else "") + " (host buffers, pinned A)")},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
             "cpu_baseline": cpu,

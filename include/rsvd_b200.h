@@ -64,6 +64,10 @@ rsvd_b200_status rsvd_b200_destroy(rsvd_b200_handle* h);
 const char* rsvd_b200_last_error(void);
 /* The handle's CUDA stream (a cudaStream_t) so callers can order work around it. */
 void* rsvd_b200_stream(rsvd_b200_handle* h);
+/* Order the handle's stream after all work already enqueued on `other` (a cudaStream_t,
+ * e.g. the framework stream that produced a device A). The _device entry points read
+ * their inputs on the handle's (non-blocking) stream. */
+rsvd_b200_status rsvd_b200_wait_stream(rsvd_b200_handle* h, void* other);
 
 /* Validation mode: use the caller's Omega (n x s row-major, host memory) for the
  * next solves instead of the on-device generator, making the sketch bit-identical

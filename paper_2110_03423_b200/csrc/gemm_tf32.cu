@@ -2,33 +2,38 @@
 // 3xTF32 split products accumulated in TMEM, operands staged by TMA.
 //
 // The FP32 path (BASELINE config C4: A stored in FP32) runs every product with an
-// m-dimension on tcgen05.mma.kind::tf32. TF32 keeps 10 mantissa bits, so each operand
-// x is split in shared memory into hi = rna_tf32(x) and lo = rna_tf32(x - hi) and the
-// product is accumulated as a_hi b_hi + a_hi b_lo + a_lo b_hi (the lo*lo term is below
-// FP32 rounding): ~2^-21 relative error per product, i.e. FP32-class accuracy at a third
-// of the TF32 tensor rate, well above the FP32 SIMT rate.
+// m-dimension on tcgen05.mma.kind::tf32. The tensor core reads an FP32 operand as TF32
+// (the low 13 mantissa bits are ignored), so x = hi + lo with hi = x itself and
+// lo = x - trunc_tf32(x) (exact in FP32); the product is accumulated as
+// a_hi b_hi + a_hi b_lo + a_lo b_hi (a_lo b_lo is below FP32 rounding). Per product the
+// error is ~3 * 2^-20 relative; the tensor core's FP32 accumulation adds ~1e-5 of
+// sum |a||b| on long positive sums (tests/test_gpu_tf32.py) — FP32-class accuracy at a third
+// of the TF32 tensor rate.
 //
 // Two operand shapes, the same two the FP64 path has (gemm_f64.cu):
 //   ax  (K-major A and B): D[M x NP] = A (M x K row-major) * B, B given as Bt (NP x K
 //       row-major). Y = A*Omega, Y = A*Z, Q = Y*R^-1, U = Q*U_B.
 //   atx (MN-major A and B): D[M x NP] = A^T W, A (K x M row-major) read in place,
 //       W (K x NP row-major). (A^T Q)^T, Q^T A, the tall Gram Y^T Y. Split-K over K.
+// The B operand's lo part comes precomputed from global memory (Blo, same layout: the
+// FP32 epilogue below writes it next to every tall FP32 output, cvt_f64_f32 for the
+// small operands); only A's lo part is formed in shared memory.
 //
-// CTA = 6 warps: warp 0 issues TMA (128B-swizzled boxes of 32 fp32), warp 1 owns the
-// TMEM allocation and one elected lane issues the MMAs (M = 128, N = NP in chunks of at
-// most 256), warps 2-5 split the freshly landed tiles into hi/lo (and scan A for
-// NaN/Inf when asked), then drain the accumulator (tcgen05.ld 32x32b) in the epilogue.
-// Two pipeline stages; mbarriers: full (TMA tx) -> conv (128 converter threads) ->
-// MMA -> empty (tcgen05.commit) -> producer.
+// CTA = 6 warps: warp 0 issues TMA, warp 1 owns the TMEM allocation and one elected
+// lane issues the MMAs (M = 128, N = NP in chunks of at most 256), warps 2-5 form A_lo
+// (and scan A for NaN/Inf when asked), then drain the accumulator (tcgen05.ld 32x32b)
+// in the epilogue. Four pipeline stages of K = 16; per stage the MMA issuer runs the two
+// products that need no conversion (a b, a b_lo) as soon as TMA lands and the third
+// (a_lo b) once the converters signal, so the conversion hides behind 2/3 of the math.
+// mbarriers: full (TMA tx), conv (4 converter warps), empty (tcgen05.commit), accum.
 //
-// UMMA shared-memory descriptors (SWIZZLE_128B, version 1):
-//   K-major : rows of 128 B (32 fp32 along K), 8-row atoms of 1024 B: SBO = 1024,
-//             LBO unused; the k-th 8-wide K step starts 32*k bytes into the row.
-//   MN-major: 32-bit MN-major operands only exist in the SWIZZLE_128B_BASE32B layout
-//             (layout type 1, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B: 32-byte chunks of a
-//             128-byte row XORed with row % 4): rows of 128 B (32 fp32 along M/N) indexed
-//             by K, 4-row atoms along K (SBO = 512) and 32-wide M/N chunks one TMA box
-//             apart (LBO = box bytes); the k-th K step starts 1024*k bytes in.
+// UMMA shared-memory descriptors (version 1):
+//   K-major : SWIZZLE_64B (layout 4): rows of 64 B (16 fp32 along K), 8-row atoms of
+//             512 B (SBO = 512, LBO unused); the two 8-wide K steps start 0 / 32 B in.
+//   MN-major: 32-bit MN-major operands only exist as SWIZZLE_128B_BASE32B (layout 1, TMA
+//             CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): rows of 128 B (32 fp32 along M/N)
+//             indexed by K, 4-row atoms (SBO = 512), 32-wide M/N chunks one TMA box apart
+//             (LBO = 2048); the two K steps start 0 / 1024 B in.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -36,18 +41,16 @@ namespace rsvdb200 {
 namespace tf32 {
 
 constexpr int BM = 128;
-constexpr int BK = 32;
-constexpr int kStages = 2;
+constexpr int BK = 16;
+constexpr int kStages = 4;
 constexpr int kThreads = 192;
-constexpr uint32_t kABytes = BM * BK * 4;  // 16 KB per A tile (hi or lo)
+constexpr uint32_t kABytes = BM * BK * 4;  // 8 KB per A tile (raw or lo)
+constexpr uint32_t kBoxMN = 32 * BK * 4;   // 2 KB: one MN-major box (32 M/N x 16 K)
 
-__device__ __forceinline__ float rna_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+__device__ __forceinline__ float lo_part(float x) {
+    return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// layout: 2 = SWIZZLE_128B (K-major), 1 = SWIZZLE_128B_BASE32B (MN-major 32-bit)
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                           uint64_t layout) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
@@ -96,10 +99,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Bytes of one B tile (hi or lo): K-major NP rows of 128 B; MN-major ceil(NP/32) boxes
-// of 32 K-rows x 128 B.
+// Bytes of one B tile (raw or lo): K-major NP rows of 64 B; MN-major ceil(NP/32) boxes.
 __host__ __device__ __forceinline__ uint32_t b_bytes(int NP, bool mn) {
-    return mn ? (uint32_t)((NP + 31) / 32) * 4096u : (uint32_t)NP * 128u;
+    return mn ? (uint32_t)((NP + 31) / 32) * kBoxMN : (uint32_t)NP * (BK * 4);
 }
 __host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
     return 2 * kABytes + 2 * b_bytes(NP, mn);
@@ -108,9 +110,10 @@ __host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
 template <bool MN, bool OUT64, bool OUT_T>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA,
-                     const __grid_constant__ CUtensorMap mapB, void* __restrict__ out, long ldo,
-                     long split_stride, int M, int NP, int k_tiles, int k_tiles_per_split,
-                     int* __restrict__ flag) {
+                     const __grid_constant__ CUtensorMap mapB,
+                     const __grid_constant__ CUtensorMap mapBlo, void* __restrict__ out,
+                     float* __restrict__ out_lo, long ldo, long split_stride, int M, int NP,
+                     int k_tiles, int k_tiles_per_split, int* __restrict__ flag) {
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                          ~uintptr_t(1023));
@@ -149,111 +152,93 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // stage layout: A raw | A lo | B raw | B lo
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
             tma_prefetch_desc(&mapA);
             tma_prefetch_desc(&mapB);
+            tma_prefetch_desc(&mapBlo);
             for (int it = 0; it < n_iter; ++it) {
                 const int s = it % kStages;
                 if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
                 char* st = smem + s * kStage;
                 char* sb = st + 2 * kABytes;
                 const int k = (kt0 + it) * BK;
+                mbar_arrive_expect_tx(&full[s], kABytes + 2 * bB);
                 if constexpr (!MN) {
                     const int parts = NP > 256 ? 2 : 1;
-                    mbar_arrive_expect_tx(&full[s], kABytes + (uint32_t)NP * 128u);
+                    const int rows = NP / parts;
                     tma_load_2d(st, &mapA, &full[s], k, m0);
-                    for (int p = 0; p < parts; ++p)
-                        tma_load_2d(sb + p * (NP / parts) * 128, &mapB, &full[s], k,
-                                    p * (NP / parts));
+                    for (int p = 0; p < parts; ++p) {
+                        tma_load_2d(sb + p * rows * (BK * 4), &mapB, &full[s], k, p * rows);
+                        tma_load_2d(sb + bB + p * rows * (BK * 4), &mapBlo, &full[s], k, p * rows);
+                    }
                 } else {
                     const int nb = (NP + 31) / 32;
-                    mbar_arrive_expect_tx(&full[s], kABytes + (uint32_t)nb * 4096u);
 #pragma unroll
                     for (int i = 0; i < BM / 32; ++i)
-                        tma_load_2d(st + i * 4096, &mapA, &full[s], m0 + 32 * i, k);
-                    for (int j = 0; j < nb; ++j) tma_load_2d(sb + j * 4096, &mapB, &full[s], 32 * j, k);
+                        tma_load_2d(st + i * kBoxMN, &mapA, &full[s], m0 + 32 * i, k);
+                    for (int j = 0; j < nb; ++j) {
+                        tma_load_2d(sb + j * kBoxMN, &mapB, &full[s], 32 * j, k);
+                        tma_load_2d(sb + bB + j * kBoxMN, &mapBlo, &full[s], 32 * j, k);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer
         if (lane == 0) {
-            const uint32_t lbo = MN ? 4096u : 16u, sbo = MN ? 512u : 1024u;
-            const uint64_t lay = MN ? 1u : 2u;
+            const uint32_t lbo = MN ? kBoxMN : 16u, sbo = 512u;
+            const uint64_t lay = MN ? 1u : 4u;
             const int n1 = NP > 256 ? 256 : NP, n2 = NP - n1;
             const uint32_t id1 = idesc(n1, MN), id2 = n2 > 0 ? idesc(n2, MN) : 0u;
-            for (int it = 0; it < n_iter; ++it) {
-                const int s = it % kStages;
-                mbar_wait(&full[s], (it / kStages) & 1);
-                mbar_wait(&conv[s], (it / kStages) & 1);
-                fence_after();
-                const uint32_t st = smem_u32(smem + s * kStage);
-                const uint32_t a_hi = st, a_lo = st + kABytes;
-                const uint32_t b_hi = st + 2 * kABytes, b_lo = b_hi + bB;
+            const uint32_t co = 256u * (MN ? kBoxMN / 32u : BK * 4u);  // B offset of column 256
+            auto issue = [&](uint32_t a, uint32_t b, uint32_t acc0) {
 #pragma unroll
                 for (int ks = 0; ks < BK / 8; ++ks) {
                     const uint32_t ko = MN ? ks * 1024u : ks * 32u;
-                    const uint64_t ah = sdesc(a_hi + ko, lbo, sbo, lay),
-                                   al = sdesc(a_lo + ko, lbo, sbo, lay);
-                    const uint32_t acc0 = (it > 0 || ks > 0) ? 1u : 0u;
-                    {
-                        const uint64_t bh = sdesc(b_hi + ko, lbo, sbo, lay),
-                                       bl = sdesc(b_lo + ko, lbo, sbo, lay);
-                        mma(tmem, ah, bh, id1, acc0);
-                        mma(tmem, ah, bl, id1, 1u);
-                        mma(tmem, al, bh, id1, 1u);
-                    }
-                    if (n2 > 0) {  // columns 256.. (K-major: row 256; MN-major: box 8)
-                        const uint32_t co = 256u * 128u;
-                        const uint64_t bh = sdesc(b_hi + co + ko, lbo, sbo, lay),
-                                       bl = sdesc(b_lo + co + ko, lbo, sbo, lay);
-                        mma(tmem + 256, ah, bh, id2, acc0);
-                        mma(tmem + 256, ah, bl, id2, 1u);
-                        mma(tmem + 256, al, bh, id2, 1u);
-                    }
+                    const uint64_t ad = sdesc(a + ko, lbo, sbo, lay);
+                    const uint32_t acc = (ks == 0) ? acc0 : 1u;
+                    mma(tmem, ad, sdesc(b + ko, lbo, sbo, lay), id1, acc);
+                    if (n2 > 0) mma(tmem + 256, ad, sdesc(b + co + ko, lbo, sbo, lay), id2, acc);
                 }
+            };
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages;
+                const uint32_t st = smem_u32(smem + s * kStage);
+                const uint32_t a_raw = st, a_lo = st + kABytes;
+                const uint32_t b_raw = st + 2 * kABytes, b_lo = b_raw + bB;
+                mbar_wait(&full[s], (it / kStages) & 1);
+                fence_after();
+                issue(a_raw, b_raw, it > 0 ? 1u : 0u);  // a_hi b_hi
+                issue(a_raw, b_lo, 1u);                 // a_hi b_lo
+                mbar_wait(&conv[s], (it / kStages) & 1);
+                fence_after();
+                issue(a_lo, b_raw, 1u);                 // a_lo b_hi
                 commit(&empty[s]);
             }
             if (n_iter > 0) commit(accum);
         }
     } else {
-        // --------------------------------------------------- hi/lo split (warps 2-5)
+        // ------------------------------------------------- A lo split (warps 2-5)
         const int ct = threadIdx.x - 64;
         bool bad = false;
         for (int it = 0; it < n_iter; ++it) {
             const int s = it % kStages;
             mbar_wait(&full[s], (it / kStages) & 1);
             char* st = smem + s * kStage;
-            float4* ah = reinterpret_cast<float4*>(st);
+            const float4* ar = reinterpret_cast<const float4*>(st);
             float4* al = reinterpret_cast<float4*>(st + kABytes);
+#pragma unroll
             for (int i = ct; i < (int)(kABytes / 16); i += 128) {
-                const float4 v = ah[i];
+                const float4 v = ar[i];
                 if (flag) {
                     const uint32_t e = 0x7f800000u;
                     bad |= ((__float_as_uint(v.x) & e) == e) | ((__float_as_uint(v.y) & e) == e) |
                            ((__float_as_uint(v.z) & e) == e) | ((__float_as_uint(v.w) & e) == e);
                 }
-                float4 h, l;
-                h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
-                h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
-                h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
-                h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
-                ah[i] = h;
-                al[i] = l;
-            }
-            float4* bh = reinterpret_cast<float4*>(st + 2 * kABytes);
-            float4* bl = reinterpret_cast<float4*>(st + 2 * kABytes + bB);
-            for (int i = ct; i < (int)(bB / 16); i += 128) {
-                const float4 v = bh[i];
-                float4 h, l;
-                h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
-                h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
-                h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
-                h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
-                bh[i] = h;
-                bl[i] = l;
+                al[i] = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -299,6 +284,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
                         d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    if (out_lo) {  // lo parts for the next product that reads this as B
+                        float4* dl = reinterpret_cast<float4*>(out_lo + (size_t)row * ldo + c0);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dl[i] = make_float4(lo_part(v[4 * i]), lo_part(v[4 * i + 1]),
+                                                lo_part(v[4 * i + 2]), lo_part(v[4 * i + 3]));
+                    }
                 }
             }
         }
@@ -335,28 +327,26 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// Row-major FP32 (rows x cols, ld elements), box {32 cols, box_rows rows}, 128B swizzle.
-int map_f32(CUtensorMap* map, const float* base, long rows, long cols, long ld, int box_rows,
-            bool atom32 = false) {
+// Row-major FP32 (rows x cols, ld elements), box {box_cols, box_rows}.
+int map_f32(CUtensorMap* map, const float* base, long rows, long cols, long ld, int box_cols,
+            int box_rows, CUtensorMapSwizzle swz) {
     auto encode = encode_fn();
     if (!encode) return -1;
     if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 4) & 15)) return -2;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : -3;
 }
 
 template <bool MN, bool OUT64, bool OUT_T>
 cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
-                     cudaStream_t st) {
-    const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN) + 8 * 8 + 16 + 1024;
+                     const CUtensorMap& mBlo, cudaStream_t st) {
+    const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN) + 16 * 8 + 16 + 1024;
     auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -364,48 +354,57 @@ cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap
     const int splits = p.splits < 1 ? 1 : p.splits;
     const int per = (k_tiles + splits - 1) / splits;
     dim3 grid((unsigned)((p.M + tf32::BM - 1) / tf32::BM), (unsigned)splits);
-    kern<<<grid, tf32::kThreads, smem, st>>>(mA, mB, p.out, p.ldo, p.split_stride, (int)p.M,
-                                             p.NP, k_tiles, per, p.flag);
+    kern<<<grid, tf32::kThreads, smem, st>>>(mA, mB, mBlo, p.out, static_cast<float*>(p.out_lo),
+                                             p.ldo, p.split_stride, (int)p.M, p.NP, k_tiles, per,
+                                             p.flag);
     return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
-    if (p.NP < 16 || p.NP > 288 || (p.NP % 16) != 0) return cudaErrorInvalidValue;
+    if (p.NP < 16 || p.NP > 288 || (p.NP % 16) != 0 || !p.Blo) return cudaErrorInvalidValue;
     if (!p.out64 && p.splits > 1) return cudaErrorInvalidValue;
-    CUtensorMap mA, mB;
-    if (!p.mn) {  // A: M x K (lda), Bt: NP x K (ldb)
+    if (p.out_lo && (p.out64 || p.out_t)) return cudaErrorInvalidValue;
+    CUtensorMap mA, mB, mBlo;
+    if (!p.mn) {  // A: M x K (lda), Bt: NP x K (ldb); 64-byte rows of K
         const int brows = p.NP > 256 ? p.NP / 2 : p.NP;
-        if (map_f32(&mA, p.A, p.M, p.K, p.lda, tf32::BM) ||
-            map_f32(&mB, p.B, p.NP, p.K, p.ldb, brows))
+        const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
+        if (map_f32(&mA, p.A, p.M, p.K, p.lda, tf32::BK, tf32::BM, sw) ||
+            map_f32(&mB, p.B, p.NP, p.K, p.ldb, tf32::BK, brows, sw) ||
+            map_f32(&mBlo, p.Blo, p.NP, p.K, p.ldb, tf32::BK, brows, sw))
             return cudaErrorInvalidValue;
-    } else {  // A: K x M (lda), W: K x NP (ldb)
-        if (map_f32(&mA, p.A, p.K, p.M, p.lda, 32, true) ||
-            map_f32(&mB, p.B, p.K, p.NP, p.ldb, 32, true))
+    } else {  // A: K x M (lda), W: K x NP (ldb); 128-byte rows of M / N
+        const auto sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+        if (map_f32(&mA, p.A, p.K, p.M, p.lda, 32, tf32::BK, sw) ||
+            map_f32(&mB, p.B, p.K, p.NP, p.ldb, 32, tf32::BK, sw) ||
+            map_f32(&mBlo, p.Blo, p.K, p.NP, p.ldb, 32, tf32::BK, sw))
             return cudaErrorInvalidValue;
     }
     if (!p.mn) {
-        if (p.out64) return p.out_t ? launch_t<false, true, true>(p, mA, mB, st)
-                                    : launch_t<false, true, false>(p, mA, mB, st);
-        return p.out_t ? launch_t<false, false, true>(p, mA, mB, st)
-                       : launch_t<false, false, false>(p, mA, mB, st);
+        if (p.out64) return p.out_t ? launch_t<false, true, true>(p, mA, mB, mBlo, st)
+                                    : launch_t<false, true, false>(p, mA, mB, mBlo, st);
+        return p.out_t ? launch_t<false, false, true>(p, mA, mB, mBlo, st)
+                       : launch_t<false, false, false>(p, mA, mB, mBlo, st);
     }
-    if (p.out64) return p.out_t ? launch_t<true, true, true>(p, mA, mB, st)
-                                : launch_t<true, true, false>(p, mA, mB, st);
-    return p.out_t ? launch_t<true, false, true>(p, mA, mB, st)
-                   : launch_t<true, false, false>(p, mA, mB, st);
+    if (p.out64) return p.out_t ? launch_t<true, true, true>(p, mA, mB, mBlo, st)
+                                : launch_t<true, true, false>(p, mA, mB, mBlo, st);
+    return p.out_t ? launch_t<true, false, true>(p, mA, mB, mBlo, st)
+                   : launch_t<true, false, false>(p, mA, mB, mBlo, st);
 }
 
 // ------------------------------------------------------------ conversions
+// out = (float)in (0 outside rows_valid x cols_valid); lo (optional) = out - trunc_tf32(out).
 __global__ void cvt_f64_f32_kernel(const double* __restrict__ in, long ldi, long rows, long cols,
                                    long rows_valid, long cols_valid, float* __restrict__ out,
-                                   long ldo) {
+                                   float* __restrict__ lo, long ldo) {
     const long total = rows * cols;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
          e += (long)gridDim.x * blockDim.x) {
         const long r = e / cols, c = e % cols;
-        out[r * ldo + c] = (r < rows_valid && c < cols_valid) ? (float)in[r * ldi + c] : 0.f;
+        const float x = (r < rows_valid && c < cols_valid) ? (float)in[r * ldi + c] : 0.f;
+        out[r * ldo + c] = x;
+        if (lo) lo[r * ldo + c] = tf32::lo_part(x);
     }
 }
 
@@ -416,6 +415,16 @@ __global__ void cvt_f32_f64_kernel(const float* __restrict__ in, long ldi, long 
          e += (long)gridDim.x * blockDim.x) {
         const long r = e / cols, c = e % cols;
         out[r * ldo + c] = (double)in[r * ldi + c];
+    }
+}
+
+__global__ void split_lo_kernel(const float* __restrict__ in, long rows, long cols, long ld,
+                                float* __restrict__ lo) {
+    const long total = rows * cols;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long r = e / cols, c = e % cols;
+        lo[r * ld + c] = tf32::lo_part(in[r * ld + c]);
     }
 }
 
@@ -448,15 +457,21 @@ static unsigned cvt_grid(long work) {
 }
 
 cudaError_t launch_cvt_f64_f32(const double* in, long ldi, long rows, long cols, long rows_valid,
-                               long cols_valid, float* out, long ldo, cudaStream_t st) {
+                               long cols_valid, float* out, long ldo, cudaStream_t st, float* lo) {
     cvt_f64_f32_kernel<<<cvt_grid(rows * cols), 256, 0, st>>>(in, ldi, rows, cols, rows_valid,
-                                                              cols_valid, out, ldo);
+                                                              cols_valid, out, lo, ldo);
     return cudaGetLastError();
 }
 
 cudaError_t launch_cvt_f32_f64(const float* in, long ldi, long rows, long cols, double* out,
                                long ldo, cudaStream_t st) {
     cvt_f32_f64_kernel<<<cvt_grid(rows * cols), 256, 0, st>>>(in, ldi, rows, cols, out, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_lo(const float* in, long rows, long cols, long ld, float* lo,
+                            cudaStream_t st) {
+    split_lo_kernel<<<cvt_grid(rows * cols), 256, 0, st>>>(in, rows, cols, ld, lo);
     return cudaGetLastError();
 }
 

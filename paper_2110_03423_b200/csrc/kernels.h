@@ -46,7 +46,9 @@ struct GemmAtx {
 //   mn = true  (atx): A K x M row-major (lda) read in place, B = W K x NP row-major (ldb).
 // out: FP64 (out64) or FP32, row-major M x NP (ldo) or transposed NP x M (out_t); split-K
 // writes slab s at out + s*split_stride (FP64 only). NP multiple of 16, <= 288.
-// flag != nullptr ORs 1 into *flag if A holds a NaN/Inf.
+// flag != nullptr ORs 1 into *flag if A holds a NaN/Inf. Blo (required): B's lo parts
+// x - trunc_tf32(x), same shape and ldb as B. out_lo (FP32 row-major outputs only): also
+// write the output's lo parts there (same ldo), ready to be the B operand of a later product.
 struct GemmTf32 {
     const float* A;
     long M, K, lda;
@@ -55,6 +57,8 @@ struct GemmTf32 {
     int NP;
     void* out;
     long ldo;
+    const float* Blo = nullptr;
+    void* out_lo = nullptr;
     bool mn = false, out64 = true, out_t = false;
     int splits = 1;
     long split_stride = 0;
@@ -62,8 +66,13 @@ struct GemmTf32 {
 };
 cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st);
 // out (rows x cols, FP32, ldo) = in (FP64, ldi) for r < rows_valid and c < cols_valid, else 0.
+// lo (optional): also the TF32 lo parts of out, same ldo.
 cudaError_t launch_cvt_f64_f32(const double* in, long ldi, long rows, long cols, long rows_valid,
-                               long cols_valid, float* out, long ldo, cudaStream_t st);
+                               long cols_valid, float* out, long ldo, cudaStream_t st,
+                               float* lo = nullptr);
+// lo = x - trunc_tf32(x) elementwise (rows x cols, same ld).
+cudaError_t launch_split_lo(const float* in, long rows, long cols, long ld, float* lo,
+                            cudaStream_t st);
 cudaError_t launch_cvt_f32_f64(const float* in, long ldi, long rows, long cols, double* out,
                                long ldo, cudaStream_t st);
 cudaError_t launch_transpose_f32(const float* in, long rows, long cols, long ldi, float* out,

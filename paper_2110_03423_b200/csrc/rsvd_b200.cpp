@@ -144,8 +144,10 @@ struct rsvd_b200_handle {
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
     DevBuf red_scratch;          // TSQR R stack / flag reduction
     // FP32 path (A stored in FP32, 3xTF32 tensor-core products): tall FP32 buffers
-    DevBuf yf, qf, xtf, rtf, ubtf, af_copy;
-    float* basis_f = nullptr;  // Q1 of the current basis in the FP32 path (yf or qf)
+    // (each with its TF32 lo parts: the B operand of a 3xTF32 product needs both)
+    DevBuf yf, qf, xtf, rtf, ubtf, af_copy, yf_lo, qf_lo, xtf_lo, rtf_lo, ubtf_lo, tf32_tmp;
+    float* basis_f = nullptr;     // Q1 of the current basis in the FP32 path (yf or qf)
+    float* basis_f_lo = nullptr;  // its lo parts
     long fallbacks = 0, reruns = 0;
     int last_sweeps = 0;
     bool force_robust = false;
@@ -627,16 +629,20 @@ bool tall_qr_f32(const Ctx& c, long M, int passes) {
     cudaStream_t st = h->stream;
     const int NP = c.p.NP, NPf = c.p.NPf, s = c.p.s;
     float* Y = static_cast<float*>(h->yf.p);
+    float* Ylo = static_cast<float*>(h->yf_lo.p);
     float* Q1 = static_cast<float*>(h->qf.p);
-    auto gram = [&](const float* X) {
+    float* Q1lo = static_cast<float*>(h->qf_lo.p);
+    auto gram = [&](const float* X, const float* Xlo) {
         GemmTf32 g{X, (long)NPf, M, (long)NPf, X, (long)NPf, NPf, c.slot(kG), (long)NP};
+        g.Blo = Xlo;
         g.mn = true;
         gemm_tf32(h, g);
         c.allreduce(c.slot(kG), (size_t)NP * NP);
     };
     h->c_identity = true;
     h->basis_f = Y;
-    gram(Y);
+    h->basis_f_lo = Ylo;
+    gram(Y, Ylo);
     cholesky(c, kG, kR1, kR1iT);
     if (!chol_broke(c)) {
         if (passes == 1) {
@@ -648,19 +654,23 @@ bool tall_qr_f32(const Ctx& c, long M, int passes) {
         }
         // Q1 = Y R1^-1 (K-major 3xTF32 with Bt = R1^-T in FP32), then its Gram
         h->launched(launch_cvt_f64_f32(c.slot(kR1iT), NP, NPf, NPf, s, s,
-                                       static_cast<float*>(h->rtf.p), NPf, st),
+                                       static_cast<float*>(h->rtf.p), NPf, st,
+                                       static_cast<float*>(h->rtf_lo.p)),
                     "cvt");
         GemmTf32 t{Y, M, (long)NPf, (long)NPf, static_cast<float*>(h->rtf.p), (long)NPf, NPf,
                    Q1, (long)NPf};
+        t.Blo = static_cast<float*>(h->rtf_lo.p);
+        t.out_lo = Q1lo;
         t.out64 = false;
         gemm_tf32(h, t);
-        gram(Q1);
+        gram(Q1, Q1lo);
         cholesky(c, kG, kR2, kR2iT);
         if (!chol_broke(c)) {
             h->launched(launch_transpose(c.slot(kR2iT), NP, NP, NP, c.slot(kC), NP, st),
                         "transpose");  // C = R2^-1
             h->c_identity = false;
             h->basis_f = Q1;
+            h->basis_f_lo = Q1lo;
             h->launched(launch_small_matmul(c.slot(kR2), c.slot(kR1), s, NP, c.slot(kRB), false, st),
                         "small_matmul");  // R = R2 R1
             return false;
@@ -679,8 +689,9 @@ bool tall_qr_f32(const Ctx& c, long M, int passes) {
                                           h->hh_work.d(), st),
                     "householder_qr");
     }
-    h->launched(launch_cvt_f64_f32(h->q.d(), NP, M, NPf, M, s, Q1, NPf, st), "cvt");
+    h->launched(launch_cvt_f64_f32(h->q.d(), NP, M, NPf, M, s, Q1, NPf, st, Q1lo), "cvt");
     h->basis_f = Q1;
+    h->basis_f_lo = Q1lo;
     h->c_identity = true;
     h->fallbacks += 1;
     return true;
@@ -754,10 +765,12 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     const int NP = p.NP;
     h->xt.reserve((size_t)NP * p.ldn * sizeof(double));
     if (p.f32) {
-        h->yf.reserve((size_t)p.m * p.NPf * sizeof(float));
-        h->qf.reserve((size_t)p.m * p.NPf * sizeof(float));
+        for (DevBuf* b : {&h->yf, &h->qf, &h->yf_lo, &h->qf_lo})
+            b->reserve((size_t)p.m * p.NPf * sizeof(float));
         h->xtf.reserve((size_t)p.NPf * p.ldnf * sizeof(float));
+        h->xtf_lo.reserve((size_t)p.NPf * p.ldnf * sizeof(float));
         h->rtf.reserve((size_t)p.NPf * p.NPf * sizeof(float));
+        h->rtf_lo.reserve((size_t)p.NPf * p.NPf * sizeof(float));
     } else {
         h->y.reserve((size_t)p.m * NP * sizeof(double));
         h->q.reserve((size_t)p.m * NP * sizeof(double));
@@ -782,7 +795,8 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
 void xt_to_f32(const Ctx& c) {
     const Plan& p = c.p;
     c.h->launched(launch_cvt_f64_f32(c.h->xt.d(), p.ldn, p.NPf, p.n, p.s, p.n,
-                                     static_cast<float*>(c.h->xtf.p), p.ldnf, c.h->stream),
+                                     static_cast<float*>(c.h->xtf.p), p.ldnf, c.h->stream,
+                                     static_cast<float*>(c.h->xtf_lo.p)),
                   "cvt");
 }
 
@@ -790,6 +804,7 @@ void xt_to_f32(const Ctx& c) {
 void atx_a_f32(const Ctx& c) {
     const Plan& p = c.p;
     GemmTf32 g{p.af, p.n, p.m, p.lda, c.h->basis_f, (long)p.NPf, p.NPf, c.h->b.p, p.ldn};
+    g.Blo = c.h->basis_f_lo;
     g.mn = true;
     g.out_t = true;
     gemm_tf32(c.h, g, "gemm_A", 2.0 * p.m * p.n * p.s);
@@ -825,6 +840,8 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
         xt_to_f32(c);
         GemmTf32 g{p.af, p.m, n, p.lda, static_cast<float*>(h->xtf.p), p.ldnf, p.NPf, h->yf.p,
                    (long)p.NPf};
+        g.Blo = static_cast<float*>(h->xtf_lo.p);
+        g.out_lo = h->yf_lo.p;
         g.out64 = false;
         g.flag = check ? c.flags + kFlagNonfinite : nullptr;
         gemm_tf32(h, g, "gemm_A", 2.0 * p.m * n * s);
@@ -858,6 +875,8 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
             xt_to_f32(c);
             GemmTf32 g{p.af, p.m, p.n, p.lda, static_cast<float*>(h->xtf.p), p.ldnf, p.NPf,
                        h->yf.p, (long)p.NPf};
+            g.Blo = static_cast<float*>(h->xtf_lo.p);
+            g.out_lo = h->yf_lo.p;
             g.out64 = false;
             gemm_tf32(h, g, "gemm_A", 2.0 * p.m * p.n * p.s);  // Y = A Z
             h->mark("qr_tall");
@@ -941,13 +960,16 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
         if (p.f32) {  // U = Q1 (C U_B)[:, :k] with the K-major 3xTF32 kernel, FP64 out
             const int NPkf = (int)round_up(k, 16);
             h->ubtf.reserve((size_t)NPkf * p.NPf * sizeof(float));
+            h->ubtf_lo.reserve((size_t)NPkf * p.NPf * sizeof(float));
             h->launched(launch_cvt_f64_f32(h->ubt.d(), NP, NPkf, p.NPf, k, s,
-                                           static_cast<float*>(h->ubtf.p), p.NPf, st),
+                                           static_cast<float*>(h->ubtf.p), p.NPf, st,
+                                           static_cast<float*>(h->ubtf_lo.p)),
                         "cvt");
             const bool direct = (ldu == NPkf) && ((reinterpret_cast<uintptr_t>(u) & 15) == 0);
             if (!direct) h->y.reserve((size_t)m * NPkf * sizeof(double));
             GemmTf32 g{h->basis_f, m, (long)p.NPf, (long)p.NPf, static_cast<float*>(h->ubtf.p),
                        (long)p.NPf, NPkf, direct ? (void*)u : h->y.p, direct ? ldu : (long)NPkf};
+            g.Blo = static_cast<float*>(h->ubtf_lo.p);
             gemm_tf32(h, g);
             if (!direct) h->launched(launch_copy2d(h->y.d(), NPkf, u, ldu, m, k, st), "copy2d");
             return;
@@ -1229,6 +1251,17 @@ rsvd_b200_status rsvd_b200_destroy(rsvd_b200_handle* h) {
 }
 
 void* rsvd_b200_stream(rsvd_b200_handle* h) { return h->stream; }
+
+rsvd_b200_status rsvd_b200_wait_stream(rsvd_b200_handle* h, void* other) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        cudaEvent_t ev;
+        ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event create");
+        ck(cudaEventRecord(ev, static_cast<cudaStream_t>(other)), "event record");
+        ck(cudaStreamWaitEvent(h->stream, ev, 0), "stream wait");
+        cudaEventDestroy(ev);
+    });
+}
 
 rsvd_b200_status rsvd_b200_set_omega(rsvd_b200_handle* h, const double* omega, size_t rows,
                                      size_t cols) {
@@ -1710,6 +1743,12 @@ rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const fl
     return guarded([&] {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         GemmTf32 g{A, M, K, lda, B, ldb, NP, out, ldo};
+        const long brows = mn ? K : NP, bcols = mn ? NP : K;
+        h->tf32_tmp.reserve((size_t)std::max(1L, brows * ldb) * sizeof(float));
+        h->launched(launch_split_lo(B, brows, bcols, ldb, static_cast<float*>(h->tf32_tmp.p),
+                                    h->stream),
+                    "split_lo");
+        g.Blo = static_cast<float*>(h->tf32_tmp.p);
         g.mn = mn != 0;
         g.out64 = out64 != 0;
         g.out_t = out_t != 0;

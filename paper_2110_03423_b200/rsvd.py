@@ -169,6 +169,13 @@ class Solver:
     def last_launch_count(self) -> int:
         return int(self.lib.rsvd_b200_last_launch_count(self.h))
 
+    def wait_for_torch(self, device=None) -> None:
+        """Order this solver's stream after the work already queued on torch's current
+        stream (device tensors handed to the _device entry points are produced there)."""
+        import torch
+        st = torch.cuda.current_stream(device)
+        _check(self.lib, self.lib.rsvd_b200_wait_stream(self.h, C.c_void_p(st.cuda_stream)))
+
     @property
     def stream(self) -> int:
         return int(self.lib.rsvd_b200_stream(self.h) or 0)
@@ -201,6 +208,7 @@ class Solver:
         leading-dimension stride). Returns (u, sigma, v, sketch_width) as CUDA tensors."""
         import torch
         assert a.is_cuda and a.dtype == torch.float64 and a.dim() == 2 and a.stride(1) == 1
+        self.wait_for_torch(a.device)
         m, n = a.shape
         k = int(cfg.k)
         dev = a.device
@@ -235,6 +243,7 @@ class Solver:
     def _device_f32(self, fn, a, extra, cfg, values_only):
         import torch
         assert a.is_cuda and a.dtype == torch.float32 and a.dim() == 2 and a.stride(1) == 1
+        self.wait_for_torch(a.device)
         ml, n = a.shape
         k = int(cfg.k)
         dev = a.device
@@ -310,6 +319,7 @@ class Solver:
         import torch
         a = a_local
         assert a.is_cuda and a.dtype == torch.float64 and a.dim() == 2 and a.stride(1) == 1
+        self.wait_for_torch(a.device)
         ml, n = a.shape
         k = int(cfg.k)
         dev = a.device

@@ -17,6 +17,7 @@ def run(solver, mn, a, b, NP, out64, out_t, splits=1):
     M = a.shape[1] if mn else a.shape[0]
     dt = torch.float64 if out64 else torch.float32
     out = torch.full((NP, M) if out_t else (M, NP), float("nan"), dtype=dt, device="cuda")
+    solver.wait_for_torch()  # inputs come from torch's stream; the solver's is non-blocking
     st = solver.lib.rsvd_b200_debug_gemm_tf32(
         solver.h, int(mn), C.c_void_p(a.data_ptr()), M, a.shape[0] if mn else a.shape[1],
         a.stride(0), C.c_void_p(b.data_ptr()), b.stride(0), NP, C.c_void_p(out.data_ptr()),
@@ -25,12 +26,12 @@ def run(solver, mn, a, b, NP, out64, out_t, splits=1):
     return out.T if out_t else out
 
 
-def check(got, a64, b64):
+def check(got, a64, b64, tol=TOL):
     ref = a64 @ b64
     bound = a64.abs() @ b64.abs()
     err = (got.double() - ref).abs()
     ratio = (err / bound.clamp_min(1e-300)).max().item()
-    assert ratio <= TOL, ratio
+    assert ratio <= tol, ratio
 
 
 @pytest.mark.parametrize("M,K,NP", [(1000, 4096, 80), (333, 1000, 16), (700, 777, 272),
@@ -60,12 +61,15 @@ def test_atx_tf32(solver, K, M, NP, splits, out_t):
 
 
 def test_gram_tf32(solver):
-    """Y^T Y through the MN-major kernel with A = W = Y (the tall Gram of CholeskyQR)."""
+    """Y^T Y through the MN-major kernel with A = W = Y (the tall Gram of CholeskyQR). The
+    diagonal sums ~1350 positive terms per split in the tensor core's FP32 accumulator, whose
+    rounding is not unbiased: measured 1.4e-5 of the bound (~1e-5 relative on the diagonal),
+    the figure DESIGN.md's CholeskyQR tolerance for the FP32 path is based on."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(3)
     y = torch.randn(50000, 272, device="cuda", generator=g)
     got = run(solver, True, y, y, 272, True, False, 37)
-    check(got, y.double().T, y.double())
+    check(got, y.double().T, y.double(), tol=3e-5)
 
 
 def test_nan_flag_tf32(solver):
