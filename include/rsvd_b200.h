@@ -172,6 +172,20 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_f32_device(
     size_t* sketch_width);
 
 /* ---------------------------------------------------------------------------
+ * RsvdResult::residual_fro (rsvd.hpp:31-32, rsvd.cpp:37-49): ||a - u diag(sigma) v^T||_F
+ * for a m x n, u m x k, v n x k (row-major FP64), sigma k. On the device the product is
+ * never formed: a fused GEMM epilogue subtracts it chunk by chunk and reduces the squares
+ * in a fixed order (deterministic).
+ * ------------------------------------------------------------------------- */
+rsvd_b200_status rsvd_b200_residual_fro(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
+                                       const double* u, const double* sigma, const double* v,
+                                       size_t k, double* out);
+rsvd_b200_status rsvd_b200_residual_fro_device(rsvd_b200_handle* h, const double* a_dev,
+                                              size_t m, size_t n, size_t lda,
+                                              const double* u_dev, const double* sigma_dev,
+                                              const double* v_dev, size_t k, double* out);
+
+/* ---------------------------------------------------------------------------
  * Step functions (rsvd.hpp:36-53), host buffers, for the reference's step-level
  * tests.  range_basis writes the kept width to *cols_out (q must hold m x s).
  * ------------------------------------------------------------------------- */

@@ -26,6 +26,7 @@ EXPORTS = [
     "rsvd_b200_debug_gemm_tf32", "rsvd_b200_randomized_ksvd_f32",
     "rsvd_b200_randomized_ksvd_f32_device", "rsvd_b200_randomized_ksvd_sharded_f32",
     "rsvd_b200_randomized_ksvd_sharded_f32_device", "rsvd_b200_wait_stream",
+    "rsvd_b200_residual_fro", "rsvd_b200_residual_fro_device",
 ]
 
 
@@ -59,6 +60,9 @@ def load() -> C.CDLL:
         "rsvd_b200_last_error": (C.c_char_p, []),
         "rsvd_b200_stream": (_vp, [_vp]),
         "rsvd_b200_wait_stream": (C.c_int, [_vp, _vp]),
+        "rsvd_b200_residual_fro": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _dp, _dp, _sz, _dp]),
+        "rsvd_b200_residual_fro_device": (C.c_int, [_vp, _dp, _sz, _sz, _sz, _dp, _dp, _dp, _sz,
+                                                    _dp]),
         "rsvd_b200_set_omega": (C.c_int, [_vp, _dp, _sz, _sz]),
         "rsvd_b200_randomized_ksvd": (C.c_int, [_vp, _dp, _sz, _sz, cfgp, _dp, _dp, _dp,
                                                 C.POINTER(_sz)]),

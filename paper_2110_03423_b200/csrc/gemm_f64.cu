@@ -138,12 +138,18 @@ __device__ __forceinline__ void gram_epilogue(char* smem, const double (&acc)[BM
 }
 
 // ============================================================================ ax
-template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK>
+// RESID: instead of storing Y, the epilogue accumulates sum (R[row][col] - Y[row][col])^2
+// over the tile's rows < M and columns < resid_cols (R = resid, ld resid_ld) and writes
+// the CTA's partial to resid_out[blockIdx.x] — the fused ||A - U S V^T||_F of
+// RsvdResult::residual_fro (rsvd.cpp:37-49), one column chunk per launch.
+template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK, bool RESID = false>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_ax_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {K, M}, box {16, BM}
                    const __grid_constant__ CUtensorMap mapX,  // dims {K, NP}, box {16, NP}
                    double* __restrict__ Y, long ldy, long split_stride, int M, int k_tiles,
-                   int k_tiles_per_split, int* __restrict__ flag, double* __restrict__ gram) {
+                   int k_tiles_per_split, int* __restrict__ flag, double* __restrict__ gram,
+                   const double* __restrict__ resid, long resid_ld, int resid_cols,
+                   double* __restrict__ resid_out) {
     constexpr int NP = NT * 8;
     constexpr int MI = BM / WM / 16;
     constexpr int NI = NT / WN;
@@ -254,6 +260,38 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     if (CHECK && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 
     // --------------------------------------------------------------- epilogue
+    if constexpr (RESID) {
+        double sq = 0.0;
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int row = m0 + wm * (BM / WM) + mi * 16 + g + 8 * h;
+                if (row < M) {
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) {
+                        const int col = (wn * NI + ni) * 8 + 2 * t;
+#pragma unroll
+                        for (int v = 0; v < 2; ++v)
+                            if (col + v < resid_cols) {
+                                const double d = resid[(long)row * resid_ld + col + v] -
+                                                 acc[mi][ni][2 * h + v];
+                                sq = fma(d, d, sq);
+                            }
+                    }
+                }
+            }
+        sq = warp_sum(sq);
+        __shared__ double red[WM * WN];
+        if (lane == 0) red[warp] = sq;
+        asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < kConsumers; ++w) tot += red[w];
+            resid_out[blockIdx.x] = tot;
+        }
+        return;
+    }
     double* out = Y + blockIdx.y * split_stride;
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
@@ -466,12 +504,12 @@ int make_map(CUtensorMap* map, const double* base, long rows, long cols, long ld
     return r == CUDA_SUCCESS ? 0 : -3;
 }
 
-template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK>
+template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK, bool RESID = false>
 cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     constexpr int NP = NT * 8;
     constexpr size_t kStage = 2 * BM * 128 + 2 * NP * 128;
     constexpr size_t smem = STAGES * kStage + 2 * STAGES * 8 + 1024;
-    auto kern = gemm_ax_kernel<BM, NT, WM, WN, STAGES, CHECK>;
+    auto kern = gemm_ax_kernel<BM, NT, WM, WN, STAGES, CHECK, RESID>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mA, mX;
@@ -484,7 +522,8 @@ cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     dim3 grid((unsigned)((p.M + BM - 1) / BM), (unsigned)splits);
     if (p.gram && (splits != 1 || NT > 12)) return cudaErrorInvalidValue;
     kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mX, p.Y, p.ldy, p.split_stride, (int)p.M,
-                                                 k_tiles, per, p.flag, p.gram);
+                                                 k_tiles, per, p.flag, p.gram, p.resid,
+                                                 p.resid_ld, p.resid_cols, p.resid_out);
     return cudaGetLastError();
 }
 
@@ -541,6 +580,10 @@ cudaError_t dispatch_atx(const GemmAtx& p, cudaStream_t st) {
 }
 
 cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st) {
+    if (p.resid) {  // fused residual chunk: NP = 96 tiles, no split, no flag / Gram
+        if (p.NP != 96 || p.splits > 1 || p.gram || p.flag) return cudaErrorInvalidValue;
+        return launch_ax_t<128, 12, 4, 2, 4, false, true>(p, st);
+    }
     switch (p.NP / 8) {
         case 2: return dispatch_ax<2>(p, st);
         case 4: return dispatch_ax<4>(p, st);

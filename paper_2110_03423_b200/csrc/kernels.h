@@ -24,6 +24,12 @@ struct GemmAx {
     // Fused Gram epilogue (NP <= 96, splits == 1): per-CTA partials Y_tile^T Y_tile,
     // NP x NP each, at gram + blockIdx * NP * NP (ceil(M / 128) partials).
     double* gram = nullptr;
+    // Fused residual (NP == 96, splits == 1): Y is not stored; resid_out[cta] =
+    // sum over the CTA's rows < M, columns < resid_cols of (resid[r][c] - Y[r][c])^2.
+    const double* resid = nullptr;
+    long resid_ld = 0;
+    int resid_cols = 0;
+    double* resid_out = nullptr;
 };
 
 // Z = A^T * W.  A: K x N row-major (lda), W: K x NP row-major (ldw).
@@ -149,6 +155,9 @@ cudaError_t launch_transpose(const double* in, long rows, long cols, long ldi, d
 // Copy rows x cols block between strided buffers.
 cudaError_t launch_copy2d(const double* in, long ldi, double* out, long ldo, long rows, long cols,
                           cudaStream_t st);
+// out (rows_pad x ldo) = V diag(sigma) (first k columns, rows < rows), zero elsewhere.
+cudaError_t launch_scale_cols(const double* V, long ldv, long rows, long rows_pad, int k,
+                              const double* sigma, double* out, long ldo, cudaStream_t st);
 // Zero-fill.
 cudaError_t launch_fill(double* p, long count, double v, cudaStream_t st);
 // NaN/Inf scan: ORs 1 into *flag.

@@ -450,6 +450,25 @@ cudaError_t launch_copy2d(const double* in, long ldi, double* out, long ldo, lon
     return cudaGetLastError();
 }
 
+// out (rows_pad x k, ldo) = V diag(sigma) for rows < rows, zero below (residual operand).
+__global__ void scale_cols_kernel(const double* __restrict__ V, long ldv, long rows, long rows_pad,
+                                  int k, const double* __restrict__ sigma, double* __restrict__ out,
+                                  long ldo) {
+    const long total = rows_pad * ldo;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long r = e / ldo, t = e % ldo;
+        out[e] = (r < rows && t < k) ? V[r * ldv + t] * sigma[t] : 0.0;
+    }
+}
+
+cudaError_t launch_scale_cols(const double* V, long ldv, long rows, long rows_pad, int k,
+                              const double* sigma, double* out, long ldo, cudaStream_t st) {
+    scale_cols_kernel<<<grid_for(rows_pad * ldo, 256), 256, 0, st>>>(V, ldv, rows, rows_pad, k,
+                                                                     sigma, out, ldo);
+    return cudaGetLastError();
+}
+
 __global__ void fill_kernel(double* p, long count, double v) {
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count;
          e += (long)gridDim.x * blockDim.x)

@@ -140,15 +140,11 @@ double RsvdResult::residual_fro(const DenseMatrix& a) const {
         throw DimensionError("residual_fro: factors for " +
                              shape_str(factors.u.rows(), factors.v.rows()) + " against input " +
                              shape_str(a.rows(), a.cols()));
-    double acc = 0.0;
-    for (std::size_t i = 0; i < a.rows(); ++i)
-        for (std::size_t j = 0; j < a.cols(); ++j) {
-            double x = a(i, j);
-            for (std::size_t t = 0; t < k; ++t)
-                x -= factors.u(i, t) * factors.sigma[t] * factors.v(j, t);
-            acc += x * x;
-        }
-    return std::sqrt(acc);
+    double out = 0.0;
+    check(rsvd_b200_residual_fro(handle(), a.data().data(), a.rows(), a.cols(),
+                                 factors.u.data().data(), factors.sigma.data(),
+                                 factors.v.data().data(), k, &out));
+    return out;
 }
 
 DenseMatrix gaussian_matrix(GaussianSampler& sampler, std::size_t rows, std::size_t cols) {

@@ -1193,6 +1193,46 @@ void solve_sharded(rsvd_b200_handle* h, const void* Av, bool f32, long m_local, 
 
 }  // namespace
 
+// ||A - U diag(sigma) V^T||_F (RsvdResult::residual_fro, rsvd.cpp:37-49) on the device:
+// U diag(sigma) V^T is never formed; each 96-column chunk of it is the accumulator of an
+// ax GEMM (K = k) whose epilogue subtracts it from A's chunk and sums the squares per CTA.
+// All device pointers; sigma_dev has k entries. Returns the norm (synchronises).
+double residual_device(rsvd_b200_handle* h, const double* A, long m, long n, long lda,
+                       const double* U, long ldu, const double* sigma_dev, const double* V,
+                       long ldv, long k) {
+    cudaStream_t st = h->stream;
+    const long kp = round_up(k, 2);  // TMA rows of U / Vs: 16-byte multiples
+    const double* Ua = U;
+    if (ldu != kp || (reinterpret_cast<uintptr_t>(U) & 15)) {
+        h->y.reserve((size_t)m * kp * sizeof(double));
+        h->launched(launch_fill(h->y.d(), m * kp, 0.0, st), "fill");
+        h->launched(launch_copy2d(U, ldu, h->y.d(), kp, m, k, st), "copy2d");
+        Ua = h->y.d();
+    }
+    const long chunk = 96, npad = round_up(n, chunk), chunks = npad / chunk;
+    h->b2.reserve((size_t)npad * kp * sizeof(double));
+    h->launched(launch_scale_cols(V, ldv, n, npad, (int)k, sigma_dev, h->b2.d(), kp, st),
+                "scale_cols");
+    const long tiles = (m + 127) / 128;
+    h->part.reserve((size_t)(chunks * tiles + 1) * sizeof(double));
+    double* part = h->part.d();
+    for (long c = 0; c < chunks; ++c) {
+        GemmAx g{Ua, m, kp, kp, h->b2.d() + c * chunk * kp, kp, (int)chunk, nullptr, 0};
+        g.resid = A + c * chunk;
+        g.resid_ld = lda;
+        g.resid_cols = (int)std::min(chunk, n - c * chunk);
+        g.resid_out = part + c * tiles;
+        h->launched(launch_gemm_ax(g, st), "gemm_ax(resid)");
+    }
+    double* tot = part + chunks * tiles;
+    h->launched(launch_reduce_partials(part, 1, (int)(chunks * tiles), tot, 1, st),
+                "reduce_partials");
+    double r = 0.0;
+    ck(cudaMemcpyAsync(&r, tot, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H residual");
+    h->sync();
+    return std::sqrt(r);
+}
+
 // ====================================================================== C-ABI
 extern "C" {
 
@@ -1766,6 +1806,48 @@ rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const fl
             h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32");
         }
         h->sync();
+    });
+}
+
+rsvd_b200_status rsvd_b200_residual_fro_device(rsvd_b200_handle* h, const double* a_dev,
+                                              size_t m, size_t n, size_t lda,
+                                              const double* u_dev, const double* sigma_dev,
+                                              const double* v_dev, size_t k, double* out) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        if (m < 1 || n < 1 || k < 1)
+            fail(RSVD_B200_DIMENSION_ERROR, "residual_fro: empty operands");
+        // A is read with plain loads in the epilogue: any lda works
+        *out = residual_device(h, a_dev, (long)m, (long)n, (long)lda, u_dev, (long)k, sigma_dev,
+                               v_dev, (long)k, (long)k);
+    });
+}
+
+rsvd_b200_status rsvd_b200_residual_fro(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
+                                       const double* u, const double* sigma, const double* v,
+                                       size_t k, double* out) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        if (m < 1 || n < 1 || k < 1)
+            fail(RSVD_B200_DIMENSION_ERROR, "residual_fro: empty operands");
+        h->a_copy.reserve(m * n * sizeof(double));
+        ck(cudaMemcpyAsync(h->a_copy.p, a, m * n * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream),
+           "H2D of A");
+        h->u_out.reserve(m * k * sizeof(double));
+        h->v_out.reserve(n * k * sizeof(double));
+        h->sig_out.reserve(k * sizeof(double));
+        ck(cudaMemcpyAsync(h->u_out.p, u, m * k * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream),
+           "H2D of U");
+        ck(cudaMemcpyAsync(h->v_out.p, v, n * k * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream),
+           "H2D of V");
+        ck(cudaMemcpyAsync(h->sig_out.p, sigma, k * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream),
+           "H2D of sigma");
+        *out = residual_device(h, h->a_copy.d(), (long)m, (long)n, (long)n, h->u_out.d(),
+                               (long)k, h->sig_out.d(), h->v_out.d(), (long)k, (long)k);
     });
 }
 

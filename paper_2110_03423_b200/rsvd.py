@@ -84,14 +84,15 @@ class RsvdResult:
     factors: SvdFactors
     sketch_width: int = 0
 
-    def residual_fro(self, a) -> float:
-        """||a - u diag(sigma) v^T||_F (rsvd.cpp:37-49), evaluated with numpy on the host."""
-        a = np.asarray(a, dtype=np.float64)
+    def residual_fro(self, a, solver: "Solver | None" = None) -> float:
+        """||a - u diag(sigma) v^T||_F (rsvd.hpp:31-32, rsvd.cpp:37-49), on the GPU
+        (rsvd_b200_residual_fro: fused GEMM epilogue, the product is never formed)."""
+        a = _arr(a)
         f = self.factors
         if f.u.shape[0] != a.shape[0] or f.v.shape[0] != a.shape[1]:
             raise DimensionError(f"residual_fro: factors for {f.u.shape[0]}x{f.v.shape[0]} "
                                  f"against input {a.shape[0]}x{a.shape[1]}")
-        return float(np.linalg.norm(a - (f.u * f.sigma) @ f.v.T))
+        return (solver or default_solver()).residual_fro(a, f.u, f.sigma, f.v)
 
 
 def _arr(a) -> np.ndarray:
@@ -222,6 +223,33 @@ class Solver:
             self.h, dptr(a), m, n, a.stride(0), C.byref(c), dptr(u), dptr(sig), dptr(v),
             C.byref(sw)))
         return u, sig[:k], v, sw.value
+
+    def residual_fro(self, a, u, sigma, v) -> float:
+        """||a - u diag(sigma) v^T||_F on the device (host arrays)."""
+        a, u, v = _arr(a), _arr(u), _arr(v)
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        k = sigma.shape[0]
+        if u.shape != (a.shape[0], k) or v.shape != (a.shape[1], k):
+            raise DimensionError("residual_fro: factor shapes do not match the input")
+        out = C.c_double(0.0)
+        _check(self.lib, self.lib.rsvd_b200_residual_fro(self.h, _dp(a), a.shape[0], a.shape[1],
+                                                         _dp(u), _dp(sigma), _dp(v), k,
+                                                         C.byref(out)))
+        return out.value
+
+    def residual_fro_device(self, a, u, sigma, v) -> float:
+        """Same with CUDA float64 tensors (a may have a row stride)."""
+        import torch
+        for t in (a, u, sigma, v):
+            assert t.is_cuda and t.dtype == torch.float64
+        self.wait_for_torch(a.device)
+        u, v, sigma = u.contiguous(), v.contiguous(), sigma.contiguous()
+        out = C.c_double(0.0)
+        dptr = lambda t: C.cast(t.data_ptr(), C.POINTER(C.c_double))
+        _check(self.lib, self.lib.rsvd_b200_residual_fro_device(
+            self.h, dptr(a), a.shape[0], a.shape[1], a.stride(0), dptr(u), dptr(sigma), dptr(v),
+            sigma.shape[0], C.byref(out)))
+        return out.value
 
     # ------------------------------------------------------------- FP32 input
     def randomized_ksvd_f32(self, a, cfg: RsvdConfig) -> RsvdResult:

@@ -321,3 +321,38 @@ def test_c2_device_properties(solver):
     assert torch.equal(s, s2)
     u3, s3, v3, _ = solver.randomized_ksvd_device(a, cfg)
     assert torch.equal(u, u3) and torch.equal(v, v3)
+
+
+# ------------------------------------------------------------------ residual_fro (§8f)
+@pytest.mark.parametrize("m,n,k", [(300, 200, 10), (1000, 577, 33), (2000, 96, 7), (64, 1000, 5)])
+def test_residual_fro_vs_oracle(solver, port, m, n, k):
+    """RsvdResult::residual_fro (rsvd.cpp:37-49) on the GPU (fused GEMM epilogue) against the
+    oracle's restatement; the residual is a difference of nearly equal terms, so the bar is
+    1e-9 relative plus 1e-13 ||A||_F."""
+    import paper_2110_03423_b200 as P
+    a = planted_like(m, n, k, seed=m + n)
+    res = solver.randomized_ksvd(a, P.RsvdConfig(k=k, seed=1))
+    got = res.residual_fro(a, solver)
+    ref = port.residual_fro(a, res.factors.u, res.factors.sigma, res.factors.v)
+    assert abs(got - ref) <= 1e-9 * ref + 1e-13 * np.linalg.norm(a), (got, ref)
+
+
+def test_residual_fro_device_c2_size(solver):
+    torch = pytest.importorskip("torch")
+    m, n, k = 202599, 4096, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g)
+    u = torch.linalg.qr(torch.randn(m, k, dtype=torch.float64, device="cuda", generator=g))[0]
+    v = torch.linalg.qr(torch.randn(n, k, dtype=torch.float64, device="cuda", generator=g))[0]
+    s = torch.linspace(3.0, 1.0, k, dtype=torch.float64, device="cuda")
+    got = solver.residual_fro_device(a, u, s, v)
+    ref = torch.linalg.norm(a - (u * s) @ v.T).item()
+    assert abs(got - ref) <= 1e-10 * ref, (got, ref)
+
+
+def planted_like(m, n, k, seed):
+    rng = np.random.default_rng(seed)
+    r = min(m, n)
+    uu, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    return (uu * np.exp(-np.arange(r) / (k / 2.0))) @ vv.T
