@@ -186,6 +186,33 @@ rsvd_b200_status rsvd_b200_residual_fro_device(rsvd_b200_handle* h, const double
                                               const double* v_dev, size_t k, double* out);
 
 /* ---------------------------------------------------------------------------
+ * PCA, the paper's CelebA application (randsvd::pca, pca.hpp:13-28, pca.cpp:10-52):
+ * fit_pca centers the N x d samples-as-rows x on the device (column sums by the atx GEMM,
+ * then X - 1 mean^T), runs the randomized k-SVD of the centered data and returns
+ * mean (d), components = V (d x k, row-major) and explained_variance = sigma^2 / (N - 1).
+ * Errors as the reference: N < 2 or k outside [1, min(N, d)] -> ArgumentError.
+ * transform: out (N x k) = (x - mean) components (DimensionError on a feature mismatch).
+ * ------------------------------------------------------------------------- */
+rsvd_b200_status rsvd_b200_fit_pca(rsvd_b200_handle* h, const double* x, size_t N, size_t d,
+                                   size_t k, const rsvd_b200_config* cfg, double* mean,
+                                   double* components, double* explained_variance);
+rsvd_b200_status rsvd_b200_pca_transform(rsvd_b200_handle* h, const double* x, size_t N,
+                                         size_t d, const double* mean, const double* components,
+                                         size_t k, double* out);
+
+/* ---------------------------------------------------------------------------
+ * DMAT files (the reference's interchange format, dmat.hpp:10-19) straight into HBM:
+ * rows [row0, row0 + nrows) of the file (a rank's shard) stream through two pinned
+ * staging buffers into a_dev (lda >= cols doubles), file reads overlapping the copies.
+ * Return 0, or 7 (randsvd::IoError: bad magic / header / truncation, with the byte offset
+ * in rsvd_b200_dmat_last_error()).
+ * ------------------------------------------------------------------------- */
+int rsvd_b200_dmat_shape(const char* path, uint64_t* rows, uint64_t* cols);
+int rsvd_b200_load_dmat_device(rsvd_b200_handle* h, const char* path, uint64_t row0,
+                               uint64_t nrows, double* a_dev, size_t lda);
+const char* rsvd_b200_dmat_last_error(void);
+
+/* ---------------------------------------------------------------------------
  * Step functions (rsvd.hpp:36-53), host buffers, for the reference's step-level
  * tests.  range_basis writes the kept width to *cols_out (q must hold m x s).
  * ------------------------------------------------------------------------- */

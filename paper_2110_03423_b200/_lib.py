@@ -26,7 +26,9 @@ EXPORTS = [
     "rsvd_b200_debug_gemm_tf32", "rsvd_b200_randomized_ksvd_f32",
     "rsvd_b200_randomized_ksvd_f32_device", "rsvd_b200_randomized_ksvd_sharded_f32",
     "rsvd_b200_randomized_ksvd_sharded_f32_device", "rsvd_b200_wait_stream",
-    "rsvd_b200_residual_fro", "rsvd_b200_residual_fro_device",
+    "rsvd_b200_residual_fro", "rsvd_b200_residual_fro_device", "rsvd_b200_fit_pca",
+    "rsvd_b200_pca_transform", "rsvd_b200_dmat_shape", "rsvd_b200_load_dmat_device",
+    "rsvd_b200_dmat_last_error",
 ]
 
 
@@ -60,6 +62,13 @@ def load() -> C.CDLL:
         "rsvd_b200_last_error": (C.c_char_p, []),
         "rsvd_b200_stream": (_vp, [_vp]),
         "rsvd_b200_wait_stream": (C.c_int, [_vp, _vp]),
+        "rsvd_b200_dmat_shape": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_uint64)]),
+        "rsvd_b200_load_dmat_device": (C.c_int, [_vp, C.c_char_p, C.c_uint64, C.c_uint64, _dp,
+                                                 _sz]),
+        "rsvd_b200_dmat_last_error": (C.c_char_p, []),
+        "rsvd_b200_fit_pca": (C.c_int, [_vp, _dp, _sz, _sz, _sz, cfgp, _dp, _dp, _dp]),
+        "rsvd_b200_pca_transform": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _dp, _sz, _dp]),
         "rsvd_b200_residual_fro": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _dp, _dp, _sz, _dp]),
         "rsvd_b200_residual_fro_device": (C.c_int, [_vp, _dp, _sz, _sz, _sz, _dp, _dp, _dp, _sz,
                                                     _dp]),

@@ -27,8 +27,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
 
 SOURCES = ["gemm_f64.cu", "gemm_tf32.cu", "omega.cu", "linalg_small.cu", "linalg_blocked.cu", "householder.cu",
-           "comm.cu", "rsvd_b200.cpp",
-           "randsvd_dropin.cpp"]
+           "comm.cu", "rsvd_b200.cpp", "randsvd_dropin.cpp", "dmat.cpp"]
+CLI = os.path.join(LIBDIR, "randsvd_b200")
 
 
 def _newer(src_files, target):
@@ -74,6 +74,16 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    # the reference CLI's hot-path subcommands, built against the C++ drop-in headers
+    cli_src = os.path.join(CSRC, "cli_rsvd.cpp")
+    if _newer([cli_src, LIB] + _headers(), CLI):
+        cmd = [NVCC, "-O2", "-std=c++20", "-I" + os.path.join(ROOT, "include"), cli_src, "-o", CLI,
+               "-L" + LIBDIR, "-lrsvd_b200", "-Xlinker", "-rpath=$ORIGIN"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

@@ -158,6 +158,10 @@ cudaError_t launch_copy2d(const double* in, long ldi, double* out, long ldo, lon
 // out (rows_pad x ldo) = V diag(sigma) (first k columns, rows < rows), zero elsewhere.
 cudaError_t launch_scale_cols(const double* V, long ldv, long rows, long rows_pad, int k,
                               const double* sigma, double* out, long ldo, cudaStream_t st);
+// out = x - 1 mean^T with mean = colsum / rows (written to mean_out) or mean_in if given.
+cudaError_t launch_center(const double* x, long ldx, long rows, long cols, const double* colsum,
+                          const double* mean_in, double* out, long ldo, double* mean_out,
+                          cudaStream_t st);
 // Zero-fill.
 cudaError_t launch_fill(double* p, long count, double v, cudaStream_t st);
 // NaN/Inf scan: ORs 1 into *flag.

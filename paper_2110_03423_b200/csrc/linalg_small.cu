@@ -469,6 +469,30 @@ cudaError_t launch_scale_cols(const double* V, long ldv, long rows, long rows_pa
     return cudaGetLastError();
 }
 
+// PCA centering (pca.cpp:10-26): mean[j] = colsum[j] / n (when mean_out is given) and
+// out[i][j] = x[i][j] - mean[j]; `mean_in` supplies a fixed mean instead (transform).
+__global__ void center_kernel(const double* __restrict__ x, long ldx, long rows, long cols,
+                              const double* __restrict__ colsum, const double* __restrict__ mean_in,
+                              double inv_rows, double* __restrict__ out, long ldo,
+                              double* __restrict__ mean_out) {
+    const long total = rows * cols;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+         e += (long)gridDim.x * blockDim.x) {
+        const long i = e / cols, j = e % cols;
+        const double mu = mean_in ? mean_in[j] : colsum[j] * inv_rows;
+        out[i * ldo + j] = x[i * ldx + j] - mu;
+        if (mean_out && i == 0) mean_out[j] = mu;
+    }
+}
+
+cudaError_t launch_center(const double* x, long ldx, long rows, long cols, const double* colsum,
+                          const double* mean_in, double* out, long ldo, double* mean_out,
+                          cudaStream_t st) {
+    center_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(
+        x, ldx, rows, cols, colsum, mean_in, 1.0 / (double)rows, out, ldo, mean_out);
+    return cudaGetLastError();
+}
+
 __global__ void fill_kernel(double* p, long count, double v) {
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count;
          e += (long)gridDim.x * blockDim.x)

@@ -9,6 +9,7 @@
 #include <memory>
 #include <string>
 
+#include "../../include/randsvd/pca.hpp"
 #include "../../include/randsvd/rsvd.hpp"
 #include "../../include/rsvd_b200.h"
 
@@ -228,5 +229,43 @@ std::vector<double> singular_values_only(const DenseMatrix& a, const RsvdConfig&
     sigma.resize(cfg.k);
     return sigma;
 }
+
+// ------------------------------------------------------------------ PCA (pca.cpp)
+namespace pca {
+
+std::pair<DenseMatrix, std::vector<double>> center_columns(const DenseMatrix& x) {
+    const std::size_t n = x.rows(), d = x.cols();
+    if (n < 2) throw ArgumentError("center_columns needs at least 2 rows, got " + std::to_string(n));
+    std::vector<double> mean(d, 0.0);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < d; ++j) mean[j] += x(i, j);
+    for (double& m : mean) m /= static_cast<double>(n);
+    DenseMatrix centered(n, d);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < d; ++j) centered(i, j) = x(i, j) - mean[j];
+    return {std::move(centered), std::move(mean)};
+}
+
+PcaModel fit_pca(const DenseMatrix& x, std::size_t k, const RsvdConfig& cfg) {
+    const rsvd_b200_config c = to_c(cfg);
+    const std::size_t kk = std::max<std::size_t>(k, 1);
+    std::vector<double> mean(x.cols()), var(kk), comp(x.cols() * kk);
+    check(rsvd_b200_fit_pca(handle(), x.data().data(), x.rows(), x.cols(), k, &c, mean.data(),
+                            comp.data(), var.data()));
+    return PcaModel{std::move(mean), DenseMatrix(x.cols(), k, std::move(comp)), std::move(var)};
+}
+
+DenseMatrix transform(const PcaModel& model, const DenseMatrix& x) {
+    const std::size_t d = model.components.rows(), k = model.components.cols();
+    if (x.cols() != d)
+        throw DimensionError("transform: data has " + std::to_string(x.cols()) +
+                             " features, model has " + std::to_string(d));
+    DenseMatrix out(x.rows(), k);
+    check(rsvd_b200_pca_transform(handle(), x.data().data(), x.rows(), d, model.mean.data(),
+                                  model.components.data().data(), k, out.data().data()));
+    return out;
+}
+
+}  // namespace pca
 
 }  // namespace randsvd

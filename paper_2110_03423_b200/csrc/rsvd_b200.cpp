@@ -143,6 +143,7 @@ struct rsvd_b200_handle {
         hh_work, omega_host_dev, jscratch, cwork, ubt;
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
     DevBuf red_scratch;          // TSQR R stack / flag reduction
+    DevBuf pca_ones, pca_sums, pca_mean, pca_comp;  // PCA (fit_pca / transform)
     // FP32 path (A stored in FP32, 3xTF32 tensor-core products): tall FP32 buffers
     // (each with its TF32 lo parts: the B operand of a 3xTF32 product needs both)
     DevBuf yf, qf, xtf, rtf, ubtf, af_copy, yf_lo, qf_lo, xtf_lo, rtf_lo, ubtf_lo, tf32_tmp;
@@ -1233,6 +1234,26 @@ double residual_device(rsvd_b200_handle* h, const double* A, long m, long n, lon
     return std::sqrt(r);
 }
 
+// PCA centering on the device (pca.cpp:10-26): column sums of X (N x d, ldx) by the atx
+// GEMM against a ones operand (deterministic split-K), then Xc = X - 1 mean^T into
+// Xc (ld ldc, may alias X) and mean into h->pca_mean.
+void pca_center(rsvd_b200_handle* h, const double* X, long N, long d, long ldx, double* Xc,
+                long ldc) {
+    cudaStream_t st = h->stream;
+    const int NP = 16;
+    const long ldd = round_up(d, 2);
+    h->pca_ones.reserve((size_t)N * NP * sizeof(double));
+    h->pca_sums.reserve((size_t)NP * ldd * sizeof(double));
+    h->pca_mean.reserve((size_t)d * sizeof(double));
+    h->launched(launch_fill(h->pca_ones.d(), N * NP, 1.0, st), "fill");
+    // part must hold the split-K slabs of this product
+    const int sp = choose_splits(ax_tiles(d, NP), (N + 31) / 32);
+    h->part.reserve((size_t)std::max(1, sp) * NP * ldd * sizeof(double));
+    gemm_atx(h, X, N, d, ldx, h->pca_ones.d(), NP, NP, h->pca_sums.d(), ldd, true);
+    h->launched(launch_center(X, ldx, N, d, h->pca_sums.d(), nullptr, Xc, ldc, h->pca_mean.d(), st),
+                "center");
+}
+
 // ====================================================================== C-ABI
 extern "C" {
 
@@ -1848,6 +1869,85 @@ rsvd_b200_status rsvd_b200_residual_fro(rsvd_b200_handle* h, const double* a, si
            "H2D of sigma");
         *out = residual_device(h, h->a_copy.d(), (long)m, (long)n, (long)n, h->u_out.d(),
                                (long)k, h->sig_out.d(), h->v_out.d(), (long)k, (long)k);
+    });
+}
+
+// ------------------------------------------------------------------- PCA (§8f)
+rsvd_b200_status rsvd_b200_fit_pca(rsvd_b200_handle* h, const double* x, size_t N, size_t d,
+                                   size_t k, const rsvd_b200_config* cfg, double* mean,
+                                   double* components, double* explained_variance) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        h->launches = 0;
+        if (N < 2) fail(RSVD_B200_ARGUMENT_ERROR, "center_columns needs at least 2 rows, got %zu", N);
+        if (k < 1 || k > std::min(N, d))
+            fail(RSVD_B200_ARGUMENT_ERROR, "fit_pca k=%zu outside [1, %zu]", k, std::min(N, d));
+        const long ld = round_up((long)d, 2);
+        h->a_copy.reserve((size_t)N * ld * sizeof(double));
+        ck(cudaMemcpy2DAsync(h->a_copy.p, ld * sizeof(double), x, d * sizeof(double),
+                             d * sizeof(double), N, cudaMemcpyHostToDevice, h->stream),
+           "H2D of X");
+        pca_center(h, h->a_copy.d(), (long)N, (long)d, ld, h->a_copy.d(), ld);
+        rsvd_b200_config c = *cfg;
+        c.k = k;
+        h->sig_out.reserve(k * sizeof(double));
+        h->v_out.reserve((size_t)d * k * sizeof(double));
+        solve_device(h, h->a_copy.d(), (long)N, (long)d, ld, c, nullptr, h->sig_out.d(),
+                     h->v_out.d(), nullptr);
+        std::vector<double> sig(k);
+        ck(cudaMemcpyAsync(sig.data(), h->sig_out.p, k * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream),
+           "D2H sigma");
+        ck(cudaMemcpyAsync(components, h->v_out.p, d * k * sizeof(double),
+                           cudaMemcpyDeviceToHost, h->stream),
+           "D2H components");
+        ck(cudaMemcpyAsync(mean, h->pca_mean.p, d * sizeof(double), cudaMemcpyDeviceToHost,
+                           h->stream),
+           "D2H mean");
+        h->sync();
+        const double denom = (double)(N - 1);  // pca.cpp:36-38
+        for (size_t i = 0; i < k; ++i) explained_variance[i] = sig[i] * sig[i] / denom;
+    });
+}
+
+rsvd_b200_status rsvd_b200_pca_transform(rsvd_b200_handle* h, const double* x, size_t N,
+                                         size_t d, const double* mean, const double* components,
+                                         size_t k, double* out) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        if (N < 1 || d < 1 || k < 1 || k > d)
+            fail(RSVD_B200_DIMENSION_ERROR, "transform: %zu components for %zu features", k, d);
+        cudaStream_t st = h->stream;
+        const long ld = round_up((long)d, 2);
+        h->a_copy.reserve((size_t)N * ld * sizeof(double));
+        ck(cudaMemcpy2DAsync(h->a_copy.p, ld * sizeof(double), x, d * sizeof(double),
+                             d * sizeof(double), N, cudaMemcpyHostToDevice, st),
+           "H2D of X");
+        h->pca_mean.reserve(d * sizeof(double));
+        h->pca_comp.reserve((size_t)d * k * sizeof(double));
+        ck(cudaMemcpyAsync(h->pca_mean.p, mean, d * sizeof(double), cudaMemcpyHostToDevice, st),
+           "H2D mean");
+        ck(cudaMemcpyAsync(h->pca_comp.p, components, d * k * sizeof(double),
+                           cudaMemcpyHostToDevice, st),
+           "H2D components");
+        h->launched(launch_center(h->a_copy.d(), ld, (long)N, (long)d, nullptr, h->pca_mean.d(),
+                                  h->a_copy.d(), ld, nullptr, st),
+                    "center");
+        // (X - mean) components: ax with Xt = components^T (NPk x d, zero padded)
+        const int NPk = pad_np((long)k);
+        h->ubt.reserve((size_t)NPk * ld * sizeof(double));
+        h->launched(launch_fill(h->ubt.d(), (long)NPk * ld, 0.0, st), "fill");
+        h->launched(launch_transpose(h->pca_comp.d(), (long)d, (long)k, (long)k, h->ubt.d(), ld, st),
+                    "transpose");
+        const long tiles = ax_tiles((long)N, NPk);
+        const int sp = choose_splits(tiles, (ld + 31) / 32);
+        h->part.reserve((size_t)std::max(1, sp) * N * NPk * sizeof(double));
+        h->y.reserve((size_t)N * NPk * sizeof(double));
+        gemm_ax(h, h->a_copy.d(), (long)N, (long)d, ld, h->ubt.d(), ld, NPk, h->y.d(), NPk);
+        ck(cudaMemcpy2DAsync(out, k * sizeof(double), h->y.p, NPk * sizeof(double),
+                             k * sizeof(double), N, cudaMemcpyDeviceToHost, st),
+           "D2H projection");
+        h->sync();
     });
 }
 

@@ -42,6 +42,8 @@ def test_kernels_use_tma_and_dmma():
                           timeout=600).stdout
     assert "DMMA" in sass  # FP64 tensor-core MMA
     assert "UTMALDG" in sass  # TMA tensor loads
+    assert "UTCHMMA" in sass  # tcgen05.mma (the FP32 path's 3xTF32 products)
+    assert "LDTM" in sass  # tcgen05.ld: accumulators read back from TMEM
 
 
 def test_sketch_width_matches_reference_rule():
