@@ -144,6 +144,7 @@ struct rsvd_b200_handle {
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
     DevBuf red_scratch;          // TSQR R stack / flag reduction
     DevBuf pca_ones, pca_sums, pca_mean, pca_comp;  // PCA (fit_pca / transform)
+    DevBuf res_vs, res_part, res_u;                 // residual_fro
     // FP32 path (A stored in FP32, 3xTF32 tensor-core products): tall FP32 buffers
     // (each with its TF32 lo parts: the B operand of a 3xTF32 product needs both)
     DevBuf yf, qf, xtf, rtf, ubtf, af_copy, yf_lo, qf_lo, xtf_lo, rtf_lo, ubtf_lo, tf32_tmp;
@@ -1205,20 +1206,20 @@ double residual_device(rsvd_b200_handle* h, const double* A, long m, long n, lon
     const long kp = round_up(k, 2);  // TMA rows of U / Vs: 16-byte multiples
     const double* Ua = U;
     if (ldu != kp || (reinterpret_cast<uintptr_t>(U) & 15)) {
-        h->y.reserve((size_t)m * kp * sizeof(double));
-        h->launched(launch_fill(h->y.d(), m * kp, 0.0, st), "fill");
-        h->launched(launch_copy2d(U, ldu, h->y.d(), kp, m, k, st), "copy2d");
-        Ua = h->y.d();
+        h->res_u.reserve((size_t)m * kp * sizeof(double));
+        h->launched(launch_fill(h->res_u.d(), m * kp, 0.0, st), "fill");
+        h->launched(launch_copy2d(U, ldu, h->res_u.d(), kp, m, k, st), "copy2d");
+        Ua = h->res_u.d();
     }
     const long chunk = 96, npad = round_up(n, chunk), chunks = npad / chunk;
-    h->b2.reserve((size_t)npad * kp * sizeof(double));
-    h->launched(launch_scale_cols(V, ldv, n, npad, (int)k, sigma_dev, h->b2.d(), kp, st),
+    h->res_vs.reserve((size_t)npad * kp * sizeof(double));
+    h->launched(launch_scale_cols(V, ldv, n, npad, (int)k, sigma_dev, h->res_vs.d(), kp, st),
                 "scale_cols");
     const long tiles = (m + 127) / 128;
-    h->part.reserve((size_t)(chunks * tiles + 1) * sizeof(double));
-    double* part = h->part.d();
+    h->res_part.reserve((size_t)(chunks * tiles + 1) * sizeof(double));
+    double* part = h->res_part.d();
     for (long c = 0; c < chunks; ++c) {
-        GemmAx g{Ua, m, kp, kp, h->b2.d() + c * chunk * kp, kp, (int)chunk, nullptr, 0};
+        GemmAx g{Ua, m, kp, kp, h->res_vs.d() + c * chunk * kp, kp, (int)chunk, nullptr, 0};
         g.resid = A + c * chunk;
         g.resid_ld = lda;
         g.resid_cols = (int)std::min(chunk, n - c * chunk);

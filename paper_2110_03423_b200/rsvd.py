@@ -242,8 +242,8 @@ class Solver:
         import torch
         for t in (a, u, sigma, v):
             assert t.is_cuda and t.dtype == torch.float64
-        self.wait_for_torch(a.device)
-        u, v, sigma = u.contiguous(), v.contiguous(), sigma.contiguous()
+        u, v, sigma = u.contiguous(), v.contiguous(), sigma.contiguous()  # may copy on torch's
+        self.wait_for_torch(a.device)  # stream: order the solver's stream after those copies
         out = C.c_double(0.0)
         dptr = lambda t: C.cast(t.data_ptr(), C.POINTER(C.c_double))
         _check(self.lib, self.lib.rsvd_b200_residual_fro_device(

@@ -1,6 +1,6 @@
 #!/bin/bash
 set -x
-OUT=gpurun_out/${1:-r1f}
+OUT=gpurun_out/${1:-check}
 mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.log 2>&1; echo "exit $?" >> $OUT/pytest_gpu.log
 timeout 600 python bench.py --steps 5 --no-cpu > $OUT/bench_c2.json 2> $OUT/bench_c2.err
