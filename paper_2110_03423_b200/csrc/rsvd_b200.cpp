@@ -389,9 +389,21 @@ void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, co
 // 3xTF32 tensor-core product (gemm_tf32.cu) with split-K over K for FP64 outputs when the
 // output tiles alone would not fill the GPU (1 CTA per SM); slabs reduced in fixed order.
 // Slab: the out_t rows NP x ldo, else M x ldo.
+// The tensor core's FP32 accumulation is biased (it shrinks long sums by ~1e-8 per added
+// term), so an FP64-output product never accumulates more than kTf32Chain K-values in
+// TMEM: longer contractions are split and the slabs summed in FP64. This keeps the
+// relative bias of e.g. B = Q^T A (K = m = 200000) at ~1e-5 instead of ~2e-4.
+constexpr long kTf32Chain = 2048;
+
+int tf32_splits(long M, long K) {
+    const long tiles = (M + 127) / 128;
+    const long k_tiles = (K + 15) / 16;  // tf32 k-tiles of 16
+    const int by_chain = (int)((K + kTf32Chain - 1) / kTf32Chain);
+    return std::max(choose_splits(tiles, k_tiles), by_chain);
+}
+
 void gemm_tf32(rsvd_b200_handle* h, GemmTf32 g, const char* tag = nullptr, double flops = 0.0) {
-    const long tiles = (g.M + 127) / 128;
-    const int splits = g.out64 ? choose_splits(tiles, (g.K + 31) / 32) : 1;
+    const int splits = g.out64 ? tf32_splits(g.M, g.K) : 1;
     if (splits == 1) {
         h->kernel_begin(tag, flops);
         h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32");
@@ -432,10 +444,12 @@ size_t partial_doubles(const Plan& p) {
     ax(p.m, NP, NP);             // tall TRSM, back-projection
     ax(NP, p.n, NP);             // wide Gram
     if (p.f32) {  // 3xTF32: A-pass (A^T Q)^T (NPf x ldn slabs) and the tall Gram (NPf x NP)
-        const int sp1 = choose_splits((p.n + 127) / 128, (p.m + 31) / 32);
+        const int sp1 = tf32_splits(p.n, p.m);
         if (sp1 > 1) need = std::max(need, (size_t)sp1 * p.NPf * p.ldn);
-        const int sp2 = choose_splits((p.NPf + 127) / 128, (p.m + 31) / 32);
+        const int sp2 = tf32_splits(p.NPf, p.m);
         if (sp2 > 1) need = std::max(need, (size_t)sp2 * p.NPf * NP);
+        const int sp3 = tf32_splits(p.m, p.NPf);  // U = Q (C U_B) (FP64 out, K = NPf)
+        if (sp3 > 1) need = std::max(need, (size_t)sp3 * p.m * p.NPf);
     }
     return std::max<size_t>(need, 1);
 }
