@@ -1,12 +1,14 @@
-// Small dense linear algebra for wide sketches (s > ~140), where an s x s FP64 matrix
-// no longer fits one CTA's shared memory (s = 272 is 592 KB):
+// Small dense linear algebra beyond one CTA: the blocked Cholesky's pieces for s > ~150 (an
+// s x s FP64 matrix no longer fits one CTA's shared memory: s = 272 is 592 KB) and the
+// multi-CTA block Jacobi, used for every s > 64 (more SMs, 8 warps each, beat one CTA's
+// 32 IPC-bound warps):
 //   * small_gemm_kernel — generic C = alpha op(A) op(B) + beta Cin on s-sized
 //     operands (tiles of 32 x 32 per CTA), the building block of the blocked Cholesky
 //     that rsvd_b200.cpp assembles from two in-smem Cholesky factorisations;
 //   * block_jacobi_kernel — one-sided block Jacobi SVD of the s x s triangular factor
 //     R_B, the wide-sketch twin of jacobi_kernel (linalg_small.cu). Columns live in
-//     global memory (L2 resident); the s/16 column blocks are paired in round-robin
-//     (tournament) order, each block pair is one CTA that loads its 32 columns into
+//     global memory (L2 resident); the s/8 column blocks are paired in round-robin
+//     (tournament) order, each block pair is one CTA that loads its 16 columns into
 //     shared memory and runs an inner one-sided Jacobi sweep over them with the
 //     reference's rotation rule and skip thresholds (svd.cpp:35-36, 60-90); a grid-wide
 //     barrier (cooperative launch) separates rounds. A sweep without any rotation ends
@@ -74,8 +76,8 @@ cudaError_t launch_small_gemm(int M, int N, int K, double alpha, const double* A
 }
 
 // ========================================================= block Jacobi SVD
-constexpr int kBJW = 16;          // columns per block
-constexpr int kBJThreads = 512;   // 16 warps: one per column pair of an inner round
+constexpr int kBJW = 8;           // columns per block
+constexpr int kBJThreads = 256;   // 8 warps: one per column pair of an inner round
 constexpr int kBJMaxSweeps = 30;
 
 __device__ __forceinline__ int bj_rr(int slot, int round, int sp) {
@@ -158,8 +160,11 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
             int bi = bj_rr(k, round, sp), bj = bj_rr(sp - 1 - k, round, sp);
             if (bi > bj) { const int t = bi; bi = bj; bj = t; }
             int cnt = 0;
-            if (k < sp / 2 && bj < nb) {
-                const int e0 = min(s, (bi + 1) * kBJW), e1 = min(s, (bj + 1) * kBJW);
+            // a block paired with the bye slot (bj == nb, odd block count) still sweeps its
+            // own pairs — with a single block that is the whole matrix
+            if (k < sp / 2 && bi < nb) {
+                const int e0 = min(s, (bi + 1) * kBJW);
+                const int e1 = bj < nb ? min(s, (bj + 1) * kBJW) : bj * kBJW;
                 cnt = (e0 - bi * kBJW) + (e1 - bj * kBJW);
                 if (tid < cnt) {
                     const int n0 = e0 - bi * kBJW;

@@ -174,7 +174,9 @@ cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP,
 // Columns are stored contiguously in shared memory; the rotation accumulator J lives
 // in shared memory when both fit, else in global scratch (L2 resident).
 constexpr int kJacobiThreads = 1024;
-constexpr int kJacobiSmemMax = 160;  // widths beyond run the block Jacobi (linalg_blocked.cu)
+// widths beyond run the multi-CTA block Jacobi (linalg_blocked.cu): measured faster from
+// s ~ 64 on (C1, s = 74: 0.9 -> 0.7 ms)
+constexpr int kJacobiSmemMax = 64;
 constexpr int kMaxSweeps = 30;
 
 __device__ __forceinline__ int rr_index(int slot, int round, int sp) {
