@@ -20,105 +20,325 @@ namespace rsvdb200 {
 // G (s x s, ldg) symmetric positive definite -> G = R^T R with R upper and a positive
 // diagonal, plus Rinv^T = (R^-1)^T. Breakdown when a pivot falls below tol * max_i G_ii
 // (status[0] = 1 and, if `abort` is given, *abort |= 1).
-// Latency-lean single-CTA kernel (1024 threads): one __syncthreads per column, every
-// element update of a step independent (a few per thread), no division in the inner
-// loops. The s x s shared buffer (odd leading dimension) holds the unscaled LDL^T rows
-// in its upper triangle (R[j][c] = a[j][c] / sqrt(a[j][j])); the inversion R X = I runs
-// bottom-up, keeping the not-yet-scaled rows of X transposed in the strict lower
-// triangle with their scale 1/R_ii in dinv[]. An upper-triangle index table (row-major)
-// lets step j address the trailing triangle as one flat range.
-constexpr int kCholThreads = 1024;
+// Single CTA (512 threads), blocked by 16-wide panels. The matrix is padded to sp = s
+// rounded up to 16 with a decoupled diagonal (max_i G_ii) so every panel is full.
+//  * factorisation (right-looking, two barriers per panel): warp 0 factors the 16 x 16
+//    diagonal block in registers (lane c holds column c; pivot rows travel by shuffle;
+//    the pivot chain is one shuffle, a Newton reciprocal and an FMA per step - the square
+//    roots are off the chain). The panel row block is solved column-parallel against it
+//    (forward substitution in registers with the block's multipliers), then the trailing
+//    upper triangle gets the rank-16 update in 4 x 4 register tiles while warp 0 updates
+//    and factors the next diagonal block (lookahead).
+//  * R is written transposed into the strict lower triangle as it is produced, and the
+//    upper triangle is reset to I panel by panel, so the inversion R X = I runs in place
+//    bottom-up by panels: 16 rows of X column-parallel (back substitution with broadcast R
+//    loads), then the rank-16 update of every row above in 4 x 4 tiles.
+// Shared memory: sp x (sp + 2) doubles + diag(R) and its reciprocals.
+#ifdef CHOL_TRACE  // tools/probe/small_probe.cu: per-phase clock64 stamps of thread 0
+__device__ long long g_chol_trace[256];
+__device__ int g_chol_ntrace;
+#define CHOL_MARK(tag)                                                   \
+    do {                                                                 \
+        if (threadIdx.x == 0 && g_chol_ntrace < 128) {                   \
+            g_chol_trace[2 * g_chol_ntrace] = (tag);                     \
+            g_chol_trace[2 * g_chol_ntrace + 1] = clock64();             \
+            ++g_chol_ntrace;                                             \
+        }                                                                \
+    } while (0)
+#else
+#define CHOL_MARK(tag) \
+    do {               \
+    } while (0)
+#endif
+constexpr int kCholThreads = 512;
+constexpr int kCholPanel = 16;
+
+__host__ __device__ inline int chol_pad(int s) { return (s + kCholPanel - 1) & ~(kCholPanel - 1); }
+
+// flat index e of the upper triangle of a T x T tile grid (row-major) -> (tr, tc), tc >= tr
+__device__ __forceinline__ void chol_tri_index(int e, int T, int& tr, int& tc) {
+    const float b = 2.0f * T + 1.0f;
+    int r = (int)((b - sqrtf(fmaxf(b * b - 8.0f * e, 0.0f))) * 0.5f);
+    auto start = [T](int q) { return q * T - q * (q - 1) / 2; };
+    while (r > 0 && start(r) > e) --r;
+    while (r + 1 < T && start(r + 1) <= e) ++r;
+    tr = r;
+    tc = r + (e - start(r));
+}
+
+// 1/d to full precision off the MUFU seed: two Newton steps
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+struct __align__(16) CholShared {
+    double U[kCholPanel * kCholPanel];  // U[k][i] = u_k[i]: pivot row k of the diagonal block
+    double L[kCholPanel * 17];          // L[k][i] = u_k[i] / d_k (pivot row k over its pivot)
+    double rs[kCholPanel];              // pivots d_k, then 1 / sqrt(d_k)
+    int bad;
+};
+
+// Pivot step K of the diagonal block (template recursion: fully unrolled, a[] in registers;
+// lane c holds column c, entries below the diagonal are don't-care). The pivot d = u_K[K]
+// comes by shuffle (the chain: shuffle, Newton reciprocal, multiply, FMA); the rest of
+// pivot row K is published through shared memory and read back as broadcasts, off the chain.
+template <int K>
+__device__ __forceinline__ void chol_pivot_steps(double (&a)[kCholPanel], int c, int lane,
+                                                 double thresh, CholShared& cs, bool& ok) {
+    if constexpr (K < kCholPanel) {
+        constexpr unsigned kFull = 0xffffffffu;
+        const double d = __shfl_sync(kFull, a[K], K);
+        if constexpr (K + 1 < kCholPanel) {
+            if (lane < kCholPanel) cs.U[K * kCholPanel + c] = a[K];
+        }
+        __syncwarp();
+        ok = ok && (d > thresh);  // also catches NaN
+        const double m = a[K] * rcp_nr(d);
+        if (lane < kCholPanel) cs.L[K * 17 + c] = m;
+        if (lane == 0) cs.rs[K] = d;
+#pragma unroll
+        for (int i = K + 1; i < kCholPanel; ++i) a[i] = fma(-cs.U[K * kCholPanel + i], m, a[i]);
+        chol_pivot_steps<K + 1>(a, c, lane, thresh, cs, ok);
+    }
+}
+
+// Warp 0: the diagonal block at j0 (after the updates of the panels before it; with
+// `update`, panel jp's rank-16 update is applied here first). Lane c < 16 holds column c.
+// Leaves L / rs for the panel solve, rdiag / dinv, the block's R transposed in S's strict
+// lower triangle and I in its upper triangle; cs.bad = 1 on breakdown.
+__device__ __forceinline__ void chol_diag_factor(double* S, int ld, int j0, double thresh,
+                                                 CholShared& cs, double* rdiag, double* dinv,
+                                                 int lane, bool update, int jp) {
+    const int c = lane & (kCholPanel - 1);
+    double a[kCholPanel];
+#pragma unroll
+    for (int i = 0; i < kCholPanel; ++i) a[i] = S[(j0 + i) * ld + j0 + c];
+    if (update) {
+#pragma unroll
+        for (int k = 0; k < kCholPanel; ++k) {
+            const double* row = S + (jp + k) * ld + j0;
+            const double2* row2 = reinterpret_cast<const double2*>(row);
+            const double rc = row[c];
+#pragma unroll
+            for (int i = 0; i < kCholPanel / 2; ++i) {
+                const double2 v = row2[i];
+                a[2 * i] = fma(-v.x, rc, a[2 * i]);
+                a[2 * i + 1] = fma(-v.y, rc, a[2 * i + 1]);
+            }
+        }
+    }
+    CHOL_MARK(8);
+    bool ok = true;
+    chol_pivot_steps<0>(a, c, lane, thresh, cs, ok);
+    __syncwarp();
+    CHOL_MARK(9);
+    if (lane < kCholPanel) {  // square roots off the pivot chain, one pivot per lane
+        const double sq = sqrt(cs.rs[lane]), is = 1.0 / sq;
+        rdiag[j0 + lane] = sq;
+        dinv[j0 + lane] = is;
+        cs.rs[lane] = is;
+    }
+    __syncwarp();
+    if (lane < kCholPanel) {
+#pragma unroll
+        for (int k = 0; k < kCholPanel; ++k) {
+            if (k < c) S[(j0 + c) * ld + j0 + k] = a[k] * cs.rs[k];  // R[k][c], transposed
+            if (k <= c) S[(j0 + k) * ld + j0 + c] = (k == c) ? 1.0 : 0.0;
+        }
+    }
+    if (lane == 0 && !ok) cs.bad = 1;
+    CHOL_MARK(10);
+}
 
 __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
     const double* __restrict__ G, long ldg, int s, int NP, double* __restrict__ R,
     double* __restrict__ RinvT, int* __restrict__ status, int* __restrict__ abort_flag,
     double tol, const double* __restrict__ Gref, long ldref, int sref, bool accumulate) {
-    extern __shared__ double S[];
-    const int ld = s | 1;
-    double* dinv = S + (size_t)s * ld;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(dinv + s);  // (r << 16 | c), c >= r, row-major
-    int* rstart = reinterpret_cast<int*>(tab + s * (s + 1) / 2);  // first table index of row r
+    extern __shared__ __align__(16) double S[];
+    const int sp = chol_pad(s), ld = sp + 2;
+    double* rdiag = S + (size_t)sp * ld;
+    double* dinv = rdiag + sp;
     __shared__ double gmax;
+    __shared__ CholShared cs;
     const int tid = threadIdx.x, nth = blockDim.x;
-    const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
-    for (int e = tid; e < s * s; e += nth) {
-        const int r = e / s, c = e % s;
-        S[r * ld + c] = (c >= r) ? G[r * ldg + c] : 0.0;
-    }
-    for (int r = tid; r <= s; r += nth) rstart[r] = r * s - r * (r - 1) / 2;
-    __syncthreads();
-    for (int r = warp; r < s; r += nw)
-        for (int c = r + lane; c < s; c += 32) tab[rstart[r] + (c - r)] = ((uint32_t)r << 16) | c;
+    const int warp = tid >> 5, lane = tid & 31;
+    constexpr unsigned kFull = 0xffffffffu;
     if (warp == 0) {  // breakdown threshold relative to the largest diagonal of Gref
         double m = 0.0;
         for (int i = lane; i < sref; i += 32) m = fmax(m, Gref[i * ldref + i]);
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) gmax = m;
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+        if (lane == 0) {
+            gmax = m;
+            cs.bad = 0;
+        }
     }
     __syncthreads();
     const double thresh = tol * gmax;
-    const int total = s * (s + 1) / 2;
-    bool broke = false;
-    for (int j = 0; j < s; ++j) {
-        const double d = S[j * ld + j];
-        if (!(d > thresh)) {  // uniform across threads; also catches NaN
-            broke = true;
-            break;
-        }
-        const double rd = 1.0 / d;
-        const double* rowj = S + j * ld;
-        for (int e = rstart[j + 1] + tid; e < total; e += nth) {
-            const uint32_t rc = tab[e];
-            const int r = rc >> 16, c = rc & 0xffff;
-            S[r * ld + c] -= (rowj[r] * rd) * rowj[c];
+    for (int e = tid; e < sp * sp; e += nth) {
+        const int r = e / sp, c = e - r * sp;
+        S[r * ld + c] = (r < s && c < s) ? (c >= r ? G[r * ldg + c] : 0.0) : (r == c ? gmax : 0.0);
+    }
+    __syncthreads();
+    CHOL_MARK(0);
+
+    // ---------------------------------------------------------------- factorisation
+    // Phase A: warp 0 updates (with panel jp's rows) and factors the diagonal block of
+    // panel j0 while warps 1.. apply panel jp's trailing update elsewhere. Phase B: the
+    // panel row block of j0 is solved column-parallel. One call site for the diagonal
+    // factor keeps its pivot loop unrolled in registers.
+    for (int j0 = 0; j0 < sp; j0 += kCholPanel) {
+        const int jp = j0 - kCholPanel;
+        if (warp == 0) {
+            chol_diag_factor(S, ld, j0, thresh, cs, rdiag, dinv, lane, jp >= 0, jp);
+        } else if (jp >= 0 && (warp & 3)) {
+            // trailing update A[j0:sp, j0:sp] -= R[jp:j0, j0:sp]^T R[jp:j0, j0:sp] (upper 4 x 4
+            // tiles) except the diagonal block (warp 0's). Warps 4, 8, 12 stay idle so warp 0
+            // has its scheduler (warp % 4) to itself: it is the critical path.
+            const int nt = (sp - j0) >> 2;
+            const int wq = warp - 1 - (warp >> 2);  // 0 .. 11 over the warps with warp % 4 != 0
+            const int nsy = (nth >> 5) * 3 / 4 * 32;
+            for (int e = wq * 32 + lane; e < nt * (nt + 1) / 2; e += nsy) {
+                int tr, tc;
+                chol_tri_index(e, nt, tr, tc);
+                if (tc < kCholPanel / 4) continue;
+                const int r = j0 + 4 * tr, cl = j0 + 4 * tc;
+                double acc[4][4] = {};
+#pragma unroll 4
+                for (int k = 0; k < kCholPanel; ++k) {
+                    const double2* pr = reinterpret_cast<const double2*>(S + (jp + k) * ld + r);
+                    const double2* pc = reinterpret_cast<const double2*>(S + (jp + k) * ld + cl);
+                    const double2 r01 = pr[0], r23 = pr[1], c01 = pc[0], c23 = pc[1];
+                    const double rv[4] = {r01.x, r01.y, r23.x, r23.y};
+                    const double cv[4] = {c01.x, c01.y, c23.x, c23.y};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(rv[i], cv[jj], acc[i][jj]);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) S[(r + i) * ld + cl + jj] -= acc[i][jj];
+            }
         }
         __syncthreads();
+        CHOL_MARK(3);
+        if (cs.bad) break;
+        const int j1 = j0 + kCholPanel;
+        if (jp >= 0)  // the previous panel's rows over this diagonal block -> I (0)
+            for (int e = tid; e < kCholPanel * kCholPanel; e += nth)
+                S[(jp + (e >> 4)) * ld + j0 + (e & 15)] = 0.0;
+        // panel row block: R[j0:j1, j1:sp] = R_dd^-T A[j0:j1, j1:sp], one column per thread;
+        // R goes to the upper rows (for the trailing update) and transposed below
+        for (int cc = j1 + tid; cc < sp; cc += nth) {
+            double x[kCholPanel];
+#pragma unroll
+            for (int i = 0; i < kCholPanel; ++i) x[i] = S[(j0 + i) * ld + cc];
+            if (jp >= 0)
+#pragma unroll
+                for (int i = 0; i < kCholPanel; ++i) S[(jp + i) * ld + cc] = 0.0;
+#pragma unroll
+            for (int k = 0; k < kCholPanel; ++k) {
+#pragma unroll
+                for (int i = k + 1; i < kCholPanel; ++i) x[i] = fma(-cs.L[k * 17 + i], x[k], x[i]);
+                asm volatile("" ::: "memory");  // one multiplier row in registers at a time
+            }
+#pragma unroll
+            for (int k = 0; k < kCholPanel; ++k) {
+                const double r = x[k] * cs.rs[k];
+                S[(j0 + k) * ld + cc] = r;
+                S[cc * ld + j0 + k] = r;
+            }
+        }
+        __syncthreads();
+        CHOL_MARK(2);
     }
-    if (broke) {
+    if (cs.bad) {
         if (tid == 0) {
             status[0] = 1;  // (accumulate: OR into a status a previous block may have set)
             if (abort_flag) atomicOr(abort_flag, 1);
         }
         return;
     }
-    // normalise: R[j][c] = a[j][c] / sqrt(a[j][j]); zero the strict lower triangle
-    for (int j = warp; j < s; j += nw) {
-        const double rs = rsqrt(S[j * ld + j]);
-        const double rjj = S[j * ld + j] * rs;  // sqrt(d)
-        for (int c = j + lane; c < s; c += 32) S[j * ld + c] = (c == j) ? rjj : S[j * ld + c] * rs;
-        for (int c = lane; c < j; c += 32) S[j * ld + c] = 0.0;
-        if (lane == 0) dinv[j] = 1.0 / rjj;
-    }
-    __syncthreads();
-    // X = R^-1, rows bottom-up: B[i][c] (c > i) lives at S[c][i]; X[i][c] = B[i][c] * dinv[i];
-    // step i subtracts R[r][i] X[i][c] from B[r][c] for every r < i <= c (an i x (s-i) block).
-    for (int i = s - 1; i > 0; --i) {
-        const double di = dinv[i];
-        const int w = s - i;
-        for (int e = tid; e < i * w; e += nth) {
-            const int r = e / w, c = i + e % w;
-            const double xic = (c == i) ? di : S[c * ld + i] * di;
-            S[c * ld + r] -= S[r * ld + i] * xic;
+
+    // ---------------------------------------------------------------- inversion
+    // upper triangle = B (I, updated) -> X = R^-1; R[m][l] (m < l) at S[l][m]
+    for (int i0 = sp - kCholPanel; i0 >= 0; i0 -= kCholPanel) {
+        for (int c = i0 + tid; c < sp; c += nth) {  // rows i0..i0+16 of X, column c
+            double b[kCholPanel];
+#pragma unroll
+            for (int l = 0; l < kCholPanel; ++l) b[l] = (c >= i0 + l) ? S[(i0 + l) * ld + c] : 0.0;
+#pragma unroll
+            for (int l = kCholPanel - 1; l >= 0; --l) {
+                b[l] *= dinv[i0 + l];
+#pragma unroll
+                for (int m = 0; m < l; ++m) b[m] = fma(-S[(i0 + l) * ld + i0 + m], b[l], b[m]);
+                asm volatile("" ::: "memory");
+            }
+#pragma unroll
+            for (int l = 0; l < kCholPanel; ++l)
+                if (c >= i0 + l) S[(i0 + l) * ld + c] = b[l];
         }
         __syncthreads();
+        CHOL_MARK(5);
+        if (i0 == 0) break;
+        // B[0:i0, i0:sp] -= R[0:i0, i0:i0+16] X[i0:i0+16, i0:sp]
+        const int nr = i0 >> 2, nc = (sp - i0) >> 2;
+        for (int e = tid; e < nr * nc; e += nth) {
+            const int tr = e / nc, tc = e - tr * nc;
+            const int r = 4 * tr, cl = i0 + 4 * tc;
+            double acc[4][4] = {};
+#pragma unroll 4
+            for (int l = 0; l < kCholPanel; ++l) {
+                const double2* pr = reinterpret_cast<const double2*>(S + (i0 + l) * ld + r);
+                const double2* px = reinterpret_cast<const double2*>(S + (i0 + l) * ld + cl);
+                const double2 r01 = pr[0], r23 = pr[1], x01 = px[0], x23 = px[1];
+                const double rv[4] = {r01.x, r01.y, r23.x, r23.y};
+                double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (cl + jj < i0 + l) xv[jj] = 0.0;  // X is upper: below it lives R^T
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(rv[i], xv[jj], acc[i][jj]);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) S[(r + i) * ld + cl + jj] -= acc[i][jj];
+        }
+        __syncthreads();
+        CHOL_MARK(6);
     }
+    // R[r][c] (c > r) and Rinv^T[r][c] = X[c][r] (c < r) both live at S[c][r]
     for (int e = tid; e < NP * NP; e += nth) {
-        const int r = e / NP, c = e % NP;
+        const int r = e / NP, c = e - r * NP;
         double rv = 0.0, xv = 0.0;
         if (r < s && c < s) {
-            if (c >= r) rv = S[r * ld + c];
-            if (c < r) xv = S[r * ld + c] * dinv[c];  // RinvT[r][c] = X[c][r], stored at S[r][c]
-            else if (c == r) xv = dinv[r];
+            const double v = S[c * ld + r];
+            if (c > r) rv = v;
+            else if (c < r) xv = v;
+            else {
+                rv = rdiag[r];
+                xv = v;
+            }
         }
         R[e] = rv;
         RinvT[e] = xv;
     }
     if (tid == 0 && !accumulate) status[0] = 0;
+    CHOL_MARK(7);
 }
 
 size_t cholesky_smem(int s) {
-    return ((size_t)s * (s | 1) + (size_t)s) * sizeof(double) +
-           ((size_t)s * (s + 1) / 2 + s + 1) * sizeof(uint32_t);
+    const size_t sp = chol_pad(s), ld = sp + 2;
+    return (sp * ld + 2 * sp) * sizeof(double);
 }
 
 int cholesky_max_width() {

@@ -1,0 +1,89 @@
+// Microbenchmark of the single-CTA small-side kernels (not part of the library):
+// per-phase clock64 trace of the Cholesky kernel and event timings.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DCHOL_TRACE \
+//        -I paper_2110_03423_b200/csrc tools/probe/small_probe.cu -o /tmp/small_probe
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+#include "../../paper_2110_03423_b200/csrc/linalg_small.cu"
+#include "../../paper_2110_03423_b200/csrc/linalg_blocked.cu"
+
+using namespace rsvdb200;
+
+int main(int argc, char** argv) {
+    const int sizes[] = {74, 136, 148};
+    for (int s : sizes) {
+        const int NP = (s + 15) / 16 * 16;
+        // SPD: G = M^T M + s I
+        std::vector<double> M(s * s), G(NP * NP, 0.0);
+        srand(1);
+        for (auto& v : M) v = rand() / (double)RAND_MAX - 0.5;
+        for (int i = 0; i < s; ++i)
+            for (int j = 0; j < s; ++j) {
+                double acc = (i == j) ? s : 0.0;
+                for (int k = 0; k < s; ++k) acc += M[k * s + i] * M[k * s + j];
+                G[i * NP + j] = acc;
+            }
+        double *dG, *dR, *dRi;
+        int* dst;
+        cudaMalloc(&dG, NP * NP * 8);
+        cudaMalloc(&dR, NP * NP * 8);
+        cudaMalloc(&dRi, NP * NP * 8);
+        cudaMalloc(&dst, 16);
+        cudaMemcpy(dG, G.data(), NP * NP * 8, cudaMemcpyHostToDevice);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        for (int it = 0; it < 3; ++it)
+            launch_cholesky(dG, NP, s, NP, dR, dRi, dst, nullptr, 1e-14, 0);
+        const int reps = 20;
+        cudaEventRecord(e0);
+        for (int it = 0; it < reps; ++it)
+            launch_cholesky(dG, NP, s, NP, dR, dRi, dst, nullptr, 1e-14, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        int zero = 0;
+        cudaMemcpyToSymbol(g_chol_ntrace, &zero, 4);
+        launch_cholesky(dG, NP, s, NP, dR, dRi, dst, nullptr, 1e-14, 0);
+        cudaDeviceSynchronize();
+        int n;
+        long long tr[256];
+        cudaMemcpyFromSymbol(&n, g_chol_ntrace, 4);
+        cudaMemcpyFromSymbol(tr, g_chol_trace, sizeof(tr));
+        // check: R^T R = G, R * RinvT^T = I
+        std::vector<double> R(NP * NP), Ri(NP * NP);
+        cudaMemcpy(R.data(), dR, NP * NP * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(Ri.data(), dRi, NP * NP * 8, cudaMemcpyDeviceToHost);
+        double e1m = 0, e2m = 0;
+        for (int i = 0; i < s; ++i)
+            for (int j = 0; j < s; ++j) {
+                double a = 0, b = 0;
+                for (int k = 0; k < s; ++k) {
+                    a += R[k * NP + i] * R[k * NP + j];
+                    b += R[i * NP + k] * Ri[j * NP + k];
+                }
+                e1m = fmax(e1m, fabs(a - G[i * NP + j]) / G[0]);
+                e2m = fmax(e2m, fabs(b - (i == j)));
+            }
+        printf("s=%d  %.2f us/launch  |RtR-G|/G00=%.2e |R Rinv - I|=%.2e\n", s, ms * 1000 / reps,
+               e1m, e2m);
+        const char* names[] = {"load", "-", "trsm", "diag+syrk", "-", "inv_diag", "inv_upd",
+                               "out", "dg_load", "dg_pivots", "dg_tail"};
+        long long prev = tr[1];
+        long long sums[16] = {};
+        for (int i = 1; i < n; ++i) {
+            sums[tr[2 * i]] += tr[2 * i + 1] - prev;
+            prev = tr[2 * i + 1];
+        }
+        for (int t = 1; t < 11; ++t) printf("   %-9s %8lld cycles\n", names[t], sums[t]);
+        printf("   total    %8lld cycles (from load end)\n", prev - tr[1]);
+        cudaFree(dG);
+        cudaFree(dR);
+        cudaFree(dRi);
+        cudaFree(dst);
+    }
+    return 0;
+}
