@@ -389,27 +389,38 @@ cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP,
 //   skip the pair (i, j) iff |d| <= 1e-14 * ||R||_F^2  and  d^2 <= (1e-13)^2 ||r_i||^2 ||r_j||^2
 // (the norms and d are recomputed from the columns for every pair). A sweep visits
 // all pairs in round-robin (tournament) order so the s/2 pairs of a round run
-// concurrently, one warp per pair; a sweep without any rotation ends the iteration
-// (svd.cpp:196-199); more than 30 sweeps is a convergence failure (svd.hpp:20).
-// Columns are stored contiguously in shared memory; the rotation accumulator J lives
-// in shared memory when both fit, else in global scratch (L2 resident).
-constexpr int kJacobiThreads = 1024;
-// widths beyond run the multi-CTA block Jacobi (linalg_blocked.cu): measured faster from
-// s ~ 64 on (C1, s = 74: 0.9 -> 0.7 ms)
-constexpr int kJacobiSmemMax = 64;
+// concurrently, one 8-lane group per pair: each lane holds NQ row pairs of both columns
+// in registers (double2 shared-memory accesses; the column stride is padded to 16 doubles
+// when it fits so every group reads whole 128-byte lines), the reduction is three
+// shuffles, and the CTA has just the warps the round needs. A sweep without any rotation
+// ends the iteration (svd.cpp:196-199); more than 30 sweeps is a convergence failure
+// (svd.hpp:20). The columns and the rotation accumulator J live in shared memory.
+constexpr int kJacobiGroup = 8;
+constexpr int kJacobiMaxNQ = 7;  // row pairs per lane: s <= 8 * 2 * 7 = 112
+// widths beyond (columns + J over 200 KB of shared memory) run the multi-CTA block Jacobi
+// (linalg_blocked.cu)
+constexpr int kJacobiSmemMax = 112;
 constexpr int kMaxSweeps = 30;
 
 __device__ __forceinline__ int rr_index(int slot, int round, int sp) {
     return slot == 0 ? 0 : 1 + (slot - 1 + round) % (sp - 1);
 }
 
-__global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
+__host__ __device__ inline int jacobi_ld(int s) {
+    const int l16 = (s + 15) & ~15;
+    return 2 * (size_t)s * l16 * sizeof(double) <= 200 * 1024 ? l16 : (s + 1) & ~1;
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(512) jacobi_kernel(
     const double* __restrict__ Rin, int s, int NP, double* __restrict__ sigma_out,
     double* __restrict__ Uout, double* __restrict__ Wout, int* __restrict__ status,
-    double* __restrict__ Jglobal, const int* __restrict__ abort_flag) {
-    extern __shared__ double sh[];
-    double* Rc = sh;                             // s columns of length s
-    double* J = Jglobal ? Jglobal : sh + s * s;  // s columns of length s
+    const int* __restrict__ abort_flag) {
+    extern __shared__ __align__(16) double sh[];
+    constexpr int G = kJacobiGroup;
+    const int ls = jacobi_ld(s);
+    double* Rc = sh;            // s columns, stride ls (rows s..ls-1 zero)
+    double* J = sh + s * ls;    // s columns, stride ls
     __shared__ double abs_thresh;
     __shared__ double norms[kJacobiSmemMax];
     __shared__ int order[kJacobiSmemMax];
@@ -432,15 +443,15 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
     }
     __syncthreads();
     const double scale = scale_sh;
-    for (int e = tid; e < s * s; e += nth) {
-        const int c = e / s, r = e % s;
-        Rc[e] = Rin[r * NP + c] * scale;
+    for (int e = tid; e < s * ls; e += nth) {
+        const int c = e / ls, r = e - c * ls;
+        Rc[e] = r < s ? Rin[r * NP + c] * scale : 0.0;
         J[e] = (r == c) ? 1.0 : 0.0;
     }
     __syncthreads();
     if (warp == 0) {
         double acc = 0.0;
-        for (int e = lane; e < s * s; e += 32) acc += Rc[e] * Rc[e];
+        for (int e = lane; e < s * ls; e += 32) acc += Rc[e] * Rc[e];
         acc = warp_sum(acc);
         if (lane == 0) abs_thresh = 1e-14 * acc;
     }
@@ -448,59 +459,60 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
     const double athr = abs_thresh;
 
     const int sp = (s + 1) & ~1;  // even number of tournament slots (slot s is a bye)
-    // one half-warp (16 lanes) per pair: 64 pairs per pass of the 1024 threads
-    const int hw = tid >> 4, hl = tid & 15, nhw = nth >> 4;
+    const int k = tid / G, gl = tid % G;  // this group's pair slot (one pass: k < sp / 2)
     int sweeps = 0;
     bool converged = false;
     while (sweeps < kMaxSweeps) {
         ++sweeps;
         int rotated = 0;
         for (int round = 0; round < sp - 1; ++round) {
-            for (int k0 = 0; k0 < sp / 2; k0 += nhw) {
-                const int k = k0 + hw;
-                int i = 0, j = 0;
-                bool live = k < sp / 2;
-                if (live) {
-                    i = rr_index(k, round, sp);
-                    j = rr_index(sp - 1 - k, round, sp);
-                    if (i > j) { const int t = i; i = j; j = t; }
-                    live = j < s;
-                }
-                double* ci = Rc + i * s;
-                double* cj = Rc + j * s;
-                double aii = 0.0, ajj = 0.0, d = 0.0;
-                if (live)
-                    for (int r = hl; r < s; r += 16) {
-                        const double x = ci[r], y = cj[r];
-                        aii = fma(x, x, aii);
-                        ajj = fma(y, y, ajj);
-                        d = fma(x, y, d);
-                    }
+            int i = 0, j = 0;
+            bool live = k < sp / 2;
+            if (live) {
+                i = rr_index(k, round, sp);
+                j = rr_index(sp - 1 - k, round, sp);
+                if (i > j) { const int t = i; i = j; j = t; }
+                live = j < s;
+            }
+            double2* ci = reinterpret_cast<double2*>(Rc + i * ls) + gl;
+            double2* cj = reinterpret_cast<double2*>(Rc + j * ls) + gl;
+            double2 xi[NQ], xj[NQ];
+            double aii = 0.0, ajj = 0.0, d = 0.0;
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) {  // xor offsets < 16 stay inside the half
-                    aii += __shfl_xor_sync(0xffffffffu, aii, o);
-                    ajj += __shfl_xor_sync(0xffffffffu, ajj, o);
-                    d += __shfl_xor_sync(0xffffffffu, d, o);
-                }
-                if (!live || (fabs(d) <= athr && d * d <= (1e-13 * 1e-13) * aii * ajj)) continue;
+            for (int q = 0; q < NQ; ++q) {
+                const bool in = live && 2 * (gl + q * G) < ls;
+                xi[q] = in ? ci[q * G] : make_double2(0.0, 0.0);
+                xj[q] = in ? cj[q * G] : make_double2(0.0, 0.0);
+                aii = fma(xi[q].x, xi[q].x, fma(xi[q].y, xi[q].y, aii));
+                ajj = fma(xj[q].x, xj[q].x, fma(xj[q].y, xj[q].y, ajj));
+                d = fma(xi[q].x, xj[q].x, fma(xi[q].y, xj[q].y, d));
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {  // xor offsets < G stay inside the group
+                aii += __shfl_xor_sync(0xffffffffu, aii, o);
+                ajj += __shfl_xor_sync(0xffffffffu, ajj, o);
+                d += __shfl_xor_sync(0xffffffffu, d, o);
+            }
+            if (live && !(fabs(d) <= athr && d * d <= (1e-13 * 1e-13) * aii * ajj)) {
                 // zeta = (ajj - aii) / (2d), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2))
                 //      = sign(zeta) 2|d| / (|ajj - aii| + sqrt((ajj - aii)^2 + 4 d^2))
                 const double diff = ajj - aii;
                 const double sgn = ((diff >= 0.0) == (d >= 0.0)) || diff == 0.0 ? 1.0 : -1.0;
-                const double t = sgn * 2.0 * fabs(d) / (fabs(diff) + sqrt(fma(diff, diff, 4.0 * d * d)));
+                const double t =
+                    sgn * 2.0 * fabs(d) / (fabs(diff) + sqrt(fma(diff, diff, 4.0 * d * d)));
                 const double c = rsqrt(fma(t, t, 1.0));
                 const double sn = c * t;
-                for (int r = hl; r < s; r += 16) {
-                    const double x = ci[r], y = cj[r];
-                    ci[r] = c * x - sn * y;
-                    cj[r] = sn * x + c * y;
-                }
-                double* ji = J + i * s;
-                double* jj = J + j * s;
-                for (int r = hl; r < s; r += 16) {
-                    const double x = ji[r], y = jj[r];
-                    ji[r] = c * x - sn * y;
-                    jj[r] = sn * x + c * y;
+                double2* wi = reinterpret_cast<double2*>(J + i * ls) + gl;
+                double2* wj = reinterpret_cast<double2*>(J + j * ls) + gl;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    if (2 * (gl + q * G) < ls) {
+                        const double2 yi = wi[q * G], yj = wj[q * G];
+                        ci[q * G] = make_double2(c * xi[q].x - sn * xj[q].x, c * xi[q].y - sn * xj[q].y);
+                        cj[q * G] = make_double2(sn * xi[q].x + c * xj[q].x, sn * xi[q].y + c * xj[q].y);
+                        wi[q * G] = make_double2(c * yi.x - sn * yj.x, c * yi.y - sn * yj.y);
+                        wj[q * G] = make_double2(sn * yi.x + c * yj.x, sn * yi.y + c * yj.y);
+                    }
                 }
                 rotated = 1;
             }
@@ -518,7 +530,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
     // singular values = column norms; stable descending order (svd.cpp:210-219)
     for (int c = warp; c < s; c += nwarps) {
         double acc = 0.0;
-        for (int r = lane; r < s; r += 32) acc += Rc[c * s + r] * Rc[c * s + r];
+        for (int r = lane; r < s; r += 32) acc += Rc[c * ls + r] * Rc[c * ls + r];
         acc = warp_sum(acc);
         if (lane == 0) norms[c] = sqrt(acc);
     }
@@ -536,8 +548,8 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
         if (r < s && cc < s) {
             const int src = order[cc];
             const double sg = norms[src];
-            u = sg > 0.0 ? Rc[src * s + r] / sg : 0.0;
-            w = J[src * s + r];
+            u = sg > 0.0 ? Rc[src * ls + r] / sg : 0.0;
+            w = J[src * ls + r];
         }
         Uout[e] = u;
         Wout[e] = w;
@@ -549,7 +561,21 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(
 size_t jacobi_max_width() { return 320; }
 
 size_t jacobi_global_scratch_doubles(int s) {
-    return block_jacobi_scratch_doubles(s);  // covers both kernels' needs
+    return block_jacobi_scratch_doubles(s);  // the block Jacobi's scratch
+}
+
+template <int NQ>
+static cudaError_t launch_jacobi_nq(const double* R, int s, int NP, double* sigma, double* U,
+                                    double* W, int* status, const int* abort_flag,
+                                    cudaStream_t st) {
+    const size_t smem = 2 * (size_t)s * jacobi_ld(s) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(jacobi_kernel<NQ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int pairs = ((s + 1) & ~1) / 2;
+    const int threads = std::max(128, (pairs * kJacobiGroup + 31) & ~31);
+    jacobi_kernel<NQ><<<1, threads, smem, st>>>(R, s, NP, sigma, U, W, status, abort_flag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U, double* W,
@@ -561,16 +587,15 @@ cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, dou
                                     : kJacobiSmemMax;
     if (s > std::min(smem_max, kJacobiSmemMax))
         return launch_block_jacobi_svd(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
-    const size_t one = (size_t)s * s * sizeof(double);
-    const bool global_j = jacobi_global_scratch_doubles(s) > 0;
-    const size_t smem = global_j ? one : 2 * one;
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e =
-        cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    jacobi_kernel<<<1, kJacobiThreads, smem, st>>>(R, s, NP, sigma, U, W, status,
-                                                   global_j ? scratch : nullptr, abort_flag);
-    return cudaGetLastError();
+    switch ((jacobi_ld(s) + 15) / 16) {  // row pairs per lane
+        case 1: return launch_jacobi_nq<1>(R, s, NP, sigma, U, W, status, abort_flag, st);
+        case 2: return launch_jacobi_nq<2>(R, s, NP, sigma, U, W, status, abort_flag, st);
+        case 3: return launch_jacobi_nq<3>(R, s, NP, sigma, U, W, status, abort_flag, st);
+        case 4: return launch_jacobi_nq<4>(R, s, NP, sigma, U, W, status, abort_flag, st);
+        case 5: return launch_jacobi_nq<5>(R, s, NP, sigma, U, W, status, abort_flag, st);
+        case 6: return launch_jacobi_nq<6>(R, s, NP, sigma, U, W, status, abort_flag, st);
+        default: return launch_jacobi_nq<7>(R, s, NP, sigma, U, W, status, abort_flag, st);
+    }
 }
 
 // ============================================================== sign convention

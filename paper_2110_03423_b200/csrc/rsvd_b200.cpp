@@ -138,6 +138,13 @@ struct StageTimer {
 struct rsvd_b200_handle {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // host-buffer solves: A is uploaded in row chunks on copy_stream and the sketch GEMM
+    // consumes each chunk as it lands (up_ev[c] recorded after chunk c)
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> up_ev;
+    cudaEvent_t up_start = nullptr;
+    long up_chunk_rows = 0, up_chunks = 0;
+    bool up_active = false;
     // workspace
     DevBuf a_copy, a_t, xt, y, q, part, b, b2, qbt, vbuf, small, flags, u_out, v_out, sig_out,
         hh_work, omega_host_dev, jscratch, cwork, ubt;
@@ -359,6 +366,35 @@ bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, con
     h->launched(launch_reduce_partials(h->part.d(), slab, splits, Y, slab, h->stream),
                 "reduce_partials");
     return false;
+}
+
+// Y = A X as gemm_ax, over row chunks of A whose upload (solve_host) is still in flight:
+// chunk c's launch waits for its copy event, so the sketch runs behind the H2D copy and
+// only the last chunk's GEMM is exposed. Chunks are whole 128/64-row tiles, so the fused
+// Gram partials line up with the unchunked launch's.
+bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long lda,
+                     const double* Xt, long ldx, int NP, double* Y, long ldy, int* flag,
+                     const char* tag, double flops, double* gram_out) {
+    const bool fuse = gram_out && NP <= 96;
+    if (fuse && h->gpart.bytes < (size_t)ax_tiles(M, NP) * NP * NP * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "Gram workspace too small");
+    long tile0 = 0;
+    h->kernel_begin(tag, flops);
+    for (long c = 0; c < h->up_chunks; ++c) {
+        const long r0 = c * h->up_chunk_rows, r1 = std::min(M, r0 + h->up_chunk_rows);
+        ck(cudaStreamWaitEvent(h->stream, h->up_ev[c], 0), "wait for chunk upload");
+        GemmAx g{A + r0 * lda, r1 - r0, K, lda, Xt, ldx, NP, Y + r0 * ldy, ldy};
+        g.flag = flag;
+        if (fuse) g.gram = h->gpart.d() + tile0 * NP * NP;
+        h->launched(launch_gemm_ax(g, h->stream), "gemm_ax(chunk)");
+        tile0 += ax_tiles(r1 - r0, NP);
+    }
+    h->kernel_end(tag);
+    if (fuse)
+        h->launched(launch_reduce_partials(h->gpart.d(), (long)NP * NP, (int)tile0, gram_out,
+                                           (long)NP * NP, h->stream),
+                    "reduce_partials");
+    return fuse;
 }
 
 // Z = A^T W.  A (K x N, lda), W (K x NP, ldw); out_t: Z^T (NP x N, ldz) else Z (N x NP, ldz).
@@ -864,6 +900,13 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
         h->gram_ready = false;
         return;
     }
+    if (h->up_active && A == h->a_copy.d() && !p.sharded) {
+        h->gram_ready = gemm_ax_chunked(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
+                                        check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
+                                        2.0 * p.m * n * s, c.slot(kG));
+        h->up_active = false;  // every chunk event has been waited on
+        return;
+    }
     h->gram_ready = gemm_ax(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                             check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
                             2.0 * p.m * n * s, c.slot(kG));
@@ -1320,6 +1363,12 @@ rsvd_b200_status rsvd_b200_destroy(rsvd_b200_handle* h) {
     if (!h) return RSVD_B200_OK;
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
+    if (h->copy_stream) {
+        cudaStreamSynchronize(h->copy_stream);
+        cudaStreamDestroy(h->copy_stream);
+    }
+    for (cudaEvent_t e : h->up_ev) cudaEventDestroy(e);
+    if (h->up_start) cudaEventDestroy(h->up_start);
     if (h->flags_host) cudaFreeHost(h->flags_host);
     cudaStreamDestroy(h->stream);
     delete h;
@@ -1406,16 +1455,67 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_device(rsvd_b200_handle* h, const dou
     });
 }
 
+// H2D of a host A (m x n) into h->a_copy (lda). Tall inputs large enough to matter go up in
+// row chunks on the copy stream (up_ev per chunk) for sketch_dev to consume as they land;
+// everything else is one copy on the solve stream.
+static void upload_a(rsvd_b200_handle* h, const double* a, long m, long n, long lda) {
+    h->a_copy.reserve((size_t)m * lda * sizeof(double));
+    const long bytes_row = lda * (long)sizeof(double);
+    const char* mb = getenv("RSVD_B200_UPLOAD_CHUNK_MB");  // tests: force small chunks
+    const long chunk_bytes = (mb && atol(mb) > 0 ? atol(mb) : 256l) << 20;
+    const long chunk_rows = round_up(std::max<long>(128, chunk_bytes / bytes_row), 128);
+    if (m < n || m < 2 * chunk_rows) {
+        ck(cudaMemcpy2DAsync(h->a_copy.p, bytes_row, a, n * sizeof(double), n * sizeof(double),
+                             m, cudaMemcpyHostToDevice, h->stream),
+           "H2D of A");
+        return;
+    }
+    if (!h->copy_stream) {
+        ck(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "stream create");
+        ck(cudaEventCreateWithFlags(&h->up_start, cudaEventDisableTiming), "event create");
+    }
+    const long chunks = (m + chunk_rows - 1) / chunk_rows;
+    while ((long)h->up_ev.size() < chunks) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+        h->up_ev.push_back(e);
+    }
+    // the copies must not overtake earlier work on the solve stream that reads a_copy
+    ck(cudaEventRecord(h->up_start, h->stream), "event record");
+    ck(cudaStreamWaitEvent(h->copy_stream, h->up_start, 0), "stream wait");
+    for (long c = 0; c < chunks; ++c) {
+        const long r0 = c * chunk_rows, rows = std::min(m - r0, chunk_rows);
+        ck(cudaMemcpy2DAsync(static_cast<double*>(h->a_copy.p) + r0 * lda, bytes_row,
+                             a + r0 * n, n * sizeof(double), n * sizeof(double), rows,
+                             cudaMemcpyHostToDevice, h->copy_stream),
+           "H2D of A");
+        ck(cudaEventRecord(h->up_ev[c], h->copy_stream), "event record");
+    }
+    h->up_chunk_rows = chunk_rows;
+    h->up_chunks = chunks;
+    h->up_active = true;
+}
+
+// Whatever path the solve took (or if it failed early), the solve stream ends up ordered
+// after the whole upload.
+struct UploadFence {
+    rsvd_b200_handle* h;
+    ~UploadFence() {
+        if (h->up_active) {
+            cudaStreamWaitEvent(h->stream, h->up_ev[h->up_chunks - 1], 0);
+            h->up_active = false;
+        }
+    }
+};
+
 static void solve_host(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                        const rsvd_b200_config* cfg, double* u, double* sigma, double* v,
                        size_t* sketch_width) {
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     h->launches = 0;
     const long lda = round_up((long)n, 2);
-    h->a_copy.reserve(m * lda * sizeof(double));
-    ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(double), a, n * sizeof(double),
-                         n * sizeof(double), m, cudaMemcpyHostToDevice, h->stream),
-       "H2D of A");
+    UploadFence fence{h};
+    upload_a(h, a, (long)m, (long)n, lda);
     const size_t k = cfg->k;
     h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
     if (u) h->u_out.reserve(std::max<size_t>(m * k, 1) * sizeof(double));

@@ -106,6 +106,22 @@ def _dp(a: np.ndarray | None):
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
 
 
+def _outputs(out, rows_u: int, n: int, k: int):
+    """Output arrays (u rows_u x k, v n x k, sigma k): fresh numpy arrays, or the caller's
+    preallocated ones (out=(u, sigma, v), C-contiguous float64 of those shapes) - e.g. views
+    of pinned host memory reused across calls, which the device-to-host copies write at full
+    PCIe speed and without first-touch page faults."""
+    if out is None:
+        return np.empty((rows_u, k)), np.empty((n, k)), np.empty(k)
+    u, s, v = out
+    for arr, shape, name in ((u, (rows_u, k), "u"), (s, (k,), "sigma"), (v, (n, k), "v")):
+        if (not isinstance(arr, np.ndarray) or arr.dtype != np.float64 or arr.shape != shape
+                or not arr.flags.c_contiguous or not arr.flags.writeable):
+            raise ArgumentError(f"out {name} must be a writeable C-contiguous float64 array of "
+                                f"shape {shape}")
+    return u, v, s
+
+
 class Solver:
     """One rsvd_b200_handle: a CUDA device, its stream and HBM workspace."""
 
@@ -182,13 +198,11 @@ class Solver:
         return int(self.lib.rsvd_b200_stream(self.h) or 0)
 
     # --------------------------------------------------------------- hot path
-    def randomized_ksvd(self, a, cfg: RsvdConfig) -> RsvdResult:
+    def randomized_ksvd(self, a, cfg: RsvdConfig, out=None) -> RsvdResult:
         a = _arr(a)
         m, n = a.shape
         k = max(int(cfg.k), 1)
-        u = np.empty((m, k))
-        v = np.empty((n, k))
-        s = np.empty(k)
+        u, v, s = _outputs(out, m, n, k)
         sw = C.c_size_t(0)
         c = cfg._c()
         _check(self.lib, self.lib.rsvd_b200_randomized_ksvd(self.h, _dp(a), m, n, C.byref(c),
@@ -252,14 +266,14 @@ class Solver:
         return out.value
 
     # ------------------------------------------------------------- FP32 input
-    def randomized_ksvd_f32(self, a, cfg: RsvdConfig) -> RsvdResult:
+    def randomized_ksvd_f32(self, a, cfg: RsvdConfig, out=None) -> RsvdResult:
         """FP32 A (host): 3xTF32 tensor-core products, FP64 outputs (BASELINE config C4)."""
         a = np.ascontiguousarray(a, dtype=np.float32)
         if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
             raise DimensionError(f"DenseMatrix requires rows >= 1 and cols >= 1, got {a.shape}")
         m, n = a.shape
         k = max(int(cfg.k), 1)
-        u, v, s = np.empty((m, k)), np.empty((n, k)), np.empty(k)
+        u, v, s = _outputs(out, m, n, k)
         sw = C.c_size_t(0)
         c = cfg._c()
         fp = a.ctypes.data_as(C.POINTER(C.c_float))
@@ -296,11 +310,12 @@ class Solver:
         return self._device_f32(self.lib.rsvd_b200_randomized_ksvd_sharded_f32_device, a_local,
                                 (m_total,), cfg, values_only)
 
-    def randomized_ksvd_sharded_f32(self, a_local, m_total: int, cfg: RsvdConfig) -> RsvdResult:
+    def randomized_ksvd_sharded_f32(self, a_local, m_total: int, cfg: RsvdConfig,
+                                    out=None) -> RsvdResult:
         a = np.ascontiguousarray(a_local, dtype=np.float32)
         ml, n = a.shape
         k = max(int(cfg.k), 1)
-        u, v, s = np.empty((ml, k)), np.empty((n, k)), np.empty(k)
+        u, v, s = _outputs(out, ml, n, k)
         sw = C.c_size_t(0)
         c = cfg._c()
         fp = a.ctypes.data_as(C.POINTER(C.c_float))
@@ -327,13 +342,14 @@ class Solver:
         self.lib.rsvd_b200_comm_info(self.h, C.byref(r), C.byref(w))
         return r.value, w.value
 
-    def randomized_ksvd_sharded(self, a_local, m_total: int, cfg: RsvdConfig) -> RsvdResult:
+    def randomized_ksvd_sharded(self, a_local, m_total: int, cfg: RsvdConfig,
+                                out=None) -> RsvdResult:
         """Collective row-sharded solve from host buffers: this rank's rows of A in, its
         rows of U and the replicated sigma, V out."""
         a = _arr(a_local)
         ml, n = a.shape
         k = max(int(cfg.k), 1)
-        u, v, s = np.empty((ml, k)), np.empty((n, k)), np.empty(k)
+        u, v, s = _outputs(out, ml, n, k)
         sw = C.c_size_t(0)
         c = cfg._c()
         _check(self.lib, self.lib.rsvd_b200_randomized_ksvd_sharded(

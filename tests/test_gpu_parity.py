@@ -356,3 +356,28 @@ def planted_like(m, n, k, seed):
     uu, _ = np.linalg.qr(rng.standard_normal((m, r)))
     vv, _ = np.linalg.qr(rng.standard_normal((n, r)))
     return (uu * np.exp(-np.arange(r) / (k / 2.0))) @ vv.T
+
+
+def test_chunked_upload_bit_identical(solver, port, monkeypatch):
+    """Host-buffer solves upload A in row chunks that the sketch GEMM consumes as they land
+    (solve_host / gemm_ax_chunked). The chunks are whole GEMM tiles, so the result is
+    bit-identical to the device-resident solve; out= buffers are filled in place."""
+    import torch
+    import paper_2110_03423_b200 as P
+    rng = np.random.default_rng(11)
+    m, n, k = 5000, 64, 8
+    a = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 12.0)
+    cfg = P.RsvdConfig(k=k, oversample=6, power_q=2, seed=5)
+    monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "1")  # 2048-row chunks: 3 of them
+    out = (np.empty((m, k)), np.empty(k), np.empty((n, k)))
+    res = solver.randomized_ksvd(a, cfg, out=out)
+    assert res.factors.u is out[0] and res.factors.sigma is out[1] and res.factors.v is out[2]
+    u_d, s_d, v_d, _ = solver.randomized_ksvd_device(torch.from_numpy(a).cuda(), cfg)
+    assert np.array_equal(res.factors.sigma, s_d.cpu().numpy())
+    assert np.array_equal(res.factors.u, u_d.cpu().numpy())
+    assert np.array_equal(res.factors.v, v_d.cpu().numpy())
+    monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "4096")  # one copy
+    res1 = solver.randomized_ksvd(a, cfg)
+    assert np.array_equal(res.factors.u, res1.factors.u)
+    with pytest.raises(P.ArgumentError):
+        solver.randomized_ksvd(a, cfg, out=(np.empty((m, k + 1)), np.empty(k), np.empty((n, k))))
