@@ -78,6 +78,38 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
         : "memory");
 }
 
+// the commit's arrive lands on the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+// TMA load broadcast into the same smem offset of every CTA in `mask` (complete_tx on the
+// barrier at the same offset in each)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c_inner, int c_outer, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c_inner), "r"(c_outer),
+        "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+
 __device__ __forceinline__ void fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -107,7 +139,11 @@ __host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
     return 2 * kABytes + 2 * b_bytes(NP, mn);
 }
 
-template <bool MN, bool OUT64, bool OUT_T>
+// PAIR: the CTA is one of a 2-CTA cluster (adjacent M tiles, same K range) that shares the
+// B operand: each CTA loads half of B and B_lo and multicasts it into both, so B's L2
+// traffic (re-read by every M tile) halves. A stage may then only be refilled once both
+// CTAs' MMAs are done with it: every MMA commit arrives on the empty barrier of both.
+template <bool MN, bool OUT64, bool OUT_T, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB,
@@ -136,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&conv[s], 4);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], PAIR ? 2 : 1);
         }
         mbar_init(accum, 1);
         fence_barrier_init();
@@ -148,9 +184,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fence_before();
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync();  // the peer's multicasts may target our barriers from here on
+    else
+        __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t crank = PAIR ? cluster_rank() : 0;
 
     // stage layout: A raw | A lo | B raw | B lo
     if (warp == 0) {
@@ -167,21 +207,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int k = (kt0 + it) * BK;
                 mbar_arrive_expect_tx(&full[s], kABytes + 2 * bB);
                 if constexpr (!MN) {
-                    const int parts = NP > 256 ? 2 : 1;
-                    const int rows = NP / parts;
                     tma_load_2d(st, &mapA, &full[s], k, m0);
-                    for (int p = 0; p < parts; ++p) {
-                        tma_load_2d(sb + p * rows * (BK * 4), &mapB, &full[s], k, p * rows);
-                        tma_load_2d(sb + bB + p * rows * (BK * 4), &mapBlo, &full[s], k, p * rows);
+                    if constexpr (PAIR) {  // rows [crank NP/2, (crank + 1) NP/2) of B, to both
+                        const int rows = NP / 2, r0 = (int)crank * rows;
+                        tma_load_2d_mc(sb + r0 * (BK * 4), &mapB, &full[s], k, r0, 3);
+                        tma_load_2d_mc(sb + bB + r0 * (BK * 4), &mapBlo, &full[s], k, r0, 3);
+                    } else {
+                        const int parts = NP > 256 ? 2 : 1;
+                        const int rows = NP / parts;
+                        for (int p = 0; p < parts; ++p) {
+                            tma_load_2d(sb + p * rows * (BK * 4), &mapB, &full[s], k, p * rows);
+                            tma_load_2d(sb + bB + p * rows * (BK * 4), &mapBlo, &full[s], k,
+                                        p * rows);
+                        }
                     }
                 } else {
                     const int nb = (NP + 31) / 32;
 #pragma unroll
                     for (int i = 0; i < BM / 32; ++i)
                         tma_load_2d(st + i * kBoxMN, &mapA, &full[s], m0 + 32 * i, k);
-                    for (int j = 0; j < nb; ++j) {
-                        tma_load_2d(sb + j * kBoxMN, &mapB, &full[s], 32 * j, k);
-                        tma_load_2d(sb + bB + j * kBoxMN, &mapBlo, &full[s], 32 * j, k);
+                    if constexpr (PAIR) {  // every other 32-wide box of B, to both
+                        for (int j = (int)crank; j < nb; j += 2) {
+                            tma_load_2d_mc(sb + j * kBoxMN, &mapB, &full[s], 32 * j, k, 3);
+                            tma_load_2d_mc(sb + bB + j * kBoxMN, &mapBlo, &full[s], 32 * j, k, 3);
+                        }
+                    } else {
+                        for (int j = 0; j < nb; ++j) {
+                            tma_load_2d(sb + j * kBoxMN, &mapB, &full[s], 32 * j, k);
+                            tma_load_2d(sb + bB + j * kBoxMN, &mapBlo, &full[s], 32 * j, k);
+                        }
                     }
                 }
             }
@@ -216,7 +270,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&conv[s], (it / kStages) & 1);
                 fence_after();
                 issue(a_lo, b_raw, 1u);                 // a_lo b_hi
-                commit(&empty[s]);
+                if constexpr (PAIR)
+                    commit_mc(&empty[s], 3);
+                else
+                    commit(&empty[s]);
             }
             if (n_iter > 0) commit(accum);
         }
@@ -296,7 +353,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     fence_before();
-    __syncthreads();
+    // PAIR: the peer's last commits arrive on our empty barriers; they precede its accum
+    // commit, which its epilogue waited for before this barrier
+    if constexpr (PAIR)
+        cluster_sync();
+    else
+        __syncthreads();
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -343,21 +405,42 @@ int map_f32(CUtensorMap* map, const float* base, long rows, long cols, long ld, 
     return r == CUDA_SUCCESS ? 0 : -3;
 }
 
-template <bool MN, bool OUT64, bool OUT_T>
+template <bool MN, bool OUT64, bool OUT_T, bool PAIR>
 cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
                      const CUtensorMap& mBlo, cudaStream_t st) {
     const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN) + 16 * 8 + 16 + 1024;
-    auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T>;
+    auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T, PAIR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int k_tiles = (int)((p.K + tf32::BK - 1) / tf32::BK);
     const int splits = p.splits < 1 ? 1 : p.splits;
     const int per = (k_tiles + splits - 1) / splits;
-    dim3 grid((unsigned)((p.M + tf32::BM - 1) / tf32::BM), (unsigned)splits);
-    kern<<<grid, tf32::kThreads, smem, st>>>(mA, mB, mBlo, p.out, static_cast<float*>(p.out_lo),
-                                             p.ldo, p.split_stride, (int)p.M, p.NP, k_tiles, per,
-                                             p.flag);
+    unsigned gx = (unsigned)((p.M + tf32::BM - 1) / tf32::BM);
+    if (PAIR) gx = (gx + 1) & ~1u;  // the odd tile's partner only reads zeros past M
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gx, (unsigned)splits);
+    cfg.blockDim = dim3(tf32::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, mA, mB, mBlo, p.out, static_cast<float*>(p.out_lo), p.ldo,
+                           p.split_stride, (int)p.M, p.NP, k_tiles, per, p.flag);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+template <bool MN, bool OUT64, bool OUT_T>
+cudaError_t launch_p(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
+                     const CUtensorMap& mBlo, cudaStream_t st) {
+    static const bool pair = !getenv("RSVD_B200_TF32_NO_PAIR");
+    if (pair && p.M > tf32::BM) return launch_t<MN, OUT64, OUT_T, true>(p, mA, mB, mBlo, st);
+    return launch_t<MN, OUT64, OUT_T, false>(p, mA, mB, mBlo, st);
 }
 
 }  // namespace
@@ -368,7 +451,11 @@ cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
     if (p.out_lo && (p.out64 || p.out_t)) return cudaErrorInvalidValue;
     CUtensorMap mA, mB, mBlo;
     if (!p.mn) {  // A: M x K (lda), Bt: NP x K (ldb); 64-byte rows of K
-        const int brows = p.NP > 256 ? p.NP / 2 : p.NP;
+        // one box per B half: the paired kernel loads NP / 2 rows per CTA, the single one
+        // NP (<= 256) or two halves
+        const int brows = (p.NP > 256 || (p.M > tf32::BM && !getenv("RSVD_B200_TF32_NO_PAIR")))
+                              ? p.NP / 2
+                              : p.NP;
         const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
         if (map_f32(&mA, p.A, p.M, p.K, p.lda, tf32::BK, tf32::BM, sw) ||
             map_f32(&mB, p.B, p.NP, p.K, p.ldb, tf32::BK, brows, sw) ||
@@ -382,15 +469,15 @@ cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
             return cudaErrorInvalidValue;
     }
     if (!p.mn) {
-        if (p.out64) return p.out_t ? launch_t<false, true, true>(p, mA, mB, mBlo, st)
-                                    : launch_t<false, true, false>(p, mA, mB, mBlo, st);
-        return p.out_t ? launch_t<false, false, true>(p, mA, mB, mBlo, st)
-                       : launch_t<false, false, false>(p, mA, mB, mBlo, st);
+        if (p.out64) return p.out_t ? launch_p<false, true, true>(p, mA, mB, mBlo, st)
+                                    : launch_p<false, true, false>(p, mA, mB, mBlo, st);
+        return p.out_t ? launch_p<false, false, true>(p, mA, mB, mBlo, st)
+                       : launch_p<false, false, false>(p, mA, mB, mBlo, st);
     }
-    if (p.out64) return p.out_t ? launch_t<true, true, true>(p, mA, mB, mBlo, st)
-                                : launch_t<true, true, false>(p, mA, mB, mBlo, st);
-    return p.out_t ? launch_t<true, false, true>(p, mA, mB, mBlo, st)
-                   : launch_t<true, false, false>(p, mA, mB, mBlo, st);
+    if (p.out64) return p.out_t ? launch_p<true, true, true>(p, mA, mB, mBlo, st)
+                                : launch_p<true, true, false>(p, mA, mB, mBlo, st);
+    return p.out_t ? launch_p<true, false, true>(p, mA, mB, mBlo, st)
+                   : launch_p<true, false, false>(p, mA, mB, mBlo, st);
 }
 
 // ------------------------------------------------------------ conversions

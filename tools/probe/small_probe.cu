@@ -55,11 +55,12 @@ static std::vector<double> graded_r(int s, double tau) {
     return R;
 }
 
-static void jacobi_probe(int s) {
+static void jacobi_probe(int s, bool transposed) {
     const int NP = (s + 15) / 16 * 16;
+    srand(7);
     std::vector<double> R = graded_r(s, s / 8.0), Rp(NP * NP, 0.0);
     for (int i = 0; i < s; ++i)
-        for (int j = 0; j < s; ++j) Rp[i * NP + j] = R[i * s + j];
+        for (int j = 0; j < s; ++j) Rp[i * NP + j] = transposed ? R[j * s + i] : R[i * s + j];
     double *dR, *sig, *U, *W, *scr;
     int* st;
     cudaMalloc(&dR, NP * NP * 8);
@@ -87,13 +88,54 @@ static void jacobi_probe(int s) {
     double err = 0;
     for (int i = 0; i < s; ++i) err = fmax(err, fabs(sg[i] - exp(-i / (s / 8.0))) / exp(-i / (s / 8.0)));
     const int rounds = ((s + 1) & ~1) - 1;
-    printf("jacobi s=%d: %.1f us, %d sweeps, %.0f cycles/round (at 1.9 GHz), max rel sigma err %.1e\n",
-           s, ms * 1000 / reps, sweeps, ms * 1e-3 / reps * 1.9e9 / (sweeps * rounds), err);
+#ifdef JAC_TRACE
+    if (s <= 112) {
+        int zero = 0, nt = 0;
+        long long tr[1024];
+        cudaMemcpyToSymbol(g_jac_ntrace, &zero, 4);
+        launch_jacobi_svd(dR, s, NP, sig, U, W, st, scr, nullptr, 0);
+        cudaDeviceSynchronize();
+        cudaMemcpyFromSymbol(&nt, g_jac_ntrace, 4);
+        cudaMemcpyFromSymbol(tr, g_jac_trace, sizeof(tr));
+        long long sums[8] = {}, cnt[8] = {};
+        for (int i = 1; i < nt; ++i) {
+            sums[tr[2 * i]] += tr[2 * i + 1] - tr[2 * i - 1];
+            cnt[tr[2 * i]] += 1;
+        }
+        const char* nm[] = {"sync->next", "load+dots", "shuffles", "rotation", "update"};
+        for (int t = 0; t < 5; ++t)
+            if (cnt[t]) printf("   %-12s %8lld cycles avg over %lld\n", nm[t], sums[t] / cnt[t], cnt[t]);
+    }
+#endif
+#ifdef BJ_TRACE
+    {
+        int zero = 0, nt = 0;
+        long long tr[512];
+        cudaMemcpyToSymbol(g_bj_ntrace, &zero, 4);
+        launch_jacobi_svd(dR, s, NP, sig, U, W, st, scr, nullptr, 0);
+        cudaDeviceSynchronize();
+        cudaMemcpyFromSymbol(&nt, g_bj_ntrace, 4);
+        cudaMemcpyFromSymbol(tr, g_bj_trace, sizeof(tr));
+        long long sums[8] = {}, cnt[8] = {};
+        for (int i = 1; i < nt; ++i) {
+            sums[tr[2 * i]] += tr[2 * i + 1] - tr[2 * i - 1];
+            cnt[tr[2 * i]] += 1;
+        }
+        const char* nm[] = {"sync->setup", "load", "inner", "store+or", "grid.sync"};
+        for (int t = 0; t < 5; ++t)
+            if (cnt[t]) printf("   %-12s %8lld cycles avg over %lld\n", nm[t], sums[t] / cnt[t], cnt[t]);
+    }
+#endif
+    printf("jacobi%s s=%d: %.1f us, %d sweeps, %.0f cycles/round (at 1.9 GHz), max rel sigma err %.1e\n",
+           transposed ? "(R^T)" : "", s, ms * 1000 / reps, sweeps, ms * 1e-3 / reps * 1.9e9 / (sweeps * rounds), err);
 }
 
 int main(int argc, char** argv) {
     if (argc > 1) {
-        for (int i = 1; i < argc; ++i) jacobi_probe(atoi(argv[i]));
+        for (int i = 1; i < argc; ++i) {
+            jacobi_probe(atoi(argv[i]), false);
+            jacobi_probe(atoi(argv[i]), true);
+        }
         return 0;
     }
     const int sizes[] = {74, 136, 148};
