@@ -84,20 +84,24 @@ __device__ __forceinline__ int bj_rr(int slot, int round, int sp) {
     return slot == 0 ? 0 : 1 + (slot - 1 + round) % (sp - 1);
 }
 
-// scratch: Rc (s*s, column c at Rc + c*s), J (s*s), sweep flags (32 ints), norms (s)
+__host__ __device__ inline int bj_ld(int s) { return (s + 1) & ~1; }  // column stride
+
+// scratch: Rc (s columns, stride bj_ld(s)), J (same), sweep flags (32 ints), norms (s)
+template <int NQ>
 __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
     const double* __restrict__ Rin, int s, int NP, double* __restrict__ sigma_out,
     double* __restrict__ Uout, double* __restrict__ Wout, int* __restrict__ status,
     double* __restrict__ scratch, const int* __restrict__ abort_flag) {
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ double sh[];
+    extern __shared__ __align__(16) double sh[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nb = (s + kBJW - 1) / kBJW;
     const int sp = (nb + 1) & ~1;
+    const int ls = bj_ld(s), l2 = ls / 2;  // column stride in doubles / double2
     double* Rc = scratch;
-    double* J = Rc + (size_t)s * s;
-    int* sweep_flag = reinterpret_cast<int*>(J + (size_t)s * s);
-    double* norms = J + (size_t)s * s + 16;
+    double* J = Rc + (size_t)s * ls;
+    int* sweep_flag = reinterpret_cast<int*>(J + (size_t)s * ls);
+    double* norms = J + (size_t)s * ls + 16;
     __shared__ double red[32];
     __shared__ double scale_sh, athr_sh;
     __shared__ int order_sh[320];
@@ -139,17 +143,19 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
         __syncthreads();
     }
     const double scale = scale_sh, athr = athr_sh;
-    for (long e = blockIdx.x * (long)kBJThreads + tid; e < (long)s * s;
+    for (long e = blockIdx.x * (long)kBJThreads + tid; e < (long)s * ls;
          e += (long)gridDim.x * kBJThreads) {
-        const int c = (int)(e / s), r = (int)(e % s);
-        Rc[e] = Rin[(long)r * NP + c] * scale;
+        const int c = (int)(e / ls), r = (int)(e % ls);
+        Rc[e] = r < s ? Rin[(long)r * NP + c] * scale : 0.0;
         J[e] = (r == c) ? 1.0 : 0.0;
     }
     if (blockIdx.x == 0 && tid < 32) sweep_flag[tid] = 0;
     grid.sync();
 
-    double* C = sh;                      // 2*kBJW columns of length s
-    double* Jl = sh + 2 * kBJW * s;      // their rotation accumulators
+    double2* C = reinterpret_cast<double2*>(sh);          // 2*kBJW columns, stride l2
+    double2* Jl = C + 2 * kBJW * l2;                       // their rotation accumulators
+    const double2* Rc2 = reinterpret_cast<const double2*>(Rc);
+    const double2* J2 = reinterpret_cast<const double2*>(J);
     __shared__ int cols[2 * kBJW];
     int sweeps = 0;
     bool converged = false;
@@ -174,10 +180,26 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
             __syncthreads();
             int rotated = 0;
             if (cnt > 0) {
-                for (int e = tid; e < cnt * s; e += kBJThreads) {
-                    const int l = e / s, r = e % s;
-                    C[e] = Rc[(long)cols[l] * s + r];
-                    Jl[e] = J[(long)cols[l] * s + r];
+                // columns in: several double2 loads in flight per thread (L2 latency)
+                for (int e0 = tid; e0 < cnt * l2; e0 += 4 * kBJThreads) {
+                    double2 vc[4], vj[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u * kBJThreads;
+                        if (e < cnt * l2) {
+                            const int l = e / l2, r = e - l * l2;
+                            vc[u] = Rc2[(long)cols[l] * l2 + r];
+                            vj[u] = J2[(long)cols[l] * l2 + r];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u * kBJThreads;
+                        if (e < cnt * l2) {
+                            C[e] = vc[u];
+                            Jl[e] = vj[u];
+                        }
+                    }
                 }
                 __syncthreads();
                 const int spl = (cnt + 1) & ~1;
@@ -191,19 +213,26 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
                         if (i > j) { const int t = i; i = j; j = t; }
                         live = j < cnt;
                     }
-                    if (live) {
-                        double* ci = C + i * s;
-                        double* cj = C + j * s;
+                    if (live) {  // warp-uniform
+                        double2* ci = C + i * l2;
+                        double2* cj = C + j * l2;
+                        double2 xi[NQ], xj[NQ];
                         double aii = 0.0, ajj = 0.0, d = 0.0;
-                        for (int r = lane; r < s; r += 32) {
-                            const double x = ci[r], y = cj[r];
-                            aii = fma(x, x, aii);
-                            ajj = fma(y, y, ajj);
-                            d = fma(x, y, d);
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q) {
+                            const int r = lane + 32 * q;
+                            xi[q] = r < l2 ? ci[r] : make_double2(0.0, 0.0);
+                            xj[q] = r < l2 ? cj[r] : make_double2(0.0, 0.0);
+                            aii = fma(xi[q].x, xi[q].x, fma(xi[q].y, xi[q].y, aii));
+                            ajj = fma(xj[q].x, xj[q].x, fma(xj[q].y, xj[q].y, ajj));
+                            d = fma(xi[q].x, xj[q].x, fma(xi[q].y, xj[q].y, d));
                         }
-                        aii = warp_sum(aii);
-                        ajj = warp_sum(ajj);
-                        d = warp_sum(d);
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            aii += __shfl_xor_sync(0xffffffffu, aii, o);
+                            ajj += __shfl_xor_sync(0xffffffffu, ajj, o);
+                            d += __shfl_xor_sync(0xffffffffu, d, o);
+                        }
                         if (!(fabs(d) <= athr && d * d <= (1e-13 * 1e-13) * aii * ajj)) {
                             const double diff = ajj - aii;
                             const double sgn =
@@ -212,27 +241,32 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
                                              (fabs(diff) + sqrt(fma(diff, diff, 4.0 * d * d)));
                             const double c = rsqrt(fma(t, t, 1.0));
                             const double sn = c * t;
-                            for (int r = lane; r < s; r += 32) {
-                                const double x = ci[r], y = cj[r];
-                                ci[r] = c * x - sn * y;
-                                cj[r] = sn * x + c * y;
-                            }
-                            double* ji = Jl + i * s;
-                            double* jj = Jl + j * s;
-                            for (int r = lane; r < s; r += 32) {
-                                const double x = ji[r], y = jj[r];
-                                ji[r] = c * x - sn * y;
-                                jj[r] = sn * x + c * y;
+                            double2* wi = Jl + i * l2;
+                            double2* wj = Jl + j * l2;
+#pragma unroll
+                            for (int q = 0; q < NQ; ++q) {
+                                const int r = lane + 32 * q;
+                                if (r < l2) {
+                                    const double2 yi = wi[r], yj = wj[r];
+                                    ci[r] = make_double2(c * xi[q].x - sn * xj[q].x,
+                                                         c * xi[q].y - sn * xj[q].y);
+                                    cj[r] = make_double2(sn * xi[q].x + c * xj[q].x,
+                                                         sn * xi[q].y + c * xj[q].y);
+                                    wi[r] = make_double2(c * yi.x - sn * yj.x, c * yi.y - sn * yj.y);
+                                    wj[r] = make_double2(sn * yi.x + c * yj.x, sn * yi.y + c * yj.y);
+                                }
                             }
                             rotated = 1;
                         }
                     }
                     __syncthreads();
                 }
-                for (int e = tid; e < cnt * s; e += kBJThreads) {
-                    const int l = e / s, r = e % s;
-                    Rc[(long)cols[l] * s + r] = C[e];
-                    J[(long)cols[l] * s + r] = Jl[e];
+                double2* Rcw = reinterpret_cast<double2*>(Rc);
+                double2* Jw = reinterpret_cast<double2*>(J);
+                for (int e = tid; e < cnt * l2; e += kBJThreads) {
+                    const int l = e / l2, r = e - l * l2;
+                    Rcw[(long)cols[l] * l2 + r] = C[e];
+                    Jw[(long)cols[l] * l2 + r] = Jl[e];
                 }
             }
             if (__syncthreads_or(rotated) && tid == 0) atomicOr(&sweep_flag[sweeps - 1], 1);
@@ -250,7 +284,7 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
     // column norms (grid-stride), then every CTA derives the same stable descending order
     for (int c = blockIdx.x * (kBJThreads / 32) + warp; c < s; c += gridDim.x * (kBJThreads / 32)) {
         double acc = 0.0;
-        for (int r = lane; r < s; r += 32) acc = fma(Rc[(long)c * s + r], Rc[(long)c * s + r], acc);
+        for (int r = lane; r < s; r += 32) acc = fma(Rc[(long)c * ls + r], Rc[(long)c * ls + r], acc);
         acc = warp_sum(acc);
         if (lane == 0) norms[c] = sqrt(acc);
     }
@@ -272,8 +306,8 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
         if (r < s && cc < s) {
             const int src = order_sh[cc];
             const double sg = norms[src];
-            u = sg > 0.0 ? Rc[(long)src * s + r] / sg : 0.0;
-            w = J[(long)src * s + r];
+            u = sg > 0.0 ? Rc[(long)src * ls + r] / sg : 0.0;
+            w = J[(long)src * ls + r];
         }
         Uout[e] = u;
         Wout[e] = w;
@@ -285,24 +319,39 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
     }
 }
 
-size_t block_jacobi_scratch_doubles(int s) { return 2 * (size_t)s * s + 16 + (size_t)s + 16; }
+size_t block_jacobi_scratch_doubles(int s) {
+    return 2 * (size_t)s * bj_ld(s) + 16 + (size_t)s + 16;
+}
 
-cudaError_t launch_block_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U,
-                                    double* W, int* status, double* scratch,
-                                    const int* abort_flag, cudaStream_t st) {
-    if (s > 320) return cudaErrorInvalidValue;
-    const size_t smem = 2 * (size_t)(2 * kBJW) * s * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(block_jacobi_kernel,
+template <int NQ>
+static cudaError_t launch_bj(const double* R, int s, int NP, double* sigma, double* U, double* W,
+                             int* status, double* scratch, const int* abort_flag, cudaStream_t st) {
+    const size_t smem = 2 * (size_t)(2 * kBJW) * bj_ld(s) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(block_jacobi_kernel<NQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nb = (s + kBJW - 1) / kBJW;
     const int sp = (nb + 1) & ~1;
     void* args[] = {(void*)&R, (void*)&s, (void*)&NP, (void*)&sigma, (void*)&U, (void*)&W,
                     (void*)&status, (void*)&scratch, (void*)&abort_flag};
-    e = cudaLaunchCooperativeKernel((void*)block_jacobi_kernel, dim3(sp / 2), dim3(kBJThreads),
+    e = cudaLaunchCooperativeKernel((void*)block_jacobi_kernel<NQ>, dim3(sp / 2), dim3(kBJThreads),
                                     args, smem, st);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+cudaError_t launch_block_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U,
+                                    double* W, int* status, double* scratch,
+                                    const int* abort_flag, cudaStream_t st) {
+    if (s > 320) return cudaErrorInvalidValue;
+    // row pairs per lane (one warp per column pair)
+    switch ((bj_ld(s) / 2 + 31) / 32) {
+        case 1: return launch_bj<1>(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
+        case 2: return launch_bj<2>(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
+        case 3: return launch_bj<3>(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
+        case 4: return launch_bj<4>(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
+        default: return launch_bj<5>(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
+    }
 }
 
 }  // namespace rsvdb200

@@ -171,14 +171,16 @@ int main(int argc, char** argv) {
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
+        int n = 0;
+        long long tr[256] = {};
+#ifdef CHOL_TRACE
         int zero = 0;
         cudaMemcpyToSymbol(g_chol_ntrace, &zero, 4);
         launch_cholesky(dG, NP, s, NP, dR, dRi, dst, nullptr, 1e-14, 0);
         cudaDeviceSynchronize();
-        int n;
-        long long tr[256];
         cudaMemcpyFromSymbol(&n, g_chol_ntrace, 4);
         cudaMemcpyFromSymbol(tr, g_chol_trace, sizeof(tr));
+#endif
         // check: R^T R = G, R * RinvT^T = I
         std::vector<double> R(NP * NP), Ri(NP * NP);
         cudaMemcpy(R.data(), dR, NP * NP * 8, cudaMemcpyDeviceToHost);
