@@ -93,7 +93,20 @@ int pad_np(long s) {
 // Split-K count so that tiles * splits fills whole waves of 148 SMs, with at least two
 // k-tiles (of 32) per split.
 int choose_splits(long tiles, long k_tiles) {
-    if (tiles >= 2 * 148 || k_tiles <= 1) return 1;
+    if (k_tiles <= 1) return 1;
+    if (tiles >= 2 * 148) {
+        // many tiles: split only to fix a ragged last wave (C5: 512 tiles = 3.46 waves, 86 %
+        // busy; 2 splits = 6.92 waves, 99 %); the slabs cost one extra pass over M x NP
+        auto eff = [](long ctas) { return (double)ctas / (148.0 * ((ctas + 147) / 148)); };
+        int best = 1;
+        double best_eff = eff(tiles);
+        for (int sp = 2; sp <= 4 && sp <= k_tiles / 64; ++sp)
+            if (eff(sp * tiles) > best_eff + 0.03) {
+                best_eff = eff(sp * tiles);
+                best = sp;
+            }
+        return best;
+    }
     const long cap = std::max(1L, k_tiles / 2);
     int best = 1;
     double best_eff = 0.0;
