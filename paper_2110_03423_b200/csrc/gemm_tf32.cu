@@ -139,6 +139,57 @@ __host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
     return 2 * kABytes + 2 * b_bytes(NP, mn);
 }
 
+// Drain the 128 x NP FP32 accumulator (warps 2-5: each its TMEM lane quarter) and store it
+// (FP32 + lo parts, FP64, or transposed), slab blockIdx.y of a split-K launch.
+template <bool OUT64, bool OUT_T>
+__device__ __forceinline__ void epilogue(uint32_t tmem, int warp, int lane, int m0, int M, int NP,
+                                         bool have, void* __restrict__ out,
+                                         float* __restrict__ out_lo, long ldo, long split_stride) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = m0 + 32 * q + lane;
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+    char* ob = reinterpret_cast<char*>(out) + (size_t)blockIdx.y * split_stride * (OUT64 ? 8 : 4);
+    for (int c0 = 0; c0 < NP; c0 += 16) {
+        float v[16];
+        if (have) {
+            tmem_ld16(trow + c0, v);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (row < M) {
+            if constexpr (OUT_T) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const size_t o = (size_t)(c0 + i) * ldo + row;
+                    if constexpr (OUT64)
+                        reinterpret_cast<double*>(ob)[o] = (double)v[i];
+                    else
+                        reinterpret_cast<float*>(ob)[o] = v[i];
+                }
+            } else if constexpr (OUT64) {
+                double2* d = reinterpret_cast<double2*>(reinterpret_cast<double*>(ob) +
+                                                        (size_t)row * ldo + c0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) d[i] = make_double2(v[2 * i], v[2 * i + 1]);
+            } else {
+                float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(ob) +
+                                                      (size_t)row * ldo + c0);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                if (out_lo) {  // lo parts for the next product that reads this as B
+                    float4* dl = reinterpret_cast<float4*>(out_lo + (size_t)row * ldo + c0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        dl[i] = make_float4(lo_part(v[4 * i]), lo_part(v[4 * i + 1]),
+                                            lo_part(v[4 * i + 2]), lo_part(v[4 * i + 3]));
+                }
+            }
+        }
+    }
+}
+
 // PAIR: the CTA is one of a 2-CTA cluster (adjacent M tiles, same K range) that shares the
 // B operand: each CTA loads half of B and B_lo and multicasts it into both, so B's L2
 // traffic (re-read by every M tile) halves. A stage may then only be refilled once both
@@ -245,9 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             const uint32_t lbo = MN ? kBoxMN : 16u, sbo = 512u;
             const uint64_t lay = MN ? 1u : 4u;
-            const int n1 = NP > 256 ? 256 : NP, n2 = NP - n1;
+            // N > 256 is two MMAs of balanced width (272 = 160 + 112): a narrow second chunk
+            // (256 + 16) costs nearly as much as a wide one (measured: NP 272 took 1.45x NP 256)
+            const int n1 = NP > 256 ? ((NP / 2 + 31) & ~31) : NP, n2 = NP - n1;
             const uint32_t id1 = idesc(n1, MN), id2 = n2 > 0 ? idesc(n2, MN) : 0u;
-            const uint32_t co = 256u * (MN ? kBoxMN / 32u : BK * 4u);  // B offset of column 256
+            const uint32_t co = (uint32_t)n1 * (MN ? kBoxMN / 32u : BK * 4u);  // B offset of chunk 2
             auto issue = [&](uint32_t a, uint32_t b, uint32_t acc0) {
 #pragma unroll
                 for (int ks = 0; ks < BK / 8; ++ks) {
@@ -255,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t ad = sdesc(a + ko, lbo, sbo, lay);
                     const uint32_t acc = (ks == 0) ? acc0 : 1u;
                     mma(tmem, ad, sdesc(b + ko, lbo, sbo, lay), id1, acc);
-                    if (n2 > 0) mma(tmem + 256, ad, sdesc(b + co + ko, lbo, sbo, lay), id2, acc);
+                    if (n2 > 0)
+                        mma(tmem + (uint32_t)n1, ad, sdesc(b + co + ko, lbo, sbo, lay), id2, acc);
                 }
             };
             for (int it = 0; it < n_iter; ++it) {
@@ -304,53 +358,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 
         // ------------------------------------------------------------ epilogue
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int row = m0 + 32 * q + lane;
-        const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
         if (n_iter > 0) {
             mbar_wait(accum, 0);
             fence_after();
         }
-        char* ob = reinterpret_cast<char*>(out) + (size_t)blockIdx.y * split_stride * (OUT64 ? 8 : 4);
-        for (int c0 = 0; c0 < NP; c0 += 16) {
-            float v[16];
-            if (n_iter > 0) {
-                tmem_ld16(trow + c0, v);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = 0.f;
-            }
-            if (row < M) {
-                if constexpr (OUT_T) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const size_t o = (size_t)(c0 + i) * ldo + row;
-                        if constexpr (OUT64)
-                            reinterpret_cast<double*>(ob)[o] = (double)v[i];
-                        else
-                            reinterpret_cast<float*>(ob)[o] = v[i];
-                    }
-                } else if constexpr (OUT64) {
-                    double2* d = reinterpret_cast<double2*>(reinterpret_cast<double*>(ob) +
-                                                            (size_t)row * ldo + c0);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) d[i] = make_double2(v[2 * i], v[2 * i + 1]);
-                } else {
-                    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(ob) +
-                                                          (size_t)row * ldo + c0);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                    if (out_lo) {  // lo parts for the next product that reads this as B
-                        float4* dl = reinterpret_cast<float4*>(out_lo + (size_t)row * ldo + c0);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dl[i] = make_float4(lo_part(v[4 * i]), lo_part(v[4 * i + 1]),
-                                                lo_part(v[4 * i + 2]), lo_part(v[4 * i + 3]));
-                    }
-                }
-            }
-        }
+        epilogue<OUT64, OUT_T>(tmem, warp, lane, m0, M, NP, n_iter > 0, out, out_lo, ldo,
+                               split_stride);
     }
     fence_before();
     // PAIR: the peer's last commits arrive on our empty barriers; they precede its accum
@@ -362,6 +375,227 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(tmem_cols));
+    }
+}
+
+}  // namespace tf32
+
+
+// ----------------------------------------------------------------------------------------
+// 2-SM variant of the K-major (ax) shape: a CTA pair runs tcgen05.mma.cta_group::2 with
+// M = 256 (each CTA's 128 rows of A in its own shared memory, its own 128 x NP accumulator in
+// its own TMEM) and each CTA holds only its half of every N chunk of B and B_lo. The tensor
+// cores of the pair share the B halves, so per CTA a stage is 8 KB A + 8 KB A_lo + NP x 64 B of
+// B/B_lo halves (33 KB at NP = 272, against 50 KB single-CTA): the kernel is bound by shared-
+// memory traffic (TMA writes + UMMA operand reads), which drops by a third, and six stages fit.
+//   full[s]  (leader)  B halves of both CTAs landed (each CTA's TMA signals the leader's barrier)
+//   afull[s] (each)    this CTA's A tile landed (for its converter warps)
+//   conv[s]  (leader)  A_lo of both CTAs written (8 converter-warp arrivals, 4 remote)
+//   empty[s] (each)    the leader's MMAs of stage s are done (commit multicast to both)
+//   accum    (each)    the last MMA is done (commit multicast)
+namespace tf32 {
+
+constexpr int kStages2 = 6;
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr)
+                 : "memory");
+}
+
+// TMA load into this CTA's smem, completion signalled on an mbarrier that may live in the
+// peer CTA of the pair (cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c_inner, int c_outer) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c_inner), "r"(c_outer)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void commit2_mc(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+// M = 256 kind::tf32 descriptor (K-major operands)
+__device__ __forceinline__ uint32_t idesc2(int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+__host__ __device__ __forceinline__ uint32_t stage_bytes2(int NP) {
+    return 2 * kABytes + 2 * (uint32_t)(NP / 2) * (BK * 4);
+}
+
+template <bool OUT64, bool OUT_T>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32_2sm_kernel(const __grid_constant__ CUtensorMap mapA,
+                         const __grid_constant__ CUtensorMap mapB1,
+                         const __grid_constant__ CUtensorMap mapBlo1,
+                         const __grid_constant__ CUtensorMap mapB2,
+                         const __grid_constant__ CUtensorMap mapBlo2, void* __restrict__ out,
+                         float* __restrict__ out_lo, long ldo, long split_stride, int M, int NP,
+                         int k_tiles, int k_tiles_per_split, int* __restrict__ flag) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                         ~uintptr_t(1023));
+    const int n1 = NP > 256 ? 256 : NP, n2 = NP - n1;  // N chunks; each CTA holds half of each
+    const uint32_t h1 = (uint32_t)(n1 / 2) * (BK * 4), h2 = (uint32_t)(n2 / 2) * (BK * 4);
+    const uint32_t bH = h1 + h2;  // this CTA's B (or B_lo) half
+    const uint32_t kStage = 2 * kABytes + 2 * bH;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage);
+    uint64_t* afull = full + kStages2;
+    uint64_t* conv = afull + kStages2;
+    uint64_t* empty = conv + kStages2;
+    uint64_t* accum = empty + kStages2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_rank();
+    const bool leader = crank == 0;
+    const int m0 = blockIdx.x * BM;
+    const int kt0 = blockIdx.y * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int n_iter = max(0, kt1 - kt0);
+    const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&afull[s], 1);
+            mbar_init(&conv[s], 8);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    fence_before();
+    cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // stage layout: A raw | A lo | B half (chunk-1 half, chunk-2 half) | B_lo half
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch_desc(&mapA);
+            tma_prefetch_desc(&mapB1);
+            tma_prefetch_desc(&mapBlo1);
+            if (n2 > 0) {
+                tma_prefetch_desc(&mapB2);
+                tma_prefetch_desc(&mapBlo2);
+            }
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages2;
+                if (it >= kStages2) mbar_wait(&empty[s], ((it / kStages2) - 1) & 1);
+                char* st = smem + s * kStage;
+                char* sb = st + 2 * kABytes;
+                const int k = (kt0 + it) * BK;
+                const uint32_t fb = mapa_u32(smem_u32(&full[s]), 0);  // the leader's full[s]
+                if (leader) mbar_arrive_expect_tx(&full[s], 4 * bH);  // both CTAs' B + B_lo halves
+                mbar_arrive_expect_tx(&afull[s], kABytes);
+                tma_load_2d(st, &mapA, &afull[s], k, m0);
+                tma_load_2d_pair(sb, &mapB1, fb, k, (int)crank * (n1 / 2));
+                tma_load_2d_pair(sb + bH, &mapBlo1, fb, k, (int)crank * (n1 / 2));
+                if (n2 > 0) {
+                    tma_load_2d_pair(sb + h1, &mapB2, fb, k, n1 + (int)crank * (n2 / 2));
+                    tma_load_2d_pair(sb + bH + h1, &mapBlo2, fb, k, n1 + (int)crank * (n2 / 2));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------- MMA issuer (leader CTA only)
+        if (leader && lane == 0) {
+            const uint32_t lbo = 16u, sbo = 512u;
+            const uint64_t lay = 4u;
+            const uint32_t id1 = idesc2(n1), id2 = n2 > 0 ? idesc2(n2) : 0u;
+            auto issue = [&](uint32_t a, uint32_t b, uint32_t acc0) {
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ++ks) {
+                    const uint32_t ko = ks * 32u;
+                    const uint64_t ad = sdesc(a + ko, lbo, sbo, lay);
+                    const uint32_t acc = (ks == 0) ? acc0 : 1u;
+                    mma2(tmem, ad, sdesc(b + ko, lbo, sbo, lay), id1, acc);
+                    if (n2 > 0) mma2(tmem + 256, ad, sdesc(b + h1 + ko, lbo, sbo, lay), id2, acc);
+                }
+            };
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages2;
+                const uint32_t st = smem_u32(smem + s * kStage);
+                const uint32_t a_raw = st, a_lo = st + kABytes;
+                const uint32_t b_raw = st + 2 * kABytes, b_lo = b_raw + bH;
+                mbar_wait(&full[s], (it / kStages2) & 1);
+                mbar_wait(&conv[s], (it / kStages2) & 1);  // also: both A tiles landed
+                fence_after();
+                issue(a_raw, b_raw, it > 0 ? 1u : 0u);  // a_hi b_hi
+                issue(a_raw, b_lo, 1u);                 // a_hi b_lo
+                issue(a_lo, b_raw, 1u);                 // a_lo b_hi
+                commit2_mc(&empty[s]);
+            }
+            if (n_iter > 0) commit2_mc(accum);
+        }
+    } else {
+        // ------------------------------------------------- A lo split (warps 2-5)
+        const int ct = threadIdx.x - 64;
+        bool bad = false;
+        for (int it = 0; it < n_iter; ++it) {
+            const int s = it % kStages2;
+            mbar_wait(&afull[s], (it / kStages2) & 1);
+            char* st = smem + s * kStage;
+            const float4* ar = reinterpret_cast<const float4*>(st);
+            float4* al = reinterpret_cast<float4*>(st + kABytes);
+#pragma unroll
+            for (int i = ct; i < (int)(kABytes / 16); i += 128) {
+                const float4 v = ar[i];
+                if (flag) {
+                    const uint32_t e = 0x7f800000u;
+                    bad |= ((__float_as_uint(v.x) & e) == e) | ((__float_as_uint(v.y) & e) == e) |
+                           ((__float_as_uint(v.z) & e) == e) | ((__float_as_uint(v.w) & e) == e);
+                }
+                al[i] = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_u32(smem_u32(&conv[s]), 0));
+        }
+        if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+
+        // ------------------------------------------------------------ epilogue
+        if (n_iter > 0) {
+            mbar_wait(accum, 0);
+            fence_after();
+        }
+        epilogue<OUT64, OUT_T>(tmem, warp, lane, m0, M, NP, n_iter > 0, out, out_lo, ldo,
+                               split_stride);
+    }
+    fence_before();
+    cluster_sync();  // no multicast commit or remote arrive is still in flight into the peer
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "r"(tmem_cols));
     }
 }
@@ -435,6 +669,38 @@ cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap
     return cudaGetLastError();
 }
 
+template <bool OUT64, bool OUT_T>
+cudaError_t launch_2sm(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap* mB,
+                       cudaStream_t st) {
+    const size_t smem = tf32::kStages2 * tf32::stage_bytes2(p.NP) + (5 * tf32::kStages2 + 1) * 8 +
+                        16 + 1024;
+    auto kern = tf32::gemm_tf32_2sm_kernel<OUT64, OUT_T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int k_tiles = (int)((p.K + tf32::BK - 1) / tf32::BK);
+    const int splits = p.splits < 1 ? 1 : p.splits;
+    const int per = (k_tiles + splits - 1) / splits;
+    unsigned gx = (unsigned)((p.M + tf32::BM - 1) / tf32::BM);
+    gx = (gx + 1) & ~1u;  // the odd tile's partner only reads zeros past M
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gx, (unsigned)splits);
+    cfg.blockDim = dim3(tf32::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, mA, mB[0], mB[1], mB[2], mB[3], p.out,
+                           static_cast<float*>(p.out_lo), p.ldo, p.split_stride, (int)p.M, p.NP,
+                           k_tiles, per, p.flag);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 template <bool MN, bool OUT64, bool OUT_T>
 cudaError_t launch_p(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
                      const CUtensorMap& mBlo, cudaStream_t st) {
@@ -450,6 +716,31 @@ cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
     if (!p.out64 && p.splits > 1) return cudaErrorInvalidValue;
     if (p.out_lo && (p.out64 || p.out_t)) return cudaErrorInvalidValue;
     CUtensorMap mA, mB, mBlo;
+    // cta_group::2 variant: correct but measured slower (2.45 ms flat in NP at C4 size against
+    // 1.7-2.5 ms for the 1-SM kernel), so opt-in only (RSVD_B200_TF32_2SM=1)
+    static const bool two_sm = getenv("RSVD_B200_TF32_2SM") != nullptr;
+    if (!p.mn && two_sm && p.M > tf32::BM) {
+        // cta_group::2: A boxes of 128 rows; B / B_lo as the two CTAs' halves of each N chunk
+        const int n1 = p.NP > 256 ? 256 : p.NP, n2 = p.NP - n1;
+        const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
+        CUtensorMap mb[4];
+        if (map_f32(&mA, p.A, p.M, p.K, p.lda, tf32::BK, tf32::BM, sw) ||
+            map_f32(&mb[0], p.B, p.NP, p.K, p.ldb, tf32::BK, n1 / 2, sw) ||
+            map_f32(&mb[1], p.Blo, p.NP, p.K, p.ldb, tf32::BK, n1 / 2, sw))
+            return cudaErrorInvalidValue;
+        if (n2 > 0) {
+            if (map_f32(&mb[2], p.B, p.NP, p.K, p.ldb, tf32::BK, n2 / 2, sw) ||
+                map_f32(&mb[3], p.Blo, p.NP, p.K, p.ldb, tf32::BK, n2 / 2, sw))
+                return cudaErrorInvalidValue;
+        } else {
+            mb[2] = mb[0];
+            mb[3] = mb[1];
+        }
+        if (p.out64) return p.out_t ? launch_2sm<true, true>(p, mA, mb, st)
+                                    : launch_2sm<true, false>(p, mA, mb, st);
+        return p.out_t ? launch_2sm<false, true>(p, mA, mb, st)
+                       : launch_2sm<false, false>(p, mA, mb, st);
+    }
     if (!p.mn) {  // A: M x K (lda), Bt: NP x K (ldb); 64-byte rows of K
         // one box per B half: the paired kernel loads NP / 2 rows per CTA, the single one
         // NP (<= 256) or two halves

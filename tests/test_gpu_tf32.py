@@ -79,3 +79,17 @@ def test_nan_flag_tf32(solver):
     bt = torch.randn(16, 256, device="cuda")
     # the flag path is exercised through the solver; here only the product must not hang
     run(solver, False, a, bt, 16, True, False)
+
+
+def test_cta_pair_variant_subprocess():
+    """The opt-in cta_group::2 variant of the K-major kernel (RSVD_B200_TF32_2SM=1, read once
+    per process) on the same shapes, in a child process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, RSVD_B200_TF32_2SM="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(os.path.dirname(__file__), "test_gpu_tf32.py"),
+                        "-k", "test_ax_tf32"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
