@@ -275,6 +275,12 @@ rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const fl
                                           long K, long lda, const float* B, long ldb, int NP,
                                           void* out, long ldo, int out64, int out_t, int splits);
 
+/* Test hook for the single-CTA Cholesky kernel (device pointers, row-major NP x NP buffers):
+ * G (s x s SPD block of an NP x NP buffer) -> R (upper, zero padded) and Rinv^T; *status = 0
+ * or 1 (a pivot below tol * max_i G_ii). s up to the shared-memory width limit. Synchronous. */
+rsvd_b200_status rsvd_b200_debug_cholesky(rsvd_b200_handle* h, const double* G, int s, int NP,
+                                         double* R, double* RinvT, double tol, int* status);
+
 /* Library build identification (sm_100a). */
 const char* rsvd_b200_version(void);
 

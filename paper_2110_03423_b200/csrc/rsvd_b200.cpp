@@ -1926,6 +1926,23 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
 
 void rsvd_b200_set_robust(rsvd_b200_handle* h, int on) { h->force_robust = on != 0; }
 
+rsvd_b200_status rsvd_b200_debug_cholesky(rsvd_b200_handle* h, const double* G, int s, int NP,
+                                         double* R, double* RinvT, double tol, int* status) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        if (s < 1 || s > cholesky_max_width() || NP < s)
+            fail(RSVD_B200_ARGUMENT_ERROR, "debug_cholesky: s=%d outside [1, %d] or NP < s", s,
+                 cholesky_max_width());
+        h->red_scratch.reserve(4 * sizeof(double));
+        int* st = reinterpret_cast<int*>(h->red_scratch.p);
+        h->launched(launch_cholesky(G, NP, s, NP, R, RinvT, st, nullptr, tol, h->stream),
+                    "cholesky");
+        ck(cudaMemcpyAsync(status, st, sizeof(int), cudaMemcpyDeviceToHost, h->stream),
+           "D2H status");
+        h->sync();
+    });
+}
+
 rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const float* A, long M,
                                           long K, long lda, const float* B, long ldb, int NP,
                                           void* out, long ldo, int out64, int out_t, int splits) {

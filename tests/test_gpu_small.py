@@ -1,0 +1,73 @@
+"""The single-CTA Cholesky kernel (csrc/linalg_small.cu: 16-wide panels, warp-0 diagonal
+factor with lookahead, in-place blocked inversion) through its test hook, against torch's FP64
+Cholesky: R^T R = G and R Rinv = I to a few ulps of cond-scaled size, R upper with a positive
+diagonal, zero padding, and the breakdown flag (pivot below tol * max diag)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def chol(solver, g, NP, tol=1e-12):
+    import torch
+    s = g.shape[0]
+    G = torch.zeros(NP, NP, dtype=torch.float64, device="cuda")
+    G[:s, :s] = g
+    R = torch.full((NP, NP), float("nan"), dtype=torch.float64, device="cuda")
+    Ri = torch.full((NP, NP), float("nan"), dtype=torch.float64, device="cuda")
+    st = C.c_int(-1)
+    solver.wait_for_torch()
+    rc = solver.lib.rsvd_b200_debug_cholesky(solver.h, C.c_void_p(G.data_ptr()), s, NP,
+                                             C.c_void_p(R.data_ptr()), C.c_void_p(Ri.data_ptr()),
+                                             tol, C.byref(st))
+    from paper_2110_03423_b200.rsvd import _check
+    _check(solver.lib, rc)
+    return R, Ri, st.value
+
+
+@pytest.mark.parametrize("s", [1, 2, 3, 7, 15, 16, 17, 31, 33, 48, 64, 74, 100, 128, 136, 148,
+                               157])
+def test_cholesky_sizes(solver, s):
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(s)
+    m = torch.randn(2 * s + 3, s, dtype=torch.float64, device="cuda", generator=gen)
+    m = m * torch.logspace(0, -3, s, dtype=torch.float64, device="cuda")  # cond(G) ~ 1e6
+    g = m.T @ m
+    NP = (s + 15) // 16 * 16
+    R, Ri, st = chol(solver, g, NP)
+    assert st == 0
+    Rs, Ris = R[:s, :s], Ri[:s, :s].T  # Ri holds Rinv^T
+    assert torch.all(torch.triu(Rs) == Rs) and torch.all(torch.diagonal(Rs) > 0)
+    assert torch.all(R[s:, :] == 0) and torch.all(R[:, s:] == 0)
+    assert torch.all(Ri[s:, :] == 0) and torch.all(Ri[:, s:] == 0)
+    ref = torch.linalg.cholesky(g, upper=True)
+    # backward error of the factorisation and of the inverse
+    err = ((Rs.T @ Rs - g).abs() / (torch.diagonal(g).sqrt()[:, None] *
+                                     torch.diagonal(g).sqrt()[None, :])).max().item()
+    assert err < 1e-13, err
+    inv_err = (Rs @ Ris - torch.eye(s, dtype=torch.float64, device="cuda")).abs().max().item()
+    assert inv_err < 1e-9, inv_err
+    rel = ((Rs - ref).abs().max() / ref.abs().max()).item()
+    assert rel < 1e-10, rel
+
+
+def test_cholesky_breakdown(solver):
+    import torch
+    s = 40
+    m = torch.randn(s, s - 5, dtype=torch.float64, device="cuda")
+    g = m @ m.T  # rank s - 5: a pivot collapses
+    R, Ri, st = chol(solver, g, 48)
+    assert st == 1
+    g2 = torch.eye(s, dtype=torch.float64, device="cuda")
+    g2[7, 7] = float("nan")
+    assert chol(solver, g2, 48)[2] == 1
+
+
+def test_cholesky_rejects_too_wide(solver):
+    import torch
+    import paper_2110_03423_b200 as P
+    g = torch.eye(300, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.ArgumentError):
+        chol(solver, g, 304)
