@@ -281,6 +281,13 @@ rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const fl
 rsvd_b200_status rsvd_b200_debug_cholesky(rsvd_b200_handle* h, const double* G, int s, int NP,
                                          double* R, double* RinvT, double tol, int* status);
 
+/* Test hook for the one-sided Jacobi SVD kernels (single CTA up to s = 112, multi-CTA block
+ * Jacobi beyond): R (s x s block of an NP x NP row-major device buffer) = U diag(sigma) W^T with
+ * sigma descending (NP entries, zero padded), U and W NP x NP row-major (columns = vectors).
+ * *sweeps = sweeps used, or -1 if 30 sweeps did not converge. Synchronous. */
+rsvd_b200_status rsvd_b200_debug_jacobi(rsvd_b200_handle* h, const double* R, int s, int NP,
+                                       double* sigma, double* U, double* W, int* sweeps);
+
 /* Library build identification (sm_100a). */
 const char* rsvd_b200_version(void);
 

@@ -23,7 +23,8 @@ EXPORTS = [
     "rsvd_b200_local_group_create", "rsvd_b200_local_group_destroy", "rsvd_b200_comm_init_local",
     "rsvd_b200_comm_info", "rsvd_b200_comm_free", "rsvd_b200_randomized_ksvd_sharded",
     "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak",
-    "rsvd_b200_debug_gemm_tf32", "rsvd_b200_debug_cholesky", "rsvd_b200_randomized_ksvd_f32",
+    "rsvd_b200_debug_gemm_tf32", "rsvd_b200_debug_cholesky", "rsvd_b200_debug_jacobi",
+    "rsvd_b200_randomized_ksvd_f32",
     "rsvd_b200_randomized_ksvd_f32_device", "rsvd_b200_randomized_ksvd_sharded_f32",
     "rsvd_b200_randomized_ksvd_sharded_f32_device", "rsvd_b200_wait_stream",
     "rsvd_b200_residual_fro", "rsvd_b200_residual_fro_device", "rsvd_b200_fit_pca",
@@ -111,6 +112,8 @@ def load() -> C.CDLL:
                                                 C.c_int, C.c_int]),
         "rsvd_b200_debug_cholesky": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, C.c_double,
                                                C.POINTER(C.c_int)]),
+        "rsvd_b200_debug_jacobi": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp,
+                                             C.POINTER(C.c_int)]),
         "rsvd_b200_comm_init_nccl": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
         "rsvd_b200_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
         "rsvd_b200_local_group_destroy": (None, [_vp]),

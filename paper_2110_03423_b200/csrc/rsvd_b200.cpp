@@ -1943,6 +1943,25 @@ rsvd_b200_status rsvd_b200_debug_cholesky(rsvd_b200_handle* h, const double* G, 
     });
 }
 
+rsvd_b200_status rsvd_b200_debug_jacobi(rsvd_b200_handle* h, const double* R, int s, int NP,
+                                       double* sigma, double* U, double* W, int* sweeps) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        if (s < 1 || s > (int)jacobi_max_width() || NP < s)
+            fail(RSVD_B200_ARGUMENT_ERROR, "debug_jacobi: s=%d outside [1, %zu] or NP < s", s,
+                 jacobi_max_width());
+        h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(s)) * sizeof(double));
+        h->red_scratch.reserve(4 * sizeof(double));
+        int* st = reinterpret_cast<int*>(h->red_scratch.p);
+        h->launched(launch_jacobi_svd(R, s, NP, sigma, U, W, st, h->jscratch.d(), nullptr,
+                                      h->stream),
+                    "jacobi_svd");
+        ck(cudaMemcpyAsync(sweeps, st, sizeof(int), cudaMemcpyDeviceToHost, h->stream),
+           "D2H sweeps");
+        h->sync();
+    });
+}
+
 rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const float* A, long M,
                                           long K, long lda, const float* B, long ldb, int NP,
                                           void* out, long ldo, int out64, int out_t, int splits) {

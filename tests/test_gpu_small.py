@@ -71,3 +71,60 @@ def test_cholesky_rejects_too_wide(solver):
     g = torch.eye(300, dtype=torch.float64, device="cuda")
     with pytest.raises(P.ArgumentError):
         chol(solver, g, 304)
+
+
+def jacobi(solver, r, NP):
+    import torch
+    from paper_2110_03423_b200.rsvd import _check
+    s = r.shape[0]
+    Rb = torch.zeros(NP, NP, dtype=torch.float64, device="cuda")
+    Rb[:s, :s] = r
+    sig = torch.full((NP,), float("nan"), dtype=torch.float64, device="cuda")
+    U = torch.full((NP, NP), float("nan"), dtype=torch.float64, device="cuda")
+    W = torch.full((NP, NP), float("nan"), dtype=torch.float64, device="cuda")
+    sw = C.c_int(-2)
+    solver.wait_for_torch()
+    _check(solver.lib, solver.lib.rsvd_b200_debug_jacobi(
+        solver.h, C.c_void_p(Rb.data_ptr()), s, NP, C.c_void_p(sig.data_ptr()),
+        C.c_void_p(U.data_ptr()), C.c_void_p(W.data_ptr()), C.byref(sw)))
+    return sig, U, W, sw.value
+
+
+@pytest.mark.parametrize("s", [1, 2, 5, 8, 9, 42, 74, 112, 113, 148, 200, 272, 320])
+def test_jacobi_sizes(solver, s):
+    """Both Jacobi kernels (single CTA s <= 112, block Jacobi beyond) on a graded triangular
+    R (the shape the pipeline hands over: R_B of B^T = Q_B R_B): sigma against torch's SVD,
+    R W = U diag(sigma), orthonormal U and W, descending order, zero padding."""
+    import torch
+    gen = torch.Generator(device="cuda").manual_seed(1000 + s)
+    a = torch.randn(s, s, dtype=torch.float64, device="cuda", generator=gen)
+    a = a * torch.logspace(0, -4, s, dtype=torch.float64, device="cuda")
+    r = torch.linalg.qr(a.T).R.T.contiguous().T.contiguous()  # upper triangular, graded
+    r = torch.triu(r)
+    NP = (s + 15) // 16 * 16
+    sig, U, W, sweeps = jacobi(solver, r, NP)
+    assert 1 <= sweeps <= 30
+    ref = torch.linalg.svdvals(r)
+    got = sig[:s]
+    assert torch.all(got[:-1] >= got[1:])
+    assert torch.all(sig[s:] == 0)
+    rel = ((got - ref).abs() / ref).max().item()
+    assert rel < 1e-12, rel
+    Us, Ws = U[:s, :s], W[:s, :s]
+    eye = torch.eye(s, dtype=torch.float64, device="cuda")
+    assert (Ws.T @ Ws - eye).abs().max().item() < 1e-12
+    assert (Us.T @ Us - eye).abs().max().item() < 1e-10
+    recon = (r @ Ws - Us * got[None, :]).abs().max().item() / ref[0].item()
+    assert recon < 1e-13, recon
+
+
+def test_jacobi_rank_deficient(solver):
+    """Zero columns: sigma exactly 0 there, U column 0 (completed later by the pipeline)."""
+    import torch
+    s = 20
+    r = torch.triu(torch.randn(s, s, dtype=torch.float64, device="cuda"))
+    r[:, 15:] = 0
+    sig, U, W, sweeps = jacobi(solver, r, 32)
+    assert sweeps >= 1
+    assert torch.all(sig[15:s] == 0)
+    assert torch.all(U[:s, 15:s] == 0)
