@@ -903,13 +903,24 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
     h->mark("sketch_gemm");
     if (p.f32) {
         xt_to_f32(c);
-        GemmTf32 g{p.af, p.m, n, p.lda, static_cast<float*>(h->xtf.p), p.ldnf, p.NPf, h->yf.p,
-                   (long)p.NPf};
-        g.Blo = static_cast<float*>(h->xtf_lo.p);
-        g.out_lo = h->yf_lo.p;
-        g.out64 = false;
-        g.flag = check ? c.flags + kFlagNonfinite : nullptr;
-        gemm_tf32(h, g, "gemm_A", 2.0 * p.m * n * s);
+        const bool chunked = h->up_active && p.af == h->a_copy.p && !p.sharded;
+        const long rows_per = chunked ? h->up_chunk_rows : p.m;
+        const long chunks = chunked ? h->up_chunks : 1;
+        h->kernel_begin("gemm_A", 2.0 * p.m * n * s);
+        for (long ci = 0; ci < chunks; ++ci) {  // chunks: the sketch consumes the upload
+            const long r0 = ci * rows_per, rows = std::min(p.m - r0, rows_per);
+            if (chunked)
+                ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
+            GemmTf32 g{p.af + r0 * p.lda, rows, n, p.lda, static_cast<float*>(h->xtf.p), p.ldnf,
+                       p.NPf, static_cast<float*>(h->yf.p) + r0 * p.NPf, (long)p.NPf};
+            g.Blo = static_cast<float*>(h->xtf_lo.p);
+            g.out_lo = static_cast<float*>(h->yf_lo.p) + r0 * p.NPf;
+            g.out64 = false;
+            g.flag = check ? c.flags + kFlagNonfinite : nullptr;
+            gemm_tf32(h, g);
+        }
+        h->kernel_end("gemm_A");
+        if (chunked) h->up_active = false;
         h->gram_ready = false;
         return;
     }
@@ -1471,15 +1482,17 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_device(rsvd_b200_handle* h, const dou
 // H2D of a host A (m x n) into h->a_copy (lda). Tall inputs large enough to matter go up in
 // row chunks on the copy stream (up_ev per chunk) for sketch_dev to consume as they land;
 // everything else is one copy on the solve stream.
-static void upload_a(rsvd_b200_handle* h, const double* a, long m, long n, long lda) {
-    h->a_copy.reserve((size_t)m * lda * sizeof(double));
-    const long bytes_row = lda * (long)sizeof(double);
+static void upload_a(rsvd_b200_handle* h, const void* av, long m, long n, long lda,
+                     size_t esz = sizeof(double)) {
+    const char* a = static_cast<const char*>(av);
+    h->a_copy.reserve((size_t)m * lda * esz);
+    const long bytes_row = lda * (long)esz;
     const char* mb = getenv("RSVD_B200_UPLOAD_CHUNK_MB");  // tests: force small chunks
     const long chunk_bytes = (mb && atol(mb) > 0 ? atol(mb) : 256l) << 20;
     const long chunk_rows = round_up(std::max<long>(128, chunk_bytes / bytes_row), 128);
     if (m < n || m < 2 * chunk_rows) {
-        ck(cudaMemcpy2DAsync(h->a_copy.p, bytes_row, a, n * sizeof(double), n * sizeof(double),
-                             m, cudaMemcpyHostToDevice, h->stream),
+        ck(cudaMemcpy2DAsync(h->a_copy.p, bytes_row, a, n * esz, n * esz, m,
+                             cudaMemcpyHostToDevice, h->stream),
            "H2D of A");
         return;
     }
@@ -1498,9 +1511,9 @@ static void upload_a(rsvd_b200_handle* h, const double* a, long m, long n, long 
     ck(cudaStreamWaitEvent(h->copy_stream, h->up_start, 0), "stream wait");
     for (long c = 0; c < chunks; ++c) {
         const long r0 = c * chunk_rows, rows = std::min(m - r0, chunk_rows);
-        ck(cudaMemcpy2DAsync(static_cast<double*>(h->a_copy.p) + r0 * lda, bytes_row,
-                             a + r0 * n, n * sizeof(double), n * sizeof(double), rows,
-                             cudaMemcpyHostToDevice, h->copy_stream),
+        ck(cudaMemcpy2DAsync(static_cast<char*>(h->a_copy.p) + r0 * bytes_row, bytes_row,
+                             a + r0 * n * esz, n * esz, n * esz, rows, cudaMemcpyHostToDevice,
+                             h->copy_stream),
            "H2D of A");
         ck(cudaEventRecord(h->up_ev[c], h->copy_stream), "event record");
     }
@@ -1686,10 +1699,15 @@ static void solve_host_f32(rsvd_b200_handle* h, const float* a, size_t m_local, 
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     h->launches = 0;
     const long lda = round_up((long)n, 4);
-    h->a_copy.reserve(std::max<size_t>(1, m_local * lda) * sizeof(float));
-    ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(float), a, n * sizeof(float),
-                         n * sizeof(float), m_local, cudaMemcpyHostToDevice, h->stream),
-       "H2D of A (FP32)");
+    UploadFence fence{h};
+    if (sharded) {
+        h->a_copy.reserve(std::max<size_t>(1, m_local * lda) * sizeof(float));
+        ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(float), a, n * sizeof(float),
+                             n * sizeof(float), m_local, cudaMemcpyHostToDevice, h->stream),
+           "H2D of A (FP32)");
+    } else {
+        upload_a(h, a, (long)m_local, (long)n, lda, sizeof(float));  // chunked when tall
+    }
     const size_t k = cfg->k;
     h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
     if (u) h->u_out.reserve(std::max<size_t>(m_local * k, 1) * sizeof(double));

@@ -68,6 +68,21 @@ def test_f32_device_matches_host(solver):
     assert torch.equal(s, s2)
 
 
+def test_f32_chunked_upload_bit_identical(solver, monkeypatch):
+    """FP32 host solves upload A in row chunks the tf32 sketch consumes as they land; chunks
+    are whole tile pairs, so the result equals the device-resident solve bit for bit."""
+    torch = pytest.importorskip("torch")
+    import paper_2110_03423_b200 as P
+    a = planted32(5000, 256, lambda i: 1.0 / (1.0 + i) ** 1.5, 6)
+    cfg = P.RsvdConfig(k=16, power_q=2, seed=8)
+    monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "1")  # 1024-row chunks: 5 of them
+    host = solver.randomized_ksvd_f32(a, cfg)
+    u, s, v, sw = solver.randomized_ksvd_f32_device(torch.from_numpy(a).cuda(), cfg)
+    assert np.array_equal(s.cpu().numpy(), host.factors.sigma)
+    assert np.array_equal(u.cpu().numpy(), host.factors.u)
+    assert np.array_equal(v.cpu().numpy(), host.factors.v)
+
+
 def test_f32_fallback_ill_conditioned(solver, port):
     """cond(Y) ~ 1e6 >> 300: the 3xTF32 CholeskyQR aborts and the robust rerun's FP64
     Householder QR takes over; the leading singular triplets still meet the FP32 bar."""
