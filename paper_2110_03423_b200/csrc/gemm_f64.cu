@@ -23,7 +23,8 @@
 // Bank-conflict-free fragment loads from the 128B-swizzled boxes come from
 // permuting which physical k each MMA k-slot reads (the same permutation on
 // both operands, so the product is unchanged):
-//   ax : k = (t&1) + 8*(t>>1) + 2*q      (K-major A and K-major Xt)
+//   ax : k = 4*t + q                     (K-major A and K-major Xt: a thread's k-slot
+//                                          pairs are adjacent doubles, one 16-byte load)
 //   atx: k = 2*t + (q&1) + 8*(q>>1)      (M-major A and N-major W)
 // with t = lane&3 and q the 4-wide k-slot group.
 #include "common.cuh"
@@ -34,7 +35,11 @@ namespace rsvdb200 {
 constexpr int kBK = 32;           // k extent of one pipeline stage (two 16-wide boxes)
 constexpr int kBoxBytesRow = 128; // 16 doubles
 
-__device__ __forceinline__ int k_ax(int t, int q) { return (t & 1) + 8 * (t >> 1) + 2 * q; }
+__device__ __forceinline__ int k_ax(int t, int q) { return 4 * t + q; }
+
+__device__ __forceinline__ double2 lds_f64x2(const char* smem_base, uint32_t byte_off) {
+    return *reinterpret_cast<const double2*>(smem_base + byte_off);
+}
 __device__ __forceinline__ int k_atx(int t, int q) { return 2 * t + (q & 1) + 8 * (q >> 1); }
 
 __device__ __forceinline__ bool nonfinite(double x) {
@@ -233,10 +238,13 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
             for (int mi = 0; mi < MI; ++mi) {
                 const int r0 = wm * (BM / WM) + mi * 16 + g;
 #pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    const int row = r0 + 8 * (v & 1);
-                    a[mi][v] = lds_f64(boxA, swz128(row, k_ax(t, v >> 1)));
-                }
+                for (int h = 0; h < 2; ++h)      // rows r0, r0 + 8
+#pragma unroll
+                    for (int qq = 0; qq < 2; ++qq) {  // k-slot groups (2qq, 2qq + 1)
+                        const double2 p = lds_f64x2(boxA, swz128(r0 + 8 * h, k_ax(t, 2 * qq)));
+                        a[mi][h + 4 * qq] = p.x;      // v = h + 2 * (2 qq)
+                        a[mi][h + 4 * qq + 2] = p.y;  // v = h + 2 * (2 qq + 1)
+                    }
             }
             if (CHECK && wn == 0) {
 #pragma unroll
@@ -249,7 +257,11 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
                 const int n = (wn * NI + ni) * 8 + g;
                 double b[4];
 #pragma unroll
-                for (int v = 0; v < 4; ++v) b[v] = lds_f64(boxX, swz128(n, k_ax(t, v)));
+                for (int qq = 0; qq < 2; ++qq) {
+                    const double2 p = lds_f64x2(boxX, swz128(n, k_ax(t, 2 * qq)));
+                    b[2 * qq] = p.x;
+                    b[2 * qq + 1] = p.y;
+                }
 #pragma unroll
                 for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], a[mi], b);
             }
