@@ -257,11 +257,15 @@ void rsvd_b200_reset_stats(rsvd_b200_handle* h);
 long rsvd_b200_last_launch_count(rsvd_b200_handle* h);
 
 /* Diagnostics of the last solve: "jacobi_sweeps", "householder_fallbacks",
- * "robust_reruns" (optimistic pipeline repeated on the robust path), "launches".
+ * "robust_reruns" (optimistic pipeline repeated on the robust path), "launches"; and,
+ * cumulative over the handle, "graph_launches" (device-resident solves that ran as one
+ * launch of the handle's cached CUDA graph of the pipeline; RSVD_B200_NO_GRAPH disables it).
  * Returns -1 for an unknown key. */
 long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key);
 /* Force the robust path (host-checked Cholesky, Householder fallback) for every solve. */
 void rsvd_b200_set_robust(rsvd_b200_handle* h, int on);
+/* Enable (default) or disable the CUDA-graph replay of repeated device-resident solves. */
+void rsvd_b200_set_graphs(rsvd_b200_handle* h, int on);
 
 /* Measured FP64 tensor-core peak of the handle's GPU (TFLOP/s): an issue-bound
  * mma.sync m16n8k16 f64 loop on every SM — the roofline denominator of the GEMMs. */

@@ -19,7 +19,7 @@ EXPORTS = [
     "rsvd_b200_splitmix_words", "rsvd_b200_uniforms", "rsvd_b200_last_profile",
     "rsvd_b200_set_profiling", "rsvd_b200_last_launch_count", "rsvd_b200_version",
     "rsvd_b200_kernel_stats", "rsvd_b200_reset_stats", "rsvd_b200_last_info",
-    "rsvd_b200_set_robust", "rsvd_b200_nccl_unique_id", "rsvd_b200_comm_init_nccl",
+    "rsvd_b200_set_robust", "rsvd_b200_set_graphs", "rsvd_b200_nccl_unique_id", "rsvd_b200_comm_init_nccl",
     "rsvd_b200_local_group_create", "rsvd_b200_local_group_destroy", "rsvd_b200_comm_init_local",
     "rsvd_b200_comm_info", "rsvd_b200_comm_free", "rsvd_b200_randomized_ksvd_sharded",
     "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak",
@@ -96,6 +96,7 @@ def load() -> C.CDLL:
         "rsvd_b200_reset_stats": (None, [_vp]),
         "rsvd_b200_last_info": (C.c_long, [_vp, C.c_char_p]),
         "rsvd_b200_set_robust": (None, [_vp, C.c_int]),
+        "rsvd_b200_set_graphs": (None, [_vp, C.c_int]),
         "rsvd_b200_nccl_unique_id": (C.c_int, [C.c_char_p]),
         "rsvd_b200_dmma_peak": (C.c_int, [_vp, _dp]),
         "rsvd_b200_randomized_ksvd_f32": (C.c_int, [_vp, _fp, _sz, _sz, cfgp, _dp, _dp, _dp,

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -123,11 +124,16 @@ int choose_splits(long tiles, long k_tiles) {
     return best;
 }
 
+// Bumped by every workspace (re)allocation: a captured solve graph (SolveGraph) holds raw
+// workspace pointers and is only replayed while the generation it was captured at is current.
+std::atomic<unsigned long> g_ws_gen{0};
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
     void reserve(size_t b) {
         if (b <= bytes) return;
+        g_ws_gen.fetch_add(1);
         if (p) cudaFree(p);
         p = nullptr;
         bytes = 0;
@@ -144,6 +150,26 @@ struct DevBuf {
 struct StageTimer {
     const char* name;
     cudaEvent_t start, stop;
+};
+
+// Everything a captured device-resident solve depends on besides the workspace generation.
+struct GraphKey {
+    const void* a = nullptr;
+    long m = 0, n = 0, lda = 0;
+    int s = 0, NP = 0;
+    bool f32 = false;
+    size_t k = 0, q = 0;
+    uint64_t seed = 0;
+    const void *u = nullptr, *sigma = nullptr, *v = nullptr;
+    long ldu = 0, ldv = 0;
+    int profiling = 0;
+    unsigned long gen = 0;
+    bool operator==(const GraphKey& o) const {
+        return a == o.a && m == o.m && n == o.n && lda == o.lda && s == o.s && NP == o.NP &&
+               f32 == o.f32 && k == o.k && q == o.q && seed == o.seed && u == o.u &&
+               sigma == o.sigma && v == o.v && ldu == o.ldu && ldv == o.ldv &&
+               profiling == o.profiling && gen == o.gen;
+    }
 };
 
 }  // namespace
@@ -195,6 +221,29 @@ struct rsvd_b200_handle {
     std::vector<std::pair<std::string, KernelStat>> kstats;
     std::vector<std::pair<const char*, double>> last_profile;
     long launches = 0;
+    // CUDA graphs of the optimistic device-resident pipeline (solve_tall): captured on the
+    // first solve of a shape/config/buffer set and replayed while the key still matches,
+    // so a repeated solve costs one graph launch instead of ~60-250 kernel launches with
+    // their host-side tensor-map encodes. A few keys are kept (LRU) because callers that
+    // allocate fresh outputs per solve alternate between buffer sets.
+    struct SolveGraph {
+        GraphKey key;
+        cudaGraphExec_t exec = nullptr;
+        long launches = 0;
+        unsigned long used = 0;
+        void reset() {
+            if (exec) cudaGraphExecDestroy(exec);
+            exec = nullptr;
+        }
+    };
+    static constexpr int kMaxGraphs = 4;
+    SolveGraph graphs[kMaxGraphs];
+    unsigned long graph_clock = 0;
+    void reset_graphs() {
+        for (auto& g : graphs) g.reset();
+    }
+    bool use_graphs = true;
+    long graph_replays = 0;
 
     // ----------------------------------------------------------------- timing
     void mark(const char* name) {
@@ -1101,6 +1150,90 @@ bool finish_run(const Ctx& c, bool checked_nonfinite) {
     return true;
 }
 
+// The optimistic pipeline of solve_tall as one CUDA graph. Eligible: single-device
+// device-resident solves (no chunked upload in flight, no validation Omega, no forced robust
+// path, no launch tracing, no profiling: events recorded by graph nodes cannot be timed). The first solve of a key is captured (relaxed
+// mode: a first-time workspace allocation inside the capture is legal, and the key then
+// records the generation after it) and launched; later solves with the same key replay it.
+// Returns 0 when the solve must take the eager path (not eligible, or the capture failed),
+// 1 when the replay produced the result, 2 when it raised the abort flag (a Cholesky
+// breakdown): solve_tall then reruns on the robust path as after an eager optimistic attempt.
+int solve_tall_graph(rsvd_b200_handle* h, const double* A, const Plan& p,
+                      const rsvd_b200_config& cfg, double* u, long ldu, double* sigma, double* v,
+                      long ldv) {
+    static const bool disabled = getenv("RSVD_B200_NO_GRAPH") != nullptr;
+    if (disabled || !h->use_graphs || h->force_robust || p.sharded || h->up_active || !h->omega_host.empty() ||
+        h->profiling != 0 || getenv("RSVD_B200_TRACE"))
+        return 0;
+    GraphKey key;
+    key.a = p.f32 ? static_cast<const void*>(p.af) : A;
+    key.m = p.m, key.n = p.n, key.lda = p.lda, key.s = p.s, key.NP = p.NP, key.f32 = p.f32;
+    key.k = cfg.k, key.q = cfg.power_q, key.seed = cfg.seed;
+    key.u = u, key.sigma = sigma, key.v = v, key.ldu = ldu, key.ldv = ldv;
+    key.profiling = h->profiling;
+    key.gen = g_ws_gen.load();
+    rsvd_b200_handle::SolveGraph* hit = nullptr;
+    rsvd_b200_handle::SolveGraph* lru = &h->graphs[0];
+    for (auto& cand : h->graphs) {
+        if (cand.exec && cand.key.gen != key.gen) cand.reset();  // stale workspace pointers
+        if (cand.exec && cand.key == key) hit = &cand;
+        if (!cand.exec || (lru->exec && cand.used < lru->used)) lru = &cand;
+    }
+    auto& g = hit ? *hit : *lru;
+    g.used = ++h->graph_clock;
+    if (!hit) {
+        g.reset();
+        // everything the pipeline allocates is reserved before the capture starts
+        begin_run(h, p, false);
+        key.gen = g_ws_gen.load();
+        const long launches0 = h->launches;
+        cudaGraph_t graph = nullptr;
+        ck(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed), "begin capture");
+        bool ok = true;
+        std::string why;
+        try {
+            const Ctx c = begin_run(h, p, false);
+            sketch_dev(c, A, cfg.seed, /*check=*/true);
+            power_iterate_dev(c, A, cfg.power_q, false);
+            project_and_solve_dev(c, A, (long)cfg.k, u, ldu, sigma, v, ldv);
+        } catch (const Failure& f) {
+            ok = false;
+            why = f.msg;
+        } catch (...) {
+            ok = false;
+            why = "exception";
+        }
+        const cudaError_t ec = cudaStreamEndCapture(h->stream, &graph);
+        cudaError_t ei = cudaSuccess;
+        if (ok && ec == cudaSuccess && graph && g_ws_gen.load() == key.gen)
+            ok = (ei = cudaGraphInstantiate(&g.exec, graph, 0)) == cudaSuccess;
+        else
+            ok = false;
+        if (graph) cudaGraphDestroy(graph);
+        if (getenv("RSVD_B200_GRAPH_DEBUG"))
+            fprintf(stderr,
+                    "[rsvd_b200] graph capture %s (end %s, instantiate %s, gen %lu -> %lu, slot "
+                    "%ld%s%s)\n",
+                    ok ? "ok" : "FAILED", cudaGetErrorString(ec), cudaGetErrorString(ei), key.gen,
+                    g_ws_gen.load(), (long)(&g - h->graphs), why.empty() ? "" : ", ",
+                    why.c_str());
+        if (!ok) {
+            cudaGetLastError();  // clear a capture error; the eager path reports real ones
+            g.reset();
+            h->launches = launches0;
+            return 0;
+        }
+        g.key = key;
+        g.launches = h->launches - launches0;
+        h->launches = launches0;
+    }
+    ck(cudaGraphLaunch(g.exec, h->stream), "graph launch");
+    h->launches += g.launches;
+    h->graph_replays += 1;
+    const Ctx c{h, p, false, static_cast<int*>(h->flags.p)};
+    return finish_run(c, true) ? 1 : 2;
+}
+
 // Tall solve (rsvd.cpp:126-134) on device data. A: m x n (lda), m >= n. The optimistic
 // pipeline runs first; a Cholesky breakdown anywhere reruns the whole solve on the robust
 // path (Householder fallbacks), which reproduces the reference's QR semantics.
@@ -1108,7 +1241,13 @@ void solve_tall(rsvd_b200_handle* h, const double* A, const Plan& p, const rsvd_
                 double* u, long ldu, double* sigma, double* v, long ldv, size_t* sketch_width) {
     h->fallbacks = 0;
     h->reruns = 0;
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    const int gr = solve_tall_graph(h, A, p, cfg, u, ldu, sigma, v, ldv);
+    if (gr == 1) {
+        if (sketch_width) *sketch_width = (size_t)p.s;
+        return;
+    }
+    if (gr == 2) h->reruns = 1;
+    for (int attempt = gr == 2 ? 1 : 0; attempt < 2; ++attempt) {
         const Ctx c = begin_run(h, p, /*robust=*/attempt > 0 || h->force_robust);
         sketch_dev(c, A, cfg.seed, /*check=*/true);
         power_iterate_dev(c, A, cfg.power_q, false);
@@ -1393,6 +1532,7 @@ rsvd_b200_status rsvd_b200_destroy(rsvd_b200_handle* h) {
     }
     for (cudaEvent_t e : h->up_ev) cudaEventDestroy(e);
     if (h->up_start) cudaEventDestroy(h->up_start);
+    h->reset_graphs();
     if (h->flags_host) cudaFreeHost(h->flags_host);
     cudaStreamDestroy(h->stream);
     delete h;
@@ -1939,10 +2079,16 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
     if (!strcmp(key, "householder_fallbacks")) return h->fallbacks;
     if (!strcmp(key, "robust_reruns")) return h->reruns;
     if (!strcmp(key, "launches")) return h->launches;
+    if (!strcmp(key, "graph_launches")) return h->graph_replays;
     return -1;
 }
 
 void rsvd_b200_set_robust(rsvd_b200_handle* h, int on) { h->force_robust = on != 0; }
+
+void rsvd_b200_set_graphs(rsvd_b200_handle* h, int on) {
+    h->use_graphs = on != 0;
+    if (!h->use_graphs) h->reset_graphs();
+}
 
 rsvd_b200_status rsvd_b200_debug_cholesky(rsvd_b200_handle* h, const double* G, int s, int NP,
                                          double* R, double* RinvT, double tol, int* status) {

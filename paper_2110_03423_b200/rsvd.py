@@ -171,6 +171,10 @@ class Solver:
         """Force the host-checked robust path (Householder fallback) for every solve."""
         self.lib.rsvd_b200_set_robust(self.h, int(on))
 
+    def set_graphs(self, on: bool) -> None:
+        """Enable (default) / disable the CUDA-graph replay of repeated device-resident solves."""
+        self.lib.rsvd_b200_set_graphs(self.h, int(on))
+
     def last_profile(self) -> dict:
         names = (C.c_char_p * 32)()
         ms = (C.c_double * 32)()
