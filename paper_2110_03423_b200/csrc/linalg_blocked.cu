@@ -9,7 +9,8 @@
 //     R_B, the wide-sketch twin of jacobi_kernel (linalg_small.cu). Columns live in
 //     global memory (L2 resident); the s/8 column blocks are paired in round-robin
 //     (tournament) order, each block pair is one CTA that loads its 16 columns into
-//     shared memory and runs an inner one-sided Jacobi sweep over them with the
+//     shared memory (cp.async) and rotates the 64 cross-block pairs (the first round of a
+//     sweep also every within-block pair) with the
 //     reference's rotation rule and skip thresholds (svd.cpp:35-36, 60-90); a grid-wide
 //     barrier (cooperative launch) separates rounds. A sweep without any rotation ends
 //     the iteration, more than 30 sweeps is a convergence failure (svd.hpp:20), and the
@@ -22,6 +23,12 @@
 namespace cg = cooperative_groups;
 
 namespace rsvdb200 {
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+                 "l"(gmem_src)
+                 : "memory");
+}
 
 // ============================================================== small GEMM
 // C (M x N, ldc) = alpha * op(A) op(B) + beta * Cin (ldcin); op(A) is M x K,
@@ -180,38 +187,40 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
             __syncthreads();
             int rotated = 0;
             if (cnt > 0) {
-                // columns in: several double2 loads in flight per thread (L2 latency)
-                for (int e0 = tid; e0 < cnt * l2; e0 += 4 * kBJThreads) {
-                    double2 vc[4], vj[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = e0 + u * kBJThreads;
-                        if (e < cnt * l2) {
-                            const int l = e / l2, r = e - l * l2;
-                            vc[u] = Rc2[(long)cols[l] * l2 + r];
-                            vj[u] = J2[(long)cols[l] * l2 + r];
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = e0 + u * kBJThreads;
-                        if (e < cnt * l2) {
-                            C[e] = vc[u];
-                            Jl[e] = vj[u];
-                        }
-                    }
+                // columns in: every 16-byte piece as its own cp.async (L2 -> shared, no register
+                // staging), all in flight at once; the scratch was written by other CTAs before
+                // the last grid barrier, and .cg reads it from L2
+                for (int e = tid; e < cnt * l2; e += kBJThreads) {
+                    const int l = e / l2, r = e - l * l2;
+                    cp_async16(C + e, Rc2 + (long)cols[l] * l2 + r);
+                    cp_async16(Jl + e, J2 + (long)cols[l] * l2 + r);
                 }
+                asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
                 __syncthreads();
+                // The first round of a sweep visits every pair of the CTA's 16 columns (so each
+                // block's own pairs are covered once per sweep); later rounds only the 8 x 8
+                // pairs across the two blocks: 8 inner rounds instead of 15, warp w pairs
+                // column w of the first block with column (w + ir) mod 8 of the second.
                 const int spl = (cnt + 1) & ~1;
-                for (int ir = 0; ir < spl - 1; ++ir) {
+                const bool full = round == 0;
+                const int n0 = min(s, (bi + 1) * kBJW) - bi * kBJW;
+                const int inner = full ? spl - 1 : kBJW;
+                for (int ir = 0; ir < inner; ++ir) {
                     const int pk = warp;
-                    bool live = pk < spl / 2;
+                    bool live;
                     int i = 0, j = 0;
-                    if (live) {
-                        i = bj_rr(pk, ir, spl);
-                        j = bj_rr(spl - 1 - pk, ir, spl);
-                        if (i > j) { const int t = i; i = j; j = t; }
-                        live = j < cnt;
+                    if (full) {
+                        live = pk < spl / 2;
+                        if (live) {
+                            i = bj_rr(pk, ir, spl);
+                            j = bj_rr(spl - 1 - pk, ir, spl);
+                            if (i > j) { const int t = i; i = j; j = t; }
+                            live = j < cnt;
+                        }
+                    } else {
+                        i = pk;
+                        j = n0 + (pk + ir) % kBJW;
+                        live = i < n0 && j < cnt;
                     }
                     if (live) {  // warp-uniform
                         double2* ci = C + i * l2;
