@@ -20,6 +20,13 @@
 // Both support split-K into fixed partial slabs that rsvd_reduce_partials
 // sums in a fixed order, so every result is deterministic run to run.
 //
+// The passes over A with a sketch width s whose last s % 8 <= 4 columns would fill a padded
+// n8 MMA tile (s = 74, 42, ...) run those columns as DFMA partial dot products instead
+// (ax only, TAIL / SKIP variants): DMMA and DFMA share the FP64 datapath at the same rate
+// per flop, so the pipe then does s columns of work instead of round_up(s, 8). (The atx
+// shape was measured slower with the one-warp-column layout the tail needs: its scalar
+// fragment loads make it shared-memory-issue bound.)
+//
 // Bank-conflict-free fragment loads from the 128B-swizzled boxes come from
 // permuting which physical k each MMA k-slot reads (the same permutation on
 // both operands, so the product is unchanged):
@@ -147,7 +154,14 @@ __device__ __forceinline__ void gram_epilogue(char* smem, const double (&acc)[BM
 // over the tile's rows < M and columns < resid_cols (R = resid, ld resid_ld) and writes
 // the CTA's partial to resid_out[blockIdx.x] — the fused ||A - U S V^T||_F of
 // RsvdResult::residual_fro (rsvd.cpp:37-49), one column chunk per launch.
-template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK, bool RESID = false>
+// TAIL (> 0, WN == 1 only): X has nonzero rows only below 8 * nd + TAIL, nd = NT - SKIP.
+// Column tiles [0, nd) run on DMMA, the TAIL columns after them as DFMA partial dot
+// products over each thread's own k-slots (reduced across the 4 k-lanes once, after the main loop), and the
+// tiles beyond are zero. DMMA and DFMA share the FP64 datapath at the same rate per flop
+// (tools/probe/mixed_fp64.cu), so this removes the padding of s up to the MMA's n8 granule
+// from the pipe: s = 74 costs 74 columns of FP64 work instead of 80.
+template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK, bool RESID = false, int TAIL = 0,
+          int SKIP = 0>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_ax_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {K, M}, box {16, BM}
                    const __grid_constant__ CUtensorMap mapX,  // dims {K, NP}, box {16, NP}
@@ -164,6 +178,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     constexpr uint32_t kStage = 2 * kABox + 2 * kXBox;
     static_assert(MI >= 1 && NI >= 1 && BM % (16 * WM) == 0 && NT % WN == 0, "tiling");
     static_assert(kABox % 1024 == 0 && kXBox % 1024 == 0, "swizzle alignment");
+    static_assert(TAIL == 0 || (WN == 1 && TAIL <= 4), "tail columns need WN == 1");
 
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -172,6 +187,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM;
+    constexpr int nd = NT - SKIP;  // DMMA column tiles (compile-time: acc stays in registers)
+    static_assert(TAIL == 0 ? SKIP == 0 : (SKIP >= 1 && SKIP <= 2), "tail layout");
     const int kt0 = blockIdx.y * k_tiles_per_split;
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
     const int n_iter = max(0, kt1 - kt0);
@@ -223,6 +240,13 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         for (int j = 0; j < NI; ++j)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+    double tl[MI][2][TAIL > 0 ? TAIL : 1];  // tail partial sums: rows g, g + 8
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < (TAIL > 0 ? TAIL : 1); ++j) tl[i][h][j] = 0.0;
     bool bad = false;
 
     for (int it = 0; it < n_iter; ++it) {
@@ -254,22 +278,67 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
             }
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
-                const int n = (wn * NI + ni) * 8 + g;
-                double b[4];
+                if (TAIL == 0 || ni < nd) {  // warp-uniform
+                    const int n = (wn * NI + ni) * 8 + g;
+                    double b[4];
 #pragma unroll
-                for (int qq = 0; qq < 2; ++qq) {
-                    const double2 p = lds_f64x2(boxX, swz128(n, k_ax(t, 2 * qq)));
-                    b[2 * qq] = p.x;
-                    b[2 * qq + 1] = p.y;
+                    for (int qq = 0; qq < 2; ++qq) {
+                        const double2 p = lds_f64x2(boxX, swz128(n, k_ax(t, 2 * qq)));
+                        b[2 * qq] = p.x;
+                        b[2 * qq + 1] = p.y;
+                    }
+#pragma unroll
+                    for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], a[mi], b);
                 }
+            }
+            if constexpr (TAIL > 0) {
+                // a[mi][h + 2 q] holds A[row g + 8h][k = 4t + q]; X row c, k = 4t .. 4t + 3
 #pragma unroll
-                for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], a[mi], b);
+                for (int j = 0; j < TAIL; ++j) {
+                    const int c = nd * 8 + j;
+                    const double2 x0 = lds_f64x2(boxX, swz128(c, k_ax(t, 0)));
+                    const double2 x1 = lds_f64x2(boxX, swz128(c, k_ax(t, 2)));
+#pragma unroll
+                    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            tl[mi][h][j] = fma(a[mi][h + 6], x1.y, fma(a[mi][h + 4], x1.x,
+                                           fma(a[mi][h + 2], x0.y, fma(a[mi][h], x0.x,
+                                                                       tl[mi][h][j]))));
+                }
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
     if (CHECK && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+    if constexpr (TAIL > 0) {
+        // sum the tail over the 4 k-lanes, then place it in tile nd's accumulator layout
+        // (lane t holds columns 8 nd + 2t, 2t + 1)
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < TAIL; ++j) {
+                    double v = tl[mi][h][j];
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    tl[mi][h][j] = v;
+                }
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni)
+            if (ni == nd)
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int v = 0; v < 2; ++v)  // explicit selects: no dynamic index
+                            acc[mi][ni][2 * h + v] =
+                                t == 0 ? tl[mi][h][v]
+                                       : (TAIL > 2 && t == 1 ? tl[mi][h][TAIL > 2 ? 2 + v : 0] : 0.0);
+    }
 
     // --------------------------------------------------------------- epilogue
     if constexpr (RESID) {
@@ -516,12 +585,13 @@ int make_map(CUtensorMap* map, const double* base, long rows, long cols, long ld
     return r == CUDA_SUCCESS ? 0 : -3;
 }
 
-template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK, bool RESID = false>
+template <int BM, int NT, int WM, int WN, int STAGES, bool CHECK, bool RESID = false, int TAIL = 0,
+          int SKIP = 0>
 cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     constexpr int NP = NT * 8;
     constexpr size_t kStage = 2 * BM * 128 + 2 * NP * 128;
     constexpr size_t smem = STAGES * kStage + 2 * STAGES * 8 + 1024;
-    auto kern = gemm_ax_kernel<BM, NT, WM, WN, STAGES, CHECK, RESID>;
+    auto kern = gemm_ax_kernel<BM, NT, WM, WN, STAGES, CHECK, RESID, TAIL, SKIP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mA, mX;
@@ -563,9 +633,32 @@ cudaError_t launch_atx_t(const GemmAtx& p, cudaStream_t st) {
 
 // NP (padded sketch width) dispatch. Widths up to 96 use 128-row tiles with a
 // 4x2 warp grid and 4 stages; wider sketches use 64-row tiles, 2x4 warps, 3 stages.
+// Tail split for a product whose Xt has nonzero rows only below `cols`: 0 = plain
+// DMMA tiles, else 4 * (NT - nd) + tail with nd = cols / 8 DMMA tiles and a DFMA tail of
+// 2 or 4 columns (cols % 8 in [1, 4]; NT - nd is 1 or 2 for NP = cols rounded up to 16).
+inline int tail_code(int cols, int NT) {
+    if (cols <= 0 || cols >= NT * 8) return 0;
+    const int r = cols % 8, skip = NT - cols / 8;
+    if (r == 0 || r > 4 || skip < 1 || skip > 2) return 0;
+    return 4 * skip + (r <= 2 ? 2 : 4);
+}
+
+template <int NT, bool CHECK>
+cudaError_t launch_ax_tail(const GemmAx& p, cudaStream_t st, int code) {
+    switch (code) {
+        case 6: return launch_ax_t<128, NT, 8, 1, 4, CHECK, false, 2, 1>(p, st);
+        case 8: return launch_ax_t<128, NT, 8, 1, 4, CHECK, false, 4, 1>(p, st);
+        case 10: return launch_ax_t<128, NT, 8, 1, 4, CHECK, false, 2, 2>(p, st);
+        default: return launch_ax_t<128, NT, 8, 1, 4, CHECK, false, 4, 2>(p, st);
+    }
+}
+
 template <int NT>
 cudaError_t dispatch_ax(const GemmAx& p, cudaStream_t st) {
     if constexpr (NT <= 12) {
+        if (const int code = tail_code(p.cols, NT))
+            return p.flag ? launch_ax_tail<NT, true>(p, st, code)
+                          : launch_ax_tail<NT, false>(p, st, code);
         return p.flag ? launch_ax_t<128, NT, 4, 2, 4, true>(p, st)
                       : launch_ax_t<128, NT, 4, 2, 4, false>(p, st);
     } else if constexpr (NT > 24) {  // sketches wider than 192: 2 stages fit in smem

@@ -30,6 +30,10 @@ struct GemmAx {
     long resid_ld = 0;
     int resid_cols = 0;
     double* resid_out = nullptr;
+    // > 0: rows >= cols of Xt are zero (a sketch of width cols < NP). NP <= 96 then runs the
+    // last cols % 8 (<= 4) columns as DFMA instead of a padded DMMA tile; output columns
+    // >= cols come out zero as before.
+    int cols = 0;
 };
 
 // Z = A^T * W.  A: K x N row-major (lda), W: K x NP row-major (ldw).

@@ -190,10 +190,12 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
                 // columns in: every 16-byte piece as its own cp.async (L2 -> shared, no register
                 // staging), all in flight at once; the scratch was written by other CTAs before
                 // the last grid barrier, and .cg reads it from L2
-                for (int e = tid; e < cnt * l2; e += kBJThreads) {
-                    const int l = e / l2, r = e - l * l2;
-                    cp_async16(C + e, Rc2 + (long)cols[l] * l2 + r);
-                    cp_async16(Jl + e, J2 + (long)cols[l] * l2 + r);
+                for (int l = warp; l < cnt; l += kBJThreads / 32) {
+                    const long src = (long)cols[l] * l2;
+                    for (int r = lane; r < l2; r += 32) {
+                        cp_async16(C + l * l2 + r, Rc2 + src + r);
+                        cp_async16(Jl + l * l2 + r, J2 + src + r);
+                    }
                 }
                 asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
                 __syncthreads();
@@ -272,10 +274,12 @@ __global__ void __launch_bounds__(kBJThreads, 1) block_jacobi_kernel(
                 }
                 double2* Rcw = reinterpret_cast<double2*>(Rc);
                 double2* Jw = reinterpret_cast<double2*>(J);
-                for (int e = tid; e < cnt * l2; e += kBJThreads) {
-                    const int l = e / l2, r = e - l * l2;
-                    Rcw[(long)cols[l] * l2 + r] = C[e];
-                    Jw[(long)cols[l] * l2 + r] = Jl[e];
+                for (int l = warp; l < cnt; l += kBJThreads / 32) {
+                    const long dst = (long)cols[l] * l2;
+                    for (int r = lane; r < l2; r += 32) {
+                        Rcw[dst + r] = C[l * l2 + r];
+                        Jw[dst + r] = Jl[l * l2 + r];
+                    }
                 }
             }
             if (__syncthreads_or(rotated) && tid == 0) atomicOr(&sweep_flag[sweeps - 1], 1);

@@ -393,11 +393,15 @@ long ax_tiles(long M, int NP) { return (M + (NP <= 96 ? 127 : 63)) / (NP <= 96 ?
 // Y (M x NP) = A (M x K) * X where Xt (NP x K) holds X^T. If `gram_out` is given and the
 // launch can fuse it (NP <= 96, no split-K), the Gram Y^T Y is produced by the GEMM's
 // epilogue and reduced into gram_out (NP x NP); returns whether that happened.
+// cols > 0: Xt's rows >= cols are zero (the sketch width s of an A-pass); lets the kernel
+// drop the MMA padding of s (GemmAx::cols).
 bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, const double* Xt,
              long ldx, int NP, double* Y, long ldy, int* flag = nullptr,
-             const char* tag = nullptr, double flops = 0.0, double* gram_out = nullptr) {
+             const char* tag = nullptr, double flops = 0.0, double* gram_out = nullptr,
+             int cols = 0) {
     GemmAx g{A, M, K, lda, Xt, ldx, NP, Y, ldy};
     g.flag = flag;
+    g.cols = cols;
     const int splits = choose_splits(ax_tiles(M, NP), (K + 31) / 32);
     if (splits == 1) {
         const bool fuse = gram_out && NP <= 96;
@@ -436,7 +440,7 @@ bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, con
 // Gram partials line up with the unchunked launch's.
 bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long lda,
                      const double* Xt, long ldx, int NP, double* Y, long ldy, int* flag,
-                     const char* tag, double flops, double* gram_out) {
+                     const char* tag, double flops, double* gram_out, int cols) {
     const bool fuse = gram_out && NP <= 96;
     if (fuse && h->gpart.bytes < (size_t)ax_tiles(M, NP) * NP * NP * sizeof(double))
         fail(RSVD_B200_ALLOC_ERROR, "Gram workspace too small");
@@ -447,6 +451,7 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
         ck(cudaStreamWaitEvent(h->stream, h->up_ev[c], 0), "wait for chunk upload");
         GemmAx g{A + r0 * lda, r1 - r0, K, lda, Xt, ldx, NP, Y + r0 * ldy, ldy};
         g.flag = flag;
+        g.cols = cols;
         if (fuse) g.gram = h->gpart.d() + tile0 * NP * NP;
         h->launched(launch_gemm_ax(g, h->stream), "gemm_ax(chunk)");
         tile0 += ax_tiles(r1 - r0, NP);
@@ -976,13 +981,13 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
     if (h->up_active && A == h->a_copy.d() && !p.sharded) {
         h->gram_ready = gemm_ax_chunked(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                                         check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
-                                        2.0 * p.m * n * s, c.slot(kG));
+                                        2.0 * p.m * n * s, c.slot(kG), s);
         h->up_active = false;  // every chunk event has been waited on
         return;
     }
     h->gram_ready = gemm_ax(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                             check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
-                            2.0 * p.m * n * s, c.slot(kG));
+                            2.0 * p.m * n * s, c.slot(kG), s);
 }
 
 // ---- power_iterate (rsvd.cpp:61-73): h->y holds Y0; result W = Q1 C (h->q, slot kC).
@@ -1028,7 +1033,8 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
         wide_qr(c, zt, p.n, p.ldn, h->xt.d(), kRB, 1);  // Z = QR(A^T W).q, as Z^T
         h->mark("power_ax");
         h->gram_ready = gemm_ax(h, A, p.m, p.n, p.lda, h->xt.d(), p.ldn, p.NP, h->y.d(), p.NP,
-                                nullptr, "gemm_A", 2.0 * p.m * p.n * p.s, c.slot(kG));  // Y = A Z
+                                nullptr, "gemm_A", 2.0 * p.m * p.n * p.s, c.slot(kG),
+                                p.s);  // Y = A Z
         h->mark("qr_tall");
         const bool last = round + 1 == q;
         tall_qr(c, h->y.d(), p.m, h->q.d(), last ? 2 : 1, materialize && last,

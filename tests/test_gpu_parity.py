@@ -381,3 +381,22 @@ def test_chunked_upload_bit_identical(solver, port, monkeypatch):
     assert np.array_equal(res.factors.u, res1.factors.u)
     with pytest.raises(P.ArgumentError):
         solver.randomized_ksvd(a, cfg, out=(np.empty((m, k + 1)), np.empty(k), np.empty((n, k))))
+
+
+# Sketch widths whose last s % 8 (<= 4) columns run as DFMA tails next to the DMMA tiles
+# (gemm_f64.cu TAIL / SKIP variants: NP = s rounded up to 16 leaves 1 or 2 padded tiles),
+# plus neighbours that take the plain DMMA kernels. Same parity bar as every FP64 solve.
+@pytest.mark.parametrize("s", [9, 10, 12, 17, 20, 25, 34, 36, 42, 49, 58, 66, 74, 76, 81, 90, 92])
+def test_tail_columns_vs_oracle(solver, port, s):
+    import paper_2110_03423_b200 as P
+    m, n = 1500, 400
+    p = min(10, s - 1)
+    k = s - p
+    rng = np.random.default_rng(s)
+    uu, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = np.exp(-np.arange(n) * (np.log(1e4) / s))
+    a = (uu * sig) @ vv.T
+    res = solver.randomized_ksvd(a, P.RsvdConfig(k=k, oversample=p, power_q=2, seed=11))
+    ref = port.randomized_ksvd(a, k, oversample=p, power_q=2, seed=11)
+    check_against(res, ref.sigma, ref.u, ref.v, f"s={s}")
