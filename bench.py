@@ -390,7 +390,10 @@ def run_ours(args):
     rank, world, local_rank = dist_env()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    # sharded: the row-sharded NCCL solve (always for N > 1; --sharded forces it at N = 1, a
+    # one-rank NCCL communicator, to exercise the multi-GPU path on a single GPU)
+    sharded = world > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfgd = CONFIGS[args.config]
@@ -400,15 +403,15 @@ def run_ours(args):
     cfg = P.RsvdConfig(k=k, oversample=p, power_q=q, seed=SEED)
     F = flops(m_total, n, k, p, q)
     solver = P.Solver(local_rank)
-    if world > 1:
+    if sharded:
         P.attach_process_group(solver)
 
     def solve_dev(a):
         if f32:
-            if world > 1:
+            if sharded:
                 return solver.randomized_ksvd_sharded_f32_device(a, m_total, cfg)
             return solver.randomized_ksvd_f32_device(a, cfg)
-        if world > 1:
+        if sharded:
             return solver.randomized_ksvd_sharded_device(a, m_total, cfg)
         return solver.randomized_ksvd_device(a, cfg)
 
@@ -418,10 +421,10 @@ def run_ours(args):
 
     def solve_host(a_host):
         if f32:
-            if world > 1:
+            if sharded:
                 return solver.randomized_ksvd_sharded_f32(a_host, m_total, cfg, out=e2e_out)
             return solver.randomized_ksvd_f32(a_host, cfg, out=e2e_out)
-        if world > 1:
+        if sharded:
             return solver.randomized_ksvd_sharded(a_host, m_total, cfg, out=e2e_out)
         return solver.randomized_ksvd(a_host, cfg, out=e2e_out)
 
@@ -435,7 +438,7 @@ def run_ours(args):
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if sharded:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
@@ -548,7 +551,7 @@ def run_ours(args):
             "data": f"synthetic ({cfgd['spectrum']} spectrum, seed 42)",
             "config": {"workload": cfgd["name"], "m": m_total, "m_per_gpu": m, "n": n, "k": k,
                        "p": p, "q": q, "sketch_width": sw,
-                       "parallelism": f"row-sharded x{world} (NCCL)" if world > 1 else "single GPU",
+                       "parallelism": f"row-sharded x{world} (NCCL)" if sharded else "single GPU",
                        "l2": f"A ({m * n * (4 if f32 else 8) / 1e9:.1f} GB per GPU) >> L2 (126 MB): every pass "
                              "streams HBM, no flush"},
             "clocks": clocks.summary(),
@@ -556,7 +559,7 @@ def run_ours(args):
                     "ms_per_step": round(1e3 * e2e_s, 2),
                     "h2d_bytes_per_step": m * n * (4 if f32 else 8),
                     "d2h_bytes_per_step": (m * k + n * k + k) * 8,
-                    "api": ("rsvd_b200_randomized_ksvd" + ("_sharded" if world > 1 else "")
+                    "api": ("rsvd_b200_randomized_ksvd" + ("_sharded" if sharded else "")
                             + ("_f32" if f32 else "")
                             + " (host buffers: pinned A in, pinned reused out= U, sigma, V)")},
             "gpu_launches": launches_per_step * args.steps,
@@ -568,7 +571,7 @@ def run_ours(args):
             "sigma1": sigma1,
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if sharded:
         solver.detach()
         torch.distributed.destroy_process_group()
 
@@ -578,6 +581,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the row-sharded NCCL solve even at one GPU (tests the N > 1 path)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--cpu-rows", type=int, default=0)
