@@ -3,7 +3,7 @@
 // multi-CTA block Jacobi, used for every s > 64 (more SMs, 8 warps each, beat one CTA's
 // 32 IPC-bound warps):
 //   * small_gemm_kernel — generic C = alpha op(A) op(B) + beta Cin on s-sized
-//     operands (tiles of 32 x 32 per CTA), the building block of the blocked Cholesky
+//     operands (tiles of 16 x 16 per CTA), the building block of the blocked Cholesky
 //     that rsvd_b200.cpp assembles from two in-smem Cholesky factorisations;
 //   * block_jacobi_kernel — one-sided block Jacobi SVD of the s x s triangular factor
 //     R_B, the wide-sketch twin of jacobi_kernel (linalg_small.cu). Columns live in
@@ -34,40 +34,42 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 // C (M x N, ldc) = alpha * op(A) op(B) + beta * Cin (ldcin); op(A) is M x K,
 // op(B) K x N; ta / tb: the operand is stored transposed (row-major K x M / N x K).
 // Cin may alias C (each element is read before it is written by the same thread).
+// 16 x 16 output tiles (one output per thread, so an s = 136 block spans 81 CTAs), K in
+// chunks of 32; both operand tiles are loaded along their contiguous dimension whatever the
+// transposition (coalesced), and transposed on the way into shared memory.
 __global__ void __launch_bounds__(256) small_gemm_kernel(int M, int N, int K, double alpha,
                                                          const double* __restrict__ A, long lda,
                                                          bool ta, const double* __restrict__ B,
                                                          long ldb, bool tb, double beta,
                                                          const double* Cin, long ldcin,
                                                          double* C, long ldc) {
-    __shared__ double As[32][33], Bs[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    __shared__ double As[16][33];  // As[r][k] = op(A)[i0 + r][k0 + k]
+    __shared__ double Bs[32][17];  // Bs[k][c] = op(B)[k0 + k][j0 + c]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int i0 = blockIdx.y * 16, j0 = blockIdx.x * 16;
+    double acc = 0.0;
     for (int k0 = 0; k0 < K; k0 += 32) {
-        for (int r = ty; r < 32; r += 8) {
-            const int i = i0 + r, k = k0 + tx;  // As[r][tx] = op(A)[i][k]
-            As[r][tx] = (i < M && k < K) ? (ta ? A[(long)k * lda + i] : A[(long)i * lda + k]) : 0.0;
-            const int kk = k0 + r, j = j0 + tx;  // Bs[r][tx] = op(B)[kk][j]
-            Bs[r][tx] = (kk < K && j < N) ? (tb ? B[(long)j * ldb + kk] : B[(long)kk * ldb + j]) : 0.0;
+#pragma unroll
+        for (int e = tid; e < 512; e += 256) {
+            int r, k;
+            if (ta) { k = e >> 4; r = e & 15; } else { r = e >> 5; k = e & 31; }
+            const int i = i0 + r, kk = k0 + k;
+            As[r][k] = (i < M && kk < K) ? (ta ? A[(long)kk * lda + i] : A[(long)i * lda + kk]) : 0.0;
+            int c, kb;
+            if (tb) { c = e >> 5; kb = e & 31; } else { kb = e >> 4; c = e & 15; }
+            const int j = j0 + c, kj = k0 + kb;
+            Bs[kb][c] = (kj < K && j < N) ? (tb ? B[(long)j * ldb + kj] : B[(long)kj * ldb + j]) : 0.0;
         }
         __syncthreads();
 #pragma unroll 8
-        for (int kk = 0; kk < 32; ++kk) {
-            const double b = Bs[kk][tx];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][kk], b, acc[q]);
-        }
+        for (int kk = 0; kk < 32; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
         __syncthreads();
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int i = i0 + ty + 8 * q, j = j0 + tx;
-        if (i < M && j < N) {
-            double v = alpha * acc[q];
-            if (beta != 0.0) v += beta * Cin[(long)i * ldcin + j];
-            C[(long)i * ldc + j] = v;
-        }
+    const int i = i0 + ty, j = j0 + tx;
+    if (i < M && j < N) {
+        double v = alpha * acc;
+        if (beta != 0.0) v += beta * Cin[(long)i * ldcin + j];
+        C[(long)i * ldc + j] = v;
     }
 }
 
@@ -76,7 +78,7 @@ cudaError_t launch_small_gemm(int M, int N, int K, double alpha, const double* A
                               const double* Cin, long ldcin, double* C, long ldc,
                               cudaStream_t st) {
     if (M <= 0 || N <= 0) return cudaSuccess;
-    dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+    dim3 grid((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16));
     small_gemm_kernel<<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta,
                                             Cin ? Cin : C, Cin ? ldcin : ldc, C, ldc);
     return cudaGetLastError();
