@@ -524,7 +524,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 // Fixed-order sum of split-K slabs: out[e] = sum_s part[s * stride + e]. Threads are
 // laid out 32 elements x 8 split-groups; group g sums splits g, g+8, ... and the 8 group
 // sums are added in a fixed order, so the result is deterministic.
-__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ part,
+// (T = float: the FP32 split-K slabs of the 3xTF32 GEMMs, summed in FP64.)
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const T* __restrict__ part,
                                                               long stride, int splits,
                                                               double* __restrict__ out,
                                                               long count) {
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __re
         const long e = base + lx;
         double acc = 0.0;
         if (e < count)
-            for (int sp = gy; sp < splits; sp += 8) acc += part[sp * stride + e];
+            for (int sp = gy; sp < splits; sp += 8) acc += (double)part[sp * stride + e];
         red[gy][lx] = acc;
         __syncthreads();
         if (gy == 0 && e < count) {
@@ -724,13 +726,24 @@ cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st) {
     }
 }
 
-cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
-                                   long count, cudaStream_t st) {
+template <typename T>
+static cudaError_t launch_reduce_t(const T* part, long stride, int splits, double* out, long count,
+                                   cudaStream_t st) {
     long blocks = (count + 31) / 32;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, stride, splits, out, count);
+    reduce_partials_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(part, stride, splits, out, count);
     return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
+                                   long count, cudaStream_t st) {
+    return launch_reduce_t(part, stride, splits, out, count, st);
+}
+
+cudaError_t launch_reduce_partials_f32(const float* part, long stride, int splits, double* out,
+                                       long count, cudaStream_t st) {
+    return launch_reduce_t(part, stride, splits, out, count, st);
 }
 
 }  // namespace rsvdb200

@@ -713,8 +713,7 @@ cudaError_t launch_p(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap
 
 cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
     if (p.NP < 16 || p.NP > 288 || (p.NP % 16) != 0 || !p.Blo) return cudaErrorInvalidValue;
-    if (!p.out64 && p.splits > 1) return cudaErrorInvalidValue;
-    if (p.out_lo && (p.out64 || p.out_t)) return cudaErrorInvalidValue;
+    if (p.out_lo && (p.out64 || p.out_t || p.splits > 1)) return cudaErrorInvalidValue;
     CUtensorMap mA, mB, mBlo;
     // cta_group::2 variant: correct but measured slower (2.45 ms flat in NP at C4 size against
     // 1.7-2.5 ms for the 1-SM kernel), so opt-in only (RSVD_B200_TF32_2SM=1)

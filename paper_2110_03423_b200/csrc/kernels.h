@@ -92,6 +92,10 @@ cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
 cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);
 cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,
                                    long count, cudaStream_t st);
+// Same over FP32 slabs (out FP64): the split-K partials of the 3xTF32 GEMMs, whose TMEM
+// accumulators are FP32, so storing them as FP32 halves the slab traffic and loses nothing.
+cudaError_t launch_reduce_partials_f32(const float* part, long stride, int splits, double* out,
+                                       long count, cudaStream_t st);
 
 // FP64 tensor-core (DMMA m16n8k16) issue-rate probe on the whole GPU, TFLOP/s.
 cudaError_t measure_dmma_peak(cudaStream_t st, double* tflops);

@@ -513,18 +513,28 @@ void gemm_tf32(rsvd_b200_handle* h, GemmTf32 g, const char* tag = nullptr, doubl
         h->kernel_end(tag);
         return;
     }
+    // the slabs hold the TMEM accumulators, which are FP32: stored as FP32 (exactly), summed
+    // in FP64 in a fixed order — half the slab traffic of FP64 slabs, the same result
+    // (row-major FP32 stores are float4: FP64 slabs unless every row stays 16-byte aligned)
     const long slab = g.out_t ? (long)g.NP * g.ldo : g.M * g.ldo;
-    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+    const bool f32_slabs = g.out_t || (g.ldo % 4 == 0 && slab % 4 == 0);
+    if (h->part.bytes < (size_t)splits * slab * (f32_slabs ? sizeof(float) : sizeof(double)))
         fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
     double* out = static_cast<double*>(g.out);
     g.out = h->part.p;
+    g.out64 = !f32_slabs;
     g.splits = splits;
     g.split_stride = slab;
     h->kernel_begin(tag, flops);
     h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32(split)");
     h->kernel_end(tag);
-    h->launched(launch_reduce_partials(h->part.d(), slab, splits, out, slab, h->stream),
-                "reduce_partials");
+    if (f32_slabs)
+        h->launched(launch_reduce_partials_f32(static_cast<const float*>(h->part.p), slab, splits,
+                                               out, slab, h->stream),
+                    "reduce_partials");
+    else
+        h->launched(launch_reduce_partials(h->part.d(), slab, splits, out, slab, h->stream),
+                    "reduce_partials");
 }
 
 // Largest split-K slab set any GEMM of a plan needs.
