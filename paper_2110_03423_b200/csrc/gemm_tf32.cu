@@ -141,18 +141,21 @@ __host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
 
 // Drain the 128 x NP FP32 accumulator (warps 2-5: each its TMEM lane quarter) and store it
 // (FP32 + lo parts, FP64, or transposed), slab blockIdx.y of a split-K launch.
+// c_off > 0 (upper-triangle Gram): the accumulator holds output columns c_off.. at TMEM
+// column 0; columns below c_off are written as zeros.
 template <bool OUT64, bool OUT_T>
 __device__ __forceinline__ void epilogue(uint32_t tmem, int warp, int lane, int m0, int M, int NP,
                                          bool have, void* __restrict__ out,
-                                         float* __restrict__ out_lo, long ldo, long split_stride) {
+                                         float* __restrict__ out_lo, long ldo, long split_stride,
+                                         int c_off) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = m0 + 32 * q + lane;
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     char* ob = reinterpret_cast<char*>(out) + (size_t)blockIdx.y * split_stride * (OUT64 ? 8 : 4);
     for (int c0 = 0; c0 < NP; c0 += 16) {
         float v[16];
-        if (have) {
-            tmem_ld16(trow + c0, v);
+        if (have && c0 >= c_off) {
+            tmem_ld16(trow + (c0 - c_off), v);
         } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap mapB,
                      const __grid_constant__ CUtensorMap mapBlo, void* __restrict__ out,
                      float* __restrict__ out_lo, long ldo, long split_stride, int M, int NP,
-                     int k_tiles, int k_tiles_per_split, int* __restrict__ flag) {
+                     int k_tiles, int k_tiles_per_split, int* __restrict__ flag, int upper) {
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                          ~uintptr_t(1023));
@@ -218,6 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
     const int n_iter = max(0, kt1 - kt0);
     const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
+    // upper (a symmetric Gram, MN shape): rows m0.. only need columns m0.. (multiple of 128)
+    const int c_off = (MN && upper) ? min(m0, (NP - 16) & ~31) : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -298,9 +303,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t lay = MN ? 1u : 4u;
             // N > 256 is two MMAs of balanced width (272 = 160 + 112): a narrow second chunk
             // (256 + 16) costs nearly as much as a wide one (measured: NP 272 took 1.45x NP 256)
-            const int n1 = NP > 256 ? ((NP / 2 + 31) & ~31) : NP, n2 = NP - n1;
+            const int ne = NP - c_off;  // columns this CTA computes (c_off: 32-column boxes)
+            const int n1 = ne > 256 ? ((ne / 2 + 31) & ~31) : ne, n2 = ne - n1;
             const uint32_t id1 = idesc(n1, MN), id2 = n2 > 0 ? idesc(n2, MN) : 0u;
             const uint32_t co = (uint32_t)n1 * (MN ? kBoxMN / 32u : BK * 4u);  // B offset of chunk 2
+            const uint32_t bo = (uint32_t)(c_off / 32) * kBoxMN;  // B offset of column c_off
             auto issue = [&](uint32_t a, uint32_t b, uint32_t acc0) {
 #pragma unroll
                 for (int ks = 0; ks < BK / 8; ++ks) {
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = it % kStages;
                 const uint32_t st = smem_u32(smem + s * kStage);
                 const uint32_t a_raw = st, a_lo = st + kABytes;
-                const uint32_t b_raw = st + 2 * kABytes, b_lo = b_raw + bB;
+                const uint32_t b_raw = st + 2 * kABytes + bo, b_lo = b_raw + bB;
                 mbar_wait(&full[s], (it / kStages) & 1);
                 fence_after();
                 issue(a_raw, b_raw, it > 0 ? 1u : 0u);  // a_hi b_hi
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_after();
         }
         epilogue<OUT64, OUT_T>(tmem, warp, lane, m0, M, NP, n_iter > 0, out, out_lo, ldo,
-                               split_stride);
+                               split_stride, c_off);
     }
     fence_before();
     // PAIR: the peer's last commits arrive on our empty barriers; they precede its accum
@@ -589,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_after();
         }
         epilogue<OUT64, OUT_T>(tmem, warp, lane, m0, M, NP, n_iter > 0, out, out_lo, ldo,
-                               split_stride);
+                               split_stride, 0);
     }
     fence_before();
     cluster_sync();  // no multicast commit or remote arrive is still in flight into the peer
@@ -664,7 +671,7 @@ cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, mA, mB, mBlo, p.out, static_cast<float*>(p.out_lo), p.ldo,
-                           p.split_stride, (int)p.M, p.NP, k_tiles, per, p.flag);
+                           p.split_stride, (int)p.M, p.NP, k_tiles, per, p.flag, (int)p.upper);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -73,6 +73,10 @@ struct GemmTf32 {
     int splits = 1;
     long split_stride = 0;
     int* flag = nullptr;
+    // mn with A == B (a Gram X^T X): compute only the column tiles at or right of each
+    // 128-row tile's diagonal block; everything left of it is written as zero (the upper
+    // triangle, all a Cholesky reads, is exact)
+    bool upper = false;
 };
 cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st);
 // out (rows x cols, FP32, ldo) = in (FP64, ldi) for r < rows_valid and c < cols_valid, else 0.

@@ -765,6 +765,7 @@ bool tall_qr_f32(const Ctx& c, long M, int passes) {
         GemmTf32 g{X, (long)NPf, M, (long)NPf, X, (long)NPf, NPf, c.slot(kG), (long)NP};
         g.Blo = Xlo;
         g.mn = true;
+        g.upper = true;  // the Cholesky reads the upper triangle only
         gemm_tf32(h, g);
         c.allreduce(c.slot(kG), (size_t)NP * NP);
     };
