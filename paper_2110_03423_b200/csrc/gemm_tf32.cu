@@ -708,11 +708,19 @@ cudaError_t launch_2sm(const GemmTf32& p, const CUtensorMap& mA, const CUtensorM
     return cudaGetLastError();
 }
 
+// 2-CTA clusters sharing B: only for more than one M tile, and for an odd count only when
+// the idle pad tile it needs is a small fraction (with few M tiles, e.g. the s x s Gram's 3,
+// it would cost a whole extra wave of the split-K grid)
+bool use_pair(const GemmTf32& p) {
+    static const bool pair = !getenv("RSVD_B200_TF32_NO_PAIR");
+    const long tiles = (p.M + tf32::BM - 1) / tf32::BM;
+    return pair && tiles > 1 && (tiles % 2 == 0 || tiles >= 16);
+}
+
 template <bool MN, bool OUT64, bool OUT_T>
 cudaError_t launch_p(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
                      const CUtensorMap& mBlo, cudaStream_t st) {
-    static const bool pair = !getenv("RSVD_B200_TF32_NO_PAIR");
-    if (pair && p.M > tf32::BM) return launch_t<MN, OUT64, OUT_T, true>(p, mA, mB, mBlo, st);
+    if (use_pair(p)) return launch_t<MN, OUT64, OUT_T, true>(p, mA, mB, mBlo, st);
     return launch_t<MN, OUT64, OUT_T, false>(p, mA, mB, mBlo, st);
 }
 
@@ -750,7 +758,7 @@ cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
     if (!p.mn) {  // A: M x K (lda), Bt: NP x K (ldb); 64-byte rows of K
         // one box per B half: the paired kernel loads NP / 2 rows per CTA, the single one
         // NP (<= 256) or two halves
-        const int brows = (p.NP > 256 || (p.M > tf32::BM && !getenv("RSVD_B200_TF32_NO_PAIR")))
+        const int brows = (p.NP > 256 || use_pair(p))
                               ? p.NP / 2
                               : p.NP;
         const auto sw = CU_TENSOR_MAP_SWIZZLE_64B;
