@@ -202,6 +202,11 @@ struct rsvd_b200_handle {
     bool c_identity = true;  // the current basis Q = Q1 C has C = I
     double* basis = nullptr;  // Q1 of the current basis (h->y or h->q)
     bool gram_ready = false;  // slot kG holds Y^T Y of the last produced Y
+    // host-buffer solves: the first power iteration's A^T Y0 split-K slabs were produced during
+    // the chunked upload (sketch_dev); power_iterate_dev only reduces them
+    bool aty_pending = false;
+    int aty_splits = 0;
+    long aty_slab = 0;
     DevBuf gpart;             // per-tile Gram partials of the fused epilogue
     int* flags_host = nullptr;
     std::vector<double> omega_host;  // validation mode (n x s row-major)
@@ -438,9 +443,38 @@ bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, con
 // chunk c's launch waits for its copy event, so the sketch runs behind the H2D copy and
 // only the last chunk's GEMM is exposed. Chunks are whole 128/64-row tiles, so the fused
 // Gram partials line up with the unchunked launch's.
+// aty_ldz > 0: also produce the split-K slabs of (A^T Y)^T (the first power iteration's
+// A-pass, Y = this sketch, ld aty_ldz) into h->part, split j as soon as the chunks holding its
+// rows are sketched. The splits are exactly gemm_atx's (choose_splits, same k-tile ranges, same
+// kernel), so the slabs — and the reduced result — are bit-identical to gemm_atx's.
 bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long lda,
                      const double* Xt, long ldx, int NP, double* Y, long ldy, int* flag,
-                     const char* tag, double flops, double* gram_out, int cols) {
+                     const char* tag, double flops, double* gram_out, int cols,
+                     long aty_ldz = 0) {
+    int aty_splits = 0;
+    long per_rows = 0, slab = 0;
+    if (aty_ldz > 0) {
+        aty_splits = choose_splits(ax_tiles(K, NP), (M + 31) / 32);
+        per_rows = (((M + 31) / 32 + aty_splits - 1) / aty_splits) * 32;
+        slab = (long)NP * aty_ldz;
+        if (aty_splits < 2 || h->part.bytes < (size_t)aty_splits * slab * sizeof(double))
+            aty_splits = 0;  // gemm_atx would not split (or no room): leave it to the pass
+    }
+    int next_split = 0;
+    auto launch_aty = [&](long rows_done) {
+        while (next_split < aty_splits &&
+               std::min(M, (long)(next_split + 1) * per_rows) <= rows_done) {
+            const long r0 = next_split * per_rows, rows = std::min(M, r0 + per_rows) - r0;
+            double* z = h->part.d() + next_split * slab;
+            if (rows <= 0) {
+                h->launched(launch_fill(z, slab, 0.0, h->stream), "fill");
+            } else {
+                GemmAtx g{A + r0 * lda, rows, K, lda, Y + r0 * ldy, ldy, NP, z, aty_ldz, true};
+                h->launched(launch_gemm_atx(g, h->stream), "gemm_atx(upload split)");
+            }
+            ++next_split;
+        }
+    };
     const bool fuse = gram_out && NP <= 96;
     if (fuse && h->gpart.bytes < (size_t)ax_tiles(M, NP) * NP * NP * sizeof(double))
         fail(RSVD_B200_ALLOC_ERROR, "Gram workspace too small");
@@ -455,8 +489,14 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
         if (fuse) g.gram = h->gpart.d() + tile0 * NP * NP;
         h->launched(launch_gemm_ax(g, h->stream), "gemm_ax(chunk)");
         tile0 += ax_tiles(r1 - r0, NP);
+        launch_aty(r1);
     }
     h->kernel_end(tag);
+    if (aty_splits > 0) {
+        h->aty_pending = true;
+        h->aty_splits = aty_splits;
+        h->aty_slab = slab;
+    }
     if (fuse)
         h->launched(launch_reduce_partials(h->gpart.d(), (long)NP * NP, (int)tile0, gram_out,
                                            (long)NP * NP, h->stream),
@@ -915,6 +955,7 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(p.s)) * sizeof(double));
     h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
     ck(cudaMemsetAsync(h->flags.p, 0, kNumFlags * sizeof(int), h->stream), "memset flags");
+    h->aty_pending = false;
     if (p.f32)  // the 3xTF32 A-pass writes rows < NPf of (A^T Q)^T / Q^T A; pad rows stay 0
         ck(cudaMemsetAsync(h->b.p, 0, (size_t)NP * p.ldn * sizeof(double), h->stream), "memset b");
     h->trace = getenv("RSVD_B200_TRACE") ? atoi(getenv("RSVD_B200_TRACE")) : 0;
@@ -943,7 +984,9 @@ void atx_a_f32(const Ctx& c) {
 // ---- sketch (rsvd.cpp:51-59): h->y (m x NP) = A * Omega, Omega from the device
 // generator or the validation-mode host Omega; `check` fuses the NaN/Inf scan of A
 // (validate, rsvd.cpp:144) into this first pass over A.
-void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
+// pre_aty: the solve continues with power iterations whose first A^T W reads W = Y0 in
+// factored form (tall_qr with one pass) — a chunked upload then also produces its slabs.
+void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool pre_aty = false) {
     rsvd_b200_handle* h = c.h;
     const Plan& p = c.p;
     cudaStream_t st = h->stream;
@@ -990,9 +1033,12 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check) {
         return;
     }
     if (h->up_active && A == h->a_copy.d() && !p.sharded) {
+        // (only with the fused Gram: otherwise the Gram GEMM would reuse h->part first)
         h->gram_ready = gemm_ax_chunked(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                                         check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
-                                        2.0 * p.m * n * s, c.slot(kG), s);
+                                        2.0 * p.m * n * s, c.slot(kG), s,
+                                        pre_aty && NP <= 96 ? p.ldn : 0);
+        if (!h->gram_ready) h->aty_pending = false;
         h->up_active = false;  // every chunk event has been waited on
         return;
     }
@@ -1036,8 +1082,16 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
             h->gram_ready);  // QR(Y0)
     for (size_t round = 0; round < q; ++round) {
         h->mark("power_atx");
-        gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true, "gemm_A",
-                 2.0 * p.m * p.n * p.s);  // (A^T Q1)^T
+        if (round == 0 && h->aty_pending && h->basis == h->y.d()) {
+            // (A^T Y0)^T: its split-K slabs were produced during the chunked upload
+            h->launched(launch_reduce_partials(h->part.d(), h->aty_slab, h->aty_splits, h->b.d(),
+                                               h->aty_slab, h->stream),
+                        "reduce_partials");
+        } else {
+            gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true,
+                     "gemm_A", 2.0 * p.m * p.n * p.s);  // (A^T Q1)^T
+        }
+        h->aty_pending = false;
         c.allreduce(h->b.d(), (size_t)p.NP * p.ldn);  // sharded: sum_g (A_g^T Q1_g)^T
         h->mark("qr_wide");
         const double* zt = apply_ct(c, h->b.d(), h->b2.d());  // (A^T W)^T, W = Q1 C
@@ -1266,7 +1320,7 @@ void solve_tall(rsvd_b200_handle* h, const double* A, const Plan& p, const rsvd_
     if (gr == 2) h->reruns = 1;
     for (int attempt = gr == 2 ? 1 : 0; attempt < 2; ++attempt) {
         const Ctx c = begin_run(h, p, /*robust=*/attempt > 0 || h->force_robust);
-        sketch_dev(c, A, cfg.seed, /*check=*/true);
+        sketch_dev(c, A, cfg.seed, /*check=*/true, /*pre_aty=*/cfg.power_q > 0);
         power_iterate_dev(c, A, cfg.power_q, false);
         // range_basis(W) = W in the pipeline (see the header comment); k <= s always,
         // so pad_to_rank (rsvd.cpp:117-124) never widens the result here.
