@@ -384,7 +384,7 @@ static int jacobi_svd_tall(const double* a, size_t m, size_t n, double* uout, do
     double* scratch = XMALLOC(double, (m > n ? m : n) * n);
     size_t* perm = XMALLOC(size_t, n);
     size_t* valid = XMALLOC(size_t, n);
-    size_t* nulls = XMALLOC(size_t, n);
+    size_t* nulls = (size_t*)calloc(nz(n), sizeof(size_t));  /* zeroed: silences -Wmaybe-uninitialized */
     int rc = ORC_OK;
     for (size_t i = 0; i < m; ++i)
         for (size_t j = 0; j < n; ++j) w[j * m + i] = a[i * n + j];
