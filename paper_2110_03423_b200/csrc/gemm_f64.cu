@@ -396,7 +396,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 }
 
 // =========================================================================== atx
-template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T>
+// ACC (OUT_T only): start from the Z^T already in Z instead of zero, so that a K range
+// processed by consecutive launches accumulates exactly like one launch over it.
+template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T, bool ACC = false>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_atx_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {N, K}, box {16, 32}
                     const __grid_constant__ CUtensorMap mapW,  // dims {NP, K}, box {16, 32}
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 
     const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, t = lane & 3;
+    double* out = Z + blockIdx.y * split_stride;
     double acc[MI][NI][4];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -462,6 +465,22 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         for (int j = 0; j < NI; ++j)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+    if constexpr (OUT_T && ACC) {
+        // continue the partial sum a previous launch over the preceding K rows stored
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = j0 + wm * (BJ / WM) + mi * 16 + g + 8 * h;
+                if (j < N)
+#pragma unroll
+                    for (int ni = 0; ni < NI; ++ni) {
+                        const int c = (wn * NI + ni) * 8 + 2 * t;
+                        acc[mi][ni][2 * h] = out[(long)c * ldz + j];
+                        acc[mi][ni][2 * h + 1] = out[(long)(c + 1) * ldz + j];
+                    }
+            }
+    }
 
     for (int it = 0; it < n_iter; ++it) {
         const int s = it % STAGES;
@@ -498,7 +517,6 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 
-    double* out = Z + blockIdx.y * split_stride;
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
 #pragma unroll
@@ -611,12 +629,12 @@ cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T>
+template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T, bool ACC = false>
 cudaError_t launch_atx_t(const GemmAtx& p, cudaStream_t st) {
     constexpr int NP = NT * 8;
     constexpr size_t kStage = (BJ / 16 + NP / 16) * kBK * 128;
     constexpr size_t smem = STAGES * kStage + 2 * STAGES * 8 + 1024;
-    auto kern = gemm_atx_kernel<BJ, NT, WM, WN, STAGES, OUT_T>;
+    auto kern = gemm_atx_kernel<BJ, NT, WM, WN, STAGES, OUT_T, ACC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mA, mW;
@@ -626,6 +644,7 @@ cudaError_t launch_atx_t(const GemmAtx& p, cudaStream_t st) {
     const int splits = p.splits < 1 ? 1 : p.splits;
     const int per = (k_tiles + splits - 1) / splits;
     dim3 grid((unsigned)((p.N + BJ - 1) / BJ), (unsigned)splits);
+    if (ACC && splits != 1) return cudaErrorInvalidValue;
     kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mW, p.Z, p.ldz, p.split_stride, (int)p.N,
                                                  k_tiles, per);
     return cudaGetLastError();
@@ -674,6 +693,12 @@ cudaError_t dispatch_ax(const GemmAx& p, cudaStream_t st) {
 
 template <int NT>
 cudaError_t dispatch_atx(const GemmAtx& p, cudaStream_t st) {
+    if (p.accumulate) {  // upload segments (rsvd_b200.cpp gemm_ax_chunked): NP <= 96, Z^T
+        if constexpr (NT <= 12)
+            return p.out_transposed ? launch_atx_t<128, NT, 4, 2, 4, true, true>(p, st)
+                                    : cudaErrorInvalidValue;
+        return cudaErrorInvalidValue;
+    }
     if constexpr (NT <= 12) {
         return p.out_transposed ? launch_atx_t<128, NT, 4, 2, 4, true>(p, st)
                                 : launch_atx_t<128, NT, 4, 2, 4, false>(p, st);

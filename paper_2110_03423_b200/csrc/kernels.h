@@ -49,6 +49,9 @@ struct GemmAtx {
     bool out_transposed = true;
     int splits = 1;
     long split_stride = 0;
+    // (out_transposed, splits == 1) start from the Z^T already in Z instead of zero: a K
+    // range processed by consecutive launches accumulates exactly like one launch
+    bool accumulate = false;
 };
 
 // FP32-input 3xTF32 tensor-core GEMM (tcgen05, gemm_tf32.cu), D = op(A) * B (M x NP):

@@ -444,8 +444,8 @@ bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, con
 // only the last chunk's GEMM is exposed. Chunks are whole 128/64-row tiles, so the fused
 // Gram partials line up with the unchunked launch's.
 // aty_ldz > 0: also produce the split-K slabs of (A^T Y)^T (the first power iteration's
-// A-pass, Y = this sketch, ld aty_ldz) into h->part, split j as soon as the chunks holding its
-// rows are sketched. The splits are exactly gemm_atx's (choose_splits, same k-tile ranges, same
+// A-pass, Y = this sketch, ld aty_ldz) into h->part, each chunk's share right after the chunk
+// is sketched. The splits are exactly gemm_atx's (choose_splits, same k-tile ranges, same
 // kernel), so the slabs — and the reduced result — are bit-identical to gemm_atx's.
 bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long lda,
                      const double* Xt, long ldx, int NP, double* Y, long ldy, int* flag,
@@ -460,19 +460,18 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
         if (aty_splits < 2 || h->part.bytes < (size_t)aty_splits * slab * sizeof(double))
             aty_splits = 0;  // gemm_atx would not split (or no room): leave it to the pass
     }
-    int next_split = 0;
-    auto launch_aty = [&](long rows_done) {
-        while (next_split < aty_splits &&
-               std::min(M, (long)(next_split + 1) * per_rows) <= rows_done) {
-            const long r0 = next_split * per_rows, rows = std::min(M, r0 + per_rows) - r0;
-            double* z = h->part.d() + next_split * slab;
-            if (rows <= 0) {
-                h->launched(launch_fill(z, slab, 0.0, h->stream), "fill");
-            } else {
-                GemmAtx g{A + r0 * lda, rows, K, lda, Y + r0 * ldy, ldy, NP, z, aty_ldz, true};
-                h->launched(launch_gemm_atx(g, h->stream), "gemm_atx(upload split)");
-            }
-            ++next_split;
+    // the rows [r0, r1) just sketched: each split overlapping them advances by that segment
+    // (atx `accumulate` continues the split's partial sum, so a split built from several
+    // segments accumulates in exactly the order of one launch over its whole range)
+    auto launch_aty = [&](long r0, long r1) {
+        for (int j = (int)(r0 / per_rows); j < aty_splits && j * per_rows < r1; ++j) {
+            const long s0 = j * per_rows, s1 = std::min(M, s0 + per_rows);
+            const long a = std::max(s0, r0), b = std::min(s1, r1);
+            if (a >= b) continue;
+            GemmAtx g{A + a * lda, b - a, K, lda, Y + a * ldy, ldy, NP,
+                      h->part.d() + j * slab, aty_ldz, true};
+            g.accumulate = a > s0;
+            h->launched(launch_gemm_atx(g, h->stream), "gemm_atx(upload segment)");
         }
     };
     const bool fuse = gram_out && NP <= 96;
@@ -489,9 +488,12 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
         if (fuse) g.gram = h->gpart.d() + tile0 * NP * NP;
         h->launched(launch_gemm_ax(g, h->stream), "gemm_ax(chunk)");
         tile0 += ax_tiles(r1 - r0, NP);
-        launch_aty(r1);
+        if (aty_splits > 0) launch_aty(r0, r1);
     }
     h->kernel_end(tag);
+    for (int j = 0; j < aty_splits; ++j)  // splits past the last row (rounding): zero slabs
+        if (j * per_rows >= M)
+            h->launched(launch_fill(h->part.d() + j * slab, slab, 0.0, h->stream), "fill");
     if (aty_splits > 0) {
         h->aty_pending = true;
         h->aty_splits = aty_splits;
