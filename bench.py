@@ -346,8 +346,7 @@ def load_traffic(config):
     if os.path.exists(path):
         with open(path) as f:
             t = json.load(f)
-        if t.get("config", "c2") == config:
-            return t
+        return t.get(config)  # per-config entries: {"c2": {...}, "c4": {...}}
     return None
 
 
