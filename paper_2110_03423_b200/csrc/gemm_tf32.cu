@@ -654,8 +654,12 @@ cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int k_tiles = (int)((p.K + tf32::BK - 1) / tf32::BK);
-    const int splits = p.splits < 1 ? 1 : p.splits;
-    const int per = (k_tiles + splits - 1) / splits;
+    int splits = p.splits < 1 ? 1 : p.splits;
+    int per = (k_tiles + splits - 1) / splits;
+    if (p.k_per_split > 0) {  // an explicit split length (a row range of a larger split-K)
+        per = p.k_per_split;
+        splits = (k_tiles + per - 1) / per;
+    }
     unsigned gx = (unsigned)((p.M + tf32::BM - 1) / tf32::BM);
     if (PAIR) gx = (gx + 1) & ~1u;  // the odd tile's partner only reads zeros past M
     cudaLaunchConfig_t cfg = {};

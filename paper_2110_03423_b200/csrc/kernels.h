@@ -80,6 +80,9 @@ struct GemmTf32 {
     // 128-row tile's diagonal block; everything left of it is written as zero (the upper
     // triangle, all a Cholesky reads, is exact)
     bool upper = false;
+    // > 0: split K into runs of this many 16-row k-tiles (the split count follows), so a row
+    // range of a larger split-K product reproduces that product's slabs exactly
+    int k_per_split = 0;
 };
 cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st);
 // out (rows x cols, FP32, ldo) = in (FP64, ldi) for r < rows_valid and c < cols_valid, else 0.

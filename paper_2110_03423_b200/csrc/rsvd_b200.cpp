@@ -207,6 +207,8 @@ struct rsvd_b200_handle {
     bool aty_pending = false;
     int aty_splits = 0;
     long aty_slab = 0;
+    DevBuf pre_part;  // FP32 path: the upload-time (A^T Y0)^T split-K slabs (FP32)
+    long upload_aty = 0;  // splits of the last solve's upload-time A^T Y0 (0: not used)
     DevBuf gpart;             // per-tile Gram partials of the fused epilogue
     int* flags_host = nullptr;
     std::vector<double> omega_host;  // validation mode (n x s row-major)
@@ -498,6 +500,7 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
         h->aty_pending = true;
         h->aty_splits = aty_splits;
         h->aty_slab = slab;
+        h->upload_aty = aty_splits;
     }
     if (fuse)
         h->launched(launch_reduce_partials(h->gpart.d(), (long)NP * NP, (int)tile0, gram_out,
@@ -958,6 +961,7 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
     ck(cudaMemsetAsync(h->flags.p, 0, kNumFlags * sizeof(int), h->stream), "memset flags");
     h->aty_pending = false;
+    h->upload_aty = 0;
     if (p.f32)  // the 3xTF32 A-pass writes rows < NPf of (A^T Q)^T / Q^T A; pad rows stay 0
         ck(cudaMemsetAsync(h->b.p, 0, (size_t)NP * p.ldn * sizeof(double), h->stream), "memset b");
     h->trace = getenv("RSVD_B200_TRACE") ? atoi(getenv("RSVD_B200_TRACE")) : 0;
@@ -1017,6 +1021,18 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
         const long rows_per = chunked ? h->up_chunk_rows : p.m;
         const long chunks = chunked ? h->up_chunks : 1;
         h->kernel_begin("gemm_A", 2.0 * p.m * n * s);
+        // pre: also the first power iteration's (A^T Y0)^T slabs, chunk by chunk, with
+        // atx_a_f32's own split-K partition (whole splits per chunk), into h->pre_part
+        bool pre = chunked && pre_aty;
+        int pre_splits = 0;
+        long pre_per = 0, pre_slab = 0;
+        if (pre) {
+            pre_splits = tf32_splits(p.n, p.m);
+            pre_per = ((p.m + 15) / 16 + pre_splits - 1) / pre_splits;  // k-tiles per split
+            pre_slab = (long)p.NPf * p.ldn;
+            pre = pre_splits > 1 && rows_per % (pre_per * 16) == 0;
+            if (pre) h->pre_part.reserve((size_t)pre_splits * pre_slab * sizeof(float));
+        }
         for (long ci = 0; ci < chunks; ++ci) {  // chunks: the sketch consumes the upload
             const long r0 = ci * rows_per, rows = std::min(p.m - r0, rows_per);
             if (chunked)
@@ -1028,8 +1044,27 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
             g.out64 = false;
             g.flag = check ? c.flags + kFlagNonfinite : nullptr;
             gemm_tf32(h, g);
+            if (pre) {
+                GemmTf32 a{p.af + r0 * p.lda, p.n, rows, p.lda,
+                           static_cast<float*>(h->yf.p) + r0 * p.NPf, (long)p.NPf, p.NPf,
+                           static_cast<float*>(h->pre_part.p) + (r0 / (pre_per * 16)) * pre_slab,
+                           p.ldn};
+                a.Blo = static_cast<float*>(h->yf_lo.p) + r0 * p.NPf;
+                a.mn = true;
+                a.out_t = true;
+                a.out64 = false;
+                a.k_per_split = (int)pre_per;
+                a.split_stride = pre_slab;
+                h->launched(launch_gemm_tf32(a, h->stream), "gemm_tf32(upload split)");
+            }
         }
         h->kernel_end("gemm_A");
+        if (pre) {
+            h->aty_pending = true;
+            h->aty_splits = pre_splits;
+            h->aty_slab = pre_slab;
+            h->upload_aty = pre_splits;
+        }
         if (chunked) h->up_active = false;
         h->gram_ready = false;
         return;
@@ -1062,7 +1097,16 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
         tall_qr_f32(c, p.m, q == 0 ? 2 : 1);  // QR(Y0)
         for (size_t round = 0; round < q; ++round) {
             h->mark("power_atx");
-            atx_a_f32(c);  // (A^T Q1)^T
+            if (round == 0 && h->aty_pending && h->basis_f == h->yf.p) {
+                // (A^T Y0)^T: its FP32 split-K slabs were produced during the chunked upload
+                h->launched(launch_reduce_partials_f32(static_cast<const float*>(h->pre_part.p),
+                                                       h->aty_slab, h->aty_splits, h->b.d(),
+                                                       h->aty_slab, h->stream),
+                            "reduce_partials");
+            } else {
+                atx_a_f32(c);  // (A^T Q1)^T
+            }
+            h->aty_pending = false;
             c.allreduce(h->b.d(), (size_t)p.NP * p.ldn);
             h->mark("qr_wide");
             const double* zt = apply_ct(c, h->b.d(), h->b2.d());
@@ -1314,6 +1358,7 @@ void solve_tall(rsvd_b200_handle* h, const double* A, const Plan& p, const rsvd_
                 double* u, long ldu, double* sigma, double* v, long ldv, size_t* sketch_width) {
     h->fallbacks = 0;
     h->reruns = 0;
+    h->upload_aty = 0;
     const int gr = solve_tall_graph(h, A, p, cfg, u, ldu, sigma, v, ldv);
     if (gr == 1) {
         if (sketch_width) *sketch_width = (size_t)p.s;
@@ -2153,6 +2198,7 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
     if (!strcmp(key, "robust_reruns")) return h->reruns;
     if (!strcmp(key, "launches")) return h->launches;
     if (!strcmp(key, "graph_launches")) return h->graph_replays;
+    if (!strcmp(key, "upload_aty_splits")) return h->upload_aty;
     return -1;
 }
 

@@ -135,3 +135,21 @@ def test_f32_sharded_local_group(port):
     assert np.array_equal(out[0].factors.v, out[1].factors.v)
     for s in solvers:
         s.detach()
+
+
+def test_f32_upload_time_aty_bit_identical(solver, monkeypatch):
+    """Chunks that hold whole splits of the first power iteration's (A^T Y0)^T (here 2048-row
+    splits, 4096-row chunks): its slabs are produced during the upload, and the result still
+    equals the device-resident solve bit for bit."""
+    torch = pytest.importorskip("torch")
+    import paper_2110_03423_b200 as P
+    a = planted32(163840, 256, lambda i: 1.0 / (1.0 + i) ** 1.5, 9)
+    cfg = P.RsvdConfig(k=16, power_q=2, seed=3)
+    monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "4")  # 4096 rows of 1 KB
+    host = solver.randomized_ksvd_f32(a, cfg)
+    assert solver.last_info("upload_aty_splits") == 80
+    u, s, v, sw = solver.randomized_ksvd_f32_device(torch.from_numpy(a).cuda(), cfg)
+    assert solver.last_info("upload_aty_splits") == 0
+    assert np.array_equal(s.cpu().numpy(), host.factors.sigma)
+    assert np.array_equal(u.cpu().numpy(), host.factors.u)
+    assert np.array_equal(v.cpu().numpy(), host.factors.v)

@@ -371,6 +371,7 @@ def test_chunked_upload_bit_identical(solver, port, monkeypatch):
     monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "1")  # 2048-row chunks: 3 of them
     out = (np.empty((m, k)), np.empty(k), np.empty((n, k)))
     res = solver.randomized_ksvd(a, cfg, out=out)
+    assert solver.last_info("upload_aty_splits") > 1  # A^T Y0 produced during the upload
     assert res.factors.u is out[0] and res.factors.sigma is out[1] and res.factors.v is out[2]
     u_d, s_d, v_d, _ = solver.randomized_ksvd_device(torch.from_numpy(a).cuda(), cfg)
     assert np.array_equal(res.factors.sigma, s_d.cpu().numpy())
