@@ -693,11 +693,14 @@ cudaError_t dispatch_ax(const GemmAx& p, cudaStream_t st) {
 
 template <int NT>
 cudaError_t dispatch_atx(const GemmAtx& p, cudaStream_t st) {
-    if (p.accumulate) {  // upload segments (rsvd_b200.cpp gemm_ax_chunked): NP <= 96, Z^T
+    if (p.accumulate) {  // upload segments (rsvd_b200.cpp gemm_ax_chunked): Z^T only
+        if (!p.out_transposed) return cudaErrorInvalidValue;
         if constexpr (NT <= 12)
-            return p.out_transposed ? launch_atx_t<128, NT, 4, 2, 4, true, true>(p, st)
-                                    : cudaErrorInvalidValue;
-        return cudaErrorInvalidValue;
+            return launch_atx_t<128, NT, 4, 2, 4, true, true>(p, st);
+        else if constexpr (NT > 24)
+            return launch_atx_t<64, NT, 4, 4, 2, true, true>(p, st);
+        else
+            return launch_atx_t<64, NT, 2, 4, 3, true, true>(p, st);
     }
     if constexpr (NT <= 12) {
         return p.out_transposed ? launch_atx_t<128, NT, 4, 2, 4, true>(p, st)

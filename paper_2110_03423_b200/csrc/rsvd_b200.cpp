@@ -207,7 +207,7 @@ struct rsvd_b200_handle {
     bool aty_pending = false;
     int aty_splits = 0;
     long aty_slab = 0;
-    DevBuf pre_part;  // FP32 path: the upload-time (A^T Y0)^T split-K slabs (FP32)
+    DevBuf pre_part;  // the upload-time (A^T Y0)^T split-K slabs (FP64, or FP32 in the FP32 path)
     long upload_aty = 0;  // splits of the last solve's upload-time A^T Y0 (0: not used)
     DevBuf gpart;             // per-tile Gram partials of the fused epilogue
     int* flags_host = nullptr;
@@ -459,8 +459,10 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
         aty_splits = choose_splits(ax_tiles(K, NP), (M + 31) / 32);
         per_rows = (((M + 31) / 32 + aty_splits - 1) / aty_splits) * 32;
         slab = (long)NP * aty_ldz;
-        if (aty_splits < 2 || h->part.bytes < (size_t)aty_splits * slab * sizeof(double))
-            aty_splits = 0;  // gemm_atx would not split (or no room): leave it to the pass
+        if (aty_splits < 2)
+            aty_splits = 0;  // gemm_atx would not split: leave it to the pass
+        else  // own buffer: the tall QR's Gram (when not fused) reuses h->part first
+            h->pre_part.reserve((size_t)aty_splits * slab * sizeof(double));
     }
     // the rows [r0, r1) just sketched: each split overlapping them advances by that segment
     // (atx `accumulate` continues the split's partial sum, so a split built from several
@@ -471,7 +473,7 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
             const long a = std::max(s0, r0), b = std::min(s1, r1);
             if (a >= b) continue;
             GemmAtx g{A + a * lda, b - a, K, lda, Y + a * ldy, ldy, NP,
-                      h->part.d() + j * slab, aty_ldz, true};
+                      h->pre_part.d() + j * slab, aty_ldz, true};
             g.accumulate = a > s0;
             h->launched(launch_gemm_atx(g, h->stream), "gemm_atx(upload segment)");
         }
@@ -495,7 +497,7 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
     h->kernel_end(tag);
     for (int j = 0; j < aty_splits; ++j)  // splits past the last row (rounding): zero slabs
         if (j * per_rows >= M)
-            h->launched(launch_fill(h->part.d() + j * slab, slab, 0.0, h->stream), "fill");
+            h->launched(launch_fill(h->pre_part.d() + j * slab, slab, 0.0, h->stream), "fill");
     if (aty_splits > 0) {
         h->aty_pending = true;
         h->aty_splits = aty_splits;
@@ -1070,12 +1072,9 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
         return;
     }
     if (h->up_active && A == h->a_copy.d() && !p.sharded) {
-        // (only with the fused Gram: otherwise the Gram GEMM would reuse h->part first)
         h->gram_ready = gemm_ax_chunked(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                                         check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
-                                        2.0 * p.m * n * s, c.slot(kG), s,
-                                        pre_aty && NP <= 96 ? p.ldn : 0);
-        if (!h->gram_ready) h->aty_pending = false;
+                                        2.0 * p.m * n * s, c.slot(kG), s, pre_aty ? p.ldn : 0);
         h->up_active = false;  // every chunk event has been waited on
         return;
     }
@@ -1130,8 +1129,8 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
         h->mark("power_atx");
         if (round == 0 && h->aty_pending && h->basis == h->y.d()) {
             // (A^T Y0)^T: its split-K slabs were produced during the chunked upload
-            h->launched(launch_reduce_partials(h->part.d(), h->aty_slab, h->aty_splits, h->b.d(),
-                                               h->aty_slab, h->stream),
+            h->launched(launch_reduce_partials(h->pre_part.d(), h->aty_slab, h->aty_splits,
+                                               h->b.d(), h->aty_slab, h->stream),
                         "reduce_partials");
         } else {
             gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true,

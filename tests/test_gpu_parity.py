@@ -358,17 +358,20 @@ def planted_like(m, n, k, seed):
     return (uu * np.exp(-np.arange(r) / (k / 2.0))) @ vv.T
 
 
-def test_chunked_upload_bit_identical(solver, port, monkeypatch):
+@pytest.mark.parametrize("m,n,k,p", [(5000, 64, 8, 6), (37888, 128, 100, 10)])
+def test_chunked_upload_bit_identical(solver, port, monkeypatch, m, n, k, p):
     """Host-buffer solves upload A in row chunks that the sketch GEMM consumes as they land
-    (solve_host / gemm_ax_chunked). The chunks are whole GEMM tiles, so the result is
-    bit-identical to the device-resident solve; out= buffers are filled in place."""
+    (solve_host / gemm_ax_chunked), and the first power iteration's A^T Y0 advances chunk by
+    chunk. The chunks are whole GEMM tiles and the A^T Y0 splits match the device pass's, so
+    the result is bit-identical to the device-resident solve whenever the device sketch does
+    not split K either (sketch widths 14: fused Gram; 110: NP = 128, 592 row tiles = 4 full
+    waves, Gram by its own GEMM); out= buffers are filled in place."""
     import torch
     import paper_2110_03423_b200 as P
     rng = np.random.default_rng(11)
-    m, n, k = 5000, 64, 8
     a = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 12.0)
-    cfg = P.RsvdConfig(k=k, oversample=6, power_q=2, seed=5)
-    monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "1")  # 2048-row chunks: 3 of them
+    cfg = P.RsvdConfig(k=k, oversample=p, power_q=2, seed=5)
+    monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "1")  # 1-MB chunks: 3-5 of them
     out = (np.empty((m, k)), np.empty(k), np.empty((n, k)))
     res = solver.randomized_ksvd(a, cfg, out=out)
     assert solver.last_info("upload_aty_splits") > 1  # A^T Y0 produced during the upload
