@@ -87,6 +87,72 @@ __device__ __forceinline__ dd dd_div(dd a, dd b) {
     return dd_add(fast_two_sum(q1, q2), dd{q3, 0.0});
 }
 
+// 1/(2j+1), j = 0..24, as double-doubles (hi + lo, exact rational rounding; generated)
+__constant__ double kInvOdd[25][2] = {
+    {0x1.0000000000000p+0, 0x0.0p+0},
+    {0x1.5555555555555p-2, 0x1.5555555555555p-56},
+    {0x1.999999999999ap-3, -0x1.999999999999ap-57},
+    {0x1.2492492492492p-3, 0x1.2492492492492p-57},
+    {0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-58},
+    {0x1.745d1745d1746p-4, -0x1.745d1745d1746p-59},
+    {0x1.3b13b13b13b14p-4, -0x1.3b13b13b13b14p-58},
+    {0x1.1111111111111p-4, 0x1.1111111111111p-60},
+    {0x1.e1e1e1e1e1e1ep-5, 0x1.e1e1e1e1e1e1ep-61},
+    {0x1.af286bca1af28p-5, 0x1.af286bca1af28p-59},
+    {0x1.8618618618618p-5, 0x1.8618618618618p-59},
+    {0x1.642c8590b2164p-5, 0x1.642c8590b2164p-60},
+    {0x1.47ae147ae147bp-5, -0x1.eb851eb851eb8p-61},
+    {0x1.2f684bda12f68p-5, 0x1.2f684bda12f68p-59},
+    {0x1.1a7b9611a7b96p-5, 0x1.1a7b9611a7b96p-61},
+    {0x1.0842108421084p-5, 0x1.0842108421084p-60},
+    {0x1.f07c1f07c1f08p-6, -0x1.f07c1f07c1f08p-61},
+    {0x1.d41d41d41d41dp-6, 0x1.0750750750750p-60},
+    {0x1.bacf914c1bad0p-6, -0x1.bacf914c1bad0p-60},
+    {0x1.a41a41a41a41ap-6, 0x1.0690690690690p-60},
+    {0x1.8f9c18f9c18fap-6, -0x1.f3831f3831f38p-61},
+    {0x1.7d05f417d05f4p-6, 0x1.7d05f417d05f4p-62},
+    {0x1.6c16c16c16c17p-6, -0x1.f49f49f49f49fp-61},
+    {0x1.5c9882b931057p-6, 0x1.310572620ae4cp-61},
+    {0x1.4e5e0a72f0539p-6, 0x1.e0a72f0539783p-60},
+};
+// 1/n!, n = 0..31, as double-doubles
+__constant__ double kInvFact[32][2] = {
+    {0x1.0000000000000p+0, 0x0.0p+0},
+    {0x1.0000000000000p+0, 0x0.0p+0},
+    {0x1.0000000000000p-1, 0x0.0p+0},
+    {0x1.5555555555555p-3, 0x1.5555555555555p-57},
+    {0x1.5555555555555p-5, 0x1.5555555555555p-59},
+    {0x1.1111111111111p-7, 0x1.1111111111111p-63},
+    {0x1.6c16c16c16c17p-10, -0x1.f49f49f49f49fp-65},
+    {0x1.a01a01a01a01ap-13, 0x1.a01a01a01a01ap-73},
+    {0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-76},
+    {0x1.71de3a556c734p-19, -0x1.c154f8ddc6c00p-73},
+    {0x1.27e4fb7789f5cp-22, 0x1.cbbc05b4fa99ap-76},
+    {0x1.ae64567f544e4p-26, -0x1.c062e06d1f209p-80},
+    {0x1.1eed8eff8d898p-29, -0x1.2aec959e14c06p-83},
+    {0x1.6124613a86d09p-33, 0x1.f28e0cc748ebep-87},
+    {0x1.93974a8c07c9dp-37, 0x1.05d6f8a2efd1fp-92},
+    {0x1.ae7f3e733b81fp-41, 0x1.1d8656b0ee8cbp-97},
+    {0x1.ae7f3e733b81fp-45, 0x1.1d8656b0ee8cbp-101},
+    {0x1.952c77030ad4ap-49, 0x1.ac981465ddc6cp-103},
+    {0x1.6827863b97d97p-53, 0x1.eec01221a8b0bp-107},
+    {0x1.2f49b46814157p-57, 0x1.2650f61dbdcb4p-112},
+    {0x1.e542ba4020225p-62, 0x1.ea72b4afe3c2fp-120},
+    {0x1.71b8ef6dcf572p-66, -0x1.d043ae40c4647p-120},
+    {0x1.0ce396db7f853p-70, -0x1.aebcdbd20331cp-124},
+    {0x1.761b41316381ap-75, -0x1.3423c7d91404fp-130},
+    {0x1.f2cf01972f578p-80, -0x1.9ada5fcc1ab14p-135},
+    {0x1.3f3ccdd165fa9p-84, -0x1.58ddadf344487p-139},
+    {0x1.88e85fc6a4e5ap-89, -0x1.71c37ebd16540p-143},
+    {0x1.d1ab1c2dccea3p-94, 0x1.054d0c78aea14p-149},
+    {0x1.0a18a2635085dp-98, 0x1.b9e2e28e1aa54p-153},
+    {0x1.259f98b4358adp-103, 0x1.eaf8c39dd9bc5p-157},
+    {0x1.3932c5047d60ep-108, 0x1.832b7b530a627p-162},
+    {0x1.434d2e783f5bcp-113, 0x1.0b87b91be9affp-167},
+};
+
+__device__ __forceinline__ dd kdd(const double (&t)[2]) { return dd{t[0], t[1]}; }
+
 // Correctly rounded (to ~2^-104 before the final rounding) natural log of u in (0, 1]:
 // u = 2^e m, m in [sqrt(2)/2, sqrt(2)); log m = 2 atanh(f), f = (m - 1)/(m + 1).
 __device__ double log_cr(double u) {
@@ -102,9 +168,8 @@ __device__ double log_cr(double u) {
     const dd f = dd_div(num, den);
     const dd f2 = dd_mul(f, f);
     // atanh(f)/f = sum_j f^(2j) / (2j + 1), |f| <= 0.1716: 24 terms reach 2^-120
-    dd acc = dd_div(dd{1.0, 0.0}, dd{49.0, 0.0});
-    for (int j = 23; j >= 0; --j)
-        acc = dd_add(dd_mul(acc, f2), dd_div(dd{1.0, 0.0}, dd{2.0 * j + 1.0, 0.0}));
+    dd acc = kdd(kInvOdd[24]);
+    for (int j = 23; j >= 0; --j) acc = dd_add(dd_mul(acc, f2), kdd(kInvOdd[j]));
     dd lm = dd_mul(dd_mul_d(f, 2.0), acc);
     const dd ln2 = {0.69314718055994528623, 2.3190468138462996e-17};
     return dd_add(dd_mul_d(ln2, (double)e), lm).hi;
@@ -121,13 +186,10 @@ __device__ void sincos_cr(double x, double* sn, double* cs) {
     r = dd_sub(r, dd{kq * p3, 0.0});
     const dd r2 = dd_mul(r, r);
     // sin r = r * sum (-1)^j r^(2j) / (2j+1)!,  cos r = sum (-1)^j r^(2j) / (2j)!, j <= 15
-    dd inv_fact[32];
-    inv_fact[0] = dd{1.0, 0.0};
-    for (int n = 1; n < 32; ++n) inv_fact[n] = dd_div(inv_fact[n - 1], dd{(double)n, 0.0});
-    dd s = inv_fact[31], c = inv_fact[30];
+    dd s = kdd(kInvFact[31]), c = kdd(kInvFact[30]);
     for (int j = 14; j >= 0; --j) {
-        s = dd_add(dd_neg(dd_mul(s, r2)), inv_fact[2 * j + 1]);
-        c = dd_add(dd_neg(dd_mul(c, r2)), inv_fact[2 * j]);
+        s = dd_add(dd_neg(dd_mul(s, r2)), kdd(kInvFact[2 * j + 1]));
+        c = dd_add(dd_neg(dd_mul(c, r2)), kdd(kInvFact[2 * j]));
     }
     s = dd_mul(s, r);
     const int q = ((int)kq) & 3;
