@@ -563,7 +563,7 @@ def run_ours(args):
                             + " (host buffers: pinned A in, pinned reused out= U, sigma, V)")},
             "gpu_launches": launches_per_step * args.steps,
             "cuda_graph": {"timed_steps_as_graph_launch": graph_steps,
-                           "kernels_per_graph": launches_per_step},
+                           "kernels_per_solve": launches_per_step},
             "roofline": roof,
             "cpu_baseline": cpu,
             "wall_s_timed": round(wall, 3),
