@@ -1019,7 +1019,7 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
     h->mark("sketch_gemm");
     if (p.f32) {
         xt_to_f32(c);
-        const bool chunked = h->up_active && p.af == h->a_copy.p && !p.sharded;
+        const bool chunked = h->up_active && p.af == h->a_copy.p;
         const long rows_per = chunked ? h->up_chunk_rows : p.m;
         const long chunks = chunked ? h->up_chunks : 1;
         h->kernel_begin("gemm_A", 2.0 * p.m * n * s);
@@ -1071,7 +1071,7 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
         h->gram_ready = false;
         return;
     }
-    if (h->up_active && A == h->a_copy.d() && !p.sharded) {
+    if (h->up_active && A == h->a_copy.d()) {
         h->gram_ready = gemm_ax_chunked(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                                         check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
                                         2.0 * p.m * n * s, c.slot(kG), s, pre_aty ? p.ldn : 0);
@@ -1896,10 +1896,9 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_sharded(rsvd_b200_handle* h, const do
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         h->launches = 0;
         const long lda = round_up((long)n, 2);
-        h->a_copy.reserve(std::max<size_t>(1, m_local * lda) * sizeof(double));
-        ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(double), a, n * sizeof(double),
-                             n * sizeof(double), m_local, cudaMemcpyHostToDevice, h->stream),
-           "H2D of A shard");
+        UploadFence fence{h};
+        // chunked when tall: the sketch consumes the shard's rows as they land, as unsharded
+        upload_a(h, a, (long)m_local, (long)n, lda);
         const size_t k = cfg->k;
         h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
         if (u) h->u_out.reserve(std::max<size_t>(m_local * k, 1) * sizeof(double));
@@ -1957,14 +1956,7 @@ static void solve_host_f32(rsvd_b200_handle* h, const float* a, size_t m_local, 
     h->launches = 0;
     const long lda = round_up((long)n, 4);
     UploadFence fence{h};
-    if (sharded) {
-        h->a_copy.reserve(std::max<size_t>(1, m_local * lda) * sizeof(float));
-        ck(cudaMemcpy2DAsync(h->a_copy.p, lda * sizeof(float), a, n * sizeof(float),
-                             n * sizeof(float), m_local, cudaMemcpyHostToDevice, h->stream),
-           "H2D of A (FP32)");
-    } else {
-        upload_a(h, a, (long)m_local, (long)n, lda, sizeof(float));  // chunked when tall
-    }
+    upload_a(h, a, (long)m_local, (long)n, lda, sizeof(float));  // chunked when tall
     const size_t k = cfg->k;
     h->sig_out.reserve(std::max<size_t>(k, 1) * sizeof(double));
     if (u) h->u_out.reserve(std::max<size_t>(m_local * k, 1) * sizeof(double));
