@@ -5,10 +5,12 @@ Default workload (config C2, the metric's 1-GPU case): a CelebA-shaped synthetic
 matrix A (202599 x 4096) with a controlled, exponentially decaying spectrum, rank k=64,
 oversampling p=10, q=2 power iterations, seed 42. One step = one full `randomized_ksvd`
 (Algorithm 1) with A resident in HBM. A (6.6 GB) is much larger than the 126 MB L2, so
-every pass streams it from HBM (no explicit flush needed).
+every pass streams it from HBM (no explicit flush needed). A is generated on the host by
+`synth_host` (numpy, fixed seed) so that both arms, the CPU baseline and the full-size parity
+tests (tests/test_gpu_fullsize_parity.py) solve the same bits.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c1|c2|c3|c5]
+                  [--config c1|c2|c3|c4|c5|c5ill]
 
 Prints ONE JSON line (rank 0). value = whole-job TFLOP/s with the algorithmic flop count
 F = (2q+2)*2*m*n*s + 2*m*s*k (s = k+p), i.e. the reference's arithmetic, not padded
@@ -18,8 +20,8 @@ N > 1 (torchrun): A is row-sharded, each rank holding the config's m rows (weak 
 m_total = N*m), and the solve runs collectively with NCCL all-reduces of the Gram and
 n x s partial sums (rsvd_b200_randomized_ksvd_sharded_device).
 --impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
-the unmodified reference sources; else the C restatement) on the host cores, on a bounded
-row sample of the same workload.
+the unmodified reference sources; else the C restatement) on all host cores, on the same
+full-size matrix and config (C1, C2; the larger configs time a stated row sample).
 """
 from __future__ import annotations
 
@@ -43,7 +45,7 @@ SEED = 42
 CONFIGS = {
     "c1": dict(m=4096, n=4096, k=64, p=10, q=2, spectrum="exp", cpu_rows=4096,
                name="C1 rSVD 4096x4096 k=64 p=10 q=2 FP64 (exponential decay)"),
-    "c2": dict(m=202599, n=4096, k=64, p=10, q=2, spectrum="exp", cpu_rows=16384,
+    "c2": dict(m=202599, n=4096, k=64, p=10, q=2, spectrum="exp", cpu_rows=202599,
                name="C2 rSVD 202599x4096 k=64 p=10 q=2 FP64 (CelebA-shaped)"),
     "c3": dict(m=202599, n=16384, k=128, p=20, q=2, spectrum="exp", cpu_rows=2048,
                name="C3 rSVD 202599x16384 k=128 p=20 q=2 FP64 (CelebA 128x128-shaped)"),
@@ -78,20 +80,64 @@ def spectrum(cfg, n, xp):
 
 
 # ----------------------------------------------------------------- synthetic inputs
-def synth_host(cfg, rows):
-    """Host matrix for the CPU legs: the first `rows` rows of a tall G diag(sigma) V^T
-    with the config's n and spectrum (G Gaussian / sqrt(m), V Haar)."""
-    n = cfg["n"]
-    rng = np.random.default_rng(SEED)
+def synth_host(cfg, rows=None, rank=0, out=None, threads=None):
+    """The config's synthetic matrix on the host, identical bits for every arm and test
+    (both bench arms, the CPU baseline and the full-size parity tests solve THIS matrix).
+
+    Tall configs: A = G diag(sigma) V^T / sqrt(m) with G Gaussian (numpy PCG64, one
+    SeedSequence child per 4096-row chunk, so the chunks are generated in parallel and the
+    result does not depend on the thread count; rank r of a weak-scaled run draws its own
+    children) and V Haar (QR of a Gaussian, shared by all ranks); n > 8192 uses V = (H D)^T
+    instead (a Haar QR of n x n is too slow on the host). Columns of G/sqrt(m) are
+    near-isometric, so the singular values are sigma up to (1 +- sqrt(n/m)).
+    Square power-of-two configs: the exact Hadamard-conjugated construction of
+    _hadamard_rows. `rows` (default m) takes the first rows of the rank's block; `out`
+    (rows x n, float64 or float32, e.g. a pinned buffer) receives the matrix."""
+    from concurrent.futures import ThreadPoolExecutor
+    n, m = cfg["n"], cfg["m"]
+    rows = m if rows is None else rows
+    if out is None:
+        out = np.empty((rows, n), dtype=np.float32 if cfg.get("f32") else np.float64)
+    threads = threads or os.cpu_count() or 1
+    if m == n and (n & (n - 1)) == 0:
+        step = max(1, (1 << 24) // n)
+
+        def had(r0):
+            out[r0:min(rows, r0 + step)] = _hadamard_rows(cfg, r0, min(rows, r0 + step), np)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(had, range(0, rows, step)))
+        return out
     sig = spectrum(cfg, n, np)
-    if not (cfg["m"] == n and (n & (n - 1)) == 0):
-        g = rng.standard_normal((rows, n)) / np.sqrt(cfg["m"])
-        if n > 8192:  # V = (H D)^T: a Haar QR of n x n is too slow on the host here
-            return np.ascontiguousarray(_fwht(g * sig, np) * rng.choice([-1.0, 1.0], size=n))
-        v, _ = np.linalg.qr(rng.standard_normal((n, n)))
-        return np.ascontiguousarray((g * sig) @ v.T)
-    # rows of the square Hadamard-conjugated matrix (see synth_device)
-    return np.ascontiguousarray(_hadamard_rows(cfg, 0, rows, np))
+    rng = np.random.default_rng(SEED)
+    signs = None
+    if n > 8192:
+        signs = rng.choice([-1.0, 1.0], size=n)
+    else:
+        vt = np.ascontiguousarray(np.linalg.qr(rng.standard_normal((n, n)))[0].T)
+    chunk = 4096
+    nchunks = (rows + chunk - 1) // chunk
+    kids = np.random.SeedSequence([SEED, 1 + rank]).spawn(nchunks)
+    scale = sig / np.sqrt(m)
+    batch = max(1, min(threads, nchunks))
+    buf = np.empty((batch * chunk, n))
+
+    def gen(j, slot):
+        r = min(chunk, rows - j * chunk)
+        g = buf[slot * chunk: slot * chunk + r]
+        np.random.default_rng(kids[j]).standard_normal(out=g)
+        g *= scale
+        return r
+
+    with ThreadPoolExecutor(threads) as ex:
+        for j0 in range(0, nchunks, batch):
+            js = range(j0, min(nchunks, j0 + batch))
+            got = sum(ex.map(lambda t: gen(t[1], t[0]), enumerate(js)))
+            r0 = j0 * chunk
+            if signs is not None:
+                out[r0:r0 + got] = _fwht(buf[:got] * signs, np)
+            else:
+                out[r0:r0 + got] = buf[:got] @ vt
+    return out
 
 
 def _fwht(x, xp):
@@ -116,81 +162,89 @@ def _hadamard_rows(cfg, r0, r1, xp, device=None):
     A[i, j] = d1_i d2_j f(i xor pi(j)) is generated elementwise with singular values
     exactly sigma (to rounding)."""
     n = cfg["n"]
-    rng = np.random.default_rng(SEED + 7)
-    d1 = rng.choice([-1.0, 1.0], size=n)
-    d2 = rng.choice([-1.0, 1.0], size=n)
-    perm = rng.permutation(n)
-    sig = spectrum(cfg, n, np)
-    f = _fwht(sig[None, :], np)[0] / np.sqrt(n)  # f(t) = (1/n) sum_l sigma_l (-1)^{<l,t>}
-    if xp is np:
-        i = np.arange(r0, r1)[:, None]
-        return d1[r0:r1, None] * d2[None, :] * f[np.bitwise_xor(i, perm[None, :])]
-    t = xp
-    ft = t.from_numpy(f).to(device)
-    i = t.arange(r0, r1, device=device)[:, None]
-    pj = t.from_numpy(perm).to(device)[None, :]
-    return (t.from_numpy(d1[r0:r1]).to(device)[:, None] * t.from_numpy(d2).to(device)[None, :]
-            * ft[t.bitwise_xor(i, pj)])
+    d1, d2, perm, f = _hadamard_parts(cfg)
+    i = np.arange(r0, r1)[:, None]
+    return d1[r0:r1, None] * d2[None, :] * f[np.bitwise_xor(i, perm[None, :])]
+
+
+_HAD_CACHE = {}
+
+
+def _hadamard_parts(cfg):
+    key = (cfg["n"], cfg["spectrum"], cfg["k"], cfg["p"], cfg.get("ratio"))
+    if key not in _HAD_CACHE:
+        n = cfg["n"]
+        rng = np.random.default_rng(SEED + 7)
+        d1 = rng.choice([-1.0, 1.0], size=n)
+        d2 = rng.choice([-1.0, 1.0], size=n)
+        perm = rng.permutation(n)
+        f = _fwht(spectrum(cfg, n, np)[None, :], np)[0] / np.sqrt(n)
+        _HAD_CACHE[key] = (d1, d2, perm, f)
+    return _HAD_CACHE[key]
 
 
 def synth_device(torch, cfg, m, rank, device):
-    """A on the device. Tall configs: A = G diag(sigma) V^T / sqrt(m), G Gaussian (per-rank
-    stream under sharding), V Haar (shared by all ranks), near-isometric columns so the
-    spectrum is sigma up to (1 +- sqrt(n/m)). Square power-of-two configs: the exact
-    Hadamard-conjugated construction of _hadamard_rows."""
-    n = cfg["n"]
-    if m == n and (n & (n - 1)) == 0:
-        a = torch.empty(m, n, dtype=torch.float64, device=device)
-        step = max(1, (1 << 28) // n)
-        for r0 in range(0, m, step):
-            r1 = min(m, r0 + step)
-            a[r0:r1] = _hadamard_rows(cfg, r0, r1, torch, device)
-        return a
-    sig = spectrum(cfg, n, torch).to(device)
-    gv = torch.Generator(device=device).manual_seed(SEED)
-    v = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device=device, generator=gv))[0]
-    gg = torch.Generator(device=device).manual_seed(SEED + 1 + rank)
-    a = torch.empty(m, n, dtype=torch.float64, device=device)
-    step = max(1, (1 << 26) // n)
-    scale = sig / np.sqrt(cfg["m"])
-    for r0 in range(0, m, step):
-        r1 = min(m, r0 + step)
-        g = torch.randn(r1 - r0, n, dtype=torch.float64, device=device, generator=gg)
-        a[r0:r1] = (g * scale) @ v.T
-    del v
-    return a
+    """synth_host's matrix (rank `rank`'s m rows) copied to `device` (tools/ scripts)."""
+    out = synth_host(cfg, m, rank=rank)
+    return torch.from_numpy(out).to(device)
+
+
+def workload_config(cfgd, world):
+    """The `config` object of BOTH arms' JSON lines (identical dicts: same workload)."""
+    m, n = cfgd["m"], cfgd["n"]
+    w = 4 if cfgd.get("f32") else 8
+    return {"workload": cfgd["name"], "m": m * world, "m_per_gpu": m, "n": n, "k": cfgd["k"],
+            "p": cfgd["p"], "q": cfgd["q"], "seed": SEED,
+            "sketch_width": min(cfgd["k"] + cfgd["p"], m * world, n),
+            "input": "bench.synth_host (same bits in both arms)",
+            "l2": f"A ({m * n * w / 1e9:.1f} GB per GPU) >> L2 (126 MB): every pass streams "
+                  "HBM, no flush"}
+
+
+DATA = "synthetic (controlled decaying spectrum, seed 42; numpy host generator, same A in both arms)"
 
 
 # ----------------------------------------------------------------- CPU reference
-def cpu_reference_run(cfg, rows, threads, reps=1):
-    """Time randsvd::randomized_ksvd (the unmodified reference library) on the first
-    `rows` rows of the config's synthetic matrix (same n, k, p, q, seed), all host threads."""
+def cpu_reference_run(cfg, a, threads, reps=1, budget_s=None):
+    """Time randsvd::randomized_ksvd (the unmodified reference library, all host threads) on
+    the host matrix `a` with the config's k, p, q and seed. Returns per-solve seconds (at
+    most `reps`; stops early once the next solve would overrun `budget_s`)."""
     from oracle.oracle import Oracle, available
     kind = "reference" if available("reference") else "port"
     orc = Oracle(kind)
-    a = synth_host(cfg, rows)
     note = ""
-    if cfg.get("f32"):  # the reference is FP64-only: it runs on the FP32-rounded sample
-        a = a.astype(np.float32).astype(np.float64)
-        note = " (FP64 reference on the FP32-rounded sample; it has no FP32 path)"
+    if a.dtype != np.float64:  # the reference is FP64-only: it runs on the FP32-rounded input
+        a = a.astype(np.float64)
+        note = " (FP64 reference on the FP32-rounded matrix; it has no FP32 path)"
     k, p, q = cfg["k"], cfg["p"], cfg["q"]
+    times = []
+    t_start = time.perf_counter()
     if kind == "reference":
         orc.set_max_threads(threads)
-        times, _ = orc.timed_solve(a, k, p, q, SEED, reps=reps)
         cores = threads
-    else:
-        times = []
         for _ in range(reps):
+            if budget_s and times and (time.perf_counter() - t_start) + max(times) > budget_s:
+                break
+            t, _ = orc.timed_solve(a, k, p, q, SEED, reps=1)
+            times += t
+    else:
+        cores = 1
+        for _ in range(reps):
+            if budget_s and times and (time.perf_counter() - t_start) + max(times) > budget_s:
+                break
             t0 = time.perf_counter()
             orc.randomized_ksvd(a, k, p, q, SEED, values_only=False)
             times.append(time.perf_counter() - t0)
-        cores = 1
-    t = min(times)
+    rows = a.shape[0]
     f = flops(rows, cfg["n"], k, p, q)
+    full = rows == cfg["m"]
+    what = (f"the full {rows}x{cfg['n']} matrix" if full else
+            f"a {rows}x{cfg['n']} row block (bounded sample) of the {cfg['name'].split()[0]} matrix")
+    t = statistics.median(times)
     return {"value": f / t / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
-            "sample": f"{rows}x{cfg['n']} row block of the {cfg['name'].split()[0]} synthetic "
-                      f"matrix, k={k} p={p} q={q}; {t:.2f} s per solve ({reps} run){note}",
-            "seconds": t}
+            "sample": f"{what}, k={k} p={p} q={q} seed={SEED}; median {t:.2f} s per solve over "
+                      f"{len(times)} solve(s){note}",
+            "seconds": t, "times": times, "same_config": full}
 
 
 # ----------------------------------------------------------------- GPU helpers
@@ -352,32 +406,49 @@ def load_traffic(config):
 
 # ----------------------------------------------------------------- main arms
 def run_reference(args):
+    """The reference arm: randsvd::randomized_ksvd (oracle/_ref, the unmodified reference
+    library) on the host cores, on the SAME matrix and config as our arm (bench.synth_host,
+    seed 42; at N > 1 the concatenation of every rank's shard, i.e. the whole weak-scaled
+    matrix). Rank 0 alone runs; the others exit. Warm-up solves run on a 4096-row block
+    (bounded time); the K timed solves are full-size. If K full solves would overrun
+    --ref-budget-s, the line reports how many ran ("steps") next to "steps_requested"."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
     threads = os.cpu_count() or 1
     rows = args.cpu_rows or cfg["cpu_rows"]
-    for _ in range(args.warmup):  # untimed warm-up on a quarter-size sample (bounded time)
-        cpu_reference_run(cfg, max(256, rows // 4), threads)
-    samples = [cpu_reference_run(cfg, rows, threads) for _ in range(args.steps)]
-    secs = [r["seconds"] for r in samples]
-    value = statistics.median([r["value"] for r in samples])
-    base = samples[0]
+    t0 = time.perf_counter()
+    if world == 1:
+        a = synth_host(cfg, rows)
+    else:
+        a = np.concatenate([synth_host(cfg, rows, rank=r) for r in range(world)])
+    synth_s = time.perf_counter() - t0
+    af = a.astype(np.float64) if a.dtype != np.float64 else a
+    if args.warmup:
+        cpu_reference_run(cfg, np.ascontiguousarray(af[:4096]), threads, reps=args.warmup)
+    run = cpu_reference_run(cfg, af, threads, reps=args.steps, budget_s=args.ref_budget_s)
+    f = flops(af.shape[0], cfg["n"], cfg["k"], cfg["p"], cfg["q"])
+    value = f / run["seconds"] / 1e12
+    conf = workload_config(cfg, world)
+    if rows != cfg["m"]:
+        conf["workload"] += f" (CPU row sample {rows})"
     out = {
         "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * statistics.median(secs), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (controlled decaying spectrum, seed 42)",
-        "config": {"workload": f"{cfg['name']}, CPU sample {rows}x{cfg['n']}", "m": cfg["m"],
-                   "n": cfg["n"], "k": cfg["k"], "p": cfg["p"], "q": cfg["q"],
-                   "parallelism": "host threads"},
+        "steps": len(run["times"]), "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * run["seconds"], 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": DATA, "config": conf,
+        "parallelism": f"host threads ({threads})",
         "impl": "reference",
-        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": base["cores"],
-                         "kind": base["kind"], "sample": base["sample"]},
+        "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": run["cores"],
+                         "kind": run["kind"], "sample": run["sample"]},
         "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "seconds_per_solve": [round(t, 3) for t in run["times"]],
+        "synth_s": round(synth_s, 1),
+        "host": {"cores": threads, "ram_gb": round(os.sysconf("SC_PAGE_SIZE")
+                                                   * os.sysconf("SC_PHYS_PAGES") / 2**30, 1)},
     }
     print(json.dumps(out), flush=True)
 
@@ -427,10 +498,13 @@ def run_ours(args):
             return solver.randomized_ksvd_sharded(a_host, m_total, cfg, out=e2e_out)
         return solver.randomized_ksvd(a_host, cfg, out=e2e_out)
 
-    a = synth_device(torch, cfgd, m, rank, dev)
-    if f32:
-        a = a.float()
-        torch.cuda.empty_cache()
+    # A: bench.synth_host (the same bits the reference arm and the CPU baseline solve),
+    # generated straight into pinned host memory (the e2e leg's input), then copied to HBM
+    a_host_t = torch.empty((m, n), dtype=torch.float32 if f32 else torch.float64,
+                           pin_memory=True)
+    a_host = a_host_t.numpy()
+    synth_host(cfgd, m, rank=rank, out=a_host)
+    a = a_host_t.to(dev)
     peak_cublas = cublas_dgemm_peak(torch, dev) if not f32 else None
     torch.cuda.synchronize()
     lib_stream = torch.cuda.ExternalStream(solver.stream, device=dev)
@@ -491,9 +565,6 @@ def run_ours(args):
 
     # ---- e2e: the public host-buffer API (pinned A in, U, sigma, V out), same config
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    a_host_t = torch.empty((m, n), dtype=a.dtype, pin_memory=True)
-    a_host_t.copy_(a)
-    a_host = a_host_t.numpy()
     del a, u, v
     torch.cuda.empty_cache()
     res = solve_host(a_host)  # warm the host path
@@ -511,8 +582,10 @@ def run_ours(args):
     # ---- CPU baseline (rank 0, N=1 only): the reference on a bounded row sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_reference_run(cfgd, args.cpu_rows or cfgd["cpu_rows"], os.cpu_count() or 1)
-        cpu.pop("seconds", None)
+        rows = min(m, args.cpu_rows or cfgd["cpu_rows"])
+        cpu = cpu_reference_run(cfgd, a_host[:rows], os.cpu_count() or 1)
+        for key in ("seconds", "times"):
+            cpu.pop(key, None)
 
     if rank == 0:
         if f32:
@@ -547,12 +620,9 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (A; 3xTF32 tensor cores, f64 small side)" if f32 else "f64",
-            "data": f"synthetic ({cfgd['spectrum']} spectrum, seed 42)",
-            "config": {"workload": cfgd["name"], "m": m_total, "m_per_gpu": m, "n": n, "k": k,
-                       "p": p, "q": q, "sketch_width": sw,
-                       "parallelism": f"row-sharded x{world} (NCCL)" if sharded else "single GPU",
-                       "l2": f"A ({m * n * (4 if f32 else 8) / 1e9:.1f} GB per GPU) >> L2 (126 MB): every pass "
-                             "streams HBM, no flush"},
+            "data": DATA, "config": workload_config(cfgd, world),
+            "parallelism": f"row-sharded x{world} (NCCL)" if sharded else "single GPU",
+            "sketch_width": sw,
             "clocks": clocks.summary(),
             "e2e": {"value": round(e2e_value, 4), "unit": "TFLOP/s",
                     "ms_per_step": round(1e3 * e2e_s, 2),
@@ -587,6 +657,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=1500.0,
+                    help="reference arm: stop timing full-size solves past this many seconds")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

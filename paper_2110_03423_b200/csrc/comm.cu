@@ -56,22 +56,36 @@ class LocalGroupComm final : public Comm {
 
     std::string allreduce_sum(double* buf, size_t count, cudaStream_t st) override {
         if (count == 0) return "";
+        // Every rank takes part in both barriers whatever happens locally (a rank that
+        // returned early would leave the others blocked forever); failures are published in
+        // the group and every rank reports the collective as failed after the barrier.
+        std::string err;
         cudaError_t e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return cuda_msg(e, "local allreduce: stream sync");
-        if (count > cap_) {
+        if (e != cudaSuccess) err = cuda_msg(e, "local allreduce: stream sync");
+        if (err.empty() && count > cap_) {
             if (scratch_) cudaFree(scratch_);
             scratch_ = nullptr;
             cap_ = 0;
             e = cudaMalloc(&scratch_, count * sizeof(double));
-            if (e != cudaSuccess) return cuda_msg(e, "local allreduce: scratch");
-            cap_ = count;
+            if (e != cudaSuccess) err = cuda_msg(e, "local allreduce: scratch");
+            else cap_ = count;
         }
+        if (!err.empty()) g_->failed.fetch_add(1);
         g_->ptrs[rank] = buf;
-        g_->bar.arrive_and_wait();  // every buffer is complete and published
-        e = launch_sum_buffers(g_->ptrs.data(), world, count, scratch_, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        g_->bar.arrive_and_wait();  // every buffer is complete and published (or a rank failed)
+        const bool group_ok = g_->failed.load() == 0;
+        if (group_ok) {
+            e = launch_sum_buffers(g_->ptrs.data(), world, count, scratch_, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) err = cuda_msg(e, "local allreduce: sum");
+        }
         g_->bar.arrive_and_wait();  // every rank has read every buffer
-        if (e != cudaSuccess) return cuda_msg(e, "local allreduce: sum");
+        if (!group_ok) {
+            if (rank == 0) g_->failed.store(0);  // reset for the next call (all ranks read it)
+            g_->bar.arrive_and_wait();
+            return err.empty() ? "local allreduce: another rank of the group failed" : err;
+        }
+        if (!err.empty()) return err;
         e = cudaMemcpyAsync(buf, scratch_, count * sizeof(double), cudaMemcpyDeviceToDevice, st);
         return e == cudaSuccess ? "" : cuda_msg(e, "local allreduce: copy back");
     }

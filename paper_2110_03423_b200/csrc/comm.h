@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <atomic>
 #include <barrier>
 #include <memory>
 #include <string>
@@ -45,10 +46,11 @@ std::string make_nccl_comm(const unsigned char id[128], int rank, int world,
                            std::unique_ptr<Comm>* out);
 
 struct LocalGroup {
-    explicit LocalGroup(int w) : world(w), bar(w), ptrs(w, nullptr) {}
+    explicit LocalGroup(int w) : world(w), bar(w), ptrs(w, nullptr), failed(0) {}
     int world;
     std::barrier<> bar;
     std::vector<double*> ptrs;
+    std::atomic<int> failed;  // ranks whose local step failed in the current all-reduce
 };
 
 std::unique_ptr<Comm> make_local_comm(LocalGroup* g, int rank);

@@ -1062,6 +1062,14 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
         }
         h->kernel_end("gemm_A");
         if (pre) {
+            // splits past the last row (ceil rounding of the partition) got no chunk: their
+            // slabs must be zero, not stale, because the reduce sums all pre_splits of them
+            const long written = ((p.m + 15) / 16 + pre_per - 1) / pre_per;
+            if (written < pre_splits)
+                ck(cudaMemsetAsync(static_cast<float*>(h->pre_part.p) + written * pre_slab, 0,
+                                   (size_t)(pre_splits - written) * pre_slab * sizeof(float),
+                                   h->stream),
+                   "zero trailing upload slabs");
             h->aty_pending = true;
             h->aty_splits = pre_splits;
             h->aty_slab = pre_slab;

@@ -38,7 +38,9 @@ def broadcast_unique_id(uid: bytes | None, group=None) -> bytes:
     buf = torch.zeros(128, dtype=torch.uint8, device=dev)
     if rank == 0:
         buf.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
-    dist.broadcast(buf, src=0, group=group)
+    # src is a global rank: the group's rank 0 (not global rank 0) created the id
+    src = 0 if group is None else dist.get_global_rank(group, 0)
+    dist.broadcast(buf, src=src, group=group)
     return bytes(buf.cpu().tolist())
 
 
