@@ -9,6 +9,7 @@
 
 #include "randsvd/errors.hpp"
 #include "randsvd/matrix.hpp"
+#include "randsvd/parallel.hpp"
 #include "randsvd/rng.hpp"
 #include "randsvd/svd.hpp"
 
@@ -40,7 +41,5 @@ std::vector<double> singular_values_only(const DenseMatrix& a, const RsvdConfig&
 
 /// Select the CUDA device used by this thread's solver (default: $RSVD_B200_DEVICE or 0).
 void set_device(int device);
-/// Reference API compatibility: the host thread budget does not apply to the GPU path.
-inline void set_max_threads(unsigned) {}
 
 }  // namespace randsvd

@@ -220,6 +220,17 @@ rsvd_b200_status rsvd_b200_gaussian_matrix(rsvd_b200_handle* h, uint64_t seed, s
                                            size_t cols, double* out);
 rsvd_b200_status rsvd_b200_sketch(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                                   size_t s, uint64_t seed, double* y0);
+/* The same from a sampler part-way through its stream (GaussianSampler state,
+ * rng.hpp:21-42): `counter` words already drawn, and, if has_cached, the cached sine half
+ * `cached` that the sampler's next normal() returns first (rng.cpp:35-38). A fresh sampler
+ * is (0, 0, 0.0). The reference's sketch/gaussian_matrix continue a sampler this way
+ * (rng.cpp:48-53); after drawing N normals the caller advances its sampler state. */
+rsvd_b200_status rsvd_b200_gaussian_stream(rsvd_b200_handle* h, uint64_t seed, uint64_t counter,
+                                           int has_cached, double cached, size_t rows,
+                                           size_t cols, double* out);
+rsvd_b200_status rsvd_b200_sketch_stream(rsvd_b200_handle* h, const double* a, size_t m,
+                                         size_t n, size_t s, uint64_t seed, uint64_t counter,
+                                         int has_cached, double cached, double* y0);
 rsvd_b200_status rsvd_b200_power_iterate(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                                          const double* y0, size_t s, size_t q, double* w);
 rsvd_b200_status rsvd_b200_range_basis(rsvd_b200_handle* h, const double* y, size_t m, size_t s,

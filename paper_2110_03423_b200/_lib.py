@@ -15,6 +15,7 @@ EXPORTS = [
     "rsvd_b200_destroy", "rsvd_b200_last_error", "rsvd_b200_stream", "rsvd_b200_set_omega",
     "rsvd_b200_randomized_ksvd", "rsvd_b200_singular_values_only",
     "rsvd_b200_randomized_ksvd_device", "rsvd_b200_gaussian_matrix", "rsvd_b200_sketch",
+    "rsvd_b200_gaussian_stream", "rsvd_b200_sketch_stream",
     "rsvd_b200_power_iterate", "rsvd_b200_range_basis", "rsvd_b200_project_and_solve",
     "rsvd_b200_splitmix_words", "rsvd_b200_uniforms", "rsvd_b200_last_profile",
     "rsvd_b200_set_profiling", "rsvd_b200_last_launch_count", "rsvd_b200_version",
@@ -81,6 +82,10 @@ def load() -> C.CDLL:
                                                        _dp, C.POINTER(_sz)]),
         "rsvd_b200_gaussian_matrix": (C.c_int, [_vp, C.c_uint64, _sz, _sz, _dp]),
         "rsvd_b200_sketch": (C.c_int, [_vp, _dp, _sz, _sz, _sz, C.c_uint64, _dp]),
+        "rsvd_b200_gaussian_stream": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_int, C.c_double,
+                                                _sz, _sz, _dp]),
+        "rsvd_b200_sketch_stream": (C.c_int, [_vp, _dp, _sz, _sz, _sz, C.c_uint64, C.c_uint64,
+                                              C.c_int, C.c_double, _dp]),
         "rsvd_b200_power_iterate": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _sz, _sz, _dp]),
         "rsvd_b200_range_basis": (C.c_int, [_vp, _dp, _sz, _sz, _dp, C.POINTER(_sz)]),
         "rsvd_b200_project_and_solve": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _sz, _sz, _dp, _dp,

@@ -26,10 +26,6 @@ using namespace randsvd;
 
 namespace {
 
-struct UsageError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
 std::string fmt3(double x) {
     std::ostringstream o;
     o.precision(3);

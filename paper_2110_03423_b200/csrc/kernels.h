@@ -110,18 +110,28 @@ cudaError_t launch_reduce_partials_f32(const float* part, long stride, int split
 // FP64 tensor-core (DMMA m16n8k16) issue-rate probe on the whole GPU, TFLOP/s.
 cudaError_t measure_dmma_peak(cudaStream_t st, double* tflops);
 
+// A GaussianSampler state (rng.hpp:21-42): words drawn so far (`counter`) and the cached
+// sine half of an unfinished pair, which the next normal() returns first. A fresh
+// sampler is {0, 0, 0}; after drawing N normals from fresh, counter = 2 ceil(N/2) and
+// has_cached = N odd.
+struct StreamPos {
+    uint64_t counter = 0;
+    int has_cached = 0;
+    double cached = 0.0;
+};
+
 // Omega^T (NP x n, ld) for the reference's SplitMix64 + Box-Muller stream:
-// Omega(r, c) = normal #(r*s + c) of GaussianSampler(seed); rows c >= s of
-// Omega^T are zero.
+// Omega(r, c) = the (r*s + c)-th normal a GaussianSampler(seed) in state `pos` returns
+// (default: fresh); rows c >= s of Omega^T are zero.
 cudaError_t launch_omega(uint64_t seed, long n, int s, int NP, double* omega_t, long ld,
-                         cudaStream_t st);
+                         cudaStream_t st, StreamPos pos = {});
 // Raw stream pieces for the bit-exactness tests.
 cudaError_t launch_splitmix_words(uint64_t seed, uint64_t first_counter, long count,
                                   uint64_t* out, cudaStream_t st);
 cudaError_t launch_uniforms(uint64_t seed, uint64_t first_counter, long count, double* out,
                             cudaStream_t st);
 cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double* out,
-                                     cudaStream_t st);
+                                     cudaStream_t st, StreamPos pos = {});
 
 // Small dense linear algebra, one CTA, matrices in shared memory.
 // Cholesky of the s x s Gram G (ld ldg): writes R (upper, NP x NP, ld NP, zero padded)

@@ -202,11 +202,12 @@ __device__ void sincos_cr(double x, double* sn, double* cs) {
     }
 }
 
-// Both normals of pair p.
-__device__ __forceinline__ void box_muller_pair(uint64_t seed, uint64_t p, double& n0,
-                                                double& n1) {
-    const double u1 = uniform_from_word(word_at(seed, 2 * p + 1));
-    const double u2 = uniform_from_word(word_at(seed, 2 * p + 2));
+// Both normals of the pair whose words sit at counters base + 1 (radius) and base + 2
+// (angle); a fresh sampler's pair p has base 2p.
+__device__ __forceinline__ void box_muller_at(uint64_t seed, uint64_t base, double& n0,
+                                              double& n1) {
+    const double u1 = uniform_from_word(word_at(seed, base + 1));
+    const double u2 = uniform_from_word(word_at(seed, base + 2));
     const double radius = __dsqrt_rn(__dmul_rn(-2.0, log_cr(u1)));
     const double angle = __dmul_rn(2.0 * 3.14159265358979323846, u2);
     double s, c;
@@ -215,19 +216,31 @@ __device__ __forceinline__ void box_muller_pair(uint64_t seed, uint64_t p, doubl
     n1 = __dmul_rn(radius, s);
 }
 
-__global__ void omega_t_kernel(uint64_t seed, long n, int s, int NP, double* __restrict__ out,
-                               long ld) {
-    const long total = n * (long)s;
-    const long pairs = (total + 1) / 2;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < pairs;
-         p += (long)gridDim.x * blockDim.x) {
+// Output element i (0 <= i < total) is the i-th normal a GaussianSampler in state `pos`
+// would return (rng.cpp:34-46): its cached sine half first when pos.has_cached (passed in
+// bit for bit), then pairs j = 0, 1, ... built from the words at counters
+// pos.counter + 2j + 1 (radius) and pos.counter + 2j + 2 (angle), cosine half first.
+template <class Store>
+__device__ __forceinline__ void stream_normals(uint64_t seed, StreamPos pos, long total,
+                                               Store store) {
+    if (total <= 0) return;
+    const long off = pos.has_cached ? 1 : 0;
+    if (off && blockIdx.x == 0 && threadIdx.x == 0) store(0, pos.cached);
+    const long rest = total - off, pairs = (rest + 1) / 2;
+    for (long j = blockIdx.x * (long)blockDim.x + threadIdx.x; j < pairs;
+         j += (long)gridDim.x * blockDim.x) {
         double v0, v1;
-        box_muller_pair(seed, (uint64_t)p, v0, v1);
-        const long i0 = 2 * p;
-        out[(i0 % s) * ld + i0 / s] = v0;
-        const long i1 = i0 + 1;
-        if (i1 < total) out[(i1 % s) * ld + i1 / s] = v1;
+        box_muller_at(seed, pos.counter + 2 * (uint64_t)j, v0, v1);
+        store(off + 2 * j, v0);
+        if (2 * j + 1 < rest) store(off + 2 * j + 1, v1);
     }
+}
+
+__global__ void omega_t_kernel(uint64_t seed, StreamPos pos, long n, int s, int NP,
+                               double* __restrict__ out, long ld) {
+    const long total = n * (long)s;
+    stream_normals(seed, pos, total,
+                   [&](long i, double v) { out[(i % s) * ld + i / s] = v; });
     // zero the padding rows s..NP-1 of Omega^T
     const long pad = (long)(NP - s) * n;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < pad;
@@ -235,15 +248,9 @@ __global__ void omega_t_kernel(uint64_t seed, long n, int s, int NP, double* __r
         out[(s + e / n) * ld + e % n] = 0.0;
 }
 
-__global__ void gaussian_rowmajor_kernel(uint64_t seed, long total, double* __restrict__ out) {
-    const long pairs = (total + 1) / 2;
-    for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < pairs;
-         p += (long)gridDim.x * blockDim.x) {
-        double v0, v1;
-        box_muller_pair(seed, (uint64_t)p, v0, v1);
-        out[2 * p] = v0;
-        if (2 * p + 1 < total) out[2 * p + 1] = v1;
-    }
+__global__ void gaussian_rowmajor_kernel(uint64_t seed, StreamPos pos, long total,
+                                         double* __restrict__ out) {
+    stream_normals(seed, pos, total, [&](long i, double v) { out[i] = v; });
 }
 
 __global__ void words_kernel(uint64_t seed, uint64_t first, long count, uint64_t* out) {
@@ -265,16 +272,17 @@ static unsigned grid_for(long work, int threads) {
 }
 
 cudaError_t launch_omega(uint64_t seed, long n, int s, int NP, double* omega_t, long ld,
-                         cudaStream_t st) {
-    const long work = (n * (long)s + 1) / 2;
-    omega_t_kernel<<<grid_for(work, 256), 256, 0, st>>>(seed, n, s, NP, omega_t, ld);
+                         cudaStream_t st, StreamPos pos) {
+    const long work = (n * (long)s + 2) / 2;
+    omega_t_kernel<<<grid_for(work, 256), 256, 0, st>>>(seed, pos, n, s, NP, omega_t, ld);
     return cudaGetLastError();
 }
 
 cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double* out,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, StreamPos pos) {
     const long total = rows * cols;
-    gaussian_rowmajor_kernel<<<grid_for((total + 1) / 2, 256), 256, 0, st>>>(seed, total, out);
+    gaussian_rowmajor_kernel<<<grid_for((total + 2) / 2, 256), 256, 0, st>>>(seed, pos, total,
+                                                                             out);
     return cudaGetLastError();
 }
 

@@ -4,8 +4,13 @@
 // const RsvdConfig&)` (rsvd.hpp:58) relinks against librsvd_b200.so and keeps
 // the same calls, value types, layout and exception types. Each host thread
 // lazily owns one rsvd_b200_handle on its selected device.
+#include <algorithm>
+#include <atomic>
+#include <thread>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <memory>
 #include <string>
 
@@ -26,7 +31,12 @@ std::string shape_str(std::size_t r, std::size_t c) {
     switch (st) {
         case RSVD_B200_ARGUMENT_ERROR: throw ArgumentError(msg);
         case RSVD_B200_DIMENSION_ERROR: throw DimensionError(msg);
-        case RSVD_B200_CONVERGENCE_ERROR: throw ConvergenceError(msg, kSvdMaxSweeps);
+        case RSVD_B200_CONVERGENCE_ERROR:
+            // svd.cpp:148 reports 0 iterations for a failed basis completion, svd.cpp:202
+            // the sweep count, which is kSvdMaxSweeps when the Jacobi loop runs out
+            throw ConvergenceError(msg, msg.find("orthonormal basis") != std::string::npos
+                                            ? 0
+                                            : kSvdMaxSweeps);
         default: throw DeviceError(msg);
     }
 }
@@ -118,10 +128,137 @@ bool DenseMatrix::all_finite() const noexcept {
     return true;
 }
 
+namespace {
+
+constexpr std::size_t kPairwiseBase = 64;  // matrix.cpp's cascade base case
+
+double cascade_sum(const double* x, std::size_t n) {
+    if (n <= kPairwiseBase) {
+        double acc = 0.0;
+        for (std::size_t i = 0; i < n; ++i) acc += x[i];
+        return acc;
+    }
+    const std::size_t h = n / 2;
+    return cascade_sum(x, h) + cascade_sum(x + h, n - h);
+}
+
+double cascade_dot(const double* x, const double* y, std::size_t n) {
+    if (n <= kPairwiseBase) {
+        double acc = 0.0;
+        for (std::size_t i = 0; i < n; ++i) acc += x[i] * y[i];
+        return acc;
+    }
+    const std::size_t h = n / 2;
+    return cascade_dot(x, y, h) + cascade_dot(x + h, y + h, n - h);
+}
+
+}  // namespace
+
+double pairwise_sum(std::span<const double> x) { return cascade_sum(x.data(), x.size()); }
+
+double pairwise_dot(std::span<const double> x, std::span<const double> y) {
+    if (x.size() != y.size())
+        throw DimensionError("dot of length " + std::to_string(x.size()) + " against length " +
+                             std::to_string(y.size()));
+    return cascade_dot(x.data(), y.data(), x.size());
+}
+
 double frobenius_norm(const DenseMatrix& a) {
-    double acc = 0.0;
-    for (double x : a.data()) acc += x * x;
-    return std::sqrt(acc);
+    return std::sqrt(cascade_dot(a.data().data(), a.data().data(), a.size()));
+}
+
+double max_abs(const DenseMatrix& a) {
+    double best = 0.0;
+    for (double x : a.data()) best = std::max(best, std::abs(x));
+    return best;
+}
+
+double max_abs_diff(const DenseMatrix& a, const DenseMatrix& b) {
+    if (a.rows() != b.rows() || a.cols() != b.cols())
+        throw DimensionError("max_abs_diff between " + shape_str(a.rows(), a.cols()) + " and " +
+                             shape_str(b.rows(), b.cols()));
+    double best = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i)
+        best = std::max(best, std::abs(a.data()[i] - b.data()[i]));
+    return best;
+}
+
+// ------------------------------------------------------------------ GaussianSampler
+// The scalar draws restate rng.cpp:22-46 on the host (same libm calls as the reference).
+namespace {
+constexpr std::uint64_t kGoldenGamma = 0x9E3779B97F4A7C15ULL;
+
+std::uint64_t mix64(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+}  // namespace
+
+std::uint64_t GaussianSampler::next_u64() { return mix64(seed_ + (++counter_) * kGoldenGamma); }
+
+double GaussianSampler::uniform01() {
+    return static_cast<double>((next_u64() >> 11) + 1) * 0x1.0p-53;
+}
+
+double GaussianSampler::normal() {
+    if (has_cached_) {
+        has_cached_ = false;
+        return cached_;
+    }
+    const double u1 = uniform01();
+    const double u2 = uniform01();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double t = 2.0 * M_PI * u2;
+    cached_ = r * std::sin(t);
+    has_cached_ = true;
+    return r * std::cos(t);
+}
+
+namespace detail {
+// Device draws continue the sampler's state and advance it as `count` normal() calls would.
+struct SamplerAccess {
+    static void draw(GaussianSampler& g, std::size_t count,
+                     const std::function<void(std::uint64_t, int, double)>& device) {
+        device(g.counter_, g.has_cached_ ? 1 : 0, g.cached_);
+        std::size_t rest = count;
+        if (g.has_cached_ && rest > 0) {
+            g.has_cached_ = false;
+            --rest;
+        }
+        const std::uint64_t base = g.counter_;
+        g.counter_ += 2 * ((rest + 1) / 2);
+        if (rest % 2 == 1) {  // the last pair's sine half stays cached in the sampler
+            double two[2];
+            check(rsvd_b200_gaussian_stream(handle(), g.seed_, base + rest - 1, 0, 0.0, 1, 2,
+                                            two));
+            g.cached_ = two[1];
+            g.has_cached_ = true;
+        }
+    }
+};
+}  // namespace detail
+
+// ------------------------------------------------------------------ thread budget
+namespace {
+std::atomic<unsigned> g_threads{1};
+}
+
+void set_max_threads(unsigned n) { g_threads.store(n == 0 ? 1 : n); }
+
+unsigned max_threads() { return g_threads.load(); }
+
+void parallel_for(std::size_t count, const std::function<void(std::size_t, std::size_t)>& body) {
+    const std::size_t workers = std::min<std::size_t>(g_threads.load(), count);
+    if (workers <= 1) {
+        body(0, count);
+        return;
+    }
+    const std::size_t chunk = (count + workers - 1) / workers;
+    std::vector<std::thread> pool;
+    for (std::size_t lo = 0; lo < count; lo += chunk)
+        pool.emplace_back([&body, lo, hi = std::min(count, lo + chunk)] { body(lo, hi); });
+    for (auto& t : pool) t.join();
 }
 
 // ------------------------------------------------------------------ rsvd API
@@ -149,26 +286,30 @@ double RsvdResult::residual_fro(const DenseMatrix& a) const {
 }
 
 DenseMatrix gaussian_matrix(GaussianSampler& sampler, std::size_t rows, std::size_t cols) {
-    if (sampler.counter() != 0)
-        throw ArgumentError("gaussian_matrix on the device needs a fresh sampler (counter 0)");
     DenseMatrix out(rows, cols);
-    check(rsvd_b200_gaussian_matrix(handle(), sampler.seed(), rows, cols, out.data().data()));
-    sampler.advance(2 * ((rows * cols + 1) / 2));
+    detail::SamplerAccess::draw(sampler, rows * cols,
+                                [&](std::uint64_t counter, int has_cached, double cached) {
+                                    check(rsvd_b200_gaussian_stream(
+                                        handle(), sampler.seed(), counter, has_cached, cached,
+                                        rows, cols, out.data().data()));
+                                });
     return out;
 }
 
 DenseMatrix sketch(const DenseMatrix& a, std::size_t s, GaussianSampler& sampler) {
-    if (sampler.counter() != 0)
-        throw ArgumentError("sketch on the device needs a fresh sampler (counter 0)");
     const std::size_t md = std::min(a.rows(), a.cols());
     if (s < 1 || s > md)
         throw ArgumentError("sketch width " + std::to_string(s) + " outside [1, " +
                             std::to_string(md) + "] for a " + shape_str(a.rows(), a.cols()) +
                             " input");
     DenseMatrix y(a.rows(), s);
-    check(rsvd_b200_sketch(handle(), a.data().data(), a.rows(), a.cols(), s, sampler.seed(),
-                           y.data().data()));
-    sampler.advance(2 * ((a.cols() * s + 1) / 2));
+    detail::SamplerAccess::draw(sampler, a.cols() * s,
+                                [&](std::uint64_t counter, int has_cached, double cached) {
+                                    check(rsvd_b200_sketch_stream(
+                                        handle(), a.data().data(), a.rows(), a.cols(), s,
+                                        sampler.seed(), counter, has_cached, cached,
+                                        y.data().data()));
+                                });
     return y;
 }
 

@@ -211,6 +211,7 @@ struct rsvd_b200_handle {
     long upload_aty = 0;  // splits of the last solve's upload-time A^T Y0 (0: not used)
     DevBuf gpart;             // per-tile Gram partials of the fused epilogue
     int* flags_host = nullptr;
+    StreamPos omega_pos;  // sampler state the next sketch's Omega continues (default: fresh)
     std::vector<double> omega_host;  // validation mode (n x s row-major)
     size_t omega_rows = 0, omega_cols = 0;
     int profiling = 0;  // 1: stage events, 2: + per-launch events on the A-pass GEMMs
@@ -1014,7 +1015,7 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
         h->launched(launch_transpose(h->omega_host_dev.d(), n, s, s, h->xt.d(), p.ldn, st),
                     "transpose");
     } else {
-        h->launched(launch_omega(seed, n, s, NP, h->xt.d(), p.ldn, st), "omega");
+        h->launched(launch_omega(seed, n, s, NP, h->xt.d(), p.ldn, st, h->omega_pos), "omega");
     }
     h->mark("sketch_gemm");
     if (p.f32) {
@@ -2020,11 +2021,18 @@ rsvd_b200_status rsvd_b200_randomized_ksvd_sharded_f32_device(
 
 rsvd_b200_status rsvd_b200_gaussian_matrix(rsvd_b200_handle* h, uint64_t seed, size_t rows,
                                            size_t cols, double* out) {
+    return rsvd_b200_gaussian_stream(h, seed, 0, 0, 0.0, rows, cols, out);
+}
+
+rsvd_b200_status rsvd_b200_gaussian_stream(rsvd_b200_handle* h, uint64_t seed, uint64_t counter,
+                                           int has_cached, double cached, size_t rows,
+                                           size_t cols, double* out) {
     return guarded([&] {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         DevBuf d;
         d.reserve(std::max<size_t>(rows * cols, 1) * sizeof(double));
-        h->launched(launch_gaussian_rowmajor(seed, (long)rows, (long)cols, d.d(), h->stream),
+        const StreamPos pos{counter, has_cached ? 1 : 0, cached};
+        h->launched(launch_gaussian_rowmajor(seed, (long)rows, (long)cols, d.d(), h->stream, pos),
                     "gaussian");
         ck(cudaMemcpyAsync(out, d.p, rows * cols * sizeof(double), cudaMemcpyDeviceToHost,
                            h->stream),
@@ -2097,6 +2105,17 @@ extern "C" {
 
 rsvd_b200_status rsvd_b200_sketch(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                                   size_t s, uint64_t seed, double* y0) {
+    return rsvd_b200_sketch_stream(h, a, m, n, s, seed, 0, 0, 0.0, y0);
+}
+
+rsvd_b200_status rsvd_b200_sketch_stream(rsvd_b200_handle* h, const double* a, size_t m,
+                                         size_t n, size_t s, uint64_t seed, uint64_t counter,
+                                         int has_cached, double cached, double* y0) {
+    struct PosGuard {  // the solve pipelines always start from a fresh sampler
+        rsvd_b200_handle* h;
+        ~PosGuard() { h->omega_pos = StreamPos{}; }
+    } guard{h};
+    h->omega_pos = StreamPos{counter, has_cached ? 1 : 0, cached};
     return guarded([&] {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         check_shape((long)m, (long)n, "sketch");

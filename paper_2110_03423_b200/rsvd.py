@@ -389,6 +389,26 @@ class Solver:
                                                             cols, _dp(out)))
         return out
 
+    def gaussian_stream(self, seed: int, counter: int, rows: int, cols: int,
+                        cached: float | None = None) -> np.ndarray:
+        """rows x cols normals from a GaussianSampler(seed) that has drawn `counter` words and
+        holds `cached` (a pending sine half) or nothing (rng.cpp:22-53)."""
+        out = np.empty((rows, cols))
+        _check(self.lib, self.lib.rsvd_b200_gaussian_stream(
+            self.h, seed & (2**64 - 1), counter, int(cached is not None),
+            0.0 if cached is None else float(cached), rows, cols, _dp(out)))
+        return out
+
+    def sketch_stream(self, a, s: int, seed: int, counter: int,
+                      cached: float | None = None) -> np.ndarray:
+        """sketch() from a sampler part-way through its stream (see gaussian_stream)."""
+        a = _arr(a)
+        y = np.empty((a.shape[0], max(int(s), 1)))
+        _check(self.lib, self.lib.rsvd_b200_sketch_stream(
+            self.h, _dp(a), a.shape[0], a.shape[1], s, seed & (2**64 - 1), counter,
+            int(cached is not None), 0.0 if cached is None else float(cached), _dp(y)))
+        return y
+
     def splitmix_words(self, seed: int, count: int, first_counter: int = 1) -> np.ndarray:
         out = np.empty(count, dtype=np.uint64)
         _check(self.lib, self.lib.rsvd_b200_splitmix_words(

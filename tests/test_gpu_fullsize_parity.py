@@ -50,8 +50,15 @@ def _compare(torch, u, s, v, ru, rs, rv, sig_tol, ang_tol, what):
     assert rel <= sig_tol, (what, rel)
     assert au <= ang_tol, (what, au)
     assert av <= ang_tol, (what, av)
-    if ang_tol <= ANG64:  # the sign convention (svd.cpp:237-254): elementwise comparable too
-        assert (v.double() - rv).abs().max().item() <= 1e-6, what
+    if ang_tol <= ANG64:
+        # the sign convention (svd.cpp:237-254) makes V elementwise comparable wherever a
+        # column's largest |entry| is unambiguous (Hadamard inputs have all-equal |entries|,
+        # where the pick is decided by rounding on both sides)
+        top2 = rv.abs().topk(2, dim=0).values
+        pinned = (top2[0] - top2[1]) > 1e-9 * top2[0]
+        if pinned.any():
+            d = (v.double()[:, pinned] - rv[:, pinned]).abs().max().item()
+            assert d <= 1e-6, (what, d)
 
 
 def _assert_optimistic(solver, what):

@@ -71,6 +71,34 @@ def test_device_normals_vs_reference(solver):
         assert np.mean(dev != ref) < 0.005, key  # glibc misrounds ~0.1-0.2%
 
 
+def test_sampler_continuation(solver, port):
+    """gaussian_matrix / sketch continue a sampler part-way through its stream
+    (rng.cpp:22-53): after t normals the sampler holds counter 2*ceil(t/2) and, for odd t,
+    the cached sine half; after raw next_u64() calls the pairs start at an odd counter."""
+    import math
+    seed = 1234
+    fresh = solver.gaussian_matrix(seed, 1, 400).ravel()
+    for t in (0, 1, 2, 7, 8, 33, 250):
+        counter = 2 * ((t + 1) // 2)
+        cached = fresh[t] if t % 2 else None
+        got = solver.gaussian_stream(seed, counter, 3, 40, cached=cached).ravel()
+        assert np.array_equal(got, fresh[t:t + 120]), t
+        # sketch(I) of a continued sampler is that sampler's Omega, bit for bit
+        y = solver.sketch_stream(np.eye(40), 3, seed, counter, cached=cached)
+        assert np.array_equal(y, got.reshape(40, 3)), t
+    # odd counter: pairs built from words (c+1, c+2); host restatement with glibc's libm
+    u = port.uniforms(seed, 64)  # counters 1..64
+    c = 3
+    want = []
+    for j in range(10):
+        u1, u2 = u[c + 2 * j], u[c + 2 * j + 1]  # counters c+2j+1, c+2j+2
+        r = math.sqrt(-2.0 * math.log(u1))
+        want += [r * math.cos(2.0 * math.pi * u2), r * math.sin(2.0 * math.pi * u2)]
+    got = solver.gaussian_stream(seed, c, 1, 20).ravel()
+    ulp = np.abs(got.view(np.int64) - np.array(want).view(np.int64))
+    assert ulp.max() <= 2
+
+
 def test_device_normals_correctly_rounded(solver, port):
     mp = pytest.importorskip("mpmath")
     import math
