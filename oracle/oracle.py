@@ -96,6 +96,7 @@ class Oracle:
             f("splitmix_words").argtypes = [_u64, _sz, C.POINTER(_u64)]
             f("uniforms").argtypes = [_u64, _sz, _dp]
             f("set_max_threads").argtypes = [C.c_uint]
+            f("sampler_normals").argtypes = [_u64, _sz, _sz, _sz, _dp]
             f("matrix_new").argtypes = [_dp, _sz, _sz]
             f("matrix_new").restype = C.c_void_p
             f("matrix_free").argtypes = [C.c_void_p]
@@ -129,6 +130,14 @@ class Oracle:
     def gaussian_matrix(self, seed: int, rows: int, cols: int) -> np.ndarray:
         out = np.empty((rows, cols), dtype=np.float64)
         self._f("gaussian_matrix")(seed, rows, cols, _ptr(out))
+        return out
+
+    def sampler_normals(self, seed: int, count: int, skip_words: int = 0,
+                        skip_normals: int = 0) -> np.ndarray:
+        """Reference only: `count` normals of GaussianSampler(seed) after `skip_words`
+        next_u64() calls and `skip_normals` normal() calls (rng.cpp:22-46)."""
+        out = np.empty(count, dtype=np.float64)
+        self._f("sampler_normals")(seed, skip_words, skip_normals, count, _ptr(out))
         return out
 
     # ------------------------------------------------------------ dense core

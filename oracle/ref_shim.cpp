@@ -78,6 +78,16 @@ void ref_gaussian_matrix(std::uint64_t seed, std::size_t rows, std::size_t cols,
     to(gaussian_matrix(s, rows, cols), out);
 }
 
+// `count` normals of a sampler that first returned `skip_words` raw words (next_u64) and
+// then `skip_normals` normals: the continuation cases of sketch / gaussian_matrix
+void ref_sampler_normals(std::uint64_t seed, std::size_t skip_words, std::size_t skip_normals,
+                         std::size_t count, double* out) {
+    GaussianSampler s(seed);
+    for (std::size_t i = 0; i < skip_words; ++i) s.next_u64();
+    for (std::size_t i = 0; i < skip_normals; ++i) s.normal();
+    for (std::size_t i = 0; i < count; ++i) out[i] = s.normal();
+}
+
 double ref_pairwise_dot(const double* x, const double* y, std::size_t n) {
     return pairwise_dot(std::span<const double>(x, n), std::span<const double>(y, n));
 }

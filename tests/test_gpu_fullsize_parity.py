@@ -8,7 +8,8 @@ the bench arms solve) and assert that this path is the one that ran
 
 * C1, C2: the reference library itself (oracle/_ref, the unmodified reference sources, all
   host threads; ~40 s at C2) on the same host matrix and seed — in the default mode (device
-  Omega, correctly rounded normals) and in validation mode (the reference's Omega);
+  Omega, bit-identical to the reference's) and in validation mode (the reference's Omega
+  handed in);
 * C3, C4 (FP32), C5: a literal FP64 restatement of the algorithm on the vendor libraries
   (tests/torch_restatement.py) fed the reference's Omega, itself checked against the
   reference library at C1/C2 here. The CPU reference would need 4-20 minutes per solve at
