@@ -51,6 +51,12 @@ CONFIGS = {
                name="C3 rSVD 202599x16384 k=128 p=20 q=2 FP64 (CelebA 128x128-shaped)"),
     "c5": dict(m=65536, n=65536, k=32, p=10, q=6, spectrum="slow", cpu_rows=1024,
                name="C5 rSVD 65536x65536 k=32 p=10 q=6 FP64 (slow decay 1/i^0.1)"),
+    # C5's shape with sigma_1/sigma_s = 1e10: every CholeskyQR2 breaks down (cond(Y) >> 1e6),
+    # so the solve is the optimistic attempt (aborted at the first Cholesky) + the robust
+    # rerun with the blocked Householder fallback in every tall QR
+    "c5ill": dict(m=65536, n=65536, k=32, p=10, q=6, spectrum="ill", ratio=1e10, cpu_rows=1024,
+                  name="C5-ill rSVD 65536x65536 k=32 p=10 q=6 FP64 (sigma_1/sigma_s = 1e10, "
+                       "CholeskyQR2 -> Householder fallback)"),
     # FP32 A, 3xTF32 tensor cores; m is per GPU (weak scaling up to 1.6M x 4096 at 8 GPUs).
     # sigma_1/sigma_s = 1e2 keeps the FP32 bar (1e-4 on sigma) meaningful.
     "c4": dict(m=200000, n=4096, k=256, p=16, q=4, spectrum="exp", ratio=1e2, cpu_rows=2048,
@@ -71,10 +77,14 @@ def dist_env():
 def spectrum(cfg, n, xp):
     """Controlled decaying spectra: "exp" sigma_i = exp(-i/tau) + 1e-6 with
     sigma_1/sigma_s = 1e4 over the sketch width; "slow" sigma_i = 1/(i+1)^0.1
-    (synth.cpp:37's slow decay)."""
+    (synth.cpp:37's slow decay); "ill" sigma_i = ratio^(-i/(s-1)) floored at 1e-14
+    (sigma_1/sigma_s = ratio over the sketch width)."""
     i = xp.arange(n, dtype=xp.float64)
     if cfg["spectrum"] == "slow":
         return 1.0 / (i + 1.0) ** 0.1
+    if cfg["spectrum"] == "ill":
+        s = cfg["k"] + cfg["p"]
+        return xp.maximum(cfg["ratio"] ** (-i / (s - 1)), 1e-14)
     tau = (cfg["k"] + cfg["p"] - 1) / np.log(cfg.get("ratio", 1e4))
     return xp.exp(-i / tau) + 1e-6
 
@@ -537,6 +547,8 @@ def run_ours(args):
         barrier()
     dev_ms = e0.elapsed_time(e1)
     graph_steps = solver.last_info("graph_launches") - graphs0
+    robust = {"robust_reruns": solver.last_info("robust_reruns"),
+              "householder_fallbacks": solver.last_info("householder_fallbacks")}
 
     # ---- the same K solves once more with per-launch CUDA events around every pass over A
     # (profiling level 2 runs the pipeline eagerly: events recorded by graph nodes cannot be
@@ -636,6 +648,7 @@ def run_ours(args):
                            "kernels_per_solve": launches_per_step},
             "roofline": roof,
             "cpu_baseline": cpu,
+            "robust_path": robust,
             "wall_s_timed": round(wall, 3),
             "sigma1": sigma1,
         }

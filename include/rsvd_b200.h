@@ -233,6 +233,17 @@ rsvd_b200_status rsvd_b200_sketch_stream(rsvd_b200_handle* h, const double* a, s
                                          int has_cached, double cached, double* y0);
 rsvd_b200_status rsvd_b200_power_iterate(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                                          const double* y0, size_t s, size_t q, double* w);
+/* Householder thin QR (replaces randsvd::householder_qr, qr.hpp:16 / qr.cpp:27-102):
+ * a m x n row-major (m >= n, n <= 288) -> q m x n with orthonormal columns and r n x n
+ * upper triangular with a non-negative diagonal (strictly-lower entries exact zeros).
+ * The blocked (compact WY) Householder kernel of the CholeskyQR2 fallback. m < n is
+ * RSVD_B200_DIMENSION_ERROR (the reference's DimensionError). The _device variant takes
+ * device pointers with leading dimensions and is stream-ordered (rsvd_b200_stream). */
+rsvd_b200_status rsvd_b200_householder_qr(rsvd_b200_handle* h, const double* a, size_t m,
+                                          size_t n, double* q, double* r);
+rsvd_b200_status rsvd_b200_householder_qr_device(rsvd_b200_handle* h, const double* a, size_t lda,
+                                                 size_t m, size_t n, double* q, size_t ldq,
+                                                 double* r, size_t ldr);
 rsvd_b200_status rsvd_b200_range_basis(rsvd_b200_handle* h, const double* y, size_t m, size_t s,
                                        double* q, size_t* cols_out);
 rsvd_b200_status rsvd_b200_project_and_solve(rsvd_b200_handle* h, const double* a, size_t m,

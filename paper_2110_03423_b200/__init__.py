@@ -6,6 +6,6 @@ C-ABI in include/rsvd_b200.h, C++ API in include/randsvd/*.hpp, this Python mirr
 """
 from .rsvd import (ArgumentError, ConvergenceError, DeviceError, DimensionError, Error,  # noqa: F401
                    RsvdConfig, RsvdResult, Solver, SvdFactors, power_iterate, project_and_solve,
-                   LocalGroup, nccl_unique_id, randomized_ksvd, range_basis,
+                   LocalGroup, nccl_unique_id, randomized_ksvd, range_basis, householder_qr,
                    singular_values_only, sketch)
 from .dist import attach_process_group, shard_rows  # noqa: F401

@@ -168,7 +168,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
                    double* __restrict__ Y, long ldy, long split_stride, int M, int k_tiles,
                    int k_tiles_per_split, int* __restrict__ flag, double* __restrict__ gram,
                    const double* __restrict__ resid, long resid_ld, int resid_cols,
-                   double* __restrict__ resid_out) {
+                   double* __restrict__ resid_out, const int* __restrict__ abort_flag) {
+    // a Cholesky breakdown earlier in an optimistic pipeline: the run is discarded and
+    // repeated robustly, so skip the pass (all threads of the CTA return together)
+    if (abort_flag && *(const volatile int*)abort_flag) return;
     constexpr int NP = NT * 8;
     constexpr int MI = BM / WM / 16;
     constexpr int NI = NT / WN;
@@ -403,7 +406,8 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_atx_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {N, K}, box {16, 32}
                     const __grid_constant__ CUtensorMap mapW,  // dims {NP, K}, box {16, 32}
                     double* __restrict__ Z, long ldz, long split_stride, int N, int k_tiles,
-                    int k_tiles_per_split) {
+                    int k_tiles_per_split, const int* __restrict__ abort_flag) {
+    if (abort_flag && *(const volatile int*)abort_flag) return;  // see gemm_ax_kernel
     constexpr int NP = NT * 8;
     constexpr int MI = BJ / WM / 16;
     constexpr int NI = NT / WN;
@@ -625,7 +629,7 @@ cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     if (p.gram && (splits != 1 || NT > 12)) return cudaErrorInvalidValue;
     kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mX, p.Y, p.ldy, p.split_stride, (int)p.M,
                                                  k_tiles, per, p.flag, p.gram, p.resid,
-                                                 p.resid_ld, p.resid_cols, p.resid_out);
+                                                 p.resid_ld, p.resid_cols, p.resid_out, p.abort);
     return cudaGetLastError();
 }
 
@@ -646,7 +650,7 @@ cudaError_t launch_atx_t(const GemmAtx& p, cudaStream_t st) {
     dim3 grid((unsigned)((p.N + BJ - 1) / BJ), (unsigned)splits);
     if (ACC && splits != 1) return cudaErrorInvalidValue;
     kern<<<grid, (WM * WN + 1) * 32, smem, st>>>(mA, mW, p.Z, p.ldz, p.split_stride, (int)p.N,
-                                                 k_tiles, per);
+                                                 k_tiles, per, p.abort);
     return cudaGetLastError();
 }
 

@@ -203,7 +203,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap mapB,
                      const __grid_constant__ CUtensorMap mapBlo, void* __restrict__ out,
                      float* __restrict__ out_lo, long ldo, long split_stride, int M, int NP,
-                     int k_tiles, int k_tiles_per_split, int* __restrict__ flag, int upper) {
+                     int k_tiles, int k_tiles_per_split, int* __restrict__ flag, int upper,
+                     const int* __restrict__ abort_flag) {
+    // an aborted optimistic pipeline skips its remaining passes (both CTAs of a pair read
+    // the same flag, set before this launch in stream order, so they return together)
+    if (abort_flag && *(const volatile int*)abort_flag) return;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                          ~uintptr_t(1023));
@@ -675,7 +679,8 @@ cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, kern, mA, mB, mBlo, p.out, static_cast<float*>(p.out_lo), p.ldo,
-                           p.split_stride, (int)p.M, p.NP, k_tiles, per, p.flag, (int)p.upper);
+                           p.split_stride, (int)p.M, p.NP, k_tiles, per, p.flag, (int)p.upper,
+                           p.abort);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -1,267 +1,450 @@
 // Robust paths of the rSVD on B200:
 //
-//  * the Householder QR fallback of CholeskyQR2 — a restatement of the reference's
-//    unblocked Householder QR (qr.cpp:27-102): reflector v ~ x + sign(x_1)||x|| e_1
-//    per column, applied to the trailing columns, thin Q accumulated backwards from
-//    the identity, then diag(R) >= 0 by flipping R rows / Q columns. Each CTA owns a
-//    contiguous row slab; every reduction is a fixed-order sum over per-CTA partials,
-//    so the result is deterministic. Two launches per column (factorisation) and two
-//    per column (Q accumulation); it only runs on ill-conditioned input.
+//  * the Householder QR fallback of CholeskyQR2 — the reference's Householder QR
+//    (qr.cpp:27-102: reflector v ~ x + sign(x_1)||x|| e_1 per column, thin Q accumulated
+//    backwards from the identity, diag(R) >= 0 by flipping R rows / Q columns) blocked
+//    into 32-column panels with the compact WY form, in one cooperative launch (below);
+//    it only runs on ill-conditioned input.
 //
 //  * complete_basis_kernel — the reference's deterministic orthonormal completion
 //    (svd.cpp:111-151): for each missing column, canonical vectors e_t are tried in
 //    ascending order of row load (sum of squares of the row over the valid columns,
 //    ties by index, i.e. the stable sort of svd.cpp:126-130), orthogonalised by two
 //    modified Gram-Schmidt passes and accepted when the remaining norm >= 1e-4.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
 
+namespace cg = cooperative_groups;
+
 namespace rsvdb200 {
 
-constexpr int kHHThreads = 256;
+// =============================================== blocked Householder QR (compact WY)
+// One cooperative launch per QR. CTA b owns the contiguous rows [lo, hi) of the M x NP
+// working copy A of Y. Columns are factored in panels of up to 32 (one warp lane per
+// panel column):
+//  * column step k (one grid barrier each): every CTA re-reduces, in a fixed order, the
+//    partials p_l = sum_{i > k} A[i][k] A[i][j0 + l] the previous step left behind
+//    (p_k is the tail norm^2 of column k, p_j its dots with the later panel columns) and
+//    reads row k from a broadcast buffer; that gives the reflector v = (x + sign(x_k)
+//    ||x|| e_k) / ||.|| of qr.cpp:44-58 and v.w_j = (p_j + alpha A[k][j]) / ||v|| without a
+//    second reduction; the CTA then updates its rows of the panel (w_j -= 2 (v.w_j) v) and
+//    accumulates the partials of column k + 1 in the same pass. The panel slice lives in
+//    shared memory when it fits (rows_per * 32 doubles), else it is updated in place in HBM.
+//  * panel end (two barriers): V^T V and W = V^T A_trail partials per CTA, a distributed
+//    fixed-order reduction, then T of the compact WY form H_j0 ... H_j0+jb-1 = I - V T V^T
+//    (T(1:i-1, i) = -tau_i T(1:i-1, 1:i-1) V^T v_i, tau = 2 for the unit reflectors) and
+//    A_trail -= V (T^T W) on every CTA's rows (DFMA; the first column of the next panel
+//    gets its partials from the same pass).
+//  * Q: backward over the panels from [I; 0] (qr.cpp:71-84 accumulates reflectors
+//    backwards the same way), Q[:, j0:] -= V (T (V^T Q[:, j0:])), two barriers per panel.
+//  * diag(R) >= 0 by flipping R rows / Q columns (qr.cpp:86-93).
+// Every cross-CTA sum is a fixed-order sum, so the result is deterministic. Barriers: s
+// column steps plus two per panel for the factorisation and two per panel for Q (s = 74:
+// 86), instead of the unblocked version's 4s + 3 launches that each re-read the m x s
+// working matrix.
+constexpr int kPW = 32;           // panel width = warp lanes
+constexpr int kHHThreads = 512;
 constexpr int kHHWarps = kHHThreads / 32;
-constexpr int kMaxCh = 9;  // up to 288 columns, 32 per lane-chunk
-constexpr int kMaxCols = 32 * kMaxCh;
+constexpr int kMaxCols = 288;
+constexpr int kPartStride = kPW * kPW + kPW * kMaxCols;  // V^T V, then W (kPW x kMaxCols)
+// shared memory: per-warp reduction buffer (kHHWarps x kPW x kPW) + M2 (kPW x kMaxCols) +
+// T (kPW x (kPW + 1)); the panel slice of the column steps aliases the first two
+constexpr int kSmRed = kHHWarps * kPW * kPW;
+constexpr int kSmM2 = kPW * kMaxCols;
+constexpr int kSmT = kPW * (kPW + 1);
+constexpr size_t kHHSmem = (size_t)(kSmRed + kSmM2 + kSmT) * sizeof(double);
+constexpr long kSlabRows = (kSmRed + kSmM2) / kPW;  // rows of a panel slice that fit
 
-// Block-wide partial sums of sum_{rows i in [lo,hi)} x_i * w[i][j] for j in [j0, s),
-// x_i given by a functor; written to out[j].
-template <typename XF>
-__device__ void block_col_dots(const double* __restrict__ w, long ld, long lo, long hi, int j0,
-                               int s, XF xval, double* __restrict__ out /* [s] */,
-                               double* __restrict__ red /* smem kHHWarps x kMaxCols */) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double acc[kMaxCh];
-#pragma unroll
-    for (int c = 0; c < kMaxCh; ++c) acc[c] = 0.0;
-    for (long i = lo + warp; i < hi; i += kHHWarps) {
-        const double x = xval(i);
-        const double* row = w + i * ld;
-#pragma unroll
-        for (int c = 0; c < kMaxCh; ++c) {
-            const int j = j0 + lane + 32 * c;
-            if (j < s) acc[c] += x * row[j];
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < kMaxCh; ++c) {
-        const int j = j0 + lane + 32 * c;
-        if (j < s) red[warp * kMaxCols + j] = acc[c];
-    }
-    __syncthreads();
-    for (int j = j0 + threadIdx.x; j < s; j += blockDim.x) {
-        double t = 0.0;
-        for (int q = 0; q < kHHWarps; ++q) t += red[q * kMaxCols + j];
-        out[j] = t;
-    }
-    __syncthreads();
-}
-
-// The factorisation is a sequence of ordinary launches (two per column, one grid-wide
-// reduction each), so no grid-wide barrier or co-residency assumption is needed.
-// Partial sums live in part[block][0..NP-1] (column dots) and part[block][NP] (tail
-// norm^2); every block re-reduces the partials in the same fixed order, so all blocks
-// derive bit-identical reflectors.
 struct HH {
     const double* Y;
-    long M;
-    int s;
     long ldy;
-    double* Q;
+    long M;
+    int s, NP, G;
+    long rows_per;
+    double* A;        // M x NP working copy, R in its upper triangle at the end
+    double* V;        // M x NP reflectors (column k: rows >= k, unit norm)
+    double* Q;        // output M x ldq
     long ldq;
-    double* R;
-    int NP;
-    double* work;  // M x NP row-major working copy
-    double* refl;  // M x NP reflector columns
-    double* part;  // nb x (NP + 2)
-    int* act;      // NP
+    double* R;        // output NP x NP
+    double* colpart;  // [2][G][kPW] column-step partials (double-buffered by k parity)
+    double* rowbuf;   // [2][kPW] row k of the panel (double-buffered)
+    double* part;     // [G][kPartStride] panel-pass partials
+    double* red;      // [2][kPartStride] reduced panel-pass sums (double-buffered)
+    double* T;        // [panels][kPW][kPW]
 };
 
-__device__ __forceinline__ void hh_rows(const HH& h, long& lo, long& hi) {
-    const long rpb = (h.M + gridDim.x - 1) / gridDim.x;
-    lo = blockIdx.x * rpb;
-    hi = min(h.M, lo + rpb);
+// Deterministic sum over the CTAs of the 32-lane column-step partials of parity `par`
+// into out[32]: warp w sums the CTAs g = w (mod 16) in order, then lane l adds the 16
+// warp sums in order. Cross-CTA data is read with ld.global.cg (L2), never a stale L1 line.
+__device__ __forceinline__ void sum_colpart(const HH& h, int par, double* wred, double* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double* p = h.colpart + (size_t)par * h.G * kPW;
+    double t = 0.0;
+    for (int g = warp; g < h.G; g += kHHWarps) t += __ldcg(p + g * kPW + lane);
+    wred[warp * kPW + lane] = t;
+    __syncthreads();
+    if (threadIdx.x < kPW) {
+        double u = 0.0;
+        for (int w = 0; w < kHHWarps; ++w) u += wred[w * kPW + threadIdx.x];
+        out[threadIdx.x] = u;
+    }
 }
 
-// tail norm^2 of column k (rows > k) into slot NP + (k & 1): consecutive columns use
-// different slots, so a launch never overwrites a value another block may still read.
-__device__ void hh_tail_norm(const HH& h, int k, long lo, long hi, double* red) {
+// Warp partials acc (one per lane) of all warps -> CTA partial written to out[lane].
+__device__ __forceinline__ void cta_lane_sum(double acc, double* wred, double* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    wred[warp * kPW + lane] = acc;
+    __syncthreads();
+    if (threadIdx.x < kPW) {
+        double t = 0.0;
+        for (int w = 0; w < kHHWarps; ++w) t += wred[w * kPW + threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+// Pass over rows [r0, hi) of this CTA accumulating, per job, acc[a] (a < jb) at lane l:
+// job 0 (if with_vtv): sum v_a v_{j0+l};  job 1 + c: sum v_a X[i][c0 + 32 c + l].
+// Per-CTA sums go to part[cta][a * kPW + l] (V^T V) and part[cta][kPW*kPW + a*kMaxCols + j]
+// (W, j = column offset from c0).
+__device__ void panel_dots(const HH& h, const double* X, long ldx, long r0, long hi, int j0,
+                           int jb, int c0, int ncols, bool with_vtv, double* sred) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nch = (ncols + kPW - 1) / kPW;
+    const int jobs = nch + (with_vtv ? 1 : 0);
+    double* out = h.part + (size_t)blockIdx.x * kPartStride;
+    if (jobs == 0) return;
+    const int groups = kHHWarps / jobs;
+    const int job = warp % jobs, grp = warp / jobs;
+    double acc[kPW];
+#pragma unroll
+    for (int a = 0; a < kPW; ++a) acc[a] = 0.0;
+    if (grp < groups) {
+        const bool vtv = with_vtv && job == 0;
+        const int c = with_vtv ? job - 1 : job;
+        const int col = c0 + c * kPW + lane;
+        const bool colok = vtv ? lane < jb : (c * kPW + lane) < ncols;
+        for (long i = r0 + grp; i < hi; i += groups) {
+            const double vl = lane < jb ? h.V[i * h.NP + j0 + lane] : 0.0;
+            const double x = vtv ? vl : (colok ? X[i * ldx + col] : 0.0);
+#pragma unroll
+            for (int a = 0; a < kPW; ++a) acc[a] = fma(__shfl_sync(0xffffffffu, vl, a), x, acc[a]);
+        }
+    }
+    // cross-warp (same job) reduction in a fixed order
+#pragma unroll
+    for (int a = 0; a < kPW; ++a) sred[(warp * kPW + a) * kPW + lane] = acc[a];
+    __syncthreads();
+    for (int e = threadIdx.x; e < jobs * kPW * kPW; e += kHHThreads) {
+        const int jj = e / (kPW * kPW), a = (e / kPW) % kPW, l = e % kPW;
+        if (a >= jb) continue;
+        double t = 0.0;
+        for (int g = 0; g < groups; ++g) t += sred[((g * jobs + jj) * kPW + a) * kPW + l];
+        const bool vtv = with_vtv && jj == 0;
+        const int c = with_vtv ? jj - 1 : jj;
+        if (vtv) {
+            out[a * kPW + l] = t;
+        } else if (c * kPW + l < ncols) {
+            out[kPW * kPW + a * kMaxCols + c * kPW + l] = t;
+        }
+    }
+    __syncthreads();
+}
+
+// Distributed fixed-order reduction of entries [0, n) of every CTA's part into red.
+__device__ void reduce_part(const HH& h, double* red, int n_vtv, int jb, int ncols) {
+    const long nw = (long)jb * kMaxCols;
+    const long total = kPW * kPW + nw;
+    for (long e = (long)blockIdx.x * kHHThreads + threadIdx.x; e < total;
+         e += (long)h.G * kHHThreads) {
+        bool ok;
+        if (e < kPW * kPW) ok = n_vtv && (e / kPW) < jb && (e % kPW) < jb;
+        else ok = ((e - kPW * kPW) % kMaxCols) < ncols;
+        if (!ok) continue;
+        double t = 0.0;
+        for (int g = 0; g < h.G; ++g) t += __ldcg(h.part + (size_t)g * kPartStride + e);
+        red[e] = t;
+    }
+}
+
+// X[i][c0 + j] -= sum_a v_a[i] M2[a][j] for the CTA's rows [r0, hi), j < ncols. With
+// `next_k` >= 0 the warps on the first chunk also accumulate the column-step partials of
+// column next_k = c0 (lanes < next_jb) and the owner of row next_k broadcasts it.
+__device__ void panel_update(const HH& h, double* X, long ldx, long r0, long hi, int j0, int jb,
+                             int c0, int ncols, const double* M2, long next_k, int next_jb,
+                             double* wred) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nch = (ncols + kPW - 1) / kPW;
     double acc = 0.0;
-    for (long i = max(lo, (long)k + 1) + threadIdx.x; i < hi; i += blockDim.x) {
-        const double x = h.work[i * h.NP + k];
-        acc += x * x;
+    if (nch > 0) {
+        const int groups = kHHWarps / nch;
+        const int c = warp % nch, grp = warp / nch;
+        if (grp < groups) {
+            const int j = c * kPW + lane;
+            const bool colok = j < ncols;
+            for (long i = r0 + grp; i < hi; i += groups) {
+                const double vl = lane < jb ? h.V[i * h.NP + j0 + lane] : 0.0;
+                double x = colok ? X[i * ldx + c0 + j] : 0.0;
+                double upd = 0.0;
+#pragma unroll
+                for (int a = 0; a < kPW; ++a)
+                    upd = fma(__shfl_sync(0xffffffffu, vl, a), M2[a * kMaxCols + j], upd);
+                x -= upd;
+                if (colok) X[i * ldx + c0 + j] = x;
+                if (next_k >= 0 && c == 0) {
+                    const double xk = __shfl_sync(0xffffffffu, x, 0);
+                    if (i > next_k && lane < next_jb) acc = fma(xk, x, acc);
+                    if (i == next_k && lane < next_jb)
+                        h.rowbuf[(next_k & 1) * kPW + lane] = x;
+                }
+            }
+        }
     }
-    acc = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int q = 0; q < kHHWarps; ++q) t += red[q];
-        h.part[blockIdx.x * (h.NP + 2) + h.NP + (k & 1)] = t;
-    }
-    __syncthreads();
+    if (next_k >= 0)
+        cta_lane_sum(acc, wred, h.colpart + ((size_t)(next_k & 1) * h.G + blockIdx.x) * kPW);
 }
 
-__global__ void __launch_bounds__(kHHThreads) hh_init_kernel(HH h) {
-    __shared__ double red[kHHWarps];
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    for (long i = lo; i < hi; ++i)
-        for (int j = threadIdx.x; j < h.NP; j += blockDim.x) {
-            h.work[i * h.NP + j] = j < h.s ? h.Y[i * h.ldy + j] : 0.0;
-            h.refl[i * h.NP + j] = 0.0;
-        }
-    __syncthreads();
-    hh_tail_norm(h, 0, lo, hi, red);
-}
+__global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double sm[];
+    double* sred = sm;                  // kSmRed
+    double* M2 = sm + kSmRed;           // kSmM2
+    double* Ts = M2 + kSmM2;            // kSmT
+    __shared__ double cs[kPW], rowk[kPW], dd[kPW], wred[kHHWarps * kPW], diag[kMaxCols];
+    __shared__ int taus[kPW];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = h.s, NP = h.NP;
+    const long lo = (long)blockIdx.x * h.rows_per, hi = min(h.M, lo + h.rows_per);
+    const int panels = (s + kPW - 1) / kPW;
 
-// column k, phase A: reflector v_k (qr.cpp:44-58) and partial dots v_k . w_j, j > k
-__global__ void __launch_bounds__(kHHThreads) hh_col_a_kernel(HH h, int k) {
-    __shared__ double red[kHHWarps * kMaxCols];
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    const int NP = h.NP;
-    double tail2 = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) tail2 += h.part[b * (NP + 2) + NP + (k & 1)];
-    const double x0 = h.work[(long)k * NP + k];
-    const double norm_x = sqrt(tail2 + x0 * x0);
-    if (norm_x == 0.0) {  // zero column: H_k = I, r_kk = 0 (qr.cpp:47)
-        if (blockIdx.x == 0 && threadIdx.x == 0) h.act[k] = 0;
-        return;
+    // ---- init: A = Y (pad columns zero), V = 0, partials of column 0
+    {
+        double acc = 0.0;
+        const int jb0 = min(kPW, s);
+        for (long i = lo + warp; i < hi; i += kHHWarps) {
+            double a0 = 0.0;
+            for (int c = lane; c < NP; c += kPW) {
+                const double y = c < s ? h.Y[i * h.ldy + c] : 0.0;
+                h.A[i * NP + c] = y;
+                h.V[i * NP + c] = 0.0;
+                if (c == lane) a0 = y;
+            }
+            const double x0 = __shfl_sync(0xffffffffu, a0, 0);
+            if (i > 0 && lane < jb0) acc = fma(x0, a0, acc);
+            if (i == 0 && lane < jb0) h.rowbuf[lane] = a0;
+        }
+        cta_lane_sum(acc, wred, h.colpart + (size_t)blockIdx.x * kPW);
     }
-    const double sign = x0 >= 0.0 ? 1.0 : -1.0;
-    const double alpha = x0 + sign * norm_x;
-    const double inv_nv = 1.0 / sqrt(tail2 + alpha * alpha);
-    if (blockIdx.x == 0 && threadIdx.x == 0) h.act[k] = 1;
-    for (long i = max(lo, (long)k) + threadIdx.x; i < hi; i += blockDim.x)
-        h.refl[i * NP + k] = (i == k ? alpha : h.work[i * NP + k]) * inv_nv;
-    __syncthreads();
-    block_col_dots(h.work, NP, max(lo, (long)k), hi, k + 1, h.s,
-                   [&](long i) { return h.refl[i * NP + k]; }, h.part + blockIdx.x * (NP + 2), red);
-}
+    grid.sync();
 
-// column k, phase B: w_j -= 2 (v.w_j) v for j > k, r_kk, tail norm of column k + 1
-__global__ void __launch_bounds__(kHHThreads) hh_col_b_kernel(HH h, int k) {
-    __shared__ double dj[kMaxCols];
-    __shared__ double red[kHHWarps];
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    const int NP = h.NP;
-    const bool active = h.act[k] != 0;
-    if (active) {
-        for (int j = k + 1 + threadIdx.x; j < h.s; j += blockDim.x) {
-            double t = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) t += h.part[b * (NP + 2) + j];
-            dj[j] = 2.0 * t;
+    for (int p = 0; p < panels; ++p) {
+        const int j0 = p * kPW, jb = min(kPW, s - j0);
+        // the panel slice [max(lo, j0), hi) x jb in shared memory when it fits
+        const long r0 = max(lo, (long)j0);
+        const bool in_smem = hi - r0 <= kSlabRows;
+        double* P;
+        long ldp;
+        long base;
+        if (in_smem) {
+            P = sm;
+            ldp = kPW;
+            base = r0;
+            for (long i = r0 + warp; i < hi; i += kHHWarps)
+                if (lane < jb) P[(i - base) * kPW + lane] = h.A[i * NP + j0 + lane];
+            __syncthreads();
+        } else {
+            P = h.A + j0;
+            ldp = NP;
+            base = 0;
         }
-        double tail2 = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) tail2 += h.part[b * (NP + 2) + NP + (k & 1)];
-        __syncthreads();
-        for (long i = max(lo, (long)k); i < hi; ++i) {
-            const double vi = h.refl[i * NP + k];
-            for (int j = k + 1 + threadIdx.x; j < h.s; j += blockDim.x)
-                h.work[i * NP + j] -= dj[j] * vi;
-        }
-        if (k >= lo && k < hi && threadIdx.x == 0) {
-            const double x0 = h.work[(long)k * NP + k];
+        for (int kl = 0; kl < jb; ++kl) {
+            const long k = j0 + kl;
+            const int par = (int)(k & 1);
+            sum_colpart(h, par, wred, cs);
+            if (threadIdx.x < kPW) rowk[threadIdx.x] = __ldcg(h.rowbuf + par * kPW + threadIdx.x);
+            __syncthreads();
+            const double tail2 = cs[kl], x0 = rowk[kl];
             const double norm_x = sqrt(tail2 + x0 * x0);
-            h.work[(long)k * NP + k] = -(x0 >= 0.0 ? 1.0 : -1.0) * norm_x;
+            const bool active = norm_x != 0.0;  // zero column: H_k = I, r_kk = 0
+            const double sign = x0 >= 0.0 ? 1.0 : -1.0;
+            const double alpha = x0 + sign * norm_x;
+            const double inv_nv = active ? 1.0 / sqrt(tail2 + alpha * alpha) : 0.0;
+            if (threadIdx.x < kPW) {
+                const int l = threadIdx.x;
+                dd[l] = (l > kl && l < jb) ? 2.0 * (inv_nv * (cs[l] + alpha * rowk[l])) : 0.0;
+                if (l == 0) taus[kl] = active ? 1 : 0;
+            }
+            __syncthreads();
+            const bool more = kl + 1 < jb;
+            double acc = 0.0;
+            for (long i = max(lo, k) + warp; i < hi; i += kHHWarps) {
+                double a = lane < jb ? P[(i - base) * ldp + lane] : 0.0;
+                const double xk = __shfl_sync(0xffffffffu, a, kl);
+                const double v = (i == k ? alpha : xk) * inv_nv;
+                if (lane == kl) {
+                    h.V[i * NP + k] = v;
+                    if (i == k && active) a = -sign * norm_x;
+                } else if (lane > kl && lane < jb && active) {
+                    a = fma(-dd[lane], v, a);
+                }
+                if (lane < jb && (lane > kl || i == k)) P[(i - base) * ldp + lane] = a;
+                if (more) {
+                    const double xn = __shfl_sync(0xffffffffu, a, kl + 1);
+                    if (i > k + 1 && lane < jb) acc = fma(xn, a, acc);
+                    if (i == k + 1 && lane < jb) h.rowbuf[(par ^ 1) * kPW + lane] = a;
+                }
+            }
+            if (more) {
+                cta_lane_sum(acc, wred, h.colpart + ((size_t)(par ^ 1) * h.G + blockIdx.x) * kPW);
+                grid.sync();
+            }
+        }
+        if (in_smem) {
+            __syncthreads();
+            for (long i = r0 + warp; i < hi; i += kHHWarps)
+                if (lane < jb) h.A[i * NP + j0 + lane] = P[(i - base) * kPW + lane];
+            __syncthreads();
+        }
+        // ---- panel end: V^T V and W = V^T A_trail, reduced over the grid
+        const int c0 = j0 + jb, ncols = s - c0;
+        double* red = h.red + (size_t)(p & 1) * kPartStride;
+        panel_dots(h, h.A, NP, r0, hi, j0, jb, c0, ncols, true, sred);
+        grid.sync();
+        reduce_part(h, red, 1, jb, ncols);
+        grid.sync();
+        // T (every CTA the same; CTA 0 keeps it for the Q pass)
+        if (warp == 0) {
+            for (int i = 0; i < kPW; ++i) Ts[lane * (kPW + 1) + i] = 0.0;
+            __syncwarp();
+            for (int i = 0; i < jb; ++i) {
+                const double ti = taus[i] ? 2.0 : 0.0;
+                double w = 0.0;
+                if (lane < i)
+                    for (int c = lane; c < i; ++c)
+                        w = fma(Ts[lane * (kPW + 1) + c], __ldcg(red + c * kPW + i), w);
+                __syncwarp();
+                if (lane < i) Ts[lane * (kPW + 1) + i] = -ti * w;
+                if (lane == i) Ts[i * (kPW + 1) + i] = ti;
+                __syncwarp();
+            }
         }
         __syncthreads();
+        if (blockIdx.x == 0)
+            for (int e = threadIdx.x; e < kPW * kPW; e += kHHThreads)
+                h.T[(size_t)p * kPW * kPW + e] = Ts[(e / kPW) * (kPW + 1) + e % kPW];
+        // M2 = T^T W (jb x ncols)
+        for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
+            const int a = e / kMaxCols, j = e % kMaxCols;
+            double t = 0.0;
+            if (a < jb && j < ncols)
+                for (int c = 0; c <= a; ++c)
+                    t = fma(Ts[c * (kPW + 1) + a], __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
+            M2[e] = t;
+        }
+        __syncthreads();
+        const bool next = p + 1 < panels;
+        panel_update(h, h.A, NP, r0, hi, j0, jb, c0, ncols, M2, next ? c0 : -1,
+                     next ? min(kPW, s - c0) : 0, wred);
+        grid.sync();
     }
-    if (k + 1 < h.s) hh_tail_norm(h, k + 1, lo, hi, red);
-}
 
-__global__ void __launch_bounds__(kHHThreads) hh_q_init_kernel(HH h) {
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    for (long i = lo; i < hi; ++i)
-        for (int j = threadIdx.x; j < h.NP; j += blockDim.x)
-            h.Q[i * h.ldq + j] = (i == j && j < h.s) ? 1.0 : 0.0;
-}
-
-// backward accumulation (qr.cpp:71-84), reflector kk: partial dots, then the update
-__global__ void __launch_bounds__(kHHThreads) hh_q_a_kernel(HH h, int kk) {
-    __shared__ double red[kHHWarps * kMaxCols];
-    if (!h.act[kk]) return;
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    block_col_dots(h.Q, h.ldq, max(lo, (long)kk), hi, kk, h.s,
-                   [&](long i) { return h.refl[i * h.NP + kk]; },
-                   h.part + blockIdx.x * (h.NP + 2), red);
-}
-
-__global__ void __launch_bounds__(kHHThreads) hh_q_b_kernel(HH h, int kk) {
-    __shared__ double dj[kMaxCols];
-    if (!h.act[kk]) return;
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    const int NP = h.NP;
-    for (int j = kk + threadIdx.x; j < h.s; j += blockDim.x) {
-        double t = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) t += h.part[b * (NP + 2) + j];
-        dj[j] = 2.0 * t;
-    }
+    // ---- Q = H_0 ... H_{s-1} [I; 0], backward over the panels
+    for (long i = lo + warp; i < hi; i += kHHWarps)
+        for (int c = lane; c < NP; c += kPW) h.Q[i * h.ldq + c] = (i == c && c < s) ? 1.0 : 0.0;
     __syncthreads();
-    for (long i = max(lo, (long)kk); i < hi; ++i) {
-        const double vi = h.refl[i * NP + kk];
-        for (int j = kk + threadIdx.x; j < h.s; j += blockDim.x) h.Q[i * h.ldq + j] -= dj[j] * vi;
+    for (int p = panels - 1; p >= 0; --p) {
+        const int j0 = p * kPW, jb = min(kPW, s - j0), ncols = s - j0;
+        const long r0 = max(lo, (long)j0);
+        double* red = h.red + (size_t)(p & 1) * kPartStride;
+        panel_dots(h, h.Q, h.ldq, r0, hi, j0, jb, j0, ncols, false, sred);
+        grid.sync();
+        reduce_part(h, red, 0, jb, ncols);
+        grid.sync();
+        for (int e = threadIdx.x; e < kPW * kPW; e += kHHThreads)
+            Ts[(e / kPW) * (kPW + 1) + e % kPW] = __ldcg(h.T + (size_t)p * kPW * kPW + e);
+        __syncthreads();
+        // M2 = T W
+        for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
+            const int a = e / kMaxCols, j = e % kMaxCols;
+            double t = 0.0;
+            if (a < jb && j < ncols)
+                for (int c = a; c < jb; ++c)
+                    t = fma(Ts[a * (kPW + 1) + c], __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
+            M2[e] = t;
+        }
+        __syncthreads();
+        panel_update(h, h.Q, h.ldq, r0, hi, j0, jb, j0, ncols, M2, -1, 0, wred);
+        __syncthreads();
     }
-}
-
-// diag(R) >= 0 (qr.cpp:86-93): flip R rows / Q columns; R written from the owned rows
-__global__ void __launch_bounds__(kHHThreads) hh_finish_kernel(HH h) {
-    long lo, hi;
-    hh_rows(h, lo, hi);
-    const int NP = h.NP;
-    for (long i = lo; i < hi && i < NP; ++i)
-        for (int j = threadIdx.x; j < NP; j += blockDim.x) {
-            double r = (i < h.s && j < h.s && j >= i) ? h.work[i * NP + j] : 0.0;
-            if (i < h.s && h.work[i * NP + i] < 0.0) r = -r;
+    // ---- diag(R) >= 0 (qr.cpp:86-93)
+    for (int j = threadIdx.x; j < s; j += kHHThreads) diag[j] = __ldcg(h.A + (long)j * NP + j);
+    __syncthreads();
+    for (long i = lo + warp; i < hi; i += kHHWarps)
+        for (int c = lane; c < s; c += kPW)
+            if (diag[c] < 0.0) h.Q[i * h.ldq + c] = -h.Q[i * h.ldq + c];
+    for (long i = blockIdx.x; i < NP; i += h.G)
+        for (int j = threadIdx.x; j < NP; j += kHHThreads) {
+            double r = (i < s && j < s && j >= i) ? __ldcg(h.A + i * NP + j) : 0.0;
+            if (i < s && diag[i] < 0.0) r = -r;
             h.R[i * NP + j] = r;
         }
-    for (long i = lo; i < hi; ++i)
-        for (int j = threadIdx.x; j < h.s; j += blockDim.x)
-            if (h.work[(long)j * NP + j] < 0.0) h.Q[i * h.ldq + j] = -h.Q[i * h.ldq + j];
 }
 
-size_t householder_work_doubles(long M, int s) {
-    const int NP = kMaxCols;
-    (void)s;
-    return 2 * (size_t)M * NP + 2 * 296 * (size_t)(NP + 2) + NP + 64;
+static int hh_grid(long M) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return (int)std::max(1L, std::min((long)sms, (M + 63) / 64));
+}
+
+size_t householder_work_doubles(long M, int NP) {
+    const int G = hh_grid(M);
+    const int panels = (NP + kPW - 1) / kPW;
+    return 2 * (size_t)M * NP + 2 * (size_t)G * kPW + 2 * kPW + (size_t)G * kPartStride +
+           2 * (size_t)kPartStride + (size_t)panels * kPW * kPW + NP + 64;
 }
 
 cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, double* Qout, long ldq,
                                   double* R, int NP, double* work, cudaStream_t st) {
-    if (s > kMaxCols || NP > kMaxCols) return cudaErrorInvalidValue;
-    const unsigned nb = (unsigned)std::max(1L, std::min(296L, M));
+    if (s > kMaxCols || NP > kMaxCols || s > NP || M < s || s < 1) return cudaErrorInvalidValue;
     HH h;
     h.Y = Y;
+    h.ldy = ldy;
     h.M = M;
     h.s = s;
-    h.ldy = ldy;
+    h.NP = NP;
+    h.G = hh_grid(M);
+    h.rows_per = (M + h.G - 1) / h.G;
     h.Q = Qout;
     h.ldq = ldq;
     h.R = R;
-    h.NP = NP;
-    h.work = work;
-    h.refl = work + (size_t)M * NP;
-    h.part = h.refl + (size_t)M * NP;
-    h.act = reinterpret_cast<int*>(h.part + (size_t)nb * (NP + 2));
-    cudaError_t e = cudaMemsetAsync(R, 0, (size_t)NP * NP * sizeof(double), st);
+    h.A = work;
+    h.V = h.A + (size_t)M * NP;
+    h.colpart = h.V + (size_t)M * NP;
+    h.rowbuf = h.colpart + 2 * (size_t)h.G * kPW;
+    h.part = h.rowbuf + 2 * kPW;
+    h.red = h.part + (size_t)h.G * kPartStride;
+    h.T = h.red + 2 * (size_t)kPartStride;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(hh_blocked_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kHHSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    void* args[] = {&h};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)hh_blocked_kernel, dim3(h.G),
+                                                dim3(kHHThreads), args, kHHSmem, st);
     if (e != cudaSuccess) return e;
-    hh_init_kernel<<<nb, kHHThreads, 0, st>>>(h);
-    for (int k = 0; k < s; ++k) {
-        hh_col_a_kernel<<<nb, kHHThreads, 0, st>>>(h, k);
-        hh_col_b_kernel<<<nb, kHHThreads, 0, st>>>(h, k);
-    }
-    hh_q_init_kernel<<<nb, kHHThreads, 0, st>>>(h);
-    for (int kk = s - 1; kk >= 0; --kk) {
-        hh_q_a_kernel<<<nb, kHHThreads, 0, st>>>(h, kk);
-        hh_q_b_kernel<<<nb, kHHThreads, 0, st>>>(h, kk);
-    }
-    hh_finish_kernel<<<nb, kHHThreads, 0, st>>>(h);
     return cudaGetLastError();
 }
 

@@ -34,6 +34,9 @@ struct GemmAx {
     // last cols % 8 (<= 4) columns as DFMA instead of a padded DMMA tile; output columns
     // >= cols come out zero as before.
     int cols = 0;
+    // != nullptr and set on entry: return without touching the output (an optimistic
+    // pipeline that already aborted on a Cholesky breakdown skips its remaining passes)
+    const int* abort = nullptr;
 };
 
 // Z = A^T * W.  A: K x N row-major (lda), W: K x NP row-major (ldw).
@@ -52,6 +55,7 @@ struct GemmAtx {
     // (out_transposed, splits == 1) start from the Z^T already in Z instead of zero: a K
     // range processed by consecutive launches accumulates exactly like one launch
     bool accumulate = false;
+    const int* abort = nullptr;  // as GemmAx::abort
 };
 
 // FP32-input 3xTF32 tensor-core GEMM (tcgen05, gemm_tf32.cu), D = op(A) * B (M x NP):
@@ -83,6 +87,7 @@ struct GemmTf32 {
     // > 0: split K into runs of this many 16-row k-tiles (the split count follows), so a row
     // range of a larger split-K product reproduces that product's slabs exactly
     int k_per_split = 0;
+    const int* abort = nullptr;  // as GemmAx::abort
 };
 cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st);
 // out (rows x cols, FP32, ldo) = in (FP64, ldi) for r < rows_valid and c < cols_valid, else 0.
@@ -196,12 +201,15 @@ cudaError_t launch_fill(double* p, long count, double v, cudaStream_t st);
 cudaError_t launch_nonfinite_scan(const double* A, long rows, long cols, long lda, int* flag,
                                   cudaStream_t st);
 
-// Cooperative (grid-synchronised) unblocked Householder QR of a tall M x s matrix
-// (row-major, ld), the CholeskyQR2 fallback. Same algorithm as qr.cpp:27-102
-// (diag R >= 0, backward Q accumulation). Q overwrites Y's first s columns? No: Q to Qout.
+// Blocked (32-column panels, compact WY) Householder QR of a tall M x s matrix Y
+// (row-major, ldy; s <= NP <= 288, M >= s) in one cooperative launch, the CholeskyQR2
+// fallback: the reference's algorithm (qr.cpp:27-102; diag R >= 0, Q accumulated
+// backwards) with fixed-order reductions. Q to Qout (M x NP, ldq; columns >= s zero),
+// R to R (NP x NP, zero padded). Y is not modified. `work` holds
+// householder_work_doubles(M, NP) doubles.
 cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, double* Qout,
                                   long ldq, double* R, int NP, double* work, cudaStream_t st);
-size_t householder_work_doubles(long M, int s);
+size_t householder_work_doubles(long M, int NP);
 
 // Deterministic orthonormal completion (svd.cpp:111-151) of the null columns of the
 // small SVD: the first j with !(sigma[j] > sigma[0] * null_dim * eps) starts the null

@@ -15,6 +15,7 @@
 #include <string>
 
 #include "../../include/randsvd/pca.hpp"
+#include "../../include/randsvd/qr.hpp"
 #include "../../include/randsvd/rsvd.hpp"
 #include "../../include/rsvd_b200.h"
 
@@ -321,6 +322,13 @@ DenseMatrix power_iterate(const DenseMatrix& a, const DenseMatrix& y0, std::size
     check(rsvd_b200_power_iterate(handle(), a.data().data(), a.rows(), a.cols(),
                                   y0.data().data(), y0.cols(), q, w.data().data()));
     return w;
+}
+
+QrFactors householder_qr(const DenseMatrix& a) {
+    DenseMatrix q(a.rows(), a.cols()), r(a.cols(), a.cols());
+    check(rsvd_b200_householder_qr(handle(), a.data().data(), a.rows(), a.cols(),
+                                   q.data().data(), r.data().data()));
+    return {std::move(q), std::move(r)};
 }
 
 DenseMatrix range_basis(const DenseMatrix& y) {

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -186,7 +187,7 @@ struct rsvd_b200_handle {
     bool up_active = false;
     // workspace
     DevBuf a_copy, a_t, xt, y, q, part, b, b2, qbt, vbuf, small, flags, u_out, v_out, sig_out,
-        hh_work, omega_host_dev, jscratch, cwork, ubt;
+        hh_work, hh_rows, omega_host_dev, jscratch, cwork, ubt;
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
     DevBuf red_scratch;          // TSQR R stack / flag reduction
     DevBuf pca_ones, pca_sums, pca_mean, pca_comp;  // PCA (fit_pca / transform)
@@ -199,6 +200,9 @@ struct rsvd_b200_handle {
     long fallbacks = 0, reruns = 0;
     int last_sweeps = 0;
     bool force_robust = false;
+    // the optimistic run's abort flag while one is in flight (else nullptr): the A-pass GEMMs
+    // skip themselves once a Cholesky breakdown has doomed the run to a robust rerun
+    const int* abort_ptr = nullptr;
     bool c_identity = true;  // the current basis Q = Q1 C has C = I
     double* basis = nullptr;  // Q1 of the current basis (h->y or h->q)
     bool gram_ready = false;  // slot kG holds Y^T Y of the last produced Y
@@ -311,9 +315,15 @@ struct rsvd_b200_handle {
         timers.clear();
     }
 
+    static double trace_us() {  // host clock for the trace lines
+        using namespace std::chrono;
+        static const auto t0 = steady_clock::now();
+        return duration<double, std::micro>(steady_clock::now() - t0).count();
+    }
     void sync() {
-        if (trace) fprintf(stderr, "[rsvd_b200] -- sync\n");
+        if (trace) fprintf(stderr, "[rsvd_b200] %12.1f us -- sync\n", trace_us());
         ck(cudaStreamSynchronize(stream), "stream synchronize");
+        if (trace) fprintf(stderr, "[rsvd_b200] %12.1f us -- synced\n", trace_us());
     }
     int read_flag(int idx) {
         sync();
@@ -323,7 +333,7 @@ struct rsvd_b200_handle {
         ck(e, what);
         launches += count;
         if (trace) {
-            fprintf(stderr, "[rsvd_b200] %s\n", what);
+            fprintf(stderr, "[rsvd_b200] %12.1f us %s\n", trace_us(), what);
             if (trace > 1) ck(cudaStreamSynchronize(stream), what);
         }
     }
@@ -410,6 +420,7 @@ bool gemm_ax(rsvd_b200_handle* h, const double* A, long M, long K, long lda, con
     GemmAx g{A, M, K, lda, Xt, ldx, NP, Y, ldy};
     g.flag = flag;
     g.cols = cols;
+    g.abort = h->abort_ptr;
     const int splits = choose_splits(ax_tiles(M, NP), (K + 31) / 32);
     if (splits == 1) {
         const bool fuse = gram_out && NP <= 96;
@@ -517,6 +528,7 @@ void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, co
               long ldw, int NP, double* Z, long ldz, bool out_t, const char* tag = nullptr,
               double flops = 0.0) {
     GemmAtx g{A, K, N, lda, W, ldw, NP, Z, ldz, out_t};
+    g.abort = h->abort_ptr;
     const int splits = choose_splits(ax_tiles(N, NP), (K + 31) / 32);
     if (splits == 1) {
         h->kernel_begin(tag, flops);
@@ -554,6 +566,7 @@ int tf32_splits(long M, long K) {
 }
 
 void gemm_tf32(rsvd_b200_handle* h, GemmTf32 g, const char* tag = nullptr, double flops = 0.0) {
+    g.abort = h->abort_ptr;
     const int splits = g.out64 ? tf32_splits(g.M, g.K) : 1;
     if (splits == 1) {
         h->kernel_begin(tag, flops);
@@ -708,7 +721,7 @@ void tsqr(const Ctx& c, double* Y, long M, double* Qout) {
     double* R = h->red_scratch.d();
     double* Qs = R + stack;
     double* Xt = Qs + stack;
-    h->hh_work.reserve(householder_work_doubles(std::max(M, stack_rows), s) * sizeof(double));
+    h->hh_work.reserve(householder_work_doubles(std::max(M, stack_rows), NP) * sizeof(double));
     h->launched(launch_fill(R, (long)stack, 0.0, h->stream), "fill");
     h->launched(launch_householder_qr(Y, M, s, NP, Qout, NP, R + (size_t)rank * NP * NP, NP,
                                       h->hh_work.d(), h->stream),
@@ -787,7 +800,7 @@ bool tall_qr(const Ctx& c, double* Y, long M, double* Q1out, int passes, bool ma
         h->fallbacks += 1;
         return true;
     }
-    h->hh_work.reserve(householder_work_doubles(M, s) * sizeof(double));
+    h->hh_work.reserve(householder_work_doubles(M, NP) * sizeof(double));
     h->launched(launch_householder_qr(Y, M, s, NP, Q1out, NP, c.slot(kRB), NP, h->hh_work.d(),
                                       h->stream),
                 "householder_qr");
@@ -862,7 +875,7 @@ bool tall_qr_f32(const Ctx& c, long M, int passes) {
     if (c.p.sharded) {
         tsqr(c, h->y.d(), M, h->q.d());
     } else {
-        h->hh_work.reserve(householder_work_doubles(M, s) * sizeof(double));
+        h->hh_work.reserve(householder_work_doubles(M, NP) * sizeof(double));
         h->launched(launch_householder_qr(h->y.d(), M, s, NP, h->q.d(), NP, c.slot(kRB), NP,
                                           h->hh_work.d(), st),
                     "householder_qr");
@@ -906,16 +919,17 @@ bool wide_qr(const Ctx& c, const double* Zt, long N, long ldz, double* Qt, int r
             return false;
         }
     }
-    DevBuf zrow, qrow;
-    zrow.reserve((size_t)N * NP * sizeof(double));
-    qrow.reserve((size_t)N * NP * sizeof(double));
-    h->launched(launch_transpose(Zt, NP, N, ldz, zrow.d(), NP, h->stream), "transpose");
-    h->hh_work.reserve(householder_work_doubles(N, s) * sizeof(double));
-    h->launched(launch_householder_qr(zrow.d(), N, s, NP, qrow.d(), NP, c.slot(r_slot), NP,
+    // row-major copies of Z and Q in handle buffers (a per-call allocation would free and
+    // re-allocate, i.e. synchronise the device and invalidate the captured solve graphs)
+    h->hh_rows.reserve(2 * (size_t)N * NP * sizeof(double));
+    double* zrow = h->hh_rows.d();
+    double* qrow = zrow + (size_t)N * NP;
+    h->launched(launch_transpose(Zt, NP, N, ldz, zrow, NP, h->stream), "transpose");
+    h->hh_work.reserve(householder_work_doubles(N, NP) * sizeof(double));
+    h->launched(launch_householder_qr(zrow, N, s, NP, qrow, NP, c.slot(r_slot), NP,
                                       h->hh_work.d(), h->stream),
                 "householder_qr");
-    h->launched(launch_transpose(qrow.d(), N, NP, NP, Qt, ldz, h->stream), "transpose");
-    h->sync();  // zrow/qrow lifetime
+    h->launched(launch_transpose(qrow, N, NP, NP, Qt, ldz, h->stream), "transpose");
     h->fallbacks += 1;
     return true;
 }
@@ -968,6 +982,7 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     if (p.f32)  // the 3xTF32 A-pass writes rows < NPf of (A^T Q)^T / Q^T A; pad rows stay 0
         ck(cudaMemsetAsync(h->b.p, 0, (size_t)NP * p.ldn * sizeof(double), h->stream), "memset b");
     h->trace = getenv("RSVD_B200_TRACE") ? atoi(getenv("RSVD_B200_TRACE")) : 0;
+    h->abort_ptr = robust ? nullptr : static_cast<int*>(h->flags.p) + kFlagAbort;
     return Ctx{h, p, robust, static_cast<int*>(h->flags.p)};
 }
 
@@ -1364,6 +1379,10 @@ int solve_tall_graph(rsvd_b200_handle* h, const double* A, const Plan& p,
 // path (Householder fallbacks), which reproduces the reference's QR semantics.
 void solve_tall(rsvd_b200_handle* h, const double* A, const Plan& p, const rsvd_b200_config& cfg,
                 double* u, long ldu, double* sigma, double* v, long ldv, size_t* sketch_width) {
+    struct ClearAbort {  // no GEMM outside a solve may see a stale abort pointer
+        rsvd_b200_handle* h;
+        ~ClearAbort() { h->abort_ptr = nullptr; }
+    } clear_abort{h};
     h->fallbacks = 0;
     h->reruns = 0;
     h->upload_aty = 0;
@@ -2142,6 +2161,57 @@ rsvd_b200_status rsvd_b200_power_iterate(rsvd_b200_handle* h, const double* a, s
         h->gram_ready = false;
         power_iterate_dev(c, h->a_copy.d(), q, /*materialize=*/true);
         download(h, w, h->basis, (long)m, (long)s, c.p.NP);
+    });
+}
+
+// Householder thin QR (qr.cpp:27-102) on the device: the blocked compact-WY kernel of
+// householder.cu. a (m x n, lda) may be host or device memory per `on_device`; q (m x n,
+// ldq) and r (n x n, ldr) likewise.
+void householder_qr_impl(rsvd_b200_handle* h, const double* a, long lda, long m, long n,
+                         double* q, long ldq, double* r, long ldr, bool on_device) {
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    check_shape(m, n, "householder_qr");
+    if (m < n)
+        fail(RSVD_B200_DIMENSION_ERROR,
+             "householder_qr needs rows >= cols, got %ldx%ld; transpose the input first", m, n);
+    if (n > 288)
+        fail(RSVD_B200_ARGUMENT_ERROR, "householder_qr: at most 288 columns on the B200 path, got %ld",
+             n);
+    const int NP = pad_np(n);
+    h->y.reserve((size_t)m * NP * sizeof(double));
+    h->q.reserve((size_t)m * NP * sizeof(double));
+    h->small.reserve((size_t)kNumSmall * NP * NP * sizeof(double));
+    h->hh_work.reserve(householder_work_doubles(m, NP) * sizeof(double));
+    ck(cudaMemcpy2DAsync(h->y.p, NP * sizeof(double), a, lda * sizeof(double), n * sizeof(double),
+                         m, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                         h->stream),
+       "copy a");
+    double* R = h->small.d();
+    h->launched(launch_householder_qr(h->y.d(), m, (int)n, NP, h->q.d(), NP, R, NP,
+                                      h->hh_work.d(), h->stream),
+                "householder_qr");
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    ck(cudaMemcpy2DAsync(q, ldq * sizeof(double), h->q.p, NP * sizeof(double), n * sizeof(double),
+                         m, kind, h->stream),
+       "copy q");
+    ck(cudaMemcpy2DAsync(r, ldr * sizeof(double), R, NP * sizeof(double), n * sizeof(double), n,
+                         kind, h->stream),
+       "copy r");
+    if (!on_device) h->sync();
+}
+
+rsvd_b200_status rsvd_b200_householder_qr(rsvd_b200_handle* h, const double* a, size_t m,
+                                          size_t n, double* q, double* r) {
+    return guarded([&] {
+        householder_qr_impl(h, a, (long)n, (long)m, (long)n, q, (long)n, r, (long)n, false);
+    });
+}
+
+rsvd_b200_status rsvd_b200_householder_qr_device(rsvd_b200_handle* h, const double* a, size_t lda,
+                                                 size_t m, size_t n, double* q, size_t ldq,
+                                                 double* r, size_t ldr) {
+    return guarded([&] {
+        householder_qr_impl(h, a, (long)lda, (long)m, (long)n, q, (long)ldq, r, (long)ldr, true);
     });
 }
 

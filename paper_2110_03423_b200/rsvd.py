@@ -438,6 +438,26 @@ class Solver:
                                                           _dp(y0), y0.shape[1], q, _dp(w)))
         return w
 
+    def householder_qr(self, a):
+        """Thin QR (qr.cpp:27-102) on the device: (q m x n, r n x n, diag r >= 0)."""
+        a = _arr(a)
+        m, n = a.shape
+        q, r = np.empty((m, n)), np.empty((n, n))
+        _check(self.lib, self.lib.rsvd_b200_householder_qr(self.h, _dp(a), m, n, _dp(q), _dp(r)))
+        return q, r
+
+    def householder_qr_device(self, a):
+        """Same on a CUDA float64 tensor (row stride allowed); returns CUDA tensors."""
+        import torch
+        assert a.is_cuda and a.dtype == torch.float64 and a.dim() == 2 and a.stride(1) == 1
+        self.wait_for_torch(a.device)
+        m, n = a.shape
+        q = torch.empty((m, n), dtype=torch.float64, device=a.device)
+        r = torch.empty((n, n), dtype=torch.float64, device=a.device)
+        _check(self.lib, self.lib.rsvd_b200_householder_qr_device(
+            self.h, a.data_ptr(), a.stride(0), m, n, q.data_ptr(), n, r.data_ptr(), n))
+        return q, r
+
     def range_basis(self, y) -> np.ndarray:
         y = _arr(y)
         q = np.empty(y.size)
@@ -515,6 +535,10 @@ def power_iterate(a, y0, q: int) -> np.ndarray:
 
 def range_basis(y) -> np.ndarray:
     return default_solver().range_basis(y)
+
+
+def householder_qr(a):
+    return default_solver().householder_qr(a)
 
 
 def project_and_solve(a, qbasis, k: int) -> RsvdResult:

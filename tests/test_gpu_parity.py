@@ -415,3 +415,34 @@ def test_tail_columns_vs_oracle(solver, port, s):
     res = solver.randomized_ksvd(a, P.RsvdConfig(k=k, oversample=p, power_q=2, seed=11))
     ref = port.randomized_ksvd(a, k, oversample=p, power_q=2, seed=11)
     check_against(res, ref.sigma, ref.u, ref.v, f"s={s}")
+
+
+def test_fallback_power_iterations_vs_oracle(solver, port):
+    """Ill-conditioned input with power iterations: the optimistic attempt aborts at its
+    first Cholesky (its remaining A-passes skip themselves), the robust rerun takes the
+    blocked Householder fallback in the power iteration's QRs, and the result matches the
+    reference algorithm (oracle port) and a solve forced onto the robust path bit for bit."""
+    import paper_2110_03423_b200 as P
+    rng = np.random.default_rng(21)
+    m, n, k = 1500, 700, 30
+    uu, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = np.maximum(10.0 ** (-np.arange(n) * 10.0 / 39), 1e-14)
+    a = (uu * sig) @ vv.T
+    cfg = P.RsvdConfig(k=k, power_q=2, seed=9)
+    res = solver.randomized_ksvd(a, cfg)
+    assert solver.last_info("robust_reruns") == 1
+    assert solver.last_info("householder_fallbacks") >= 3
+    solver.set_robust(True)
+    try:
+        forced = solver.randomized_ksvd(a, cfg)
+    finally:
+        solver.set_robust(False)
+    assert np.array_equal(res.factors.sigma, forced.factors.sigma)
+    assert np.array_equal(res.factors.u, forced.factors.u)
+    ref = port.randomized_ksvd(a, k, power_q=2, seed=9)
+    lead = 12
+    rel = np.abs(res.factors.sigma[:lead] - ref.sigma[:lead]) / ref.sigma[:lead]
+    assert rel.max() <= SIG_RTOL
+    assert principal_angle(res.factors.u[:, :lead], ref.u[:, :lead]) <= ANGLE_TOL
+    assert principal_angle(res.factors.v[:, :lead], ref.v[:, :lead]) <= ANGLE_TOL

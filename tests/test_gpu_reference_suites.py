@@ -59,6 +59,11 @@ def test_reference_rsvd_suite():
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif(os.environ.get("RSVD_B200_FULL_ACCEPTANCE") != "1",
+                    reason="~12 min: criterion 6 times the reference's own full dense SVD of a "
+                           "2000x2000 matrix 10 times on the host CPU (acceptance.cpp:246); set "
+                           "RSVD_B200_FULL_ACCEPTANCE=1 (run recorded in "
+                           "profiles/r2_acceptance_dropin.txt)")
 def test_reference_acceptance_criteria():
     """acceptance.cpp criteria 1-6 and 8 pass against the GPU drop-in."""
     _need(ACCEPTANCE)
