@@ -1,7 +1,6 @@
 // Drop-in thin QR (reference: include/randsvd/qr.hpp:8-18): q m x n with orthonormal
 // columns, r n x n upper triangular with a non-negative diagonal and exact zeros below it.
-// Computed on the B200 by the blocked Householder kernel (rsvd_b200_householder_qr);
-// widths up to 288 columns (wider inputs throw ArgumentError).
+// Computed on the B200 by the blocked Householder kernel (rsvd_b200_householder_qr).
 #pragma once
 
 #include "randsvd/matrix.hpp"

@@ -234,7 +234,7 @@ rsvd_b200_status rsvd_b200_sketch_stream(rsvd_b200_handle* h, const double* a, s
 rsvd_b200_status rsvd_b200_power_iterate(rsvd_b200_handle* h, const double* a, size_t m, size_t n,
                                          const double* y0, size_t s, size_t q, double* w);
 /* Householder thin QR (replaces randsvd::householder_qr, qr.hpp:16 / qr.cpp:27-102):
- * a m x n row-major (m >= n, n <= 288) -> q m x n with orthonormal columns and r n x n
+ * a m x n row-major (m >= n) -> q m x n with orthonormal columns and r n x n
  * upper triangular with a non-negative diagonal (strictly-lower entries exact zeros).
  * The blocked (compact WY) Householder kernel of the CholeskyQR2 fallback. m < n is
  * RSVD_B200_DIMENSION_ERROR (the reference's DimensionError). The _device variant takes
@@ -244,6 +244,17 @@ rsvd_b200_status rsvd_b200_householder_qr(rsvd_b200_handle* h, const double* a, 
 rsvd_b200_status rsvd_b200_householder_qr_device(rsvd_b200_handle* h, const double* a, size_t lda,
                                                  size_t m, size_t n, double* q, size_t ldq,
                                                  double* r, size_t ldr);
+/* Test-matrix generator (replaces randsvd::synth::synth_matrix, synth.cpp:58-71, for the
+ * paper's §4 grids): A = U diag(sigma) V^T, rows x cols (rows >= cols), U the Householder Q
+ * of a rows x cols draw of GaussianSampler(seed), V that of the next cols x cols draw,
+ * sigma_j = spectrum_value(kind, j + 1) with kind 0 = fast (1/i^2), 1 = sharp
+ * (1e-4 + 1/(1 + e^(i+1-beta)), beta > 0), 2 = slow (1/i^0.1). out row-major (host), or
+ * device memory with leading dimension ld (_device; returns after the copy completes). */
+rsvd_b200_status rsvd_b200_synth_matrix(rsvd_b200_handle* h, size_t rows, size_t cols, int kind,
+                                        double beta, uint64_t seed, double* out);
+rsvd_b200_status rsvd_b200_synth_matrix_device(rsvd_b200_handle* h, size_t rows, size_t cols,
+                                               int kind, double beta, uint64_t seed, double* out,
+                                               size_t ld);
 rsvd_b200_status rsvd_b200_range_basis(rsvd_b200_handle* h, const double* y, size_t m, size_t s,
                                        double* q, size_t* cols_out);
 rsvd_b200_status rsvd_b200_project_and_solve(rsvd_b200_handle* h, const double* a, size_t m,

@@ -97,6 +97,9 @@ class Oracle:
             f("uniforms").argtypes = [_u64, _sz, _dp]
             f("set_max_threads").argtypes = [C.c_uint]
             f("sampler_normals").argtypes = [_u64, _sz, _sz, _sz, _dp]
+            f("synth_matrix").argtypes = [_sz, _sz, C.c_int, C.c_double, _u64, _dp]
+            f("run_grid_csv").argtypes = [C.c_char_p, _sz, C.c_char_p, _sz]
+            f("run_grid_csv").restype = C.c_long
             f("matrix_new").argtypes = [_dp, _sz, _sz]
             f("matrix_new").restype = C.c_void_p
             f("matrix_free").argtypes = [C.c_void_p]
@@ -139,6 +142,22 @@ class Oracle:
         out = np.empty(count, dtype=np.float64)
         self._f("sampler_normals")(seed, skip_words, skip_normals, count, _ptr(out))
         return out
+
+    def synth_matrix(self, rows: int, cols: int, kind: str = "fast", beta: float = 1.0,
+                     seed: int = 0) -> np.ndarray:
+        """Reference only: synth::synth_matrix (synth.cpp:58-71)."""
+        out = np.empty((rows, cols))
+        k = {"fast": 0, "sharp": 1, "slow": 2}[kind]
+        self._check(self._f("synth_matrix")(rows, cols, k, float(beta), seed % 2**64, _ptr(out)))
+        return out
+
+    def run_grid_csv(self, preset: str, reps: int = 1) -> str:
+        """Reference only: bench::run_grid(preset) written by bench::write_csv."""
+        buf = C.create_string_buffer(1 << 20)
+        n = self._f("run_grid_csv")(preset.encode(), reps, buf, len(buf))
+        if n < 0:
+            raise RuntimeError(self._f("last_error")().decode() if n == -1 else "buffer")
+        return buf.value.decode()
 
     # ------------------------------------------------------------ dense core
     def gemm(self, alpha, a, ta, b, tb, beta=0.0, c=None) -> np.ndarray:

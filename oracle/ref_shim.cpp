@@ -12,6 +12,9 @@
 #include <exception>
 #include <string>
 
+#include <sstream>
+
+#include "randsvd/bench.hpp"
 #include "randsvd/errors.hpp"
 #include "randsvd/gemm.hpp"
 #include "randsvd/matrix.hpp"
@@ -20,6 +23,7 @@
 #include "randsvd/rng.hpp"
 #include "randsvd/rsvd.hpp"
 #include "randsvd/svd.hpp"
+#include "randsvd/synth.hpp"
 
 using namespace randsvd;
 
@@ -86,6 +90,35 @@ void ref_sampler_normals(std::uint64_t seed, std::size_t skip_words, std::size_t
     for (std::size_t i = 0; i < skip_words; ++i) s.next_u64();
     for (std::size_t i = 0; i < skip_normals; ++i) s.normal();
     for (std::size_t i = 0; i < count; ++i) out[i] = s.normal();
+}
+
+// synth::synth_matrix (synth.cpp:58-71); kind 0 fast, 1 sharp(beta), 2 slow
+int ref_synth_matrix(std::size_t rows, std::size_t cols, int kind, double beta,
+                     std::uint64_t seed, double* out) {
+    return guarded([&] {
+        const synth::SpectrumKind k = kind == 0   ? synth::SpectrumKind::fast()
+                                      : kind == 1 ? synth::SpectrumKind::sharp(beta)
+                                                  : synth::SpectrumKind::slow();
+        to(synth::synth_matrix({rows, cols, k, seed}), out);
+    });
+}
+
+// bench::run_grid of a named preset (bench.cpp:112-172, 239-260) with `reps` repetitions,
+// written by bench::write_csv into buf (NUL-terminated); returns the CSV length, or -1
+// (error text in ref_last_error) / -2 (buffer too small).
+long ref_run_grid_csv(const char* preset, std::size_t reps, char* buf, std::size_t cap) {
+    std::string csv;
+    const int rc = guarded([&] {
+        bench::GridConfig g = bench::preset(preset);
+        g.repetitions = reps;
+        std::ostringstream os;
+        bench::write_csv(bench::run_grid(g).rows, os);
+        csv = os.str();
+    });
+    if (rc != 0) return -1;
+    if (csv.size() + 1 > cap) return -2;
+    std::memcpy(buf, csv.c_str(), csv.size() + 1);
+    return (long)csv.size();
 }
 
 double ref_pairwise_dot(const double* x, const double* y, std::size_t n) {

@@ -18,6 +18,7 @@ EXPORTS = [
     "rsvd_b200_gaussian_stream", "rsvd_b200_sketch_stream",
     "rsvd_b200_power_iterate", "rsvd_b200_range_basis", "rsvd_b200_project_and_solve",
     "rsvd_b200_householder_qr", "rsvd_b200_householder_qr_device",
+    "rsvd_b200_synth_matrix", "rsvd_b200_synth_matrix_device",
     "rsvd_b200_splitmix_words", "rsvd_b200_uniforms", "rsvd_b200_last_profile",
     "rsvd_b200_set_profiling", "rsvd_b200_last_launch_count", "rsvd_b200_version",
     "rsvd_b200_kernel_stats", "rsvd_b200_reset_stats", "rsvd_b200_last_info",
@@ -90,6 +91,10 @@ def load() -> C.CDLL:
         "rsvd_b200_power_iterate": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _sz, _sz, _dp]),
         "rsvd_b200_range_basis": (C.c_int, [_vp, _dp, _sz, _sz, _dp, C.POINTER(_sz)]),
         "rsvd_b200_householder_qr": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _dp]),
+        "rsvd_b200_synth_matrix": (C.c_int, [_vp, _sz, _sz, C.c_int, C.c_double, C.c_uint64,
+                                             _dp]),
+        "rsvd_b200_synth_matrix_device": (C.c_int, [_vp, _sz, _sz, C.c_int, C.c_double,
+                                                    C.c_uint64, _vp, _sz]),
         "rsvd_b200_householder_qr_device": (C.c_int, [_vp, _vp, _sz, _sz, _sz, _vp, _sz, _vp,
                                                       _sz]),
         "rsvd_b200_project_and_solve": (C.c_int, [_vp, _dp, _sz, _sz, _dp, _sz, _sz, _dp, _dp,

@@ -309,46 +309,55 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
                 if (lane < jb) h.A[i * NP + j0 + lane] = P[(i - base) * kPW + lane];
             __syncthreads();
         }
-        // ---- panel end: V^T V and W = V^T A_trail, reduced over the grid
-        const int c0 = j0 + jb, ncols = s - c0;
+        // ---- panel end: V^T V and W = V^T A_trail (trailing columns in blocks of
+        // kMaxCols), reduced over the grid; T; A_trail -= V (T^T W)
+        const int c0 = j0 + jb, ntrail = s - c0;
         double* red = h.red + (size_t)(p & 1) * kPartStride;
-        panel_dots(h, h.A, NP, r0, hi, j0, jb, c0, ncols, true, sred);
-        grid.sync();
-        reduce_part(h, red, 1, jb, ncols);
-        grid.sync();
-        // T (every CTA the same; CTA 0 keeps it for the Q pass)
-        if (warp == 0) {
-            for (int i = 0; i < kPW; ++i) Ts[lane * (kPW + 1) + i] = 0.0;
-            __syncwarp();
-            for (int i = 0; i < jb; ++i) {
-                const double ti = taus[i] ? 2.0 : 0.0;
-                double w = 0.0;
-                if (lane < i)
-                    for (int c = lane; c < i; ++c)
-                        w = fma(Ts[lane * (kPW + 1) + c], __ldcg(red + c * kPW + i), w);
-                __syncwarp();
-                if (lane < i) Ts[lane * (kPW + 1) + i] = -ti * w;
-                if (lane == i) Ts[i * (kPW + 1) + i] = ti;
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        if (blockIdx.x == 0)
-            for (int e = threadIdx.x; e < kPW * kPW; e += kHHThreads)
-                h.T[(size_t)p * kPW * kPW + e] = Ts[(e / kPW) * (kPW + 1) + e % kPW];
-        // M2 = T^T W (jb x ncols)
-        for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
-            const int a = e / kMaxCols, j = e % kMaxCols;
-            double t = 0.0;
-            if (a < jb && j < ncols)
-                for (int c = 0; c <= a; ++c)
-                    t = fma(Ts[c * (kPW + 1) + a], __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
-            M2[e] = t;
-        }
-        __syncthreads();
         const bool next = p + 1 < panels;
-        panel_update(h, h.A, NP, r0, hi, j0, jb, c0, ncols, M2, next ? c0 : -1,
-                     next ? min(kPW, s - c0) : 0, wred);
+        for (int cb = 0; cb == 0 || cb < ntrail; cb += kMaxCols) {
+            const int nc = max(0, min(kMaxCols, ntrail - cb));
+            panel_dots(h, h.A, NP, r0, hi, j0, jb, c0 + cb, nc, cb == 0, sred);
+            grid.sync();
+            reduce_part(h, red, cb == 0, jb, nc);
+            grid.sync();
+            if (cb == 0) {
+                // T (every CTA the same; CTA 0 keeps it for the Q pass)
+                if (warp == 0) {
+                    for (int i = 0; i < kPW; ++i) Ts[lane * (kPW + 1) + i] = 0.0;
+                    __syncwarp();
+                    for (int i = 0; i < jb; ++i) {
+                        const double ti = taus[i] ? 2.0 : 0.0;
+                        double w = 0.0;
+                        if (lane < i)
+                            for (int c = lane; c < i; ++c)
+                                w = fma(Ts[lane * (kPW + 1) + c], __ldcg(red + c * kPW + i), w);
+                        __syncwarp();
+                        if (lane < i) Ts[lane * (kPW + 1) + i] = -ti * w;
+                        if (lane == i) Ts[i * (kPW + 1) + i] = ti;
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+                if (blockIdx.x == 0)
+                    for (int e = threadIdx.x; e < kPW * kPW; e += kHHThreads)
+                        h.T[(size_t)p * kPW * kPW + e] = Ts[(e / kPW) * (kPW + 1) + e % kPW];
+            }
+            // M2 = T^T W (jb x nc)
+            for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
+                const int a = e / kMaxCols, j = e % kMaxCols;
+                double t = 0.0;
+                if (a < jb && j < nc)
+                    for (int c = 0; c <= a; ++c)
+                        t = fma(Ts[c * (kPW + 1) + a],
+                                __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
+                M2[e] = t;
+            }
+            __syncthreads();
+            const bool first = next && cb == 0;
+            panel_update(h, h.A, NP, r0, hi, j0, jb, c0 + cb, nc, M2, first ? c0 : -1,
+                         first ? min(kPW, s - c0) : 0, wred);
+            __syncthreads();
+        }
         grid.sync();
     }
 
@@ -357,41 +366,51 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
         for (int c = lane; c < NP; c += kPW) h.Q[i * h.ldq + c] = (i == c && c < s) ? 1.0 : 0.0;
     __syncthreads();
     for (int p = panels - 1; p >= 0; --p) {
-        const int j0 = p * kPW, jb = min(kPW, s - j0), ncols = s - j0;
+        const int j0 = p * kPW, jb = min(kPW, s - j0), ntot = s - j0;
         const long r0 = max(lo, (long)j0);
         double* red = h.red + (size_t)(p & 1) * kPartStride;
-        panel_dots(h, h.Q, h.ldq, r0, hi, j0, jb, j0, ncols, false, sred);
-        grid.sync();
-        reduce_part(h, red, 0, jb, ncols);
-        grid.sync();
         for (int e = threadIdx.x; e < kPW * kPW; e += kHHThreads)
             Ts[(e / kPW) * (kPW + 1) + e % kPW] = __ldcg(h.T + (size_t)p * kPW * kPW + e);
         __syncthreads();
-        // M2 = T W
-        for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
-            const int a = e / kMaxCols, j = e % kMaxCols;
-            double t = 0.0;
-            if (a < jb && j < ncols)
-                for (int c = a; c < jb; ++c)
-                    t = fma(Ts[a * (kPW + 1) + c], __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
-            M2[e] = t;
+        for (int cb = 0; cb < ntot; cb += kMaxCols) {
+            const int nc = min(kMaxCols, ntot - cb);
+            panel_dots(h, h.Q, h.ldq, r0, hi, j0, jb, j0 + cb, nc, false, sred);
+            grid.sync();
+            reduce_part(h, red, 0, jb, nc);
+            grid.sync();
+            // M2 = T W
+            for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
+                const int a = e / kMaxCols, j = e % kMaxCols;
+                double t = 0.0;
+                if (a < jb && j < nc)
+                    for (int c = a; c < jb; ++c)
+                        t = fma(Ts[a * (kPW + 1) + c],
+                                __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
+                M2[e] = t;
+            }
+            __syncthreads();
+            panel_update(h, h.Q, h.ldq, r0, hi, j0, jb, j0 + cb, nc, M2, -1, 0, wred);
+            __syncthreads();
         }
+    }
+    // ---- diag(R) >= 0 (qr.cpp:86-93): the factorisation is final (grid.sync above)
+    for (int cb = 0; cb < s; cb += kMaxCols) {
+        const int nc = min(kMaxCols, s - cb);
+        for (int j = threadIdx.x; j < nc; j += kHHThreads)
+            diag[j] = __ldcg(h.A + (long)(cb + j) * NP + cb + j);
         __syncthreads();
-        panel_update(h, h.Q, h.ldq, r0, hi, j0, jb, j0, ncols, M2, -1, 0, wred);
+        for (long i = lo + warp; i < hi; i += kHHWarps)
+            for (int c = lane; c < nc; c += kPW)
+                if (diag[c] < 0.0) h.Q[i * h.ldq + cb + c] = -h.Q[i * h.ldq + cb + c];
         __syncthreads();
     }
-    // ---- diag(R) >= 0 (qr.cpp:86-93)
-    for (int j = threadIdx.x; j < s; j += kHHThreads) diag[j] = __ldcg(h.A + (long)j * NP + j);
-    __syncthreads();
-    for (long i = lo + warp; i < hi; i += kHHWarps)
-        for (int c = lane; c < s; c += kPW)
-            if (diag[c] < 0.0) h.Q[i * h.ldq + c] = -h.Q[i * h.ldq + c];
-    for (long i = blockIdx.x; i < NP; i += h.G)
+    for (long i = blockIdx.x; i < NP; i += h.G) {
+        const bool flip = i < s && __ldcg(h.A + i * NP + i) < 0.0;
         for (int j = threadIdx.x; j < NP; j += kHHThreads) {
             double r = (i < s && j < s && j >= i) ? __ldcg(h.A + i * NP + j) : 0.0;
-            if (i < s && diag[i] < 0.0) r = -r;
-            h.R[i * NP + j] = r;
+            h.R[i * NP + j] = flip ? -r : r;
         }
+    }
 }
 
 static int hh_grid(long M) {
@@ -414,7 +433,7 @@ size_t householder_work_doubles(long M, int NP) {
 
 cudaError_t launch_householder_qr(const double* Y, long M, int s, long ldy, double* Qout, long ldq,
                                   double* R, int NP, double* work, cudaStream_t st) {
-    if (s > kMaxCols || NP > kMaxCols || s > NP || M < s || s < 1) return cudaErrorInvalidValue;
+    if (s > NP || M < s || s < 1) return cudaErrorInvalidValue;
     HH h;
     h.Y = Y;
     h.ldy = ldy;

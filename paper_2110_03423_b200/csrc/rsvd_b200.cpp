@@ -187,7 +187,7 @@ struct rsvd_b200_handle {
     bool up_active = false;
     // workspace
     DevBuf a_copy, a_t, xt, y, q, part, b, b2, qbt, vbuf, small, flags, u_out, v_out, sig_out,
-        hh_work, hh_rows, omega_host_dev, jscratch, cwork, ubt;
+        hh_work, hh_rows, synth_buf, omega_host_dev, jscratch, cwork, ubt;
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
     DevBuf red_scratch;          // TSQR R stack / flag reduction
     DevBuf pca_ones, pca_sums, pca_mean, pca_comp;  // PCA (fit_pca / transform)
@@ -2174,19 +2174,16 @@ void householder_qr_impl(rsvd_b200_handle* h, const double* a, long lda, long m,
     if (m < n)
         fail(RSVD_B200_DIMENSION_ERROR,
              "householder_qr needs rows >= cols, got %ldx%ld; transpose the input first", m, n);
-    if (n > 288)
-        fail(RSVD_B200_ARGUMENT_ERROR, "householder_qr: at most 288 columns on the B200 path, got %ld",
-             n);
-    const int NP = pad_np(n);
+    const int NP = (int)(n <= 288 ? pad_np(n) : round_up(n, 8));
     h->y.reserve((size_t)m * NP * sizeof(double));
     h->q.reserve((size_t)m * NP * sizeof(double));
-    h->small.reserve((size_t)kNumSmall * NP * NP * sizeof(double));
+    h->hh_rows.reserve((size_t)NP * NP * sizeof(double));
     h->hh_work.reserve(householder_work_doubles(m, NP) * sizeof(double));
     ck(cudaMemcpy2DAsync(h->y.p, NP * sizeof(double), a, lda * sizeof(double), n * sizeof(double),
                          m, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                          h->stream),
        "copy a");
-    double* R = h->small.d();
+    double* R = h->hh_rows.d();
     h->launched(launch_householder_qr(h->y.d(), m, (int)n, NP, h->q.d(), NP, R, NP,
                                       h->hh_work.d(), h->stream),
                 "householder_qr");
@@ -2198,6 +2195,83 @@ void householder_qr_impl(rsvd_b200_handle* h, const double* a, long lda, long m,
                          kind, h->stream),
        "copy r");
     if (!on_device) h->sync();
+}
+
+// synth_matrix (synth.cpp:58-71) on the device: the reference's construction step for step
+// — one GaussianSampler(seed) stream (the device generator, bit-identical to the
+// reference's) filled row-major into the rows x cols and then the cols x cols Gaussian
+// draws, Haar factors as their Householder Q (householder.cu; diag R >= 0 is the Haar sign
+// fix), U's columns scaled by sigma_j = spectrum_value(kind, j + 1) (evaluated on the host
+// with the same libm calls as the reference), A = U V^T by the DMMA GEMM in column blocks.
+void synth_matrix_impl(rsvd_b200_handle* h, long rows, long cols, int kind, double beta,
+                       uint64_t seed, double* out, long ldo, bool on_device) {
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    if (rows < cols || cols < 1)
+        fail(RSVD_B200_ARGUMENT_ERROR, "synth_matrix needs rows >= cols >= 1, got %ldx%ld", rows,
+             cols);
+    if (kind < 0 || kind > 2) fail(RSVD_B200_ARGUMENT_ERROR, "synth_matrix: unknown spectrum kind %d", kind);
+    if (kind == 1 && !(beta > 0.0))
+        fail(RSVD_B200_ARGUMENT_ERROR, "sharp decay requires beta > 0, got %g", beta);
+    std::vector<double> sig((size_t)cols);
+    for (long j = 0; j < cols; ++j) {  // synth.cpp:28-40, 1-based index
+        const double x = (double)(j + 1);
+        sig[j] = kind == 0 ? 1.0 / (x * x)
+                 : kind == 1 ? 0.0001 + 1.0 / (1.0 + std::exp(x + 1.0 - beta))
+                             : 1.0 / std::pow(x, 0.1);
+    }
+    const long NP = cols <= 288 ? pad_np(cols) : round_up(cols, 8);
+    constexpr long kBlk = 96;                        // output columns per GEMM
+    const long vrows = round_up(cols, kBlk);         // V padded (zero rows) for the last block
+    const size_t g_n = (size_t)rows * cols + (size_t)cols * cols;
+    // workspace: Gaussian draws | U (rows x NP) | V (vrows x NP) | sigma | GEMM tile
+    const size_t need = g_n + (size_t)rows * NP + (size_t)vrows * NP + NP +
+                        (size_t)rows * kBlk;
+    h->synth_buf.reserve(need * sizeof(double));
+    double* g = h->synth_buf.d();
+    double* u = g + g_n;
+    double* v = u + (size_t)rows * NP;
+    double* sg = v + (size_t)vrows * NP;
+    double* tile = sg + NP;
+    h->hh_rows.reserve((size_t)NP * NP * sizeof(double));
+    h->hh_work.reserve(householder_work_doubles(rows, NP) * sizeof(double));
+    h->launched(launch_gaussian_rowmajor(seed, 1, (long)g_n, g, h->stream), "gaussian");
+    h->launched(launch_fill(v, vrows * NP, 0.0, h->stream), "fill");
+    h->launched(launch_householder_qr(g, rows, (int)cols, cols, u, NP, h->hh_rows.d(), (int)NP,
+                                      h->hh_work.d(), h->stream),
+                "householder_qr");
+    h->launched(launch_householder_qr(g + (size_t)rows * cols, cols, (int)cols, cols, v, NP,
+                                      h->hh_rows.d(), (int)NP, h->hh_work.d(), h->stream),
+                "householder_qr");
+    ck(cudaMemcpyAsync(sg, sig.data(), cols * sizeof(double), cudaMemcpyHostToDevice, h->stream),
+       "sigma upload");
+    // U <- U diag(sigma) in place (columns >= cols stay zero)
+    h->launched(launch_scale_cols(u, NP, rows, rows, (int)cols, sg, u, NP, h->stream), "scale_cols");
+    const cudaMemcpyKind kind_out = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const int splits = choose_splits(ax_tiles(rows, (int)kBlk), (NP + 31) / 32);
+    if (splits > 1) h->part.reserve((size_t)splits * rows * kBlk * sizeof(double));
+    for (long j0 = 0; j0 < cols; j0 += kBlk) {  // A[:, j0:j0+96] = U (V[j0:j0+96, :])^T
+        const long nb = std::min(kBlk, cols - j0);
+        gemm_ax(h, u, rows, NP, NP, v + (size_t)j0 * NP, NP, (int)kBlk, tile, kBlk);
+        ck(cudaMemcpy2DAsync(out + j0, ldo * sizeof(double), tile, kBlk * sizeof(double),
+                             nb * sizeof(double), rows, kind_out, h->stream),
+           "copy a");
+    }
+    h->sync();  // the host-side sigma vector's lifetime
+}
+
+rsvd_b200_status rsvd_b200_synth_matrix(rsvd_b200_handle* h, size_t rows, size_t cols, int kind,
+                                        double beta, uint64_t seed, double* out) {
+    return guarded([&] {
+        synth_matrix_impl(h, (long)rows, (long)cols, kind, beta, seed, out, (long)cols, false);
+    });
+}
+
+rsvd_b200_status rsvd_b200_synth_matrix_device(rsvd_b200_handle* h, size_t rows, size_t cols,
+                                               int kind, double beta, uint64_t seed, double* out,
+                                               size_t ld) {
+    return guarded([&] {
+        synth_matrix_impl(h, (long)rows, (long)cols, kind, beta, seed, out, (long)ld, true);
+    });
 }
 
 rsvd_b200_status rsvd_b200_householder_qr(rsvd_b200_handle* h, const double* a, size_t m,

@@ -9,10 +9,11 @@ the top-k singular values against the full SVD — one CSV row per cell in the r
 format (``CSV_HEADER``, 17 significant digits).
 
 On the GPU the competitor is the paper's "GESVD-GPU": the vendor full SVD
-(``torch.linalg.svdvals`` -> cuSOLVER), and matrices are synthesised on the device
-(A = U diag(sigma) V^T with Haar U, V from the QR of Gaussian draws) because the reference's
-``synth_matrix`` is O(m n^2) unblocked Householder on the host. Both are test/benchmark
-infrastructure around the measured path, which is the library's sm_100a solve.
+(``torch.linalg.svdvals`` -> cuSOLVER). Matrices come from the library's own device
+``synth_matrix`` (rsvd_b200_synth_matrix: the reference's construction, synth.cpp:58-71,
+with the bit-identical sampler stream, the blocked Householder QR and the DMMA GEMM), so
+a cell's matrix is the reference's cell matrix to rounding and the rows can be checked
+against the reference's own run_grid CSV (tests/test_gpu_grid_parity.py).
 
   python -m paper_2110_03423_b200.grid --preset fast-2000 [--out grid.csv] [--reps 10]
 """
@@ -141,13 +142,9 @@ def spectrum(kind: str, r: int, beta: float, xp):
     raise ValueError(kind)
 
 
-def synth_device(torch, m: int, n: int, kind: str, beta: float, seed: int, device):
-    """A = U diag(sigma) V^T, Haar slices U (m x r), V (n x r) with r = min(m, n)."""
-    g = torch.Generator(device=device).manual_seed(seed & 0x7FFFFFFFFFFFFFFF)
-    r = min(m, n)
-    u = torch.linalg.qr(torch.randn(m, r, dtype=torch.float64, device=device, generator=g))[0]
-    v = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device=device, generator=g))[0]
-    return (u * spectrum(kind, r, beta, torch).to(device)) @ v.T
+def synth_device(solver, m: int, n: int, kind: str, beta: float, seed: int, device):
+    """synth::synth_matrix({m, n, kind, seed}) generated by the library on the device."""
+    return solver.synth_matrix_device(m, n, kind, beta, seed, device=device)
 
 
 def run_grid(cfg: GridConfig, solver=None, device: int = 0):
@@ -179,7 +176,7 @@ def run_grid(cfg: GridConfig, solver=None, device: int = 0):
             try:
                 beta = cfg.beta if cfg.beta is not None else float(k + 1)
                 cell_seed = (cfg.seed + n * 1315423911 + k * 2654435761) % 2**64
-                a = synth_device(torch, cfg.m, n, cfg.spectrum, beta, cell_seed, dev)
+                a = synth_device(s, cfg.m, n, cfg.spectrum, beta, cell_seed, dev)
                 rc = RsvdConfig(k=k, oversample=cfg.oversample, power_q=cfg.power_q,
                                 seed=cell_seed)
                 ref = {}

@@ -438,6 +438,28 @@ class Solver:
                                                           _dp(y0), y0.shape[1], q, _dp(w)))
         return w
 
+    _SPECTRA = {"fast": 0, "sharp": 1, "slow": 2}
+
+    def synth_matrix(self, rows: int, cols: int, kind: str = "fast", beta: float = 1.0,
+                     seed: int = 0) -> np.ndarray:
+        """randsvd::synth::synth_matrix (synth.cpp:58-71) generated on the device."""
+        out = np.empty((rows, cols))
+        _check(self.lib, self.lib.rsvd_b200_synth_matrix(self.h, rows, cols, self._SPECTRA[kind],
+                                                         float(beta), seed % 2**64, _dp(out)))
+        return out
+
+    def synth_matrix_device(self, rows: int, cols: int, kind: str = "fast", beta: float = 1.0,
+                            seed: int = 0, device=None):
+        """Same, into a new CUDA float64 tensor (stream-ordered before return)."""
+        import torch
+        out = torch.empty((rows, cols), dtype=torch.float64,
+                          device=device if device is not None else f"cuda:{self.device}")
+        self.wait_for_torch(out.device)
+        _check(self.lib, self.lib.rsvd_b200_synth_matrix_device(
+            self.h, rows, cols, self._SPECTRA[kind], float(beta), seed % 2**64, out.data_ptr(),
+            cols))
+        return out
+
     def householder_qr(self, a):
         """Thin QR (qr.cpp:27-102) on the device: (q m x n, r n x n, diag r >= 0)."""
         a = _arr(a)
