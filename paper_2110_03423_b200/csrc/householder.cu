@@ -49,6 +49,7 @@ namespace rsvdb200 {
 constexpr int kPW = 32;           // panel width = warp lanes
 constexpr int kHHThreads = 512;
 constexpr int kHHWarps = kHHThreads / 32;
+constexpr int kUnroll = 4;  // independent row loads in flight per warp
 constexpr int kMaxCols = 288;
 constexpr int kPartStride = kPW * kPW + kPW * kMaxCols;  // V^T V, then W (kPW x kMaxCols)
 // shared memory: per-warp reduction buffer (kHHWarps x kPW x kPW) + M2 (kPW x kMaxCols) +
@@ -128,11 +129,23 @@ __device__ void panel_dots(const HH& h, const double* X, long ldx, long r0, long
         const int c = with_vtv ? job - 1 : job;
         const int col = c0 + c * kPW + lane;
         const bool colok = vtv ? lane < jb : (c * kPW + lane) < ncols;
-        for (long i = r0 + grp; i < hi; i += groups) {
-            const double vl = lane < jb ? h.V[i * h.NP + j0 + lane] : 0.0;
-            const double x = vtv ? vl : (colok ? X[i * ldx + col] : 0.0);
+        // rows in groups of kUnroll independent loads (the loop is L2/HBM-latency bound)
+        for (long i0 = r0 + grp; i0 < hi; i0 += (long)kUnroll * groups) {
+            double vl[kUnroll], x[kUnroll];
 #pragma unroll
-            for (int a = 0; a < kPW; ++a) acc[a] = fma(__shfl_sync(0xffffffffu, vl, a), x, acc[a]);
+            for (int u = 0; u < kUnroll; ++u) {
+                const long i = i0 + (long)u * groups;
+                const bool ok = i < hi;
+                vl[u] = ok && lane < jb ? h.V[i * h.NP + j0 + lane] : 0.0;
+                x[u] = ok && !vtv && colok ? X[i * ldx + col] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const double xv = vtv ? vl[u] : x[u];
+#pragma unroll
+                for (int a = 0; a < kPW; ++a)
+                    acc[a] = fma(__shfl_sync(0xffffffffu, vl[u], a), xv, acc[a]);
+            }
         }
     }
     // cross-warp (same job) reduction in a fixed order
@@ -186,20 +199,30 @@ __device__ void panel_update(const HH& h, double* X, long ldx, long r0, long hi,
         if (grp < groups) {
             const int j = c * kPW + lane;
             const bool colok = j < ncols;
-            for (long i = r0 + grp; i < hi; i += groups) {
-                const double vl = lane < jb ? h.V[i * h.NP + j0 + lane] : 0.0;
-                double x = colok ? X[i * ldx + c0 + j] : 0.0;
-                double upd = 0.0;
+            for (long i0 = r0 + grp; i0 < hi; i0 += (long)kUnroll * groups) {
+                double vl[kUnroll], x[kUnroll];
 #pragma unroll
-                for (int a = 0; a < kPW; ++a)
-                    upd = fma(__shfl_sync(0xffffffffu, vl, a), M2[a * kMaxCols + j], upd);
-                x -= upd;
-                if (colok) X[i * ldx + c0 + j] = x;
-                if (next_k >= 0 && c == 0) {
-                    const double xk = __shfl_sync(0xffffffffu, x, 0);
-                    if (i > next_k && lane < next_jb) acc = fma(xk, x, acc);
-                    if (i == next_k && lane < next_jb)
-                        h.rowbuf[(next_k & 1) * kPW + lane] = x;
+                for (int u = 0; u < kUnroll; ++u) {
+                    const long i = i0 + (long)u * groups;
+                    const bool ok = i < hi;
+                    vl[u] = ok && lane < jb ? h.V[i * h.NP + j0 + lane] : 0.0;
+                    x[u] = ok && colok ? X[i * ldx + c0 + j] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const long i = i0 + (long)u * groups;
+                    double upd = 0.0;
+#pragma unroll
+                    for (int a = 0; a < kPW; ++a)
+                        upd = fma(__shfl_sync(0xffffffffu, vl[u], a), M2[a * kMaxCols + j], upd);
+                    const double xv = x[u] - upd;
+                    if (i < hi && colok) X[i * ldx + c0 + j] = xv;
+                    if (next_k >= 0 && c == 0) {
+                        const double xk = __shfl_sync(0xffffffffu, xv, 0);
+                        if (i < hi && i > next_k && lane < next_jb) acc = fma(xk, xv, acc);
+                        if (i == next_k && i < hi && lane < next_jb)
+                            h.rowbuf[(next_k & 1) * kPW + lane] = xv;
+                    }
                 }
             }
         }
@@ -281,21 +304,34 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
             __syncthreads();
             const bool more = kl + 1 < jb;
             double acc = 0.0;
-            for (long i = max(lo, k) + warp; i < hi; i += kHHWarps) {
-                double a = lane < jb ? P[(i - base) * ldp + lane] : 0.0;
-                const double xk = __shfl_sync(0xffffffffu, a, kl);
-                const double v = (i == k ? alpha : xk) * inv_nv;
-                if (lane == kl) {
-                    h.V[i * NP + k] = v;
-                    if (i == k && active) a = -sign * norm_x;
-                } else if (lane > kl && lane < jb && active) {
-                    a = fma(-dd[lane], v, a);
+            for (long i0 = max(lo, k) + warp; i0 < hi; i0 += (long)kUnroll * kHHWarps) {
+                double av[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const long i = i0 + (long)u * kHHWarps;
+                    av[u] = i < hi && lane < jb ? P[(i - base) * ldp + lane] : 0.0;
                 }
-                if (lane < jb && (lane > kl || i == k)) P[(i - base) * ldp + lane] = a;
-                if (more) {
-                    const double xn = __shfl_sync(0xffffffffu, a, kl + 1);
-                    if (i > k + 1 && lane < jb) acc = fma(xn, a, acc);
-                    if (i == k + 1 && lane < jb) h.rowbuf[(par ^ 1) * kPW + lane] = a;
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const long i = i0 + (long)u * kHHWarps;
+                    double a = av[u];
+                    const double xk = __shfl_sync(0xffffffffu, a, kl);
+                    const double v = (i == k ? alpha : xk) * inv_nv;
+                    if (i < hi) {
+                        if (lane == kl) {
+                            h.V[i * NP + k] = v;
+                            if (i == k && active) a = -sign * norm_x;
+                        } else if (lane > kl && lane < jb && active) {
+                            a = fma(-dd[lane], v, a);
+                        }
+                        if (lane < jb && (lane > kl || i == k)) P[(i - base) * ldp + lane] = a;
+                    }
+                    if (more) {
+                        const double xn = __shfl_sync(0xffffffffu, a, kl + 1);
+                        if (i < hi && i > k + 1 && lane < jb) acc = fma(xn, a, acc);
+                        if (i == k + 1 && i < hi && lane < jb)
+                            h.rowbuf[(par ^ 1) * kPW + lane] = a;
+                    }
                 }
             }
             if (more) {
@@ -320,6 +356,14 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
             grid.sync();
             reduce_part(h, red, cb == 0, jb, nc);
             grid.sync();
+            // the reduced V^T V and W blocks into shared memory (sred is free here)
+            double* vtv_s = sred;              // kPW x kPW
+            double* w_s = sred + kPW * kPW;    // kPW x kMaxCols
+            for (int e = threadIdx.x; e < kPW * kPW; e += kHHThreads)
+                if (cb == 0) vtv_s[e] = (e / kPW < jb && e % kPW < jb) ? __ldcg(red + e) : 0.0;
+            for (int e = threadIdx.x; e < jb * kMaxCols; e += kHHThreads)
+                w_s[e] = (e % kMaxCols < nc) ? __ldcg(red + kPW * kPW + e) : 0.0;
+            __syncthreads();
             if (cb == 0) {
                 // T (every CTA the same; CTA 0 keeps it for the Q pass)
                 if (warp == 0) {
@@ -330,7 +374,7 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
                         double w = 0.0;
                         if (lane < i)
                             for (int c = lane; c < i; ++c)
-                                w = fma(Ts[lane * (kPW + 1) + c], __ldcg(red + c * kPW + i), w);
+                                w = fma(Ts[lane * (kPW + 1) + c], vtv_s[c * kPW + i], w);
                         __syncwarp();
                         if (lane < i) Ts[lane * (kPW + 1) + i] = -ti * w;
                         if (lane == i) Ts[i * (kPW + 1) + i] = ti;
@@ -348,8 +392,7 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
                 double t = 0.0;
                 if (a < jb && j < nc)
                     for (int c = 0; c <= a; ++c)
-                        t = fma(Ts[c * (kPW + 1) + a],
-                                __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
+                        t = fma(Ts[c * (kPW + 1) + a], w_s[c * kMaxCols + j], t);
                 M2[e] = t;
             }
             __syncthreads();
@@ -378,14 +421,17 @@ __global__ void __launch_bounds__(kHHThreads, 1) hh_blocked_kernel(HH h) {
             grid.sync();
             reduce_part(h, red, 0, jb, nc);
             grid.sync();
+            double* w_s = sred;  // the reduced W block (kPW x kMaxCols) in shared memory
+            for (int e = threadIdx.x; e < jb * kMaxCols; e += kHHThreads)
+                w_s[e] = (e % kMaxCols < nc) ? __ldcg(red + kPW * kPW + e) : 0.0;
+            __syncthreads();
             // M2 = T W
             for (int e = threadIdx.x; e < kPW * kMaxCols; e += kHHThreads) {
                 const int a = e / kMaxCols, j = e % kMaxCols;
                 double t = 0.0;
                 if (a < jb && j < nc)
                     for (int c = a; c < jb; ++c)
-                        t = fma(Ts[a * (kPW + 1) + c],
-                                __ldcg(red + kPW * kPW + c * kMaxCols + j), t);
+                        t = fma(Ts[a * (kPW + 1) + c], w_s[c * kMaxCols + j], t);
                 M2[e] = t;
             }
             __syncthreads();
