@@ -35,6 +35,30 @@ cudaError_t launch_sum_buffers(const double* const* bufs, int nbuf, size_t count
     return cudaGetLastError();
 }
 
+__global__ void flags_pack_kernel(const int* flags, int i0, int i1, double* out) {
+    if (threadIdx.x == 0) {
+        out[0] = (double)flags[i0];
+        out[1] = (double)flags[i1];
+    }
+}
+
+__global__ void flags_unpack_kernel(const double* in, int* flags, int i0, int i1) {
+    if (threadIdx.x == 0) {
+        flags[i0] = in[0] != 0.0;
+        flags[i1] = in[1] != 0.0;
+    }
+}
+
+cudaError_t launch_flags_pack(const int* flags, int i0, int i1, double* out, cudaStream_t st) {
+    flags_pack_kernel<<<1, 32, 0, st>>>(flags, i0, i1, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flags_unpack(const double* in, int* flags, int i0, int i1, cudaStream_t st) {
+    flags_unpack_kernel<<<1, 32, 0, st>>>(in, flags, i0, i1);
+    return cudaGetLastError();
+}
+
 namespace {
 
 std::string cuda_msg(cudaError_t e, const char* what) {
@@ -152,6 +176,7 @@ class NcclComm final : public Comm {
         if (comm_) nccl().comm_destroy(comm_);
     }
     const char* kind() const override { return "nccl"; }
+    bool capturable() const override { return true; }
     std::string allreduce_sum(double* buf, size_t count, cudaStream_t st) override {
         if (count == 0) return "";
         const ncclResult_t r =

@@ -36,6 +36,8 @@ class Comm {
     // `st`. Returns an empty string on success, else the error text.
     virtual std::string allreduce_sum(double* buf, size_t count, cudaStream_t st) = 0;
     virtual const char* kind() const = 0;
+    // allreduce_sum may be recorded into a CUDA graph (stream capture)
+    virtual bool capturable() const { return false; }
     int rank = 0, world = 1;
 };
 
@@ -54,6 +56,11 @@ struct LocalGroup {
 };
 
 std::unique_ptr<Comm> make_local_comm(LocalGroup* g, int rank);
+
+// Sharded status flags: out[0..1] = (double)flags[i0], (double)flags[i1]; and back,
+// flags[i] = (in[.] != 0) after the sum all-reduce (an OR over the ranks).
+cudaError_t launch_flags_pack(const int* flags, int i0, int i1, double* out, cudaStream_t st);
+cudaError_t launch_flags_unpack(const double* in, int* flags, int i0, int i1, cudaStream_t st);
 
 // out[e] = sum_{r < nbuf} bufs[r][e], fixed order (up to 16 buffers).
 cudaError_t launch_sum_buffers(const double* const* bufs, int nbuf, size_t count, double* out,

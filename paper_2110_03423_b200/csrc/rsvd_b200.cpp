@@ -165,11 +165,12 @@ struct GraphKey {
     long ldu = 0, ldv = 0;
     int profiling = 0;
     unsigned long gen = 0;
+    const void* comm = nullptr;  // sharded solves: the communicator the graph's all-reduces use
     bool operator==(const GraphKey& o) const {
         return a == o.a && m == o.m && n == o.n && lda == o.lda && s == o.s && NP == o.NP &&
                f32 == o.f32 && k == o.k && q == o.q && seed == o.seed && u == o.u &&
                sigma == o.sigma && v == o.v && ldu == o.ldu && ldv == o.ldv &&
-               profiling == o.profiling && gen == o.gen;
+               profiling == o.profiling && gen == o.gen && comm == o.comm;
     }
 };
 
@@ -189,7 +190,11 @@ struct rsvd_b200_handle {
     DevBuf a_copy, a_t, xt, y, q, part, b, b2, qbt, vbuf, small, flags, u_out, v_out, sig_out,
         hh_work, hh_rows, synth_buf, omega_host_dev, jscratch, cwork, ubt;
     std::unique_ptr<Comm> comm;  // row-sharded solves (comm.h); null = single device
-    DevBuf red_scratch;          // TSQR R stack / flag reduction
+    DevBuf red_scratch;          // TSQR R stack
+    DevBuf flag_red;             // the two flags of a sharded run, as doubles, all-reduced
+    // the last shard layout that passed the collective check (comm, m_local, m_total, n, s)
+    const void* shard_ok_comm = nullptr;
+    long shard_ok[4] = {0, 0, 0, 0};
     DevBuf pca_ones, pca_sums, pca_mean, pca_comp;  // PCA (fit_pca / transform)
     DevBuf res_vs, res_part, res_u;                 // residual_fro
     // FP32 path (A stored in FP32, 3xTF32 tensor-core products): tall FP32 buffers
@@ -982,6 +987,7 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     if (p.f32)  // the 3xTF32 A-pass writes rows < NPf of (A^T Q)^T / Q^T A; pad rows stay 0
         ck(cudaMemsetAsync(h->b.p, 0, (size_t)NP * p.ldn * sizeof(double), h->stream), "memset b");
     h->trace = getenv("RSVD_B200_TRACE") ? atoi(getenv("RSVD_B200_TRACE")) : 0;
+    if (p.sharded) h->flag_red.reserve(2 * sizeof(double));
     h->abort_ptr = robust ? nullptr : static_cast<int*>(h->flags.p) + kFlagAbort;
     return Ctx{h, p, robust, static_cast<int*>(h->flags.p)};
 }
@@ -1258,26 +1264,27 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
     }
 }
 
+// Sharded runs: NaN/Inf seen in any shard and an abort on any rank become every rank's
+// flags, on the device at the end of the pipeline (a sum all-reduce of two doubles between
+// a pack and an unpack kernel), so finish_run's one flag download serves sharded runs too
+// and the whole pipeline, collectives included, can be one CUDA graph.
+void reduce_flags(const Ctx& c) {
+    if (!c.p.sharded) return;
+    rsvd_b200_handle* h = c.h;
+    double* buf = h->flag_red.d();
+    h->launched(launch_flags_pack(c.flags, kFlagNonfinite, kFlagAbort, buf, h->stream),
+                "flags_pack");
+    c.allreduce(buf, 2);
+    h->launched(launch_flags_unpack(buf, c.flags, kFlagNonfinite, kFlagAbort, h->stream),
+                "flags_unpack");
+}
+
 // Status checks after a run (one synchronisation). Returns false if the optimistic run
 // must be repeated robustly.
 bool finish_run(const Ctx& c, bool checked_nonfinite) {
     download_flags(c.h);
     c.h->sync();
-    int* f = c.h->flags_host;
-    if (c.p.sharded) {  // NaN/Inf in any shard, abort on any rank (replicated: all agree)
-        double fl[2] = {(double)f[kFlagNonfinite], (double)f[kFlagAbort]};
-        c.h->red_scratch.reserve(2 * sizeof(double));
-        ck(cudaMemcpyAsync(c.h->red_scratch.p, fl, sizeof fl, cudaMemcpyHostToDevice,
-                           c.h->stream),
-           "flag upload");
-        c.allreduce(c.h->red_scratch.d(), 2);
-        ck(cudaMemcpyAsync(fl, c.h->red_scratch.p, sizeof fl, cudaMemcpyDeviceToHost,
-                           c.h->stream),
-           "flag download");
-        c.h->sync();
-        f[kFlagNonfinite] = fl[0] != 0.0;
-        f[kFlagAbort] = fl[1] != 0.0;
-    }
+    int* f = c.h->flags_host;  // sharded: NaN/abort already OR-reduced (reduce_flags)
     if (checked_nonfinite && f[kFlagNonfinite])
         fail(RSVD_B200_ARGUMENT_ERROR, "randomized_ksvd input contains NaN or Inf");
     if (f[kFlagAbort]) return false;
@@ -1302,8 +1309,10 @@ int solve_tall_graph(rsvd_b200_handle* h, const double* A, const Plan& p,
                       const rsvd_b200_config& cfg, double* u, long ldu, double* sigma, double* v,
                       long ldv) {
     static const bool disabled = getenv("RSVD_B200_NO_GRAPH") != nullptr;
-    if (disabled || !h->use_graphs || h->force_robust || p.sharded || h->up_active || !h->omega_host.empty() ||
-        h->profiling != 0 || getenv("RSVD_B200_TRACE"))
+    // sharded solves are captured when their transport is (NCCL's all-reduce is stream
+    // capturable; the in-process test group synchronises on the host and is not)
+    if (disabled || !h->use_graphs || h->force_robust || (p.sharded && !h->comm->capturable()) ||
+        h->up_active || !h->omega_host.empty() || h->profiling != 0 || getenv("RSVD_B200_TRACE"))
         return 0;
     GraphKey key;
     key.a = p.f32 ? static_cast<const void*>(p.af) : A;
@@ -1311,6 +1320,7 @@ int solve_tall_graph(rsvd_b200_handle* h, const double* A, const Plan& p,
     key.k = cfg.k, key.q = cfg.power_q, key.seed = cfg.seed;
     key.u = u, key.sigma = sigma, key.v = v, key.ldu = ldu, key.ldv = ldv;
     key.profiling = h->profiling;
+    key.comm = p.sharded ? static_cast<const void*>(h->comm.get()) : nullptr;
     key.gen = g_ws_gen.load();
     rsvd_b200_handle::SolveGraph* hit = nullptr;
     rsvd_b200_handle::SolveGraph* lru = &h->graphs[0];
@@ -1336,6 +1346,7 @@ int solve_tall_graph(rsvd_b200_handle* h, const double* A, const Plan& p,
             sketch_dev(c, A, cfg.seed, /*check=*/true);
             power_iterate_dev(c, A, cfg.power_q, false);
             project_and_solve_dev(c, A, (long)cfg.k, u, ldu, sigma, v, ldv);
+            reduce_flags(c);
         } catch (const Failure& f) {
             ok = false;
             why = f.msg;
@@ -1399,6 +1410,7 @@ void solve_tall(rsvd_b200_handle* h, const double* A, const Plan& p, const rsvd_
         // range_basis(W) = W in the pipeline (see the header comment); k <= s always,
         // so pad_to_rank (rsvd.cpp:117-124) never widens the result here.
         project_and_solve_dev(c, A, (long)cfg.k, u, ldu, sigma, v, ldv);
+        reduce_flags(c);
         h->mark("end");
         const bool ok = finish_run(c, true);
         h->finish_timers();
@@ -1507,8 +1519,10 @@ void solve_sharded(rsvd_b200_handle* h, const void* Av, bool f32, long m_local, 
     if (!(cfg.epsilon > 0.0 && cfg.epsilon < 1.0))
         fail(RSVD_B200_ARGUMENT_ERROR, "epsilon must lie in (0, 1)");
     const long s = (long)rsvd_b200_sketch_width(&cfg, (size_t)m_total, (size_t)n);
-    // collective shard check: sum of m_local, count of shards thinner than s
-    {
+    // collective shard check: sum of m_local, count of shards thinner than s — once per
+    // layout and communicator (every rank caches the same verdict)
+    const long layout[4] = {m_local, m_total, n, s};
+    if (h->shard_ok_comm != h->comm.get() || !std::equal(layout, layout + 4, h->shard_ok)) {
         double chk[2] = {(double)m_local, m_local < s ? 1.0 : 0.0};
         h->red_scratch.reserve(2 * sizeof(double));
         ck(cudaMemcpyAsync(h->red_scratch.p, chk, sizeof chk, cudaMemcpyHostToDevice, h->stream),
@@ -1525,6 +1539,8 @@ void solve_sharded(rsvd_b200_handle* h, const void* Av, bool f32, long m_local, 
             fail(RSVD_B200_DIMENSION_ERROR,
                  "every shard needs at least s=%ld rows (%d shard(s) are thinner)", s,
                  (int)chk[1]);
+        h->shard_ok_comm = h->comm.get();
+        std::copy(layout, layout + 4, h->shard_ok);
     }
     const long k = (long)cfg.k;
     if (f32) {

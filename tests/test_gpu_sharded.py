@@ -175,3 +175,101 @@ def test_nccl_world1_equals_single_device(solver):
     assert np.array_equal(res.factors.v, ref.factors.v)
     s.detach()
     assert s.comm_info() == (0, 1)
+
+
+def test_nccl_sharded_solve_replays_as_graph():
+    """With NCCL (capturable all-reduces) the sharded device-resident solve is captured
+    once and replayed as one CUDA graph — all-reduces, the on-device flag reduction and
+    the optimistic pipeline included — and the replay is the eager solve bit for bit."""
+    import torch
+    import paper_2110_03423_b200 as P
+    a = planted(6000, 700, lambda i: np.exp(-i / 12.0), 8)
+    cfg = P.RsvdConfig(k=30, power_q=2, seed=5)
+    s = P.Solver(0)
+    s.attach_nccl(P.nccl_unique_id(), 0, 1)
+    t = torch.from_numpy(a).cuda()
+    g0 = s.last_info("graph_launches")
+    outs = [s.randomized_ksvd_sharded_device(t, a.shape[0], cfg) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert s.last_info("graph_launches") - g0 >= 2  # second and third solve are replays
+    s.set_graphs(False)
+    eager = s.randomized_ksvd_sharded_device(t, a.shape[0], cfg)
+    torch.cuda.synchronize()
+    for o in outs:
+        for x, y in zip(o[:3], eager[:3]):
+            assert torch.equal(x, y)
+    s.set_graphs(True)
+    # an aborting (ill-conditioned) replay still reruns robustly and matches the oracle path
+    rng = np.random.default_rng(3)
+    m, n = 3000, 400
+    uu, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    vv, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    b = (uu * np.maximum(10.0 ** (-np.arange(n) / 3.0), 1e-15)) @ vv.T
+    tb = torch.from_numpy(b).cuda()
+    cfg2 = P.RsvdConfig(k=20, power_q=1, seed=2)
+    r1 = s.randomized_ksvd_sharded_device(tb, m, cfg2)
+    r2 = s.randomized_ksvd_sharded_device(tb, m, cfg2)
+    torch.cuda.synchronize()
+    assert s.last_info("robust_reruns") == 1
+    assert torch.equal(r1[1], r2[1])
+    s.detach()
+
+
+@pytest.mark.parametrize("f32", [False, True])
+def test_sharded_chunked_upload_world2(monkeypatch, f32):
+    """Host-buffer sharded solves upload each shard in chunks that the sketch (and the
+    first A^T Y0) consume as they land; forced into many small chunks at world 2 the
+    result is bit-identical to the same shards solved from device buffers. (Shapes whose
+    device-resident sketch runs un-split — 296+ row tiles per shard, like the BASELINE
+    shards — as the chunked sketch always does; the FP32 chunks hold whole 2048-row
+    splits of the first A^T Y0.)"""
+    import torch
+    import paper_2110_03423_b200 as P
+    if f32:
+        monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "4")  # 4096 rows of 1 KB
+        m, n, world = 2 * 163840, 256, 2  # 80 splits of 2048 rows per shard
+        a = planted(m, n, lambda i: 1.0 / (1.0 + i) ** 1.5, 12).astype(np.float32)
+        cfg = P.RsvdConfig(k=16, power_q=2, seed=3)
+    else:
+        monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "1")  # 1024 rows of 1 KB
+        m, n, world = 2 * 37888, 128, 2
+        a = planted(m, n, lambda i: np.exp(-i / 15.0), 12)
+        cfg = P.RsvdConfig(k=32, power_q=2, seed=7)
+    group = P.LocalGroup(world)
+    solvers = [P.Solver(0) for _ in range(world)]
+    for r, s in enumerate(solvers):
+        s.attach_local(group, r)
+    spans = [P.shard_rows(m, world, r) for r in range(world)]
+    host, dev, err = [None] * world, [None] * world, [None] * world
+
+    def work(r):
+        r0, r1 = spans[r]
+        s = solvers[r]
+        try:
+            shard = np.ascontiguousarray(a[r0:r1])
+            if f32:
+                host[r] = s.randomized_ksvd_sharded_f32(shard, m, cfg)
+                host[r] = (host[r], s.last_info("upload_aty_splits"))
+                u, sg, v, _ = s.randomized_ksvd_sharded_f32_device(torch.from_numpy(shard).cuda(), m, cfg)
+            else:
+                host[r] = s.randomized_ksvd_sharded(shard, m, cfg)
+                host[r] = (host[r], s.last_info("upload_aty_splits"))
+                u, sg, v, _ = s.randomized_ksvd_sharded_device(torch.from_numpy(shard).cuda(), m, cfg)
+            torch.cuda.synchronize()
+            dev[r] = (u.cpu().numpy(), sg.cpu().numpy(), v.cpu().numpy())
+        except Exception as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    for s in solvers:
+        s.detach()
+    assert not any(t.is_alive() for t in th)
+    assert err == [None] * world, err
+    for r in range(world):
+        res, splits = host[r]
+        assert splits > 0, r
+        assert np.array_equal(res.factors.sigma, dev[r][1]), r
+        assert np.array_equal(res.factors.u, dev[r][0]), r
+        assert np.array_equal(res.factors.v, dev[r][2]), r
