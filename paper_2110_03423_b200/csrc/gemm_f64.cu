@@ -34,6 +34,8 @@
 //                                          pairs are adjacent doubles, one 16-byte load)
 //   atx: k = 2*t + (q&1) + 8*(q>>1)      (M-major A and N-major W)
 // with t = lane&3 and q the 4-wide k-slot group.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -571,6 +573,44 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const T* __restric
     }
 }
 
+// The same for many slabs of few elements (the fused-Gram partials: 1583 slabs of 80 x 80
+// at C2): 32 elements x 32 split-groups per CTA, four independent loads in flight per
+// thread, group sums combined in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(1024) reduce_partials_wide_kernel(const T* __restrict__ part,
+                                                                    long stride, int splits,
+                                                                    double* __restrict__ out,
+                                                                    long count) {
+    __shared__ double red[32][33];
+    const int lx = threadIdx.x & 31, gy = threadIdx.x >> 5;
+    for (long base = blockIdx.x * 32L; base < count; base += gridDim.x * 32L) {
+        const long e = base + lx;
+        double acc = 0.0;
+        if (e < count) {
+            int sp = gy;
+            for (; sp + 96 < splits; sp += 128) {
+                const double v0 = (double)part[sp * stride + e];
+                const double v1 = (double)part[(sp + 32) * stride + e];
+                const double v2 = (double)part[(sp + 64) * stride + e];
+                const double v3 = (double)part[(sp + 96) * stride + e];
+                acc += v0;
+                acc += v1;
+                acc += v2;
+                acc += v3;
+            }
+            for (; sp < splits; sp += 32) acc += (double)part[sp * stride + e];
+        }
+        red[gy][lx] = acc;
+        __syncthreads();
+        if (gy == 0 && e < count) {
+            double t = red[0][lx];
+            for (int q = 1; q < 32; ++q) t += red[q][lx];
+            out[e] = t;
+        }
+        __syncthreads();
+    }
+}
+
 // ================================================================ host launchers
 namespace {
 
@@ -762,6 +802,11 @@ template <typename T>
 static cudaError_t launch_reduce_t(const T* part, long stride, int splits, double* out, long count,
                                    cudaStream_t st) {
     long blocks = (count + 31) / 32;
+    if (splits >= 128 && blocks <= 148 * 4) {  // few elements, many slabs
+        reduce_partials_wide_kernel<T><<<(unsigned)std::max(1L, blocks), 1024, 0, st>>>(
+            part, stride, splits, out, count);
+        return cudaGetLastError();
+    }
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
     reduce_partials_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(part, stride, splits, out, count);
