@@ -79,6 +79,14 @@ __device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8
           "d"(a[7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
+// The dynamic shared-memory window rounded up to 1024 bytes (128B-swizzle atoms) by pointer
+// arithmetic on the __shared__ array itself: a round trip through uintptr_t would make every
+// derived access a generic LD.E/ST.E with 64-bit addresses instead of LDS/STS.
+__device__ __forceinline__ char* align_smem_1024(char* smem_raw) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    return smem_raw + ((1024u - (a & 1023u)) & 1023u);
+}
+
 // Byte offset of element (row, col) inside a TMA box written with
 // CU_TENSOR_MAP_SWIZZLE_128B whose rows are exactly 128 bytes (16 doubles).
 // The box base must be 1024-byte aligned.

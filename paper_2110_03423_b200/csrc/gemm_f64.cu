@@ -186,7 +186,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     static_assert(TAIL == 0 || (WN == 1 && TAIL <= 4), "tail columns need WN == 1");
 
     extern __shared__ __align__(1024) char smem_raw[];
-    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    char* smem = align_smem_1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
     uint64_t* empty = full + STAGES;
 
@@ -403,7 +403,17 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 // =========================================================================== atx
 // ACC (OUT_T only): start from the Z^T already in Z instead of zero, so that a K range
 // processed by consecutive launches accumulates exactly like one launch over it.
-template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T, bool ACC = false>
+// TAIL (2, WN == 2, MI == 2): W has nonzero columns only below 8 * (NT - 1) + 2, i.e. the
+// last column tile holds at most two sketch columns (s = 74 in NP = 80). Those two columns
+// run as DFMA instead of a padded DMMA tile: warp column 1 does tiles NI .. NT - 2 on DMMA
+// plus the tail, warp column 0 tiles 0 .. NI - 1; the warp columns are laid out so that every
+// SMSP holds one warp of each (warp w and w + 4 share a scheduler), so the FP64 pipe of every
+// SMSP does 2 NI - 1 tiles + a quarter tile of work instead of 2 NI tiles. Each stage's tail
+// partial sums (over a thread's own k-slots) are reduced across the 4 k-lanes by a butterfly
+// that leaves lane t owning (mi = t & 1, row half h = t >> 1, both columns), and added to a
+// running sum: the accumulation order is per stage, so a K range split at stage boundaries
+// (ACC launches) sums exactly like one launch.
+template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T, bool ACC = false, int TAIL = 0>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     gemm_atx_kernel(const __grid_constant__ CUtensorMap mapA,  // dims {N, K}, box {16, 32}
                     const __grid_constant__ CUtensorMap mapW,  // dims {NP, K}, box {16, 32}
@@ -419,9 +429,10 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
     constexpr uint32_t kBox = kBK * kBoxBytesRow;  // 4 KB: 32 rows x 16 doubles
     constexpr uint32_t kStage = (kABoxes + kWBoxes) * kBox;
     static_assert(NP % 16 == 0 && BJ % (16 * WM) == 0 && NT % WN == 0, "tiling");
+    static_assert(TAIL == 0 || (TAIL == 2 && WN == 2 && MI == 2), "tail layout");
 
     extern __shared__ __align__(1024) char smem_raw[];
-    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    char* smem = align_smem_1024(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
     uint64_t* empty = full + STAGES;
 
@@ -461,9 +472,16 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         return;
     }
 
-    const int wm = warp / WN, wn = warp % WN;
+    // TAIL: warps w and w + 4 (one scheduler) get different warp columns
+    const int wm = TAIL ? warp % WM : warp / WN, wn = TAIL ? warp / WM : warp % WN;
     const int g = lane >> 2, t = lane & 3;
     double* out = Z + blockIdx.y * split_stride;
+    // the tail tile (warp column 1's last, ni = NI - 1): its accumulator slots hold the
+    // current stage's partial sums p[mi][h][c] at acc[mi][NI - 1][2 h + c]
+    const bool tail_warp = TAIL > 0 && wn == WN - 1;
+    constexpr int c_tail = (NT - 1) * 8;
+    double run[2] = {0.0, 0.0};  // lane t's reduced tail sums: mi = t & 1, h = t >> 1
+    const int j_run = j0 + wm * (BJ / WM) + (t & 1) * 16 + g + 8 * (t >> 1);
     double acc[MI][NI][4];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -481,11 +499,16 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
                 if (j < N)
 #pragma unroll
                     for (int ni = 0; ni < NI; ++ni) {
+                        if (tail_warp && ni == NI - 1) continue;
                         const int c = (wn * NI + ni) * 8 + 2 * t;
                         acc[mi][ni][2 * h] = out[(long)c * ldz + j];
                         acc[mi][ni][2 * h + 1] = out[(long)(c + 1) * ldz + j];
                     }
             }
+        if (tail_warp && j_run < N) {
+            run[0] = out[(long)c_tail * ldz + j_run];
+            run[1] = out[(long)(c_tail + 1) * ldz + j_run];
+        }
     }
 
     for (int it = 0; it < n_iter; ++it) {
@@ -507,6 +530,27 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
             }
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
+                if (tail_warp && ni == NI - 1) {  // warp-uniform
+                    // W[k][c_tail .. c_tail + 1] for the thread's 4 k-slots (one 16-byte pair)
+                    const char* boxW = st + (kABoxes + (c_tail >> 4)) * kBox;
+                    if (ks == 0)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) acc[0][ni][v] = acc[1][ni][v] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 w =
+                            lds_f64x2(boxW, swz128(ks * 16 + k_atx(t, q), c_tail & 15));
+#pragma unroll
+                        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                acc[mi][ni][2 * h] = fma(a[mi][h + 2 * q], w.x, acc[mi][ni][2 * h]);
+                                acc[mi][ni][2 * h + 1] =
+                                    fma(a[mi][h + 2 * q], w.y, acc[mi][ni][2 * h + 1]);
+                            }
+                    }
+                    continue;
+                }
                 const int c = (wn * NI + ni) * 8 + g;
                 const char* boxW = st + (kABoxes + (c >> 4)) * kBox;
                 double b[4];
@@ -519,8 +563,39 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
                 for (int mi = 0; mi < MI; ++mi) dmma_16x8x16(acc[mi][ni], a[mi], b);
             }
         }
+        if (tail_warp) {
+            // butterfly over the 4 k-lanes: xor 1 keeps mi = t & 1, xor 2 keeps h = t >> 1
+            double (&p0)[4] = acc[0][NI - 1];
+            double (&p1)[4] = acc[1][NI - 1];
+            const bool b0 = t & 1, b1 = t & 2;
+            double r1[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const double mine = b0 ? p1[v] : p0[v];
+                const double other = b0 ? p0[v] : p1[v];
+                r1[v] = mine + __shfl_xor_sync(0xffffffffu, other, 1);
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {  // r1[2 h + c]
+                const double mine = b1 ? r1[2 + c] : r1[c];
+                const double other = b1 ? r1[c] : r1[2 + c];
+                run[c] += mine + __shfl_xor_sync(0xffffffffu, other, 2);
+            }
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (tail_warp) {
+        // lane t = 0 of each quad takes the tile's columns 0, 1 for (mi, h) from lane mi + 2 h
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double v = __shfl_sync(0xffffffffu, run[c], (lane & ~3) | (mi + 2 * h));
+                    acc[mi][NI - 1][2 * h + c] = t == 0 ? v : 0.0;
+                }
     }
 
 #pragma unroll
@@ -673,12 +748,12 @@ cudaError_t launch_ax_t(const GemmAx& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T, bool ACC = false>
+template <int BJ, int NT, int WM, int WN, int STAGES, bool OUT_T, bool ACC = false, int TAIL = 0>
 cudaError_t launch_atx_t(const GemmAtx& p, cudaStream_t st) {
     constexpr int NP = NT * 8;
     constexpr size_t kStage = (BJ / 16 + NP / 16) * kBK * 128;
     constexpr size_t smem = STAGES * kStage + 2 * STAGES * 8 + 1024;
-    auto kern = gemm_atx_kernel<BJ, NT, WM, WN, STAGES, OUT_T, ACC>;
+    auto kern = gemm_atx_kernel<BJ, NT, WM, WN, STAGES, OUT_T, ACC, TAIL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     CUtensorMap mA, mW;
@@ -735,8 +810,24 @@ cudaError_t dispatch_ax(const GemmAx& p, cudaStream_t st) {
     }
 }
 
+// atx: the last column tile holds at most 2 of the cols nonzero W columns (s % 8 in {1, 2}
+// with NP = round_up(s, 16) - 8 < s): DFMA tail variant.
+inline bool atx_tail(int cols, int NT) {
+    return NT <= 12 && cols > (NT - 1) * 8 && cols <= (NT - 1) * 8 + 2;
+}
+
 template <int NT>
 cudaError_t dispatch_atx(const GemmAtx& p, cudaStream_t st) {
+    if constexpr (NT <= 12) {
+        if (atx_tail(p.cols, NT)) {
+            if (p.accumulate || p.out_transposed) {
+                if (!p.out_transposed) return cudaErrorInvalidValue;
+                return p.accumulate ? launch_atx_t<128, NT, 4, 2, 4, true, true, 2>(p, st)
+                                    : launch_atx_t<128, NT, 4, 2, 4, true, false, 2>(p, st);
+            }
+            return launch_atx_t<128, NT, 4, 2, 4, false, false, 2>(p, st);
+        }
+    }
     if (p.accumulate) {  // upload segments (rsvd_b200.cpp gemm_ax_chunked): Z^T only
         if (!p.out_transposed) return cudaErrorInvalidValue;
         if constexpr (NT <= 12)

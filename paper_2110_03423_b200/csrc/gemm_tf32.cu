@@ -209,8 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the same flag, set before this launch in stream order, so they return together)
     if (abort_flag && *(const volatile int*)abort_flag) return;
     extern __shared__ __align__(1024) char smem_raw[];
-    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                         ~uintptr_t(1023));
+    char* smem = align_smem_1024(smem_raw);
     const uint32_t bB = b_bytes(NP, MN);
     const uint32_t kStage = 2 * kABytes + 2 * bB;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
@@ -465,8 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          float* __restrict__ out_lo, long ldo, long split_stride, int M, int NP,
                          int k_tiles, int k_tiles_per_split, int* __restrict__ flag) {
     extern __shared__ __align__(1024) char smem_raw[];
-    char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                         ~uintptr_t(1023));
+    char* smem = align_smem_1024(smem_raw);
     const int n1 = NP > 256 ? 256 : NP, n2 = NP - n1;  // N chunks; each CTA holds half of each
     const uint32_t h1 = (uint32_t)(n1 / 2) * (BK * 4), h2 = (uint32_t)(n2 / 2) * (BK * 4);
     const uint32_t bH = h1 + h2;  // this CTA's B (or B_lo) half

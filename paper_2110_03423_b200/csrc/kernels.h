@@ -56,6 +56,9 @@ struct GemmAtx {
     // range processed by consecutive launches accumulates exactly like one launch
     bool accumulate = false;
     const int* abort = nullptr;  // as GemmAx::abort
+    // > 0: W's columns >= cols are zero (the sketch width s of an A-pass); when the last
+    // MMA column tile would hold at most 2 of them they run as DFMA (gemm_atx_kernel TAIL)
+    int cols = 0;
 };
 
 // FP32-input 3xTF32 tensor-core GEMM (tcgen05, gemm_tf32.cu), D = op(A) * B (M x NP):

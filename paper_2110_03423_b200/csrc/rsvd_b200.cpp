@@ -492,6 +492,7 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
             GemmAtx g{A + a * lda, b - a, K, lda, Y + a * ldy, ldy, NP,
                       h->pre_part.d() + j * slab, aty_ldz, true};
             g.accumulate = a > s0;
+            g.cols = cols;  // the same (tail) kernel as the device pass's gemm_atx
             h->launched(launch_gemm_atx(g, h->stream), "gemm_atx(upload segment)");
         }
     };
@@ -529,11 +530,13 @@ bool gemm_ax_chunked(rsvd_b200_handle* h, const double* A, long M, long K, long 
 }
 
 // Z = A^T W.  A (K x N, lda), W (K x NP, ldw); out_t: Z^T (NP x N, ldz) else Z (N x NP, ldz).
+// cols > 0: W's columns >= cols are zero (GemmAtx::cols).
 void gemm_atx(rsvd_b200_handle* h, const double* A, long K, long N, long lda, const double* W,
               long ldw, int NP, double* Z, long ldz, bool out_t, const char* tag = nullptr,
-              double flops = 0.0) {
+              double flops = 0.0, int cols = 0) {
     GemmAtx g{A, K, N, lda, W, ldw, NP, Z, ldz, out_t};
     g.abort = h->abort_ptr;
+    g.cols = cols;
     const int splits = choose_splits(ax_tiles(N, NP), (K + 31) / 32);
     if (splits == 1) {
         h->kernel_begin(tag, flops);
@@ -1164,7 +1167,7 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
                         "reduce_partials");
         } else {
             gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true,
-                     "gemm_A", 2.0 * p.m * p.n * p.s);  // (A^T Q1)^T
+                     "gemm_A", 2.0 * p.m * p.n * p.s, p.s);  // (A^T Q1)^T
         }
         h->aty_pending = false;
         c.allreduce(h->b.d(), (size_t)p.NP * p.ldn);  // sharded: sum_g (A_g^T Q1_g)^T
@@ -1199,7 +1202,7 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
         atx_a_f32(c);  // Q1^T A
     else
         gemm_atx(h, A, m, n, p.lda, h->basis, NP, NP, h->b.d(), p.ldn, true, "gemm_A",
-                 2.0 * m * n * s);  // Q1^T A
+                 2.0 * m * n * s, s);  // Q1^T A
     c.allreduce(h->b.d(), (size_t)NP * p.ldn);  // sharded: B = sum_g Q1_g^T A_g
     h->mark("small_svd");
     const double* bq = apply_ct(c, h->b.d(), h->b2.d());  // B = C^T Q1^T A = Q^T A (NP x n)

@@ -369,14 +369,16 @@ def planted_like(m, n, k, seed):
     return (uu * np.exp(-np.arange(r) / (k / 2.0))) @ vv.T
 
 
-@pytest.mark.parametrize("m,n,k,p", [(5000, 64, 8, 6), (37888, 128, 100, 10)])
+@pytest.mark.parametrize("m,n,k,p", [(5000, 64, 8, 6), (37888, 128, 100, 10), (37888, 512, 64, 10)])
 def test_chunked_upload_bit_identical(solver, port, monkeypatch, m, n, k, p):
     """Host-buffer solves upload A in row chunks that the sketch GEMM consumes as they land
     (solve_host / gemm_ax_chunked), and the first power iteration's A^T Y0 advances chunk by
     chunk. The chunks are whole GEMM tiles and the A^T Y0 splits match the device pass's, so
     the result is bit-identical to the device-resident solve whenever the device sketch does
     not split K either (sketch widths 14: fused Gram; 110: NP = 128, 592 row tiles = 4 full
-    waves, Gram by its own GEMM); out= buffers are filled in place."""
+    waves, Gram by its own GEMM; 74: the A^T Y0 segments run the DFMA-tail atx kernel, whose
+    per-stage tail sums must continue across segments exactly); out= buffers are filled in
+    place."""
     import torch
     import paper_2110_03423_b200 as P
     rng = np.random.default_rng(11)
