@@ -51,8 +51,12 @@ __device__ __forceinline__ double2 lds_f64x2(const char* smem_base, uint32_t byt
 }
 __device__ __forceinline__ int k_atx(int t, int q) { return 2 * t + (q & 1) + 8 * (q >> 1); }
 
-__device__ __forceinline__ bool nonfinite(double x) {
-    return ((__double_as_longlong(x) >> 52) & 0x7ff) == 0x7ff;
+// Exponent field all ones (Inf/NaN) from the high word with integer ops: the compiler turns
+// the obvious form into DSETP |x| == Inf / NaN tests, which occupy the FP64 pipe the DMMAs need.
+__device__ __forceinline__ uint32_t exp_bits(double x) {
+    uint32_t hi;
+    asm("mov.b64 {_, %0}, %1;" : "=r"(hi) : "d"(x));
+    return hi & 0x7ff00000u;
 }
 
 // Fused Gram epilogue of the ax kernel: G_tile = Y_tile^T Y_tile (NP x NP, upper
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int j = 0; j < (TAIL > 0 ? TAIL : 1); ++j) tl[i][h][j] = 0.0;
-    bool bad = false;
+    uint32_t bad_exp = 0;  // max exponent field seen (CHECK): 0x7ff00000 = Inf/NaN
 
     for (int it = 0; it < n_iter; ++it) {
         const int s = it % STAGES;
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 #pragma unroll
                 for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-                    for (int v = 0; v < 8; ++v) bad |= nonfinite(a[mi][v]);
+                    for (int v = 0; v < 8; ++v) bad_exp = max(bad_exp, exp_bits(a[mi][v]));
             }
 #pragma unroll
             for (int ni = 0; ni < NI; ++ni) {
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (CHECK && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+    if (CHECK && __any_sync(0xffffffffu, bad_exp == 0x7ff00000u) && lane == 0) atomicOr(flag, 1);
     if constexpr (TAIL > 0) {
         // sum the tail over the 4 k-lanes, then place it in tile nd's accumulator layout
         // (lane t holds columns 8 nd + 2t, 2t + 1)
