@@ -314,6 +314,15 @@ rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const fl
                                           long K, long lda, const float* B, long ldb, int NP,
                                           void* out, long ldo, int out64, int out_t, int splits);
 
+/* Test hook for the INT8-emulated FP64 GEMM (Ozaki scheme, csrc/gemm_oz.cu; device pointers):
+ * mn = 0: out (M x NP) = A (M x K) * B^T with B = Xt (NP x K, ldb; rows >= cols zero);
+ * mn = 1: out = A^T W, A (K x M), W = B (K x NP, ldb; columns >= cols zero), out Z (M x NP) or
+ * Z^T (NP x M) with out_t; splits > 1 = split-K with a fixed-order reduce. NP a multiple of 16,
+ * <= 256. Scales (row / column maxima) and digits are computed in the call. Synchronous. */
+rsvd_b200_status rsvd_b200_debug_gemm_oz(rsvd_b200_handle* h, int mn, const double* A, long M,
+                                        long K, long lda, const double* B, long ldb, int NP,
+                                        int cols, double* out, long ldo, int out_t, int splits);
+
 /* Test hook for the single-CTA Cholesky kernel (device pointers, row-major NP x NP buffers):
  * G (s x s SPD block of an NP x NP buffer) -> R (upper, zero padded) and Rinv^T; *status = 0
  * or 1 (a pivot below tol * max_i G_ii). s up to the shared-memory width limit. Synchronous. */

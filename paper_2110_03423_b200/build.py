@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC",
           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
 
-SOURCES = ["gemm_f64.cu", "gemm_tf32.cu", "omega.cu", "linalg_small.cu", "linalg_blocked.cu", "householder.cu",
+SOURCES = ["gemm_f64.cu", "gemm_tf32.cu", "gemm_oz.cu", "omega.cu", "linalg_small.cu", "linalg_blocked.cu", "householder.cu",
            "comm.cu", "rsvd_b200.cpp", "randsvd_dropin.cpp", "dmat.cpp"]
 CLI = os.path.join(LIBDIR, "randsvd_b200")
 

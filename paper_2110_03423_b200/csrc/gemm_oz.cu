@@ -1,0 +1,687 @@
+// FP64 GEMMs of the rSVD passes over A on the INT8 tensor cores (tcgen05 kind::i8), by the
+// Ozaki scheme: exact integer products of fixed-point digit slices, accumulated exactly in
+// int32 in TMEM, recombined in FP64 once per output tile.
+//
+// Why: B200's FP64 tensor path (DMMA, gemm_f64.cu) peaks at ~37 TFLOP/s, and every pass over A
+// of Algorithm 1 is bound by it (arithmetic intensity s/4 flop/B against a ridge of ~5.6). The
+// INT8 tensor cores run 4.5 POPS dense. Splitting each FP64 operand into S = 7 signed 8-bit
+// digits of a common per-row (per-column) fixed-point scale,
+//     x = 2^(E - 53) * sum_{i<7} d_i 256^i,   d_i in [-128, 127],  |x| < 2^(E + 1),
+// turns a row of A times a column of B into sum_{i,j} (d_i . e_j) 256^(i+j) 2^(E_a + E_b - 106)
+// with every d_i . e_j an exact int8 dot product. The 28 digit products with i + j >= 6 are
+// kept (the dropped ones weigh <= 2^-47 of the leading term); products of equal weight
+// g = i + j share one int32 accumulator (|sum| <= 7 * 2^14 * K < 2^31 for K <= 16384), so a
+// tile needs 7 accumulators of N columns in TMEM. Error: the fixed-point rounding of each
+// operand (2^-54 of the row / column maximum) plus the truncation, i.e. the normwise error of
+// an FP64 GEMM (measured against an exact long-double product: Frobenius-relative 1.1e-15
+// against 6.6e-16 for FP64 BLAS on the C2 operand shapes, tools/probe/ozaki_model.py), with no
+// rounding at all along K.
+//
+// Shapes (the two the FP64 path has):
+//   ax  : Y (M x NP) = A (M x K row-major) X, per-row scales of A (a_ef[M]); X as digit
+//         planes of X^T (NP x K) with per-column scales (b_ef[NP]).
+//   atx : Z = A^T W, A (K x M row-major) read in place; per-column scales of A (a_ef over the
+//         M = A's columns); W as digit planes of W^T (NP x K). Output Z^T (NP x M) or Z.
+// The digits of A are formed in shared memory by converter warps from the FP64 tile TMA
+// brought in (never stored in HBM: A is read exactly once per pass, like the DMMA kernels);
+// the digits of the small operand come from a prep kernel (launch_oz_digits_*).
+//
+// TMEM holds 7 x N int32 columns, so N <= 64 per CTA: wider sketches are split into column
+// chunks of <= 64 whose CTAs are adjacent in the grid (both read the same A tile, the second
+// from L2). CTA = 6 warps: warp 0 TMA, warp 1 TMEM owner + MMA issuer (one lane), warps 2-5
+// converters (one A row / column each) and epilogue (one TMEM lane each).
+// UMMA operands: K-major, SWIZZLE_32B (rows of 32 int8 = one K = 32 MMA step, 8-row atoms of
+// 256 B, 16-byte chunk c of row r stored at chunk c ^ ((r >> 2) & 1)) for both the digits
+// written by the converters and the B digits TMA writes with CU_TENSOR_MAP_SWIZZLE_32B.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rsvdb200 {
+namespace oz {
+
+constexpr int kDigits = 7;        // S
+constexpr int kGroups = 7;        // g = i + j in [S - 1, 2S - 2]
+constexpr int BM = 128;           // MMA M (rows of the tile)
+constexpr int BK = 32;            // K per stage = one kind::i8 MMA
+constexpr int kStages = 3;
+constexpr int kConvWarps = 8;  // warps 2..9: (row, k-half) per thread
+constexpr int kThreads = 64 + 32 * kConvWarps;
+constexpr int kMaxN = 64;         // columns per CTA (7 accumulators of N in 512 TMEM columns)
+constexpr uint32_t kAF64 = BM * BK * 8;       // 32 KB FP64 A tile
+constexpr uint32_t kADig = BM * BK;           // 4 KB per A digit tile
+constexpr uint32_t kBDigMax = kMaxN * BK;     // 2 KB per B digit tile (N <= 64)
+constexpr uint32_t kStage = kAF64 + kDigits * kADig + kDigits * kBDigMax;  // 75776 B
+constexpr uint64_t kDigitBias = 0x0080808080808080ull;  // sum_{i<7} 128 * 256^i
+
+// SW32 K-major byte offset of (row r, 16-byte chunk c) in a digit tile
+__device__ __forceinline__ uint32_t sw32(uint32_t r, uint32_t c) {
+    return (r >> 3) * 256u + (r & 7u) * 32u + ((c ^ ((r >> 2) & 1u)) << 4);
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    // start, LBO 16 B (unused for a swizzled K-major operand of K = one swizzle row), SBO 256 B
+    // (8-row atoms), version 1, layout SWIZZLE_32B (6)
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) |
+           ((uint64_t)(256u >> 4) << 32) | (1ull << 46) | (6ull << 61);
+}
+
+// kind::i8 instruction descriptor: D s32, A s8, B s8, K-major both, M = 128, N
+__device__ __forceinline__ uint32_t idesc(int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (int)r[i];
+}
+
+// The 7 digits of x at the fixed-point scale of biased exponent `ef_max` (the row / column
+// maximum): X = round(x * 2^(53 - E)), |X| < 2^54; returns the bytes of (X + bias) ^ bias,
+// i.e. byte i = d_i as int8 (balanced base-256 digits; byte 7 is 0). Zero / subnormal x -> 0.
+__device__ __forceinline__ uint64_t digits_of(double x, int ef_max) {
+    const uint64_t bits = (uint64_t)__double_as_longlong(x);
+    const int ef = (int)((bits >> 52) & 0x7ff);
+    const uint64_t m53 = (bits & 0x000FFFFFFFFFFFFFull) | 0x0010000000000000ull;
+    const int d = min(max(ef_max - ef, 0), 63);  // ef <= ef_max
+    uint64_t mag = m53 << 1;                     // X = m53 * 2^(1 - d), rounded to nearest
+    if (d > 0) mag = (mag + (1ull << (d - 1))) >> d;
+    if (ef == 0) mag = 0;
+    const uint64_t X = (bits >> 63) ? (0ull - mag) : mag;
+    return (X + kDigitBias) ^ kDigitBias;
+}
+
+// The fixed-point scale 2^(53 - E) of a row / column with maximum biased exponent ef_max, as
+// two exactly representable factors (2^(1076 - ef_max) itself over- or underflows at the ends
+// of the exponent range); 0 for an all-zero row.
+__device__ __forceinline__ void fixed_scale(int ef_max, double& f1, double& f2) {
+    const int e = 1076 - ef_max, e1 = e / 2, e2 = e - e1;
+    f1 = ef_max == 0 ? 0.0 : __longlong_as_double((long long)(e1 + 1023) << 52);
+    f2 = ef_max == 0 ? 0.0 : __longlong_as_double((long long)(e2 + 1023) << 52);
+}
+
+// digits_of with the scale applied on the FP64 pipe: (x f1) f2 is x 2^(53 - E) exactly, and
+// the conversion rounds it to the nearest integer X (the same X as the integer path above).
+__device__ __forceinline__ uint64_t digits_scaled(double x, double f1, double f2) {
+    const long long X = __double2ll_rn((x * f1) * f2);
+    return (uint64_t)X + kDigitBias;  // the bias XOR is applied to the packed plane words
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    while (!done) {
+        __nanosleep(64);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// 4 consecutive k elements (digit words w[0..3]) -> 7 plane words (byte lane = k)
+__device__ __forceinline__ void planes4(const uint64_t (&w)[4], uint32_t (&out)[kDigits]) {
+    const uint32_t l0 = (uint32_t)w[0], l1 = (uint32_t)w[1], l2 = (uint32_t)w[2], l3 = (uint32_t)w[3];
+    const uint32_t h0 = (uint32_t)(w[0] >> 32), h1 = (uint32_t)(w[1] >> 32),
+                   h2 = (uint32_t)(w[2] >> 32), h3 = (uint32_t)(w[3] >> 32);
+    uint32_t a = __byte_perm(l0, l1, 0x5140), b = __byte_perm(l2, l3, 0x5140);
+    out[0] = __byte_perm(a, b, 0x5410);
+    out[1] = __byte_perm(a, b, 0x7632);
+    a = __byte_perm(l0, l1, 0x7362);
+    b = __byte_perm(l2, l3, 0x7362);
+    out[2] = __byte_perm(a, b, 0x5410);
+    out[3] = __byte_perm(a, b, 0x7632);
+    a = __byte_perm(h0, h1, 0x5140);
+    b = __byte_perm(h2, h3, 0x5140);
+    out[4] = __byte_perm(a, b, 0x5410);
+    out[5] = __byte_perm(a, b, 0x7632);
+    a = __byte_perm(h0, h1, 0x7362);
+    b = __byte_perm(h2, h3, 0x7362);
+    out[6] = __byte_perm(a, b, 0x5410);
+}
+
+struct BMaps {  // one B digit-plane map per column chunk (box rows = the chunk's N)
+    CUtensorMap m[4];
+};
+
+// MN = false (ax): A tile = 128 rows x 32 k (two 16-wide SW128 boxes), converter thread = row.
+// MN = true (atx): A tile = 32 k-rows x 128 columns (eight 16-wide boxes), thread = column.
+template <bool MN, bool OUT_T>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_oz_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ BMaps bmaps,
+                   const int* __restrict__ a_ef, const int* __restrict__ b_ef, int M, int NP,
+                   int nch, int nfirst, double* __restrict__ out, long ldo, long split_stride,
+                   int k_tiles, int k_tiles_per_split, const int* __restrict__ abort_flag) {
+    if (abort_flag && *(const volatile int*)abort_flag) return;
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = align_smem_1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
+    uint64_t* conv = full + kStages;
+    uint64_t* empty = conv + kStages;
+    uint64_t* accum = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ch = blockIdx.x % nch;          // column chunk
+    const int tile = blockIdx.x / nch;
+    const int m0 = tile * BM;
+    const int c0 = ch == 0 ? 0 : nfirst + (ch - 1) * nfirst;
+    const int N = min(nfirst, NP - c0);       // multiple of 16
+    const int kt0 = blockIdx.y * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int n_iter = max(0, kt1 - kt0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], kConvWarps);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // stage layout: A FP64 (32 KB) | A digits 7 x 4 KB | B digits 7 x N x 32 B
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&mapA);
+            const CUtensorMap* mb = &bmaps.m[ch];
+            tma_prefetch_desc(mb);
+            const uint32_t bbytes = (uint32_t)N * BK;
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages;
+                if (it >= kStages) mbar_wait_sleep(&empty[s], ((it / kStages) - 1) & 1);
+                char* st = smem + s * kStage;
+                const int k = (kt0 + it) * BK;
+                mbar_arrive_expect_tx(&full[s], kAF64 + kDigits * bbytes);
+                if constexpr (!MN) {
+                    tma_load_2d(st, &mapA, &full[s], k, m0);
+                    tma_load_2d(st + kAF64 / 2, &mapA, &full[s], k + 16, m0);
+                } else {
+#pragma unroll
+                    for (int bx = 0; bx < BM / 16; ++bx)
+                        tma_load_2d(st + bx * (kAF64 / 8), &mapA, &full[s], m0 + 16 * bx, k);
+                }
+                // B planes back to back (plane j at rows j N): MMA i reads planes 6 - i .. 6 as
+                // one operand of (i + 1) N rows
+                char* sb = st + kAF64 + kDigits * kADig;
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i)
+                    tma_load_2d(sb + i * bbytes, mb, &full[s], k, i * NP + c0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t pb = (uint32_t)N * BK;  // bytes of one B plane
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kStages;
+                const uint32_t st = smem_u32(smem + s * kStage);
+                const uint32_t ad = st + kAF64, bd = st + kAF64 + kDigits * kADig;
+                mbar_wait_sleep(&full[s], (it / kStages) & 1);
+                mbar_wait_sleep(&conv[s], (it / kStages) & 1);
+                fence_after();
+                // digit i of A times planes j = 6 - i .. 6 of B in one operand: output block b
+                // (plane 6 - i + b) is group g = i + j - 6 = b, TMEM columns [b N, (b + 1) N) for
+                // every i. i = 6 covers all 7 groups and goes first (it initialises them in the
+                // first stage); operands wider than 256 columns are issued in two MMAs.
+#pragma unroll
+                for (int i = kDigits - 1; i >= 0; --i) {
+                    const uint64_t a = sdesc(ad + i * kADig);
+                    const uint32_t acc = (it > 0 || i != kDigits - 1) ? 1u : 0u;
+                    const int planes = i + 1;
+                    const uint32_t b0 = bd + (uint32_t)(kDigits - 1 - i) * pb;
+                    if (planes * N <= 256) {
+                        mma_i8(tmem, a, sdesc(b0), idesc(planes * N), acc);
+                    } else {
+                        const int p1 = (planes + 1) / 2, p2 = planes - p1;
+                        mma_i8(tmem, a, sdesc(b0), idesc(p1 * N), acc);
+                        mma_i8(tmem + (uint32_t)(p1 * N), a, sdesc(b0 + (uint32_t)p1 * pb),
+                               idesc(p2 * N), acc);
+                    }
+                }
+                commit(&empty[s]);
+            }
+            if (n_iter > 0) commit(accum);
+        }
+    } else {
+        // ------------------------------------------- converters (warps 2..9)
+        // thread -> tile row r (ax) / tile column r (atx) and k-half h (16 of the 32 k)
+        const int ct = threadIdx.x - 64;
+        const int r = ct & (BM - 1), h = ct >> 7;
+        const int q = warp & 3;  // TMEM lane quarter this warp may read in the epilogue
+        const int grow_c = m0 + r;
+        double f1, f2;
+        fixed_scale(grow_c < M ? a_ef[grow_c] : 0, f1, f2);
+        for (int it = 0; it < n_iter; ++it) {
+            const int s = it % kStages;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            char* st = smem + s * kStage;
+            char* dg = st + kAF64;
+            uint32_t pw[kDigits][4];
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) {  // 4 consecutive k
+                uint64_t w[4];
+                if constexpr (!MN) {
+                    const char* box = st + h * (kAF64 / 2);
+#pragma unroll
+                    for (int e = 0; e < 4; e += 2) {
+                        const double2 v =
+                            *reinterpret_cast<const double2*>(box + swz128(r, 4 * qd + e));
+                        w[e] = digits_scaled(v.x, f1, f2);
+                        w[e + 1] = digits_scaled(v.y, f1, f2);
+                    }
+                } else {
+                    const char* box = st + (r >> 4) * (kAF64 / 8);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        w[e] = digits_scaled(
+                            *reinterpret_cast<const double*>(box + swz128(h * 16 + 4 * qd + e, r & 15)),
+                            f1, f2);
+                }
+                uint32_t pl[kDigits];
+                planes4(w, pl);
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
+            }
+#pragma unroll
+            for (int i = 0; i < kDigits; ++i)
+                *reinterpret_cast<uint4*>(dg + i * kADig + sw32(r, h)) =
+                    make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[s]);
+        }
+
+        // ------------------------------------------------------------ epilogue
+        if (n_iter > 0) {
+            mbar_wait(accum, 0);
+            fence_after();
+        }
+        // the two warps of a lane quarter split the 16-column chunks
+        const int grow = m0 + 32 * q + lane;
+        const int efm = grow < M ? a_ef[grow] : 0;
+        const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+        double* ob = out + (size_t)blockIdx.y * split_stride;
+        for (int cc = 16 * ((warp - 2) >> 2); cc < N; cc += 32) {
+            double y[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) y[i] = 0.0;
+            if (n_iter > 0) {
+                // t = sum_g G_g 256^g, most significant group first (Horner)
+#pragma unroll
+                for (int g = kGroups - 1; g >= 0; --g) {
+                    int v[16];
+                    tmem_ld16(trow + (uint32_t)(g * N + cc), v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) y[i] = fma(y[i], 256.0, (double)v[i]);
+                }
+            }
+            if (grow < M) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int c = c0 + cc + i;
+                    // y_true = t * 2^(E_a + E_b - 58), E = ef - 1023
+                    const double val = y[i] == 0.0 ? 0.0 : ldexp(y[i], efm + b_ef[c] - 2104);
+                    if constexpr (OUT_T)
+                        ob[(size_t)c * ldo + grow] = val;
+                    else
+                        ob[(size_t)grow * ldo + c] = val;
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ------------------------------------------------------------------ digit preparation
+// Biased exponent of the largest |x| of each row of a row-major (rows x cols) matrix, the
+// largest over rows of each column, and the NaN/Inf flag, in one pass: CTA (cb, rb) covers
+// columns [512 cb, 512 cb + 512) of rows [R rb, R rb + R); each warp owns 64 columns (one
+// double2 per lane per row). Partial maxima go to row_part[cb][r] / col_part[rb][c] (the
+// exponent field in place, bits 20-30 of the high word) and are reduced by oz_reduce_max.
+constexpr int kScanRows = 512;
+
+__global__ void __launch_bounds__(256) oz_scan_kernel(const double* __restrict__ A, long rows,
+                                                      long cols, long lda, int* __restrict__ row_part,
+                                                      int* __restrict__ col_part,
+                                                      int* __restrict__ flag) {
+    __shared__ int rmax[kScanRows];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long r0 = (long)blockIdx.y * kScanRows;
+    const long c = (long)blockIdx.x * 512 + warp * 64 + 2 * lane;
+    for (int i = threadIdx.x; i < kScanRows; i += 256) rmax[i] = 0;
+    __syncthreads();
+    uint32_t cm0 = 0, cm1 = 0;
+    bool bad = false;
+    const long r1 = min(rows, r0 + kScanRows);
+    for (long r = r0; r < r1; ++r) {
+        uint32_t h0 = 0, h1 = 0;
+        const double* row = A + r * lda;
+        if (c + 1 < cols) {
+            const double2 v = *reinterpret_cast<const double2*>(row + c);
+            h0 = (uint32_t)__double2hiint(v.x) & 0x7ff00000u;
+            h1 = (uint32_t)__double2hiint(v.y) & 0x7ff00000u;
+        } else if (c < cols) {
+            h0 = (uint32_t)__double2hiint(row[c]) & 0x7ff00000u;
+        }
+        cm0 = max(cm0, h0);
+        cm1 = max(cm1, h1);
+        uint32_t rv = max(h0, h1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rv = max(rv, __shfl_xor_sync(0xffffffffu, rv, o));
+        if (lane == 0) atomicMax(&rmax[r - r0], (int)rv);
+    }
+    bad = cm0 == 0x7ff00000u || cm1 == 0x7ff00000u;
+    __syncthreads();
+    for (long r = r0 + threadIdx.x; r < r1; r += 256) {
+        row_part[(long)blockIdx.x * rows + r] = rmax[r - r0];
+        bad |= rmax[r - r0] == 0x7ff00000;
+    }
+    if (c < cols) col_part[(long)blockIdx.y * cols + c] = (int)cm0;
+    if (c + 1 < cols) col_part[(long)blockIdx.y * cols + c + 1] = (int)cm1;
+    if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+}
+
+// out[e] = max_p part[p * count + e] >> 20 (the biased exponent)
+__global__ void oz_reduce_max_kernel(const int* __restrict__ part, int parts, long count,
+                                     int* __restrict__ out) {
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count;
+         e += (long)gridDim.x * blockDim.x) {
+        int m = 0;
+        for (int p = 0; p < parts; ++p) m = max(m, part[(long)p * count + e]);
+        out[e] = m >> 20;
+    }
+}
+
+// Digit planes dig[i][c][k] (i < 7, c < NP, k < ldb bytes) of the rows of Xt (NP x K, ldx;
+// rows >= cols zero), each row at its own scale b_ef[c]. One CTA per row.
+__global__ void __launch_bounds__(256) oz_digits_rows_kernel(const double* __restrict__ Xt, long ldx,
+                                                            int NP, int cols, long K,
+                                                            uint8_t* __restrict__ dig, long ldb,
+                                                            int* __restrict__ b_ef) {
+    const int c = blockIdx.x;
+    __shared__ int red[8];
+    const double* row = Xt + (long)c * ldx;
+    uint32_t m = 0;
+    if (c < cols)
+        for (long k = threadIdx.x; k < K; k += 256)
+            m = max(m, (uint32_t)__double2hiint(row[k]) & 0x7ff00000u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = (int)m;
+    __syncthreads();
+    int ef = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) ef = max(ef, red[w]);
+    ef >>= 20;
+    if (threadIdx.x == 0) b_ef[c] = ef;
+    for (long k4 = threadIdx.x * 4L; k4 < ldb; k4 += 1024) {
+        uint64_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            w[e] = (c < cols && k4 + e < K) ? digits_of(row[k4 + e], ef) : 0ull;
+        uint32_t pl[kDigits];
+        planes4(w, pl);
+#pragma unroll
+        for (int i = 0; i < kDigits; ++i)
+            *reinterpret_cast<uint32_t*>(dig + ((long)i * NP + c) * ldb + k4) = pl[i];
+    }
+}
+
+// Column maxima of W (K x NP row-major, columns >= cols zero) into colmax[NP] (hi-word
+// exponent fields, atomicMax; colmax zeroed by the caller).
+__global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ W, long ldw, int NP,
+                                                       int cols, long K, int* __restrict__ colmax) {
+    __shared__ int sm[288];
+    for (int i = threadIdx.x; i < NP; i += 256) sm[i] = 0;
+    __syncthreads();
+    const long total = K * (long)NP;
+    for (long e = blockIdx.x * 256L + threadIdx.x; e < total; e += (long)gridDim.x * 256) {
+        const long k = e / NP;
+        const int c = (int)(e - k * NP);
+        if (c < cols) atomicMax(&sm[c], (int)((uint32_t)__double2hiint(W[k * ldw + c]) & 0x7ff00000u));
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NP; i += 256)
+        if (sm[i]) atomicMax(&colmax[i], sm[i]);
+}
+
+// Digit planes dig[i][c][k] of the columns of W (K x NP, ldw) at the scales colmax[c] >> 20
+// (written to b_ef): 64-row slabs of W transposed through shared memory.
+__global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __restrict__ W, long ldw,
+                                                            int NP, int cols, long K,
+                                                            uint8_t* __restrict__ dig, long ldb,
+                                                            const int* __restrict__ colmax,
+                                                            int* __restrict__ b_ef) {
+    extern __shared__ double slab[];  // 64 x (NP + 1)
+    const long k0 = (long)blockIdx.x * 64;
+    const int ld = NP + 1;
+    for (int e = threadIdx.x; e < 64 * NP; e += 256) {
+        const int kk = e / NP, c = e - kk * NP;
+        const long k = k0 + kk;
+        slab[kk * ld + c] = (k < K && c < cols) ? W[k * ldw + c] : 0.0;
+    }
+    if (blockIdx.x == 0)
+        for (int c = threadIdx.x; c < NP; c += 256) b_ef[c] = colmax[c] >> 20;
+    __syncthreads();
+    // thread -> (c, 4 consecutive k): 16 k-quads per column
+    for (int e = threadIdx.x; e < NP * 16; e += 256) {
+        const int c = e >> 4, kq = (e & 15) * 4;
+        if (k0 + kq >= ldb) continue;
+        const int ef = colmax[c] >> 20;
+        uint64_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = digits_of(slab[(kq + j) * ld + c], ef);
+        uint32_t pl[kDigits];
+        planes4(w, pl);
+#pragma unroll
+        for (int i = 0; i < kDigits; ++i)
+            *reinterpret_cast<uint32_t*>(dig + ((long)i * NP + c) * ldb + k0 + kq) = pl[i];
+    }
+}
+
+}  // namespace oz
+
+// ======================================================================== host side
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn oz_encode() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+int oz_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* base, long rows,
+           long cols, long ld_elems, int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+    auto encode = oz_encode();
+    if (!encode) return -1;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld_elems * esize) & 15)) return -2;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld_elems * esize)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -3;
+}
+
+unsigned oz_grid(long work, long per = 256) {
+    long b = (work + per - 1) / per;
+    if (b > 148L * 16) b = 148L * 16;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+// Column chunks: NP <= 64 one chunk, else chunks of round_up(NP / nch, 16) (the last smaller).
+void oz_chunks(int NP, int* nch, int* nfirst) {
+    const int n = (NP + oz::kMaxN - 1) / oz::kMaxN;
+    const int f = ((NP + n - 1) / n + 15) & ~15;
+    *nch = (NP + f - 1) / f;
+    *nfirst = f;
+}
+
+long oz_ldb(long K) { return (K + 31) & ~31L; }
+size_t oz_digits_bytes(int NP, long K) { return (size_t)oz::kDigits * NP * oz_ldb(K); }
+
+cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
+    if (p.NP < 16 || p.NP > 4 * oz::kMaxN || (p.NP % 16) != 0) return cudaErrorInvalidValue;
+    int nch, nfirst;
+    oz_chunks(p.NP, &nch, &nfirst);
+    if (nch > 4) return cudaErrorInvalidValue;
+    CUtensorMap mA;
+    if (!p.mn) {
+        if (oz_map(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, p.A, p.M, p.K, p.lda, 16, oz::BM,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    } else {
+        if (oz_map(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, p.A, p.K, p.M, p.lda, 16, oz::BK,
+                   CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    }
+    oz::BMaps bm;
+    for (int c = 0; c < nch; ++c) {
+        const int n = std::min(nfirst, p.NP - c * nfirst);
+        if (oz_map(&bm.m[c], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.bdig, (long)oz::kDigits * p.NP,
+                   p.ldb, p.ldb, oz::BK, n, CU_TENSOR_MAP_SWIZZLE_32B))
+            return cudaErrorInvalidValue;
+    }
+    for (int c = nch; c < 4; ++c) bm.m[c] = bm.m[0];
+    const int k_tiles = (int)((p.K + oz::BK - 1) / oz::BK);
+    int splits = p.splits < 1 ? 1 : p.splits;
+    int per = (k_tiles + splits - 1) / splits;
+    if (per > kOzMaxKTiles) return cudaErrorInvalidValue;  // int32 accumulator headroom
+    const size_t smem = oz::kStages * oz::kStage + 16 * 8 + 16 + 1024;
+    const unsigned gx = (unsigned)(((p.M + oz::BM - 1) / oz::BM) * nch);
+    dim3 grid(gx, (unsigned)splits);
+#define OZ_LAUNCH(MN, OT)                                                                        \
+    do {                                                                                         \
+        auto kern = oz::gemm_oz_kernel<MN, OT>;                                                  \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)smem);                                         \
+        if (e != cudaSuccess) return e;                                                          \
+        kern<<<grid, oz::kThreads, smem, st>>>(mA, bm, p.a_ef, p.b_ef, (int)p.M, p.NP, nch,     \
+                                               nfirst, p.out, p.ldo, p.split_stride, k_tiles,    \
+                                               per, p.abort);                                    \
+    } while (0)
+    if (!p.mn) {
+        if (p.out_t) return cudaErrorInvalidValue;
+        OZ_LAUNCH(false, false);
+    } else if (p.out_t) {
+        OZ_LAUNCH(true, true);
+    } else {
+        OZ_LAUNCH(true, false);
+    }
+#undef OZ_LAUNCH
+    return cudaGetLastError();
+}
+
+cudaError_t launch_oz_scan(const double* A, long rows, long cols, long lda, int* row_ef,
+                           int* col_ef, int* part, int* flag, cudaStream_t st) {
+    if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1)) return cudaErrorInvalidValue;
+    const long cb = (cols + 511) / 512, rb = (rows + oz::kScanRows - 1) / oz::kScanRows;
+    int* row_part = part;
+    int* col_part = part + cb * rows;
+    oz::oz_scan_kernel<<<dim3((unsigned)cb, (unsigned)rb), 256, 0, st>>>(A, rows, cols, lda,
+                                                                         row_part, col_part, flag);
+    oz::oz_reduce_max_kernel<<<oz_grid(rows), 256, 0, st>>>(row_part, (int)cb, rows, row_ef);
+    oz::oz_reduce_max_kernel<<<oz_grid(cols), 256, 0, st>>>(col_part, (int)rb, cols, col_ef);
+    return cudaGetLastError();
+}
+
+size_t oz_scan_part_ints(long rows, long cols) {
+    const long cb = (cols + 511) / 512, rb = (rows + oz::kScanRows - 1) / oz::kScanRows;
+    return (size_t)(cb * rows + rb * cols);
+}
+
+cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, long K,
+                                  uint8_t* dig, int* b_ef, cudaStream_t st) {
+    oz::oz_digits_rows_kernel<<<NP, 256, 0, st>>>(Xt, ldx, NP, cols, K, dig, oz_ldb(K), b_ef);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, long K,
+                                  uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(colmax, 0, NP * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    oz::oz_colmax_kernel<<<oz_grid(K * NP, 2048), 256, 0, st>>>(W, ldw, NP, cols, K, colmax);
+    const size_t smem = 64 * (NP + 1) * sizeof(double);
+    e = cudaFuncSetAttribute(oz::oz_digits_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+    const long ldb = oz_ldb(K);
+    oz::oz_digits_cols_kernel<<<(unsigned)((ldb + 63) / 64), 256, smem, st>>>(
+        W, ldw, NP, cols, K, dig, ldb, colmax, b_ef);
+    return cudaGetLastError();
+}
+
+}  // namespace rsvdb200

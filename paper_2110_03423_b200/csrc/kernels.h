@@ -106,6 +106,49 @@ cudaError_t launch_cvt_f32_f64(const float* in, long ldi, long rows, long cols, 
 cudaError_t launch_transpose_f32(const float* in, long rows, long cols, long ldi, float* out,
                                  long ldo, cudaStream_t st);
 
+// FP64 GEMM on the INT8 tensor cores (Ozaki scheme, gemm_oz.cu). A (FP64) is split into 7
+// balanced base-256 digits at a per-row (ax) / per-column (atx) scale inside the kernel; the
+// small operand comes as digit planes bdig[7][NP][ldb] (K contiguous, ldb = oz_ldb(K) bytes)
+// with per-column scales b_ef[NP] (launch_oz_digits_rows / _cols). a_ef / b_ef hold biased
+// FP64 exponents of the row / column maxima (launch_oz_scan).
+//   mn = false (ax):  out (M x NP, ldo) = A (M x K, lda) X,  a_ef[M] per row of A.
+//   mn = true  (atx): out = A^T W, A (K x M, lda); out_t: Z^T (NP x M, ldo) else Z (M x NP);
+//                     a_ef[M] per column of A; split-K slabs at out + s * split_stride.
+// K per split <= kOzMaxKTiles * 32 (int32 accumulator headroom).
+constexpr int kOzMaxKTiles = 512;
+struct GemmOz {
+    bool mn = false;
+    const double* A = nullptr;
+    long M = 0, K = 0, lda = 0;
+    const int* a_ef = nullptr;
+    const uint8_t* bdig = nullptr;
+    long ldb = 0;
+    const int* b_ef = nullptr;
+    int NP = 0;
+    double* out = nullptr;
+    long ldo = 0;
+    bool out_t = false;
+    int splits = 1;
+    long split_stride = 0;
+    const int* abort = nullptr;
+};
+cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st);
+long oz_ldb(long K);
+size_t oz_digits_bytes(int NP, long K);
+void oz_chunks(int NP, int* nch, int* nfirst);
+// Row / column maxima (biased exponents) of A (rows x cols, lda) and the NaN/Inf flag; `part`
+// holds oz_scan_part_ints(rows, cols) ints of scratch.
+cudaError_t launch_oz_scan(const double* A, long rows, long cols, long lda, int* row_ef,
+                           int* col_ef, int* part, int* flag, cudaStream_t st);
+size_t oz_scan_part_ints(long rows, long cols);
+// Digit planes of the rows of Xt (NP x K, ldx; rows >= cols zero), one scale per row.
+cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, long K,
+                                  uint8_t* dig, int* b_ef, cudaStream_t st);
+// Digit planes of the columns of W (K x NP, ldw; columns >= cols zero), one scale per column;
+// colmax: NP ints of scratch.
+cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, long K,
+                                  uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st);
+
 cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
 cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);
 cudaError_t launch_reduce_partials(const double* part, long stride, int splits, double* out,

@@ -222,6 +222,9 @@ struct rsvd_b200_handle {
     DevBuf pre_part;  // the upload-time (A^T Y0)^T split-K slabs (FP64, or FP32 in the FP32 path)
     long upload_aty = 0;  // splits of the last solve's upload-time A^T Y0 (0: not used)
     DevBuf gpart;             // per-tile Gram partials of the fused epilogue
+    // INT8-emulated FP64 passes (gemm_oz.cu): digit planes of the small operand, exponent
+    // arrays (A rows, A columns, B columns, scratch) and the scan partials
+    DevBuf oz_bdig, oz_ef, oz_part;
     int* flags_host = nullptr;
     StreamPos omega_pos;  // sampler state the next sketch's Omega continues (default: fresh)
     std::vector<double> omega_host;  // validation mode (n x s row-major)
@@ -2456,6 +2459,52 @@ rsvd_b200_status rsvd_b200_debug_gemm_tf32(rsvd_b200_handle* h, int mn, const fl
                         "reduce_partials");
         } else {
             h->launched(launch_gemm_tf32(g, h->stream), "gemm_tf32");
+        }
+        h->sync();
+    });
+}
+
+rsvd_b200_status rsvd_b200_debug_gemm_oz(rsvd_b200_handle* h, int mn, const double* A, long M,
+                                        long K, long lda, const double* B, long ldb, int NP,
+                                        int cols, double* out, long ldo, int out_t, int splits) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        // A's scales: per row (ax, A is M x K) or per column (atx, A is K x M)
+        const long arows = mn ? K : M, acols = mn ? M : K;
+        h->oz_ef.reserve((size_t)(arows + acols + 2 * NP + 8) * sizeof(int));
+        int* row_ef = static_cast<int*>(h->oz_ef.p);
+        int* col_ef = row_ef + arows;
+        int* b_ef = col_ef + acols;
+        int* scratch = b_ef + NP;
+        h->oz_part.reserve(oz_scan_part_ints(arows, acols) * sizeof(int));
+        h->launched(launch_oz_scan(A, arows, acols, lda, row_ef, col_ef,
+                                   static_cast<int*>(h->oz_part.p), nullptr, h->stream),
+                    "oz_scan");
+        h->oz_bdig.reserve(oz_digits_bytes(NP, K));
+        uint8_t* dig = static_cast<uint8_t*>(h->oz_bdig.p);
+        if (mn)
+            h->launched(launch_oz_digits_cols(B, ldb, NP, cols, K, dig, b_ef, scratch, h->stream),
+                        "oz_digits_cols");
+        else
+            h->launched(launch_oz_digits_rows(B, ldb, NP, cols, K, dig, b_ef, h->stream),
+                        "oz_digits_rows");
+        GemmOz g;
+        g.mn = mn != 0;
+        g.A = A, g.M = M, g.K = K, g.lda = lda;
+        g.a_ef = mn ? col_ef : row_ef;
+        g.bdig = dig, g.ldb = oz_ldb(K), g.b_ef = b_ef, g.NP = NP;
+        g.out = out, g.ldo = ldo, g.out_t = out_t != 0;
+        if (splits > 1) {
+            const long slab = out_t ? (long)NP * ldo : M * ldo;
+            h->part.reserve((size_t)splits * slab * sizeof(double));
+            g.out = h->part.d();
+            g.splits = splits;
+            g.split_stride = slab;
+            h->launched(launch_gemm_oz(g, h->stream), "gemm_oz(split)");
+            h->launched(launch_reduce_partials(h->part.d(), slab, splits, out, slab, h->stream),
+                        "reduce_partials");
+        } else {
+            h->launched(launch_gemm_oz(g, h->stream), "gemm_oz");
         }
         h->sync();
     });

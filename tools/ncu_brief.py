@@ -34,10 +34,17 @@ for x in rows:
     for c in cols:
         try:
             tot[c] += int(x[sh.index(c)])
-        except ValueError:
+        except (ValueError, IndexError):
             pass
 s = sum(tot.values()) or 1
 print("stall mix:", ", ".join(f"{c[6:]} {100 * n / s:.1f}%" for c, n in sorted(tot.items(), key=lambda t: -t[1])[:8]))
-for x in sorted(rows, key=lambda x: -int(x[si] or 0))[:ntop]:
-    st = sorted(((c[6:], int(x[sh.index(c)] or 0)) for c in cols), key=lambda t: -t[1])[:2]
+def num(x, i):
+    try:
+        return int(x[i] or 0)
+    except (ValueError, IndexError):
+        return 0
+
+
+for x in sorted(rows, key=lambda x: -num(x, si))[:ntop]:
+    st = sorted(((c[6:], num(x, sh.index(c))) for c in cols), key=lambda t: -t[1])[:2]
     print(f"{x[0][-5:]} {x[1][:56]:56s} {x[si]:>7s} exec {x[ex]:>9s} {st}")
