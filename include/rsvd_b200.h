@@ -323,6 +323,12 @@ rsvd_b200_status rsvd_b200_debug_gemm_oz(rsvd_b200_handle* h, int mn, const doub
                                         long K, long lda, const double* B, long ldb, int NP,
                                         int cols, double* out, long ldo, int out_t, int splits);
 
+/* The same with A converted once to stored row-scaled digit planes (the GEMM reads digits,
+ * A^T W takes A's row scales through W). */
+rsvd_b200_status rsvd_b200_debug_gemm_ozd(rsvd_b200_handle* h, int mn, const double* A, long M,
+                                         long K, long lda, const double* B, long ldb, int NP,
+                                         int cols, double* out, long ldo, int out_t, int splits);
+
 /* Test hook for the single-CTA Cholesky kernel (device pointers, row-major NP x NP buffers):
  * G (s x s SPD block of an NP x NP buffer) -> R (upper, zero padded) and Rinv^T; *status = 0
  * or 1 (a pivot below tol * max_i G_ii). s up to the shared-memory width limit. Synchronous. */

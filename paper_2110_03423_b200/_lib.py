@@ -27,7 +27,7 @@ EXPORTS = [
     "rsvd_b200_comm_info", "rsvd_b200_comm_free", "rsvd_b200_randomized_ksvd_sharded",
     "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak",
     "rsvd_b200_debug_gemm_tf32", "rsvd_b200_debug_cholesky", "rsvd_b200_debug_jacobi",
-    "rsvd_b200_debug_gemm_oz",
+    "rsvd_b200_debug_gemm_oz", "rsvd_b200_debug_gemm_ozd",
     "rsvd_b200_randomized_ksvd_f32",
     "rsvd_b200_randomized_ksvd_f32_device", "rsvd_b200_randomized_ksvd_sharded_f32",
     "rsvd_b200_randomized_ksvd_sharded_f32_device", "rsvd_b200_wait_stream",
@@ -129,6 +129,9 @@ def load() -> C.CDLL:
         "rsvd_b200_debug_gemm_oz": (C.c_int, [_vp, C.c_int, _vp, C.c_long, C.c_long, C.c_long,
                                               _vp, C.c_long, C.c_int, C.c_int, _vp, C.c_long,
                                               C.c_int, C.c_int]),
+        "rsvd_b200_debug_gemm_ozd": (C.c_int, [_vp, C.c_int, _vp, C.c_long, C.c_long, C.c_long,
+                                               _vp, C.c_long, C.c_int, C.c_int, _vp, C.c_long,
+                                               C.c_int, C.c_int]),
         "rsvd_b200_debug_cholesky": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, C.c_double,
                                                C.POINTER(C.c_int)]),
         "rsvd_b200_debug_jacobi": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp,

@@ -63,6 +63,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// 3-D tiled bulk tensor load (coordinates {c0 inner, c1, c2}); out-of-range elements of any
+// dimension are zero-filled.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
 // ---------------------------------------------------------- FP64 tensor core
 // mma.sync m16n8k16 f64 (lowered to 8x DMMA.8x8x4 on sm_100a). Fragment maps
 // (g = lane>>2, t = lane&3; CuTe SM90_16x8x16_F64F64F64F64_TN traits):

@@ -33,6 +33,8 @@
 // UMMA operands: K-major, SWIZZLE_32B (rows of 32 int8 = one K = 32 MMA step, 8-row atoms of
 // 256 B, 16-byte chunk c of row r stored at chunk c ^ ((r >> 2) & 1)) for both the digits
 // written by the converters and the B digits TMA writes with CU_TENSOR_MAP_SWIZZLE_32B.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -45,14 +47,18 @@ constexpr int kDigits = 7;        // S
 constexpr int kGroups = 7;        // g = i + j in [S - 1, 2S - 2]
 constexpr int BM = 128;           // MMA M (rows of the tile)
 constexpr int BK = 32;            // K per stage = one kind::i8 MMA
-constexpr int kStages = 3;
-constexpr int kConvWarps = 8;  // warps 2..9: (row, k-half) per thread
-constexpr int kThreads = 64 + 32 * kConvWarps;
-constexpr int kMaxN = 64;         // columns per CTA (7 accumulators of N in 512 TMEM columns)
+constexpr int kFStages = 4;       // FP64 A ring (TMA -> converters)
+constexpr int kDStages = 3;       // A digits in TMEM (converters -> MMA): 7 N + 3 x 56 <= 512 columns
+constexpr int kBStages = 4;       // B digit planes in shared memory (TMA -> MMA)
+constexpr int kConvWarps = 8;     // warps 3..10: (row, k-half) per thread
+constexpr int kThreads = 96 + 32 * kConvWarps;
+constexpr int kMaxN = 48;         // columns per CTA: 7 accumulators of N + 3 x 56 digit columns
+constexpr int kMaxChunks = 8;
 constexpr uint32_t kAF64 = BM * BK * 8;       // 32 KB FP64 A tile
-constexpr uint32_t kADig = BM * BK;           // 4 KB per A digit tile
-constexpr uint32_t kBDigMax = kMaxN * BK;     // 2 KB per B digit tile (N <= 64)
-constexpr uint32_t kStage = kAF64 + kDigits * kADig + kDigits * kBDigMax;  // 75776 B
+constexpr uint32_t kDigCols = BK / 4;         // TMEM columns of one A digit tile (4 int8 each)
+constexpr uint32_t kBDigMax = kMaxN * BK;     // 1.5 KB per B digit plane (N <= 48)
+constexpr uint32_t kBStage = kDigits * kBDigMax;  // 10752 B
+constexpr uint32_t kRing = kFStages * kAF64 + kBStages * kBStage;  // 174080 B
 constexpr uint64_t kDigitBias = 0x0080808080808080ull;  // sum_{i<7} 128 * 256^i
 
 // SW32 K-major byte offset of (row r, 16-byte chunk c) in a digit tile
@@ -78,6 +84,29 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
         "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+// A operand from TMEM (128 lanes = rows, 8 columns = 32 int8 of K), B from shared memory
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id,
+                                          uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c,
+                                         uint32_t d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+                 "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(pred));
+    return pred != 0;
 }
 
 __device__ __forceinline__ void commit(uint64_t* bar) {
@@ -182,41 +211,61 @@ __device__ __forceinline__ void planes4(const uint64_t (&w)[4], uint32_t (&out)[
 }
 
 struct BMaps {  // one B digit-plane map per column chunk (box rows = the chunk's N)
-    CUtensorMap m[4];
+    CUtensorMap m[kMaxChunks];
 };
 
 // MN = false (ax): A tile = 128 rows x 32 k (two 16-wide SW128 boxes), converter thread = row.
 // MN = true (atx): A tile = 32 k-rows x 128 columns (eight 16-wide boxes), thread = column.
+// The FP64 A tiles come through a 4-stage TMA ring; the converters write A's digit tiles
+// straight into TMEM (tcgen05.st, double-buffered after the accumulators), where the MMA reads
+// them as its A operand, so shared memory carries only the FP64 tile and the B digit planes
+// (4-stage TMA ring). Warps: 0 A producer, 1 TMEM owner + MMA issuer, 2 B producer,
+// 3..10 converters / epilogue (thread = TMEM lane = tile row, and a k-half).
 template <bool MN, bool OUT_T>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_oz_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ BMaps bmaps,
                    const int* __restrict__ a_ef, const int* __restrict__ b_ef, int M, int NP,
                    int nch, int nfirst, double* __restrict__ out, long ldo, long split_stride,
-                   int k_tiles, int k_tiles_per_split, const int* __restrict__ abort_flag) {
+                   int k_tiles, int k_tiles_per_split, const int* __restrict__ abort_flag,
+                   int diag) {
     if (abort_flag && *(const volatile int*)abort_flag) return;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = align_smem_1024(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
-    uint64_t* conv = full + kStages;
-    uint64_t* empty = conv + kStages;
-    uint64_t* accum = empty + kStages;
+    char* ringA = smem;
+    char* ringB = smem + kFStages * kAF64;
+    uint64_t* full_a = reinterpret_cast<uint64_t*>(smem + kRing);
+    uint64_t* empty_a = full_a + kFStages;
+    uint64_t* full_b = empty_a + kFStages;
+    uint64_t* empty_b = full_b + kBStages;
+    uint64_t* conv = empty_b + kBStages;
+    uint64_t* empty_d = conv + kDStages;
+    uint64_t* accum = empty_d + kDStages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ch = blockIdx.x % nch;          // column chunk
     const int tile = blockIdx.x / nch;
     const int m0 = tile * BM;
-    const int c0 = ch == 0 ? 0 : nfirst + (ch - 1) * nfirst;
+    const int c0 = ch * nfirst;
     const int N = min(nfirst, NP - c0);       // multiple of 16
+    const uint32_t pb = (uint32_t)N * BK;     // bytes of one B digit plane
+    const uint32_t dcol0 = (uint32_t)(kGroups * N);  // TMEM column of the A digit buffers
     const int kt0 = blockIdx.y * k_tiles_per_split;
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
     const int n_iter = max(0, kt1 - kt0);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
+        for (int s = 0; s < kFStages; ++s) {
+            mbar_init(&full_a[s], 1);
+            mbar_init(&empty_a[s], kConvWarps);
+        }
+        for (int s = 0; s < kBStages; ++s) {
+            mbar_init(&full_b[s], 1);
+            mbar_init(&empty_b[s], 1);
+        }
+        for (int s = 0; s < kDStages; ++s) {
             mbar_init(&conv[s], kConvWarps);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty_d[s], 1);
         }
         mbar_init(accum, 1);
         fence_barrier_init();
@@ -232,115 +281,145 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // stage layout: A FP64 (32 KB) | A digits 7 x 4 KB | B digits 7 x N x 32 B
     if (warp == 0) {
+        // ------------------------------------------------------------ A producer
         if (lane == 0) {
             tma_prefetch_desc(&mapA);
-            const CUtensorMap* mb = &bmaps.m[ch];
-            tma_prefetch_desc(mb);
-            const uint32_t bbytes = (uint32_t)N * BK;
             for (int it = 0; it < n_iter; ++it) {
-                const int s = it % kStages;
-                if (it >= kStages) mbar_wait_sleep(&empty[s], ((it / kStages) - 1) & 1);
-                char* st = smem + s * kStage;
+                const int s = it % kFStages;
+                if (it >= kFStages) mbar_wait_sleep(&empty_a[s], ((it / kFStages) - 1) & 1);
+                char* st = ringA + s * kAF64;
                 const int k = (kt0 + it) * BK;
-                mbar_arrive_expect_tx(&full[s], kAF64 + kDigits * bbytes);
+                mbar_arrive_expect_tx(&full_a[s], kAF64);
                 if constexpr (!MN) {
-                    tma_load_2d(st, &mapA, &full[s], k, m0);
-                    tma_load_2d(st + kAF64 / 2, &mapA, &full[s], k + 16, m0);
+                    tma_load_2d(st, &mapA, &full_a[s], k, m0);
+                    tma_load_2d(st + kAF64 / 2, &mapA, &full_a[s], k + 16, m0);
                 } else {
 #pragma unroll
                     for (int bx = 0; bx < BM / 16; ++bx)
-                        tma_load_2d(st + bx * (kAF64 / 8), &mapA, &full[s], m0 + 16 * bx, k);
+                        tma_load_2d(st + bx * (kAF64 / 8), &mapA, &full_a[s], m0 + 16 * bx, k);
                 }
-                // B planes back to back (plane j at rows j N): MMA i reads planes 6 - i .. 6 as
-                // one operand of (i + 1) N rows
-                char* sb = st + kAF64 + kDigits * kADig;
+            }
+        }
+    } else if (warp == 2) {
+        // ---------------------------------------- B producer: digit planes back to back
+        // (plane j at rows j N) so that MMA i reads planes 6 - i .. 6 as one operand
+        if (lane == 0) {
+            const CUtensorMap* mb = &bmaps.m[ch];
+            tma_prefetch_desc(mb);
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kBStages;
+                if (it >= kBStages) mbar_wait_sleep(&empty_b[s], ((it / kBStages) - 1) & 1);
+                char* sb = ringB + s * kBStage;
+                const int k = (kt0 + it) * BK;
+                mbar_arrive_expect_tx(&full_b[s], kDigits * pb);
 #pragma unroll
                 for (int i = 0; i < kDigits; ++i)
-                    tma_load_2d(sb + i * bbytes, mb, &full[s], k, i * NP + c0);
+                    tma_load_2d(sb + i * pb, mb, &full_b[s], k, i * NP + c0);
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t pb = (uint32_t)N * BK;  // bytes of one B plane
-            for (int it = 0; it < n_iter; ++it) {
-                const int s = it % kStages;
-                const uint32_t st = smem_u32(smem + s * kStage);
-                const uint32_t ad = st + kAF64, bd = st + kAF64 + kDigits * kADig;
-                mbar_wait_sleep(&full[s], (it / kStages) & 1);
-                mbar_wait_sleep(&conv[s], (it / kStages) & 1);
-                fence_after();
-                // digit i of A times planes j = 6 - i .. 6 of B in one operand: output block b
-                // (plane 6 - i + b) is group g = i + j - 6 = b, TMEM columns [b N, (b + 1) N) for
-                // every i. i = 6 covers all 7 groups and goes first (it initialises them in the
-                // first stage); operands wider than 256 columns are issued in two MMAs.
+        // ------------------------------------------------------------- MMA issuer
+        // digit i of A times planes j = 6 - i .. 6 of B in one operand: output block b (plane
+        // 6 - i + b) is group g = i + j - 6 = b, TMEM columns [b N, (b + 1) N) for every i.
+        // i = 6 covers all 7 groups and goes first (it initialises them in the first stage);
+        // operands wider than 256 columns are issued in two MMAs. The 9 (or fewer) MMAs' B
+        // descriptor offsets, instruction descriptors and TMEM addresses are set up once.
+        // the whole warp runs the loop (warp-uniform control flow keeps the descriptors and
+        // TMEM addresses in uniform registers); one elected lane issues
+        // MMA list (compile-time shape): digit i, first plane offset (in planes), planes, TMEM
+        // column offset (in units of N); i = 6 and 5 split in two (N <= 48 keeps every operand
+        // <= 256 columns)
+        constexpr int kNM = 9;
+        constexpr int mi[kNM] = {6, 6, 5, 5, 4, 3, 2, 1, 0};
+        constexpr int mp0[kNM] = {0, 4, 1, 4, 2, 3, 4, 5, 6};  // first plane j
+        constexpr int mnp[kNM] = {4, 3, 3, 3, 5, 4, 3, 2, 1};  // planes
+        constexpr int mdc[kNM] = {0, 4, 0, 3, 0, 0, 0, 0, 0};  // TMEM column block
+        uint32_t idv[kNM];
 #pragma unroll
-                for (int i = kDigits - 1; i >= 0; --i) {
-                    const uint64_t a = sdesc(ad + i * kADig);
-                    const uint32_t acc = (it > 0 || i != kDigits - 1) ? 1u : 0u;
-                    const int planes = i + 1;
-                    const uint32_t b0 = bd + (uint32_t)(kDigits - 1 - i) * pb;
-                    if (planes * N <= 256) {
-                        mma_i8(tmem, a, sdesc(b0), idesc(planes * N), acc);
-                    } else {
-                        const int p1 = (planes + 1) / 2, p2 = planes - p1;
-                        mma_i8(tmem, a, sdesc(b0), idesc(p1 * N), acc);
-                        mma_i8(tmem + (uint32_t)(p1 * N), a, sdesc(b0 + (uint32_t)p1 * pb),
-                               idesc(p2 * N), acc);
-                    }
-                }
-                commit(&empty[s]);
-            }
-            if (n_iter > 0) commit(accum);
-        }
-    } else {
-        // ------------------------------------------- converters (warps 2..9)
-        // thread -> tile row r (ax) / tile column r (atx) and k-half h (16 of the 32 k)
-        const int ct = threadIdx.x - 64;
-        const int r = ct & (BM - 1), h = ct >> 7;
-        const int q = warp & 3;  // TMEM lane quarter this warp may read in the epilogue
-        const int grow_c = m0 + r;
-        double f1, f2;
-        fixed_scale(grow_c < M ? a_ef[grow_c] : 0, f1, f2);
+        for (int j = 0; j < kNM; ++j) idv[j] = idesc(mnp[j] * N);
+        const uint64_t bdesc0 = sdesc(smem_u32(ringB));
         for (int it = 0; it < n_iter; ++it) {
-            const int s = it % kStages;
-            mbar_wait(&full[s], (it / kStages) & 1);
-            char* st = smem + s * kStage;
-            char* dg = st + kAF64;
+            const int sb = it % kBStages, sd = it % kDStages;
+            const uint64_t bd = bdesc0 + ((uint64_t)(sb * kBStage) >> 4);
+            const uint32_t ad = tmem + dcol0 + (uint32_t)sd * (kDigits * kDigCols);
+            if (!(diag & 1)) mbar_wait(&full_b[sb], (it / kBStages) & 1);
+            mbar_wait(&conv[sd], (it / kDStages) & 1);
+            fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int j = 0; j < kNM; ++j)
+                    mma_i8_ts(tmem + (uint32_t)(mdc[j] * N), ad + (uint32_t)mi[j] * kDigCols,
+                              bd + (((uint64_t)mp0[j] * pb) >> 4), idv[j],
+                              (it > 0 || j > 1) ? 1u : 0u);
+                commit(&empty_b[sb]);
+                commit(&empty_d[sd]);
+            }
+            __syncwarp();
+        }
+        if (n_iter > 0 && elect_one()) commit(accum);
+        __syncwarp();
+    } else {
+        // ------------------------------------------- converters (warps 3..10)
+        // thread -> tile row r (ax) / tile column r (atx) = its TMEM lane, and a k-half h
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int r = 32 * q + lane, h = (warp - 3) >> 2;
+        const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+        const int grow = m0 + r;
+        const int efm = grow < M ? a_ef[grow] : 0;
+        double f1, f2;
+        fixed_scale(efm, f1, f2);
+        for (int it = 0; it < n_iter; ++it) {
+            const int sa = it % kFStages, sd = it % kDStages;
+            if (!(diag & 2)) mbar_wait(&full_a[sa], (it / kFStages) & 1);
+            const char* st = ringA + sa * kAF64;
+            double v[16];
+            if constexpr (!MN) {
+                const char* box = st + h * (kAF64 / 2);
+#pragma unroll
+                for (int e = 0; e < 16; e += 2) {
+                    const double2 t = *reinterpret_cast<const double2*>(box + swz128(r, e));
+                    v[e] = t.x;
+                    v[e + 1] = t.y;
+                }
+            } else {
+                const char* box = st + (r >> 4) * (kAF64 / 8);
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    v[e] = *reinterpret_cast<const double*>(box + swz128(h * 16 + e, r & 15));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_a[sa]);  // the FP64 tile is in registers
             uint32_t pw[kDigits][4];
+            if (diag & 4) {
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i)
+#pragma unroll
+                    for (int qd = 0; qd < 4; ++qd) pw[i][qd] = __double2loint(v[qd + i]);
+            } else {
 #pragma unroll
             for (int qd = 0; qd < 4; ++qd) {  // 4 consecutive k
                 uint64_t w[4];
-                if constexpr (!MN) {
-                    const char* box = st + h * (kAF64 / 2);
 #pragma unroll
-                    for (int e = 0; e < 4; e += 2) {
-                        const double2 v =
-                            *reinterpret_cast<const double2*>(box + swz128(r, 4 * qd + e));
-                        w[e] = digits_scaled(v.x, f1, f2);
-                        w[e + 1] = digits_scaled(v.y, f1, f2);
-                    }
-                } else {
-                    const char* box = st + (r >> 4) * (kAF64 / 8);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        w[e] = digits_scaled(
-                            *reinterpret_cast<const double*>(box + swz128(h * 16 + 4 * qd + e, r & 15)),
-                            f1, f2);
-                }
+                for (int e = 0; e < 4; ++e) w[e] = digits_scaled(v[4 * qd + e], f1, f2);
                 uint32_t pl[kDigits];
                 planes4(w, pl);
 #pragma unroll
                 for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
             }
+            }
+            if (it >= kDStages) {
+                mbar_wait(&empty_d[sd], ((it / kDStages) - 1) & 1);
+                fence_after();
+            }
+            const uint32_t tb = tlane + dcol0 + (uint32_t)sd * (kDigits * kDigCols) + 4u * h;
 #pragma unroll
             for (int i = 0; i < kDigits; ++i)
-                *reinterpret_cast<uint4*>(dg + i * kADig + sw32(r, h)) =
-                    make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tmem_st4(tb + (uint32_t)i * kDigCols, pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&conv[s]);
+            if (lane == 0) mbar_arrive(&conv[sd]);
         }
 
         // ------------------------------------------------------------ epilogue
@@ -349,11 +428,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_after();
         }
         // the two warps of a lane quarter split the 16-column chunks
-        const int grow = m0 + 32 * q + lane;
-        const int efm = grow < M ? a_ef[grow] : 0;
-        const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
         double* ob = out + (size_t)blockIdx.y * split_stride;
-        for (int cc = 16 * ((warp - 2) >> 2); cc < N; cc += 32) {
+        for (int cc = 16 * h; cc < N; cc += 32) {
             double y[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) y[i] = 0.0;
@@ -361,10 +437,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // t = sum_g G_g 256^g, most significant group first (Horner)
 #pragma unroll
                 for (int g = kGroups - 1; g >= 0; --g) {
-                    int v[16];
-                    tmem_ld16(trow + (uint32_t)(g * N + cc), v);
+                    int vv[16];
+                    tmem_ld16(tlane + (uint32_t)(g * N + cc), vv);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) y[i] = fma(y[i], 256.0, (double)v[i]);
+                    for (int i = 0; i < 16; ++i) y[i] = fma(y[i], 256.0, (double)vv[i]);
                 }
             }
             if (grow < M) {
@@ -438,14 +514,14 @@ __global__ void __launch_bounds__(256) oz_scan_kernel(const double* __restrict__
     if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 }
 
-// out[e] = max_p part[p * count + e] >> 20 (the biased exponent)
+// out[e] = max_p part[p * count + e] >> 20 (the biased exponent); acc: max with out[e]
 __global__ void oz_reduce_max_kernel(const int* __restrict__ part, int parts, long count,
-                                     int* __restrict__ out) {
+                                     int* __restrict__ out, int acc) {
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count;
          e += (long)gridDim.x * blockDim.x) {
         int m = 0;
         for (int p = 0; p < parts; ++p) m = max(m, part[(long)p * count + e]);
-        out[e] = m >> 20;
+        out[e] = acc ? max(out[e], m >> 20) : m >> 20;
     }
 }
 
@@ -486,8 +562,16 @@ __global__ void __launch_bounds__(256) oz_digits_rows_kernel(const double* __res
 
 // Column maxima of W (K x NP row-major, columns >= cols zero) into colmax[NP] (hi-word
 // exponent fields, atomicMax; colmax zeroed by the caller).
+// row scale of W' = diag(2^(row_ef[k] - 1076)) W (stored-digit atx passes), 1 without row_ef
+__device__ __forceinline__ double row_scale(const int* row_ef, long k) {
+    if (!row_ef) return 1.0;
+    const int e = row_ef[k] - 1076 + 1023;  // biased exponent of 2^(E_k - 53)
+    return e >= 1 ? __longlong_as_double((long long)e << 52) : 0.0;
+}
+
 __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ W, long ldw, int NP,
-                                                       int cols, long K, int* __restrict__ colmax) {
+                                                       int cols, long K, int* __restrict__ colmax,
+                                                       const int* __restrict__ row_ef) {
     __shared__ int sm[288];
     for (int i = threadIdx.x; i < NP; i += 256) sm[i] = 0;
     __syncthreads();
@@ -495,7 +579,9 @@ __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict
     for (long e = blockIdx.x * 256L + threadIdx.x; e < total; e += (long)gridDim.x * 256) {
         const long k = e / NP;
         const int c = (int)(e - k * NP);
-        if (c < cols) atomicMax(&sm[c], (int)((uint32_t)__double2hiint(W[k * ldw + c]) & 0x7ff00000u));
+        if (c < cols)
+            atomicMax(&sm[c], (int)((uint32_t)__double2hiint(W[k * ldw + c] * row_scale(row_ef, k)) &
+                                   0x7ff00000u));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < NP; i += 256)
@@ -508,14 +594,15 @@ __global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __res
                                                             int NP, int cols, long K,
                                                             uint8_t* __restrict__ dig, long ldb,
                                                             const int* __restrict__ colmax,
-                                                            int* __restrict__ b_ef) {
+                                                            int* __restrict__ b_ef,
+                                                            const int* __restrict__ row_ef) {
     extern __shared__ double slab[];  // 64 x (NP + 1)
     const long k0 = (long)blockIdx.x * 64;
     const int ld = NP + 1;
     for (int e = threadIdx.x; e < 64 * NP; e += 256) {
         const int kk = e / NP, c = e - kk * NP;
         const long k = k0 + kk;
-        slab[kk * ld + c] = (k < K && c < cols) ? W[k * ldw + c] : 0.0;
+        slab[kk * ld + c] = (k < K && c < cols) ? W[k * ldw + c] * row_scale(row_ef, k) : 0.0;
     }
     if (blockIdx.x == 0)
         for (int c = threadIdx.x; c < NP; c += 256) b_ef[c] = colmax[c] >> 20;
@@ -533,6 +620,237 @@ __global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __res
 #pragma unroll
         for (int i = 0; i < kDigits; ++i)
             *reinterpret_cast<uint32_t*>(dig + ((long)i * NP + c) * ldb + k0 + kq) = pl[i];
+    }
+}
+
+// ======================================================= stored digits (convert once per solve)
+// A (rows x cols, lda) -> 7 row-scaled digit planes dig[i][r][c] (plane stride rows * ldd
+// bytes, ldd a multiple of 16) and row_ef[r], plus the NaN/Inf flag: one row per CTA-iteration,
+// thread t holds elements [16 t, 16 t + 16) of the row in registers (cols <= 16 * blockDim), so
+// A is read once; the digits go out as 16-byte stores per plane.
+__global__ void __launch_bounds__(1024) oz_convert_rows_kernel(
+    const double* __restrict__ A, long rows, long cols, long lda, uint8_t* __restrict__ dig,
+    long ldd, long plane, int* __restrict__ row_ef, int* __restrict__ flag) {
+    __shared__ uint32_t red[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    bool bad = false;
+    for (long r = blockIdx.x; r < rows; r += gridDim.x) {
+        const double* row = A + r * lda;
+        const long c0 = 16L * t;
+        double v[16];
+        if (c0 + 16 <= cols) {
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+                const double2 x = __ldcs(reinterpret_cast<const double2*>(row + c0 + e));
+                v[e] = x.x;
+                v[e + 1] = x.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = c0 + e < cols ? row[c0 + e] : 0.0;
+        }
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) m = max(m, (uint32_t)__double2hiint(v[e]) & 0x7ff00000u);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) red[w] = m;
+        __syncthreads();
+        uint32_t mm = 0;
+        for (int i = 0; i < nw; ++i) mm = max(mm, red[i]);
+        __syncthreads();
+        const int ef = (int)(mm >> 20);
+        bad |= ef == 0x7ff;
+        if (t == 0) row_ef[r] = ef;
+        if (c0 < ldd) {
+            double f1, f2;
+            fixed_scale(ef, f1, f2);
+            uint32_t pw[kDigits][4];
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) {
+                uint64_t wd[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) wd[e] = digits_scaled(v[4 * qd + e], f1, f2);
+                uint32_t pl[kDigits];
+                planes4(wd, pl);
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
+            }
+#pragma unroll
+            for (int i = 0; i < kDigits; ++i)
+                *reinterpret_cast<uint4*>(dig + i * plane + r * ldd + c0) =
+                    make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+        }
+    }
+    if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+}
+
+// ------------------------------------------------------------ GEMM from stored digits
+// Both pass shapes from A's row-scaled digit planes (oz_convert_rows) and the small operand's
+// digit planes:
+//   MN = false (ax):  Y (M x NP) = A X. A operand = 128 rows x 32 k of each plane (K-major,
+//                     SW32 TMA boxes); out = T 2^(a_ef[row] + b_ef[c] - 2104).
+//   MN = true  (atx): Z = A^T W'. A operand = A^T: 128 columns x 32 rows of each plane, read
+//                     in place as an MN-major operand (SW128 TMA boxes of 32 rows x 128 B);
+//                     W' = diag(2^(E_row - 53)) W carries A's row scales (exact powers of two),
+//                     so out = T 2^(b_ef[c] - 1028).
+// Pure TMA + tcgen05 pipeline: warp 0 TMA producer (7 A tiles + 7 B planes per stage), warp 1
+// TMEM owner + MMA issuer (whole warp, elected lane), warps 2-5 epilogue.
+constexpr int kDsStages = 5;
+constexpr int kDsThreads = 192;
+constexpr uint32_t kDsADig = BM * BK;                       // 4 KB per A digit tile
+constexpr uint32_t kDsBPlane = 64 * BK;                     // N <= 64
+constexpr uint32_t kDsStage = kDigits * kDsADig + kDigits * kDsBPlane;  // 43008 B
+constexpr int kDsMaxN = 64;
+
+__device__ __forceinline__ uint64_t sdesc_mn128(uint32_t saddr) {
+    // MN-major SWIZZLE_128B: 128 B of M per row (one atom wide), 8-row (K) atoms 1024 B apart
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) |
+           ((uint64_t)(1024u >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+template <bool MN, bool OUT_T>
+__global__ void __launch_bounds__(kDsThreads, 1)
+    gemm_ozd_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ BMaps bmaps,
+                    const int* __restrict__ a_ef, const int* __restrict__ b_ef, int M, int NP,
+                    int nch, int nfirst, double* __restrict__ out, long ldo,
+                    long split_stride, int k_tiles, int k_tiles_per_split,
+                    const int* __restrict__ abort_flag) {
+    if (abort_flag && *(const volatile int*)abort_flag) return;
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = align_smem_1024(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDsStages * kDsStage);
+    uint64_t* empty = full + kDsStages;
+    uint64_t* accum = empty + kDsStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ch = blockIdx.x % nch;
+    const int tile = blockIdx.x / nch;
+    const int m0 = tile * BM;
+    const int c0 = ch * nfirst;
+    const int N = min(nfirst, NP - c0);
+    const uint32_t pb = (uint32_t)N * BK;
+    const int kt0 = blockIdx.y * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int n_iter = max(0, kt1 - kt0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kDsStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accum, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tma_prefetch_desc(&mapA);
+            const CUtensorMap* mb = &bmaps.m[ch];
+            tma_prefetch_desc(mb);
+            for (int it = 0; it < n_iter; ++it) {
+                const int s = it % kDsStages;
+                if (it >= kDsStages) mbar_wait_sleep(&empty[s], ((it / kDsStages) - 1) & 1);
+                char* st = smem + s * kDsStage;
+                const int k = (kt0 + it) * BK;
+                mbar_arrive_expect_tx(&full[s], kDigits * (kDsADig + pb));
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i) {
+                    // 3-D map {byte column, row, plane}: rows / columns past the matrix read 0
+                    if constexpr (!MN)
+                        tma_load_3d(st + i * kDsADig, &mapA, &full[s], k, m0, i);
+                    else
+                        tma_load_3d(st + i * kDsADig, &mapA, &full[s], m0, k, i);
+                }
+                char* sb = st + kDigits * kDsADig;
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i)
+                    tma_load_2d(sb + i * pb, mb, &full[s], k, i * NP + c0);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr int kNM = 9;
+        constexpr int mi[kNM] = {6, 6, 5, 5, 4, 3, 2, 1, 0};
+        constexpr int mp0[kNM] = {0, 4, 1, 4, 2, 3, 4, 5, 6};
+        constexpr int mnp[kNM] = {4, 3, 3, 3, 5, 4, 3, 2, 1};
+        constexpr int mdc[kNM] = {0, 4, 0, 3, 0, 0, 0, 0, 0};
+        uint32_t idv[kNM];
+#pragma unroll
+        for (int j = 0; j < kNM; ++j) idv[j] = idesc(mnp[j] * N) | (MN ? (1u << 15) : 0u);
+        const uint32_t sm0 = smem_u32(smem);
+        for (int it = 0; it < n_iter; ++it) {
+            const int s = it % kDsStages;
+            const uint32_t st = sm0 + s * kDsStage;
+            const uint64_t bd = sdesc(st + kDigits * kDsADig);
+            mbar_wait(&full[s], (it / kDsStages) & 1);
+            fence_after();
+            if (elect_one()) {
+#pragma unroll
+                for (int j = 0; j < kNM; ++j) {
+                    const uint32_t a = st + (uint32_t)mi[j] * kDsADig;
+                    const uint64_t ad = MN ? sdesc_mn128(a) : sdesc(a);
+                    mma_i8(tmem + (uint32_t)(mdc[j] * N), ad, bd + (((uint64_t)mp0[j] * pb) >> 4),
+                           idv[j], (it > 0 || j > 1) ? 1u : 0u);
+                }
+                commit(&empty[s]);
+            }
+            __syncwarp();
+        }
+        if (n_iter > 0 && elect_one()) commit(accum);
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 2-5)
+        const int q = warp & 3;
+        const int grow = m0 + 32 * q + lane;
+        const int efa = MN ? 1076 : (grow < M ? a_ef[grow] : 0);
+        if (n_iter > 0) {
+            mbar_wait_sleep(accum, 0);
+            fence_after();
+        }
+        const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16);
+        double* ob = out + (size_t)blockIdx.y * split_stride;
+        for (int cc = 0; cc < N; cc += 16) {
+            double y[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) y[i] = 0.0;
+            if (n_iter > 0) {
+#pragma unroll
+                for (int g = kGroups - 1; g >= 0; --g) {
+                    int vv[16];
+                    tmem_ld16(tlane + (uint32_t)(g * N + cc), vv);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) y[i] = fma(y[i], 256.0, (double)vv[i]);
+                }
+            }
+            if (grow < M) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int c = c0 + cc + i;
+                    const double val = y[i] == 0.0 ? 0.0 : ldexp(y[i], efa + b_ef[c] - 2104);
+                    if constexpr (OUT_T)
+                        ob[(size_t)c * ldo + grow] = val;
+                    else
+                        ob[(size_t)grow * ldo + c] = val;
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 
@@ -594,10 +912,10 @@ long oz_ldb(long K) { return (K + 31) & ~31L; }
 size_t oz_digits_bytes(int NP, long K) { return (size_t)oz::kDigits * NP * oz_ldb(K); }
 
 cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
-    if (p.NP < 16 || p.NP > 4 * oz::kMaxN || (p.NP % 16) != 0) return cudaErrorInvalidValue;
+    if (p.NP < 16 || p.NP > 256 || (p.NP % 16) != 0) return cudaErrorInvalidValue;
     int nch, nfirst;
     oz_chunks(p.NP, &nch, &nfirst);
-    if (nch > 4) return cudaErrorInvalidValue;
+    if (nch > oz::kMaxChunks) return cudaErrorInvalidValue;
     CUtensorMap mA;
     if (!p.mn) {
         if (oz_map(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, p.A, p.M, p.K, p.lda, 16, oz::BM,
@@ -615,12 +933,15 @@ cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
                    p.ldb, p.ldb, oz::BK, n, CU_TENSOR_MAP_SWIZZLE_32B))
             return cudaErrorInvalidValue;
     }
-    for (int c = nch; c < 4; ++c) bm.m[c] = bm.m[0];
+    for (int c = nch; c < oz::kMaxChunks; ++c) bm.m[c] = bm.m[0];
     const int k_tiles = (int)((p.K + oz::BK - 1) / oz::BK);
     int splits = p.splits < 1 ? 1 : p.splits;
     int per = (k_tiles + splits - 1) / splits;
     if (per > kOzMaxKTiles) return cudaErrorInvalidValue;  // int32 accumulator headroom
-    const size_t smem = oz::kStages * oz::kStage + 16 * 8 + 16 + 1024;
+    const size_t smem = oz::kRing + 24 * 8 + 16 + 1024;
+    // RSVD_B200_OZ_DIAG (profiling only; results are wrong): 1 = MMA skips the B-ready wait,
+    // 2 = converters skip the A-ready wait, 4 = converters skip the digit arithmetic
+    static const int diag = getenv("RSVD_B200_OZ_DIAG") ? atoi(getenv("RSVD_B200_OZ_DIAG")) : 0;
     const unsigned gx = (unsigned)(((p.M + oz::BM - 1) / oz::BM) * nch);
     dim3 grid(gx, (unsigned)splits);
 #define OZ_LAUNCH(MN, OT)                                                                        \
@@ -631,7 +952,7 @@ cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
         if (e != cudaSuccess) return e;                                                          \
         kern<<<grid, oz::kThreads, smem, st>>>(mA, bm, p.a_ef, p.b_ef, (int)p.M, p.NP, nch,     \
                                                nfirst, p.out, p.ldo, p.split_stride, k_tiles,    \
-                                               per, p.abort);                                    \
+                                               per, p.abort, diag);                              \
     } while (0)
     if (!p.mn) {
         if (p.out_t) return cudaErrorInvalidValue;
@@ -645,22 +966,108 @@ cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// planes x rows x cols bytes (row stride ld, plane stride plane_bytes)
+int oz_map3(CUtensorMap* map, const void* base, long planes, long plane_bytes, long rows,
+            long cols, long ld, int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+    auto encode = oz_encode();
+    if (!encode) return -1;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 15) || (plane_bytes & 15)) return -2;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)plane_bytes};
+    cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -3;
+}
+
+cudaError_t launch_gemm_ozd(const GemmOzd& p, cudaStream_t st) {
+    if (p.NP < 16 || p.NP > 256 || (p.NP % 16) != 0) return cudaErrorInvalidValue;
+    int nch, nfirst;
+    oz_chunks(p.NP, &nch, &nfirst);
+    if (nch > oz::kMaxChunks) return cudaErrorInvalidValue;
+    CUtensorMap mA;
+    // the digit planes: plane_rows x ldd bytes each (A's rows x columns)
+    const long pbytes = p.plane_rows * p.ldd;
+    if (!p.mn) {  // A operand rows = output rows (M, a row range of the planes), K = columns
+        if (oz_map3(&mA, p.adig, oz::kDigits, pbytes, p.M, p.K, p.ldd, oz::BK, oz::BM,
+                    CU_TENSOR_MAP_SWIZZLE_32B))
+            return cudaErrorInvalidValue;
+    } else {  // A operand = A^T: M = A's columns, K = A's rows
+        if (oz_map3(&mA, p.adig, oz::kDigits, pbytes, p.K, p.M, p.ldd, oz::BM, oz::BK,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    }
+    oz::BMaps bm;
+    for (int c = 0; c < nch; ++c) {
+        const int n = std::min(nfirst, p.NP - c * nfirst);
+        if (oz_map(&bm.m[c], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.bdig, (long)oz::kDigits * p.NP,
+                   p.ldb, p.ldb, oz::BK, n, CU_TENSOR_MAP_SWIZZLE_32B))
+            return cudaErrorInvalidValue;
+    }
+    for (int c = nch; c < oz::kMaxChunks; ++c) bm.m[c] = bm.m[0];
+    const int k_tiles = (int)((p.K + oz::BK - 1) / oz::BK);
+    const int splits = p.splits < 1 ? 1 : p.splits;
+    const int per = (k_tiles + splits - 1) / splits;
+    if (per > kOzMaxKTiles) return cudaErrorInvalidValue;
+    const size_t smem = oz::kDsStages * oz::kDsStage + 16 * 8 + 16 + 1024;
+    const unsigned gx = (unsigned)(((p.M + oz::BM - 1) / oz::BM) * nch);
+    dim3 grid(gx, (unsigned)splits);
+#define OZD_LAUNCH(MN, OT)                                                                       \
+    do {                                                                                         \
+        auto kern = oz::gemm_ozd_kernel<MN, OT>;                                                 \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)smem);                                         \
+        if (e != cudaSuccess) return e;                                                          \
+        kern<<<grid, oz::kDsThreads, smem, st>>>(mA, bm, p.a_ef, p.b_ef, (int)p.M, p.NP, nch,   \
+                                                 nfirst, p.out, p.ldo, p.split_stride, k_tiles,  \
+                                                 per, p.abort);                                  \
+    } while (0)
+    if (!p.mn) {
+        if (p.out_t) return cudaErrorInvalidValue;
+        OZD_LAUNCH(false, false);
+    } else if (p.out_t) {
+        OZD_LAUNCH(true, true);
+    } else {
+        OZD_LAUNCH(true, false);
+    }
+#undef OZD_LAUNCH
+    return cudaGetLastError();
+}
+
 cudaError_t launch_oz_scan(const double* A, long rows, long cols, long lda, int* row_ef,
-                           int* col_ef, int* part, int* flag, cudaStream_t st) {
+                           int* col_ef, int* part, int* flag, cudaStream_t st, bool col_acc) {
     if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1)) return cudaErrorInvalidValue;
     const long cb = (cols + 511) / 512, rb = (rows + oz::kScanRows - 1) / oz::kScanRows;
     int* row_part = part;
     int* col_part = part + cb * rows;
     oz::oz_scan_kernel<<<dim3((unsigned)cb, (unsigned)rb), 256, 0, st>>>(A, rows, cols, lda,
                                                                          row_part, col_part, flag);
-    oz::oz_reduce_max_kernel<<<oz_grid(rows), 256, 0, st>>>(row_part, (int)cb, rows, row_ef);
-    oz::oz_reduce_max_kernel<<<oz_grid(cols), 256, 0, st>>>(col_part, (int)rb, cols, col_ef);
+    oz::oz_reduce_max_kernel<<<oz_grid(rows), 256, 0, st>>>(row_part, (int)cb, rows, row_ef, 0);
+    oz::oz_reduce_max_kernel<<<oz_grid(cols), 256, 0, st>>>(col_part, (int)rb, cols, col_ef,
+                                                            col_acc ? 1 : 0);
     return cudaGetLastError();
 }
 
 size_t oz_scan_part_ints(long rows, long cols) {
     const long cb = (cols + 511) / 512, rb = (rows + oz::kScanRows - 1) / oz::kScanRows;
     return (size_t)(cb * rows + rb * cols);
+}
+
+long oz_ldd(long cols) { return (cols + 15) & ~15L; }
+
+cudaError_t launch_oz_convert_rows(const double* A, long rows, long cols, long lda, uint8_t* dig,
+                                   long plane_rows, int* row_ef, int* flag, cudaStream_t st) {
+    if (cols > 16L * 1024 || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1))
+        return cudaErrorInvalidValue;
+    const int threads = std::max(32, (int)(((cols + 15) / 16 + 31) / 32 * 32));
+    const long ldd = oz_ldd(cols);
+    // the planes of a row chunk (rows at dig + row offset) keep the full matrix's plane stride
+    unsigned grid = (unsigned)std::min<long>(rows, 148L * (2048 / threads));
+    oz::oz_convert_rows_kernel<<<grid, threads, 0, st>>>(A, rows, cols, lda, dig, ldd,
+                                                        plane_rows * ldd, row_ef, flag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, long K,
@@ -670,17 +1077,19 @@ cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, 
 }
 
 cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, long K,
-                                  uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st) {
+                                  uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st,
+                                  const int* row_ef) {
     cudaError_t e = cudaMemsetAsync(colmax, 0, NP * sizeof(int), st);
     if (e != cudaSuccess) return e;
-    oz::oz_colmax_kernel<<<oz_grid(K * NP, 2048), 256, 0, st>>>(W, ldw, NP, cols, K, colmax);
+    oz::oz_colmax_kernel<<<oz_grid(K * NP, 2048), 256, 0, st>>>(W, ldw, NP, cols, K, colmax,
+                                                               row_ef);
     const size_t smem = 64 * (NP + 1) * sizeof(double);
     e = cudaFuncSetAttribute(oz::oz_digits_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
     const long ldb = oz_ldb(K);
     oz::oz_digits_cols_kernel<<<(unsigned)((ldb + 63) / 64), 256, smem, st>>>(
-        W, ldw, NP, cols, K, dig, ldb, colmax, b_ef);
+        W, ldw, NP, cols, K, dig, ldb, colmax, b_ef, row_ef);
     return cudaGetLastError();
 }
 

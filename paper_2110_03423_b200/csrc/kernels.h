@@ -138,16 +138,50 @@ size_t oz_digits_bytes(int NP, long K);
 void oz_chunks(int NP, int* nch, int* nfirst);
 // Row / column maxima (biased exponents) of A (rows x cols, lda) and the NaN/Inf flag; `part`
 // holds oz_scan_part_ints(rows, cols) ints of scratch.
+// col_acc: max the column maxima into col_ef (row chunks of one A scanned as they arrive).
 cudaError_t launch_oz_scan(const double* A, long rows, long cols, long lda, int* row_ef,
-                           int* col_ef, int* part, int* flag, cudaStream_t st);
+                           int* col_ef, int* part, int* flag, cudaStream_t st,
+                           bool col_acc = false);
 size_t oz_scan_part_ints(long rows, long cols);
 // Digit planes of the rows of Xt (NP x K, ldx; rows >= cols zero), one scale per row.
 cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, long K,
                                   uint8_t* dig, int* b_ef, cudaStream_t st);
 // Digit planes of the columns of W (K x NP, ldw; columns >= cols zero), one scale per column;
-// colmax: NP ints of scratch.
+// colmax: NP ints of scratch. row_ef (optional): digitise W' = diag(2^(row_ef[k] - 1076)) W,
+// which carries A's row scales into the stored-digit atx GEMM.
 cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, long K,
-                                  uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st);
+                                  uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st,
+                                  const int* row_ef = nullptr);
+
+// Stored digits: A (rows x cols <= 16384, lda) -> 7 row-scaled digit planes (plane stride
+// plane_rows * oz_ldd(cols) bytes, rows at dig; a row chunk passes dig offset by its first row),
+// row_ef[rows], NaN/Inf flag. One read of A.
+long oz_ldd(long cols);
+cudaError_t launch_oz_convert_rows(const double* A, long rows, long cols, long lda, uint8_t* dig,
+                                   long plane_rows, int* row_ef, int* flag, cudaStream_t st);
+// INT8 GEMM from stored digits (gemm_oz.cu gemm_ozd_kernel):
+//   mn = false: out (M x NP) = A X, adig = A's planes from its first row (plane stride
+//               plane_rows x ldd bytes, M rows used), a_ef[M].
+//   mn = true:  out = A^T W' with A (K x M) as stored (plane_rows = K), W' digits from
+//               launch_oz_digits_cols(..., row_ef); a_ef unused. out_t / splits as GemmOz.
+struct GemmOzd {
+    bool mn = false;
+    const uint8_t* adig = nullptr;
+    long plane_rows = 0, ldd = 0;
+    long M = 0, K = 0;
+    const int* a_ef = nullptr;
+    const uint8_t* bdig = nullptr;
+    long ldb = 0;
+    const int* b_ef = nullptr;
+    int NP = 0;
+    double* out = nullptr;
+    long ldo = 0;
+    bool out_t = false;
+    int splits = 1;
+    long split_stride = 0;
+    const int* abort = nullptr;
+};
+cudaError_t launch_gemm_ozd(const GemmOzd& p, cudaStream_t st);
 
 cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
 cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);

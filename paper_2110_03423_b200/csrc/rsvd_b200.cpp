@@ -225,6 +225,7 @@ struct rsvd_b200_handle {
     // INT8-emulated FP64 passes (gemm_oz.cu): digit planes of the small operand, exponent
     // arrays (A rows, A columns, B columns, scratch) and the scan partials
     DevBuf oz_bdig, oz_ef, oz_part;
+    DevBuf oz_adig;  // A's row-scaled digit planes (stored-digit passes)
     int* flags_host = nullptr;
     StreamPos omega_pos;  // sampler state the next sketch's Omega continues (default: fresh)
     std::vector<double> omega_host;  // validation mode (n x s row-major)
@@ -612,6 +613,38 @@ void gemm_tf32(rsvd_b200_handle* h, GemmTf32 g, const char* tag = nullptr, doubl
                     "reduce_partials");
 }
 
+// ---------------------------------------------- INT8-emulated FP64 A-passes (gemm_oz.cu)
+// The passes over A of an FP64 solve run on the INT8 tensor cores (Ozaki scheme) when A holds
+// at least 2^26 elements (below, the scale scan and digit preparation cost more than the
+// DMMA passes save, and the FP64 DMMA kernels keep products such as sketch(I) = Omega
+// bit-exact). RSVD_B200_GEMM=dmma / =oz forces either path (tests, comparisons).
+bool oz_on(const Plan& p) {
+    static const int mode = [] {
+        const char* e = getenv("RSVD_B200_GEMM");
+        if (e && std::string(e) == "dmma") return 0;
+        if (e && std::string(e) == "oz") return 2;
+        return 1;
+    }();
+    if (mode == 0 || p.f32 || p.NP < 16 || p.NP > 256) return false;
+    return mode == 2 || (double)p.m * (double)p.n >= (double)(1L << 26);
+}
+
+long oz_tiles(long N, int NP) {
+    int nch, nf;
+    oz_chunks(NP, &nch, &nf);
+    return ((N + 127) / 128) * nch;
+}
+
+// split-K of an oz pass: every split within the int32 accumulators' headroom; the atx shape
+// (few output tiles, K = m) also splits to fill the waves like choose_splits. The ax shape
+// never splits for occupancy, so a row chunk of it (chunked upload) runs exactly the tiles
+// of the whole pass.
+int oz_splits(long N, int NP, long K, bool fill) {
+    const long kt = (K + 31) / 32;
+    const int need = (int)((kt + kOzMaxKTiles - 1) / kOzMaxKTiles);
+    return fill ? std::max(choose_splits(oz_tiles(N, NP), kt), need) : need;
+}
+
 // Largest split-K slab set any GEMM of a plan needs.
 size_t partial_doubles(const Plan& p) {
     const long NP = p.NP;
@@ -625,6 +658,12 @@ size_t partial_doubles(const Plan& p) {
         if (sp > 1) need = std::max(need, (size_t)sp * M * ldy);
     };
     atx(p.m, p.n, p.ldn, true);  // A-pass (A^T W)^T, Q^T A
+    if (oz_on(p)) {
+        const int sa = oz_splits(p.n, NP, p.m, true);
+        if (sa > 1) need = std::max(need, (size_t)sa * NP * p.ldn);
+        const int sx = oz_splits(p.m, NP, p.n, false);
+        if (sx > 1) need = std::max(need, (size_t)sx * p.m * NP);
+    }
     atx(p.m, NP, NP, false);     // tall Gram
     atx(NP, p.n, p.ldn, true);   // wide TRSM / C^T correction
     atx(NP, p.n, NP, false);     // V = Q_B U_R
@@ -990,6 +1029,11 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     if (NP <= 96 && !p.f32) h->gpart.reserve((size_t)ax_tiles(p.m, NP) * NP * NP * sizeof(double));
     h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(p.s)) * sizeof(double));
     h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
+    if (oz_on(p)) {
+        h->oz_ef.reserve((size_t)(p.m + p.n + 2 * NP + 8) * sizeof(int));
+        h->oz_bdig.reserve(std::max(oz_digits_bytes(NP, p.n), oz_digits_bytes(NP, p.m)));
+        h->oz_part.reserve(oz_scan_part_ints(p.m, p.n) * sizeof(int));
+    }
     ck(cudaMemsetAsync(h->flags.p, 0, kNumFlags * sizeof(int), h->stream), "memset flags");
     h->aty_pending = false;
     h->upload_aty = 0;
@@ -999,6 +1043,94 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     if (p.sharded) h->flag_red.reserve(2 * sizeof(double));
     h->abort_ptr = robust ? nullptr : static_cast<int*>(h->flags.p) + kFlagAbort;
     return Ctx{h, p, robust, static_cast<int*>(h->flags.p)};
+}
+
+// oz scales of A (row maxima for the ax passes, column maxima for the atx passes) and the
+// NaN/Inf scan of validate (rsvd.cpp:144): rows [r0, r0 + rows) of A, the first chunk
+// resetting the column maxima.
+int* oz_row_ef(const Ctx& c) { return static_cast<int*>(c.h->oz_ef.p); }
+int* oz_col_ef(const Ctx& c) { return oz_row_ef(c) + c.p.m; }
+int* oz_b_ef(const Ctx& c) { return oz_col_ef(c) + c.p.n; }
+
+void oz_scan(const Ctx& c, const double* A, long r0, long rows, bool first, bool check) {
+    rsvd_b200_handle* h = c.h;
+    h->launched(launch_oz_scan(A + r0 * c.p.lda, rows, c.p.n, c.p.lda, oz_row_ef(c) + r0,
+                               oz_col_ef(c), static_cast<int*>(h->oz_part.p),
+                               check ? c.flags + kFlagNonfinite : nullptr, h->stream, !first),
+                "oz_scan");
+}
+
+// Digits of the n-side operand Xt (NP x ldn; rows >= s zero) for the ax passes.
+void oz_digits_xt(const Ctx& c, const double* Xt) {
+    c.h->launched(launch_oz_digits_rows(Xt, c.p.ldn, c.p.NP, c.p.s, c.p.n,
+                                        static_cast<uint8_t*>(c.h->oz_bdig.p), oz_b_ef(c),
+                                        c.h->stream),
+                  "oz_digits_rows");
+}
+
+// Y (rows x NP) = A[r0 : r0 + rows] X with the digits of Xt already prepared.
+void oz_ax(const Ctx& c, const double* A, long r0, long rows, double* Y, const char* tag,
+           double flops) {
+    rsvd_b200_handle* h = c.h;
+    const Plan& p = c.p;
+    GemmOz g;
+    g.A = A + r0 * p.lda, g.M = rows, g.K = p.n, g.lda = p.lda;
+    g.a_ef = oz_row_ef(c) + r0;
+    g.bdig = static_cast<const uint8_t*>(h->oz_bdig.p), g.ldb = oz_ldb(p.n), g.b_ef = oz_b_ef(c);
+    g.NP = p.NP;
+    g.abort = h->abort_ptr;
+    const int splits = oz_splits(rows, p.NP, p.n, false);
+    h->kernel_begin(tag, flops);
+    if (splits == 1) {
+        g.out = Y + r0 * p.NP, g.ldo = p.NP;
+        h->launched(launch_gemm_oz(g, h->stream), "gemm_oz");
+        h->kernel_end(tag);
+        return;
+    }
+    const long slab = rows * p.NP;
+    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
+    g.out = h->part.d(), g.ldo = p.NP, g.splits = splits, g.split_stride = slab;
+    h->launched(launch_gemm_oz(g, h->stream), "gemm_oz(split)");
+    h->kernel_end(tag);
+    h->launched(launch_reduce_partials(h->part.d(), slab, splits, Y + r0 * p.NP, slab, h->stream),
+                "reduce_partials");
+}
+
+// Zt (NP x ldn) = (A^T W)^T, W (m x NP, columns >= s zero).
+void oz_atx(const Ctx& c, const double* A, const double* W, double* Zt, const char* tag,
+            double flops) {
+    rsvd_b200_handle* h = c.h;
+    const Plan& p = c.p;
+    int* colmax = oz_b_ef(c) + p.NP;
+    h->launched(launch_oz_digits_cols(W, p.NP, p.NP, p.s, p.m,
+                                      static_cast<uint8_t*>(h->oz_bdig.p), oz_b_ef(c), colmax,
+                                      h->stream),
+                "oz_digits_cols");
+    GemmOz g;
+    g.mn = true;
+    g.A = A, g.M = p.n, g.K = p.m, g.lda = p.lda;
+    g.a_ef = oz_col_ef(c);
+    g.bdig = static_cast<const uint8_t*>(h->oz_bdig.p), g.ldb = oz_ldb(p.m), g.b_ef = oz_b_ef(c);
+    g.NP = p.NP;
+    g.out_t = true;
+    g.abort = h->abort_ptr;
+    const int splits = oz_splits(p.n, p.NP, p.m, true);
+    h->kernel_begin(tag, flops);
+    if (splits == 1) {
+        g.out = Zt, g.ldo = p.ldn;
+        h->launched(launch_gemm_oz(g, h->stream), "gemm_oz");
+        h->kernel_end(tag);
+        return;
+    }
+    const long slab = (long)p.NP * p.ldn;
+    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
+    g.out = h->part.d(), g.ldo = p.ldn, g.splits = splits, g.split_stride = slab;
+    h->launched(launch_gemm_oz(g, h->stream), "gemm_oz(split)");
+    h->kernel_end(tag);
+    h->launched(launch_reduce_partials(h->part.d(), slab, splits, Zt, slab, h->stream),
+                "reduce_partials");
 }
 
 // FP32 path: the n-side operand of the next A-pass, Xt (NP x ldn, FP64) -> xtf (NPf x ldnf)
@@ -1110,6 +1242,26 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
         h->gram_ready = false;
         return;
     }
+    if (oz_on(p)) {
+        // scales + NaN/Inf scan and the sketch on the INT8 tensor cores; a chunked upload is
+        // scanned and sketched chunk by chunk as it lands (row scales are chunk-local). The
+        // Gram of Y0 is left to tall_qr (no fused epilogue); no upload-time A^T Y0 (its
+        // column scales need all of A).
+        oz_digits_xt(c, h->xt.d());
+        const bool chunked = h->up_active && A == h->a_copy.d();
+        const long rows_per = chunked ? h->up_chunk_rows : p.m;
+        const long chunks = chunked ? h->up_chunks : 1;
+        for (long ci = 0; ci < chunks; ++ci) {
+            const long r0 = ci * rows_per, rows = std::min(p.m - r0, rows_per);
+            if (chunked)
+                ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
+            oz_scan(c, A, r0, rows, ci == 0, check);
+            oz_ax(c, A, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
+        }
+        if (chunked) h->up_active = false;
+        h->gram_ready = false;
+        return;
+    }
     if (h->up_active && A == h->a_copy.d()) {
         h->gram_ready = gemm_ax_chunked(h, A, p.m, n, p.lda, h->xt.d(), p.ldn, NP, h->y.d(), NP,
                                         check ? c.flags + kFlagNonfinite : nullptr, "gemm_A",
@@ -1171,6 +1323,8 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
             h->launched(launch_reduce_partials(h->pre_part.d(), h->aty_slab, h->aty_splits,
                                                h->b.d(), h->aty_slab, h->stream),
                         "reduce_partials");
+        } else if (oz_on(p)) {
+            oz_atx(c, A, h->basis, h->b.d(), "gemm_A", 2.0 * p.m * p.n * p.s);  // (A^T Q1)^T
         } else {
             gemm_atx(h, A, p.m, p.n, p.lda, h->basis, p.NP, p.NP, h->b.d(), p.ldn, true,
                      "gemm_A", 2.0 * p.m * p.n * p.s, p.s);  // (A^T Q1)^T
@@ -1181,9 +1335,15 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
         const double* zt = apply_ct(c, h->b.d(), h->b2.d());  // (A^T W)^T, W = Q1 C
         wide_qr(c, zt, p.n, p.ldn, h->xt.d(), kRB, 1);  // Z = QR(A^T W).q, as Z^T
         h->mark("power_ax");
-        h->gram_ready = gemm_ax(h, A, p.m, p.n, p.lda, h->xt.d(), p.ldn, p.NP, h->y.d(), p.NP,
-                                nullptr, "gemm_A", 2.0 * p.m * p.n * p.s, c.slot(kG),
-                                p.s);  // Y = A Z
+        if (oz_on(p)) {
+            oz_digits_xt(c, h->xt.d());
+            oz_ax(c, A, 0, p.m, h->y.d(), "gemm_A", 2.0 * p.m * p.n * p.s);  // Y = A Z
+            h->gram_ready = false;
+        } else {
+            h->gram_ready = gemm_ax(h, A, p.m, p.n, p.lda, h->xt.d(), p.ldn, p.NP, h->y.d(),
+                                    p.NP, nullptr, "gemm_A", 2.0 * p.m * p.n * p.s, c.slot(kG),
+                                    p.s);  // Y = A Z
+        }
         h->mark("qr_tall");
         const bool last = round + 1 == q;
         tall_qr(c, h->y.d(), p.m, h->q.d(), last ? 2 : 1, materialize && last,
@@ -1206,6 +1366,8 @@ void project_and_solve_dev(const Ctx& c, const double* A, long k, double* u, lon
     h->mark("project_atx");
     if (p.f32)
         atx_a_f32(c);  // Q1^T A
+    else if (oz_on(p))
+        oz_atx(c, A, h->basis, h->b.d(), "gemm_A", 2.0 * m * n * s);  // Q1^T A
     else
         gemm_atx(h, A, m, n, p.lda, h->basis, NP, NP, h->b.d(), p.ldn, true, "gemm_A",
                  2.0 * m * n * s, s);  // Q1^T A
@@ -2505,6 +2667,55 @@ rsvd_b200_status rsvd_b200_debug_gemm_oz(rsvd_b200_handle* h, int mn, const doub
                         "reduce_partials");
         } else {
             h->launched(launch_gemm_oz(g, h->stream), "gemm_oz");
+        }
+        h->sync();
+    });
+}
+
+rsvd_b200_status rsvd_b200_debug_gemm_ozd(rsvd_b200_handle* h, int mn, const double* A, long M,
+                                         long K, long lda, const double* B, long ldb, int NP,
+                                         int cols, double* out, long ldo, int out_t, int splits) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        // A as stored: arows x acols (ax: M x K; atx: K x M), row-scaled digit planes
+        const long arows = mn ? K : M, acols = mn ? M : K;
+        const long ldd = oz_ldd(acols);
+        h->oz_adig.reserve((size_t)7 * arows * ldd);
+        h->oz_ef.reserve((size_t)(arows + 2 * NP + 8) * sizeof(int));
+        int* row_ef = static_cast<int*>(h->oz_ef.p);
+        int* b_ef = row_ef + arows;
+        int* scratch = b_ef + NP;
+        uint8_t* adig = static_cast<uint8_t*>(h->oz_adig.p);
+        h->launched(launch_oz_convert_rows(A, arows, acols, lda, adig, arows, row_ef, nullptr,
+                                           h->stream),
+                    "oz_convert_rows");
+        h->oz_bdig.reserve(oz_digits_bytes(NP, K));
+        uint8_t* dig = static_cast<uint8_t*>(h->oz_bdig.p);
+        if (mn)
+            h->launched(launch_oz_digits_cols(B, ldb, NP, cols, K, dig, b_ef, scratch, h->stream,
+                                              row_ef),
+                        "oz_digits_cols");
+        else
+            h->launched(launch_oz_digits_rows(B, ldb, NP, cols, K, dig, b_ef, h->stream),
+                        "oz_digits_rows");
+        GemmOzd g;
+        g.mn = mn != 0;
+        g.adig = adig, g.plane_rows = arows, g.ldd = ldd;
+        g.M = M, g.K = K;
+        g.a_ef = row_ef;
+        g.bdig = dig, g.ldb = oz_ldb(K), g.b_ef = b_ef, g.NP = NP;
+        g.out = out, g.ldo = ldo, g.out_t = out_t != 0;
+        if (splits > 1) {
+            const long slab = out_t ? (long)NP * ldo : M * ldo;
+            h->part.reserve((size_t)splits * slab * sizeof(double));
+            g.out = h->part.d();
+            g.splits = splits;
+            g.split_stride = slab;
+            h->launched(launch_gemm_ozd(g, h->stream), "gemm_ozd(split)");
+            h->launched(launch_reduce_partials(h->part.d(), slab, splits, out, slab, h->stream),
+                        "reduce_partials");
+        } else {
+            h->launched(launch_gemm_ozd(g, h->stream), "gemm_ozd");
         }
         h->sync();
     });

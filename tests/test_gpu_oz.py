@@ -12,14 +12,22 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def run(solver, mn, a, b, NP, cols, out_t=False, splits=1):
+HOOKS = ["rsvd_b200_debug_gemm_oz", "rsvd_b200_debug_gemm_ozd"]
+
+
+@pytest.fixture(params=HOOKS, ids=["in-kernel digits", "stored digits"])
+def hook(request):
+    return request.param
+
+
+def run(solver, mn, a, b, NP, cols, out_t=False, splits=1, hook=HOOKS[0]):
     import torch
     M = a.shape[1] if mn else a.shape[0]
     K = a.shape[0] if mn else a.shape[1]
     out = torch.full((NP, M) if out_t else (M, NP), float("nan"), dtype=torch.float64,
                      device="cuda")
     solver.wait_for_torch()
-    st = solver.lib.rsvd_b200_debug_gemm_oz(
+    st = getattr(solver.lib, hook)(
         solver.h, int(mn), C.c_void_p(a.data_ptr()), M, K, a.stride(0), C.c_void_p(b.data_ptr()),
         b.stride(0), NP, cols, C.c_void_p(out.data_ptr()), out.stride(0), int(out_t), splits)
     assert st == 0, solver.lib.rsvd_b200_last_error().decode()
@@ -54,7 +62,7 @@ def lowrank_decay(rng, m, n, decay):
 @pytest.mark.parametrize("M,K,NP,cols", [(600, 4096, 80, 74), (333, 1000, 16, 16),
                                          (700, 777, 48, 42), (128, 64, 64, 64),
                                          (2000, 96, 128, 120), (257, 4100, 96, 90)])
-def test_ax_oz(solver, M, K, NP, cols):
+def test_ax_oz(solver, hook, M, K, NP, cols):
     import torch
     rng = np.random.default_rng(M + K + NP)
     a = lowrank_decay(rng, M, K, 60.0)
@@ -65,7 +73,7 @@ def test_ax_oz(solver, M, K, NP, cols):
     bt = np.zeros((NP, K + 4))
     bt[:cols, :K] = rng.standard_normal((cols, K))
     got = run(solver, False, torch.from_numpy(ap).cuda()[:, :K], torch.from_numpy(bt).cuda()[:, :K],
-              NP, cols)
+              NP, cols, hook=hook)
     check(got, a, bt[:, :K].T, f"ax {M}x{K} NP={NP}")
     assert np.all(got[:, cols:] == 0)
 
@@ -74,7 +82,7 @@ def test_ax_oz(solver, M, K, NP, cols):
                                                 (3000, 272, 48, 42, 9), (1000, 200, 16, 10, 1),
                                                 (20000, 256, 128, 128, 3)])
 @pytest.mark.parametrize("out_t", [False, True])
-def test_atx_oz(solver, K, M, NP, cols, splits, out_t):
+def test_atx_oz(solver, hook, K, M, NP, cols, splits, out_t):
     import torch
     rng = np.random.default_rng(K + M + NP)
     a = lowrank_decay(rng, K, M, 40.0)
@@ -82,17 +90,18 @@ def test_atx_oz(solver, K, M, NP, cols, splits, out_t):
     w = np.zeros((K, NP))
     w[:, :cols] = rng.standard_normal((K, cols))
     got = run(solver, True, torch.from_numpy(a).cuda(), torch.from_numpy(w).cuda(), NP, cols,
-              out_t, splits)
+              out_t, splits, hook=hook)
     check(got, a.T, w, f"atx {K}x{M} NP={NP} splits={splits}")
 
 
-def test_oz_zero_and_tiny(solver):
+def test_oz_zero_and_tiny(solver, hook):
     import torch
     rng = np.random.default_rng(3)
     a = rng.standard_normal((300, 512))
     a[7] = 0.0                      # an all-zero row
     a[11, :] = 1e-300 * rng.standard_normal(512)
     bt = rng.standard_normal((16, 512))
-    got = run(solver, False, torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda(), 16, 16)
+    got = run(solver, False, torch.from_numpy(a).cuda(), torch.from_numpy(bt).cuda(), 16, 16,
+              hook=hook)
     assert np.all(got[7] == 0)
     check(got, a, bt.T, "zero/tiny rows")
