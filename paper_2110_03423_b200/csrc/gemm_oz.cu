@@ -95,11 +95,86 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a_tmem, uint64_t 
         "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
 }
 
+// shared -> TMEM copy of a 128-row x 32-byte tile described by a matrix descriptor (the A
+// operand of the following TS MMAs; executes in order with them)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc_) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc_) : "memory");
+}
+
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c,
                                          uint32_t d) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
                  "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
+}
+
+// 3-D TMA load broadcast to the same smem offset of every CTA in `mask` (complete_tx on the
+// barrier at the same offset in each)
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, int c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+        "h"(mask)
+        : "memory");
+}
+
+// 1-D bulk copy global -> shared (bytes a multiple of 16), complete_tx on `bar`; the multicast
+// form lands at the same offset of every CTA in `mask`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_mc_oz(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                  int c_inner, int c_outer, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c_inner), "r"(c_outer),
+        "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t caddr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -227,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const int* __restrict__ a_ef, const int* __restrict__ b_ef, int M, int NP,
                    int nch, int nfirst, double* __restrict__ out, long ldo, long split_stride,
                    int k_tiles, int k_tiles_per_split, const int* __restrict__ abort_flag,
-                   int diag) {
+                   int diag, int mc) {
     if (abort_flag && *(const volatile int*)abort_flag) return;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = align_smem_1024(smem_raw);
@@ -243,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ncl = mc ? nch : 1;             // cluster size (multicast of the FP64 tile)
     const int ch = blockIdx.x % nch;          // column chunk
     const int tile = blockIdx.x / nch;
     const int m0 = tile * BM;
@@ -257,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kFStages; ++s) {
             mbar_init(&full_a[s], 1);
-            mbar_init(&empty_a[s], kConvWarps);
+            mbar_init(&empty_a[s], kConvWarps * ncl);  // every CTA's converters of the cluster
         }
         for (int s = 0; s < kBStages; ++s) {
             mbar_init(&full_b[s], 1);
@@ -277,12 +353,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fence_before();
-    __syncthreads();
+    if (ncl > 1)
+        cluster_sync_all();  // every CTA's barriers exist before a multicast targets them
+    else
+        __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint16_t cmask = (uint16_t)((1u << ncl) - 1u);
+    const int crank = ncl > 1 ? ch : 0;
 
     if (warp == 0) {
         // ------------------------------------------------------------ A producer
+        // the column-chunk CTAs of a tile form a cluster: rank ch loads the FP64 boxes
+        // b = ch, ch + nch, ... and multicasts them, so the tile crosses L2 -> SM once; a stage
+        // is refilled once the converters of every CTA hold it in registers
         if (lane == 0) {
             tma_prefetch_desc(&mapA);
             for (int it = 0; it < n_iter; ++it) {
@@ -291,13 +375,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 char* st = ringA + s * kAF64;
                 const int k = (kt0 + it) * BK;
                 mbar_arrive_expect_tx(&full_a[s], kAF64);
-                if constexpr (!MN) {
-                    tma_load_2d(st, &mapA, &full_a[s], k, m0);
-                    tma_load_2d(st + kAF64 / 2, &mapA, &full_a[s], k + 16, m0);
-                } else {
-#pragma unroll
-                    for (int bx = 0; bx < BM / 16; ++bx)
-                        tma_load_2d(st + bx * (kAF64 / 8), &mapA, &full_a[s], m0 + 16 * bx, k);
+                constexpr int nbox = MN ? BM / 16 : 2;
+                constexpr uint32_t bbytes = kAF64 / nbox;
+                for (int bx = crank; bx < nbox; bx += ncl) {
+                    const int x = MN ? m0 + 16 * bx : k + 16 * bx, y = MN ? k : m0;
+                    if (ncl > 1)
+                        tma_load_2d_mc_oz(st + bx * bbytes, &mapA, &full_a[s], x, y, cmask);
+                    else
+                        tma_load_2d(st + bx * bbytes, &mapA, &full_a[s], x, y);
                 }
             }
         }
@@ -389,7 +474,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     v[e] = *reinterpret_cast<const double*>(box + swz128(h * 16 + e, r & 15));
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_a[sa]);  // the FP64 tile is in registers
+            if (lane == 0) {  // the FP64 tile is in registers: release it in every CTA
+                if (ncl > 1)
+                    for (int rk = 0; rk < ncl; ++rk)
+                        mbar_arrive_remote(mapa_rank(smem_u32(&empty_a[sa]), (uint32_t)rk));
+                else
+                    mbar_arrive(&empty_a[sa]);
+            }
             uint32_t pw[kDigits][4];
             if (diag & 4) {
 #pragma unroll
@@ -458,7 +549,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     fence_before();
-    __syncthreads();
+    if (ncl > 1)
+        cluster_sync_all();  // no multicast or remote arrive is still in flight into a peer
+    else
+        __syncthreads();
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -527,10 +621,23 @@ __global__ void oz_reduce_max_kernel(const int* __restrict__ part, int parts, lo
 
 // Digit planes dig[i][c][k] (i < 7, c < NP, k < ldb bytes) of the rows of Xt (NP x K, ldx;
 // rows >= cols zero), each row at its own scale b_ef[c]. One CTA per row.
+// Byte offset of digit plane i, row c, byte k of the small operand: the plain layout
+// [i][c][k] (nfirst = 0: the in-kernel-digit GEMM's TMA boxes) or the stored-digit GEMM's
+// tiled one (nfirst = its column-chunk width): per k-tile kt, per chunk, the 7 planes of the
+// chunk's N rows x 32 B back to back in the SW32 K-major layout, so that one bulk copy moves a
+// stage.
+__device__ __forceinline__ long b_offset(int i, int c, long k, int NP, long ldb, int nfirst) {
+    if (nfirst == 0) return ((long)i * NP + c) * ldb + k;
+    const int ch = c / nfirst, cl = c - ch * nfirst, n = min(nfirst, NP - ch * nfirst);
+    const long kt = k >> 5;
+    return kt * kDigits * NP * BK + (long)kDigits * BK * ch * nfirst + (long)i * n * BK +
+           sw32((uint32_t)cl, (uint32_t)((k >> 4) & 1)) + (k & 15);
+}
+
 __global__ void __launch_bounds__(256) oz_digits_rows_kernel(const double* __restrict__ Xt, long ldx,
                                                             int NP, int cols, long K,
                                                             uint8_t* __restrict__ dig, long ldb,
-                                                            int* __restrict__ b_ef) {
+                                                            int* __restrict__ b_ef, int nfirst) {
     const int c = blockIdx.x;
     __shared__ int red[8];
     const double* row = Xt + (long)c * ldx;
@@ -556,7 +663,7 @@ __global__ void __launch_bounds__(256) oz_digits_rows_kernel(const double* __res
         planes4(w, pl);
 #pragma unroll
         for (int i = 0; i < kDigits; ++i)
-            *reinterpret_cast<uint32_t*>(dig + ((long)i * NP + c) * ldb + k4) = pl[i];
+            *reinterpret_cast<uint32_t*>(dig + b_offset(i, c, k4, NP, ldb, nfirst)) = pl[i];
     }
 }
 
@@ -595,7 +702,8 @@ __global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __res
                                                             uint8_t* __restrict__ dig, long ldb,
                                                             const int* __restrict__ colmax,
                                                             int* __restrict__ b_ef,
-                                                            const int* __restrict__ row_ef) {
+                                                            const int* __restrict__ row_ef,
+                                                            int nfirst) {
     extern __shared__ double slab[];  // 64 x (NP + 1)
     const long k0 = (long)blockIdx.x * 64;
     const int ld = NP + 1;
@@ -619,26 +727,35 @@ __global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __res
         planes4(w, pl);
 #pragma unroll
         for (int i = 0; i < kDigits; ++i)
-            *reinterpret_cast<uint32_t*>(dig + ((long)i * NP + c) * ldb + k0 + kq) = pl[i];
+            *reinterpret_cast<uint32_t*>(dig + b_offset(i, c, k0 + kq, NP, ldb, nfirst)) = pl[i];
     }
 }
 
 // ======================================================= stored digits (convert once per solve)
-// A (rows x cols, lda) -> 7 row-scaled digit planes dig[i][r][c] (plane stride rows * ldd
-// bytes, ldd a multiple of 16) and row_ef[r], plus the NaN/Inf flag: one row per CTA-iteration,
-// thread t holds elements [16 t, 16 t + 16) of the row in registers (cols <= 16 * blockDim), so
-// A is read once; the digits go out as 16-byte stores per plane.
+// A (rows x cols, lda) -> 7 row-scaled digit planes, written twice, pre-tiled and pre-swizzled
+// for the two pass shapes so that a pass stage is one contiguous 28 KB bulk copy:
+//   ax  tiles: row block rb (128 rows) x k-tile kt (32 columns): [plane][128 rows x 32 B] in
+//              the SW32 K-major layout, block (rb * KT + kt), KT = ceil(cols / 32);
+//   atx tiles: k block kb (32 rows) x column block jb (128 columns): [plane][32 rows x 128 B]
+//              in the SW128 MN-major layout, block (kb * JB + jb), JB = ceil(cols / 128).
+// Also row_ef[r] and the NaN/Inf flag. Rows [r0, r1) (absolute); rows >= `rows` (up to the
+// next 128) and columns >= cols (up to the next 128) are written as zero digits. Thread t holds
+// elements [16 t, 16 t + 16) of a row in registers, so A is read once.
 __global__ void __launch_bounds__(1024) oz_convert_rows_kernel(
-    const double* __restrict__ A, long rows, long cols, long lda, uint8_t* __restrict__ dig,
-    long ldd, long plane, int* __restrict__ row_ef, int* __restrict__ flag) {
+    const double* __restrict__ A, long r0, long r1, long rows, long cols, long lda,
+    uint8_t* __restrict__ dig_ax, uint8_t* __restrict__ dig_atx, int* __restrict__ row_ef,
+    int* __restrict__ flag) {
     __shared__ uint32_t red[32];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (blockDim.x + 31) >> 5;
+    const long KT = (cols + 31) / 32, JB = (cols + 127) / 128;
+    // whole warps; each layout is written up to its own block edge (KT 32 <= JB 128 columns)
+    const bool w_ax = 16L * t < KT * 32, w_at = 16L * t < JB * 128;
     bool bad = false;
-    for (long r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (long r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
         const double* row = A + r * lda;
         const long c0 = 16L * t;
         double v[16];
-        if (c0 + 16 <= cols) {
+        if (r < rows && c0 + 16 <= cols) {
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {
                 const double2 x = __ldcs(reinterpret_cast<const double2*>(row + c0 + e));
@@ -647,7 +764,7 @@ __global__ void __launch_bounds__(1024) oz_convert_rows_kernel(
             }
         } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = c0 + e < cols ? row[c0 + e] : 0.0;
+            for (int e = 0; e < 16; ++e) v[e] = (r < rows && c0 + e < cols) ? row[c0 + e] : 0.0;
         }
         uint32_t m = 0;
 #pragma unroll
@@ -661,25 +778,31 @@ __global__ void __launch_bounds__(1024) oz_convert_rows_kernel(
         __syncthreads();
         const int ef = (int)(mm >> 20);
         bad |= ef == 0x7ff;
-        if (t == 0) row_ef[r] = ef;
-        if (c0 < ldd) {
-            double f1, f2;
-            fixed_scale(ef, f1, f2);
-            uint32_t pw[kDigits][4];
+        if (t == 0 && r < rows) row_ef[r] = ef;
+        double f1, f2;
+        fixed_scale(ef, f1, f2);
+        uint32_t pw[kDigits][4];
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd) {
-                uint64_t wd[4];
+        for (int qd = 0; qd < 4; ++qd) {
+            uint64_t wd[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) wd[e] = digits_scaled(v[4 * qd + e], f1, f2);
-                uint32_t pl[kDigits];
-                planes4(wd, pl);
+            for (int e = 0; e < 4; ++e) wd[e] = digits_scaled(v[4 * qd + e], f1, f2);
+            uint32_t pl[kDigits];
+            planes4(wd, pl);
 #pragma unroll
-                for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
-            }
+            for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
+        }
+        const long rb = r >> 7, kb = r >> 5;
+        const uint32_t rl = (uint32_t)(r & 127), kl = (uint32_t)(r & 31);
+        uint8_t* ax = dig_ax + ((rb * KT + (c0 >> 5)) * kDigits) * 4096 + sw32(rl, (c0 >> 4) & 1);
+        const uint32_t chunk = (uint32_t)((c0 >> 4) & 7);
+        uint8_t* at = dig_atx + ((kb * JB + (c0 >> 7)) * kDigits) * 4096 + kl * 128 +
+                      ((chunk ^ (kl & 7)) << 4);
 #pragma unroll
-            for (int i = 0; i < kDigits; ++i)
-                *reinterpret_cast<uint4*>(dig + i * plane + r * ldd + c0) =
-                    make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+        for (int i = 0; i < kDigits; ++i) {
+            const uint4 q = make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+            if (w_ax) __stcs(reinterpret_cast<uint4*>(ax + i * 4096), q);
+            if (w_at) __stcs(reinterpret_cast<uint4*>(at + i * 4096), q);
         }
     }
     if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
@@ -711,7 +834,7 @@ __device__ __forceinline__ uint64_t sdesc_mn128(uint32_t saddr) {
 
 template <bool MN, bool OUT_T>
 __global__ void __launch_bounds__(kDsThreads, 1)
-    gemm_ozd_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ BMaps bmaps,
+    gemm_ozd_kernel(const uint8_t* __restrict__ adig, long a_inner, const uint8_t* __restrict__ bdig,
                     const int* __restrict__ a_ef, const int* __restrict__ b_ef, int M, int NP,
                     int nch, int nfirst, double* __restrict__ out, long ldo,
                     long split_stride, int k_tiles, int k_tiles_per_split,
@@ -725,6 +848,9 @@ __global__ void __launch_bounds__(kDsThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the nch column-chunk CTAs of an M tile form a cluster (rank = chunk): each loads
+    // planes i = rank, rank + nch, ... of A's digits and multicasts them to all, so A's digits
+    // cross L2 -> SM once per tile; a stage is refilled once every CTA's MMAs are done with it
     const int ch = blockIdx.x % nch;
     const int tile = blockIdx.x / nch;
     const int m0 = tile * BM;
@@ -734,11 +860,12 @@ __global__ void __launch_bounds__(kDsThreads, 1)
     const int kt0 = blockIdx.y * k_tiles_per_split;
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
     const int n_iter = max(0, kt1 - kt0);
+    const uint16_t cmask = (uint16_t)((1u << nch) - 1u);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kDsStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], nch);
         }
         mbar_init(accum, 1);
         fence_barrier_init();
@@ -750,33 +877,42 @@ __global__ void __launch_bounds__(kDsThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fence_before();
-    __syncthreads();
+    if (nch > 1)
+        cluster_sync_all();  // every CTA's barriers exist before a multicast targets them
+    else
+        __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            tma_prefetch_desc(&mapA);
-            const CUtensorMap* mb = &bmaps.m[ch];
-            tma_prefetch_desc(mb);
+            // A: the (M tile, k-tile) block of 7 pre-swizzled 4 KB digit tiles, contiguous
+            // (ax: block tile * a_inner + kt; atx: block kt * a_inner + tile); rank ch copies
+            // its 1 / nch of it and multicasts. B: the chunk's 7 planes of the k-tile, contiguous.
+            constexpr uint32_t kABlock = kDigits * kDsADig;
+            const uint32_t part = ((kABlock / nch) + 15) & ~15u;  // 16-byte multiples
+            // A's blocks come from HBM: prefetch them into L2 kPf stages ahead of the copies
+            constexpr int kPf = 8;
+            auto ablk = [&](long kt) {
+                return adig + (MN ? kt * a_inner + tile : (long)tile * a_inner + kt) * kABlock;
+            };
+            const uint32_t off = (uint32_t)ch * part;
+            const uint32_t len = ch == nch - 1 ? kABlock - off : part;
+            for (int it = 0; it < min(kPf, n_iter); ++it) bulk_prefetch_l2(ablk(kt0 + it) + off, len);
             for (int it = 0; it < n_iter; ++it) {
                 const int s = it % kDsStages;
-                if (it >= kDsStages) mbar_wait_sleep(&empty[s], ((it / kDsStages) - 1) & 1);
+                if (it >= kDsStages) mbar_wait(&empty[s], ((it / kDsStages) - 1) & 1);
                 char* st = smem + s * kDsStage;
-                const int k = (kt0 + it) * BK;
-                mbar_arrive_expect_tx(&full[s], kDigits * (kDsADig + pb));
-#pragma unroll
-                for (int i = 0; i < kDigits; ++i) {
-                    // 3-D map {byte column, row, plane}: rows / columns past the matrix read 0
-                    if constexpr (!MN)
-                        tma_load_3d(st + i * kDsADig, &mapA, &full[s], k, m0, i);
-                    else
-                        tma_load_3d(st + i * kDsADig, &mapA, &full[s], m0, k, i);
-                }
-                char* sb = st + kDigits * kDsADig;
-#pragma unroll
-                for (int i = 0; i < kDigits; ++i)
-                    tma_load_2d(sb + i * pb, mb, &full[s], k, i * NP + c0);
+                const long kt = kt0 + it;
+                if (it + kPf < n_iter) bulk_prefetch_l2(ablk(kt + kPf) + off, len);
+                mbar_arrive_expect_tx(&full[s], kABlock + kDigits * pb);
+                const uint8_t* src = ablk(kt);
+                if (nch > 1)
+                    bulk_load_mc(st + off, src + off, len, &full[s], cmask);
+                else
+                    bulk_load(st, src, kABlock, &full[s]);
+                bulk_load(st + kABlock, bdig + kt * kDigits * NP * BK + (long)kDigits * BK * c0,
+                          kDigits * pb, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -796,14 +932,32 @@ __global__ void __launch_bounds__(kDsThreads, 1)
             mbar_wait(&full[s], (it / kDsStages) & 1);
             fence_after();
             if (elect_one()) {
+                if constexpr (!MN) {
+                    // K-major A digits: copy the 7 tiles into a TMEM buffer (3 after the
+                    // accumulators, in-order with the MMAs) and run the MMAs with A from TMEM,
+                    // which the tensor core reads faster than shared memory at these widths
+                    const uint32_t tb = tmem + (uint32_t)(kGroups * N) + (uint32_t)(it % 3) * 56u;
 #pragma unroll
-                for (int j = 0; j < kNM; ++j) {
-                    const uint32_t a = st + (uint32_t)mi[j] * kDsADig;
-                    const uint64_t ad = MN ? sdesc_mn128(a) : sdesc(a);
-                    mma_i8(tmem + (uint32_t)(mdc[j] * N), ad, bd + (((uint64_t)mp0[j] * pb) >> 4),
-                           idv[j], (it > 0 || j > 1) ? 1u : 0u);
+                    for (int i = 0; i < kDigits; ++i)
+                        tmem_cp_128x256b(tb + 8u * i, sdesc(st + (uint32_t)i * kDsADig));
+#pragma unroll
+                    for (int j = 0; j < kNM; ++j)
+                        mma_i8_ts(tmem + (uint32_t)(mdc[j] * N), tb + 8u * mi[j],
+                                  bd + (((uint64_t)mp0[j] * pb) >> 4), idv[j],
+                                  (it > 0 || j > 1) ? 1u : 0u);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kNM; ++j) {
+                        const uint32_t a = st + (uint32_t)mi[j] * kDsADig;
+                        mma_i8(tmem + (uint32_t)(mdc[j] * N), sdesc_mn128(a),
+                               bd + (((uint64_t)mp0[j] * pb) >> 4), idv[j],
+                               (it > 0 || j > 1) ? 1u : 0u);
+                    }
                 }
-                commit(&empty[s]);
+                if (nch > 1)
+                    commit_mc(&empty[s], cmask);
+                else
+                    commit(&empty[s]);
             }
             __syncwarp();
         }
@@ -847,7 +1001,10 @@ __global__ void __launch_bounds__(kDsThreads, 1)
         }
     }
     fence_before();
-    __syncthreads();
+    if (nch > 1)
+        cluster_sync_all();  // no multicast commit or TMA is still in flight into a peer
+    else
+        __syncthreads();
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -942,6 +1099,9 @@ cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
     // RSVD_B200_OZ_DIAG (profiling only; results are wrong): 1 = MMA skips the B-ready wait,
     // 2 = converters skip the A-ready wait, 4 = converters skip the digit arithmetic
     static const int diag = getenv("RSVD_B200_OZ_DIAG") ? atoi(getenv("RSVD_B200_OZ_DIAG")) : 0;
+    // RSVD_B200_OZ_MC=1: the column-chunk CTAs of a tile share the FP64 tile by cluster
+    // multicast (measured 2x slower than independent loads served by L2: 5.1 vs 2.6 ms at C2)
+    static const int mc = getenv("RSVD_B200_OZ_MC") ? atoi(getenv("RSVD_B200_OZ_MC")) : 0;
     const unsigned gx = (unsigned)(((p.M + oz::BM - 1) / oz::BM) * nch);
     dim3 grid(gx, (unsigned)splits);
 #define OZ_LAUNCH(MN, OT)                                                                        \
@@ -950,9 +1110,21 @@ cudaError_t launch_gemm_oz(const GemmOz& p, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                              (int)smem);                                         \
         if (e != cudaSuccess) return e;                                                          \
-        kern<<<grid, oz::kThreads, smem, st>>>(mA, bm, p.a_ef, p.b_ef, (int)p.M, p.NP, nch,     \
-                                               nfirst, p.out, p.ldo, p.split_stride, k_tiles,    \
-                                               per, p.abort, diag);                              \
+        cudaLaunchConfig_t cfg = {};                                                             \
+        cfg.gridDim = grid;                                                                      \
+        cfg.blockDim = dim3(oz::kThreads);                                                       \
+        cfg.dynamicSmemBytes = smem;                                                             \
+        cfg.stream = st;                                                                         \
+        cudaLaunchAttribute attr[1];                                                             \
+        attr[0].id = cudaLaunchAttributeClusterDimension;                                        \
+        attr[0].val.clusterDim.x = mc ? (unsigned)nch : 1u;                                      \
+        attr[0].val.clusterDim.y = 1;                                                            \
+        attr[0].val.clusterDim.z = 1;                                                            \
+        cfg.attrs = attr;                                                                        \
+        cfg.numAttrs = 1;                                                                        \
+        e = cudaLaunchKernelEx(&cfg, kern, mA, bm, p.a_ef, p.b_ef, (int)p.M, p.NP, nch, nfirst,  \
+                               p.out, p.ldo, p.split_stride, k_tiles, per, p.abort, diag, mc);   \
+        if (e != cudaSuccess) return e;                                                          \
     } while (0)
     if (!p.mn) {
         if (p.out_t) return cudaErrorInvalidValue;
@@ -987,26 +1159,6 @@ cudaError_t launch_gemm_ozd(const GemmOzd& p, cudaStream_t st) {
     int nch, nfirst;
     oz_chunks(p.NP, &nch, &nfirst);
     if (nch > oz::kMaxChunks) return cudaErrorInvalidValue;
-    CUtensorMap mA;
-    // the digit planes: plane_rows x ldd bytes each (A's rows x columns)
-    const long pbytes = p.plane_rows * p.ldd;
-    if (!p.mn) {  // A operand rows = output rows (M, a row range of the planes), K = columns
-        if (oz_map3(&mA, p.adig, oz::kDigits, pbytes, p.M, p.K, p.ldd, oz::BK, oz::BM,
-                    CU_TENSOR_MAP_SWIZZLE_32B))
-            return cudaErrorInvalidValue;
-    } else {  // A operand = A^T: M = A's columns, K = A's rows
-        if (oz_map3(&mA, p.adig, oz::kDigits, pbytes, p.K, p.M, p.ldd, oz::BM, oz::BK,
-                    CU_TENSOR_MAP_SWIZZLE_128B))
-            return cudaErrorInvalidValue;
-    }
-    oz::BMaps bm;
-    for (int c = 0; c < nch; ++c) {
-        const int n = std::min(nfirst, p.NP - c * nfirst);
-        if (oz_map(&bm.m[c], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.bdig, (long)oz::kDigits * p.NP,
-                   p.ldb, p.ldb, oz::BK, n, CU_TENSOR_MAP_SWIZZLE_32B))
-            return cudaErrorInvalidValue;
-    }
-    for (int c = nch; c < oz::kMaxChunks; ++c) bm.m[c] = bm.m[0];
     const int k_tiles = (int)((p.K + oz::BK - 1) / oz::BK);
     const int splits = p.splits < 1 ? 1 : p.splits;
     const int per = (k_tiles + splits - 1) / splits;
@@ -1020,9 +1172,22 @@ cudaError_t launch_gemm_ozd(const GemmOzd& p, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                              (int)smem);                                         \
         if (e != cudaSuccess) return e;                                                          \
-        kern<<<grid, oz::kDsThreads, smem, st>>>(mA, bm, p.a_ef, p.b_ef, (int)p.M, p.NP, nch,   \
-                                                 nfirst, p.out, p.ldo, p.split_stride, k_tiles,  \
-                                                 per, p.abort);                                  \
+        cudaLaunchConfig_t cfg = {};                                                             \
+        cfg.gridDim = grid;                                                                      \
+        cfg.blockDim = dim3(oz::kDsThreads);                                                     \
+        cfg.dynamicSmemBytes = smem;                                                             \
+        cfg.stream = st;                                                                         \
+        cudaLaunchAttribute attr[1];                                                             \
+        attr[0].id = cudaLaunchAttributeClusterDimension;                                        \
+        attr[0].val.clusterDim.x = (unsigned)nch;                                                \
+        attr[0].val.clusterDim.y = 1;                                                            \
+        attr[0].val.clusterDim.z = 1;                                                            \
+        cfg.attrs = attr;                                                                        \
+        cfg.numAttrs = 1;                                                                        \
+        e = cudaLaunchKernelEx(&cfg, kern, p.adig, p.a_inner, p.bdig, p.a_ef, p.b_ef, (int)p.M,  \
+                               p.NP, nch, nfirst, p.out, p.ldo, p.split_stride, k_tiles, per,    \
+                               p.abort);                                                         \
+        if (e != cudaSuccess) return e;                                                          \
     } while (0)
     if (!p.mn) {
         if (p.out_t) return cudaErrorInvalidValue;
@@ -1055,30 +1220,38 @@ size_t oz_scan_part_ints(long rows, long cols) {
     return (size_t)(cb * rows + rb * cols);
 }
 
-long oz_ldd(long cols) { return (cols + 15) & ~15L; }
+size_t oz_tiled_bytes(long rows, long cols) {
+    const size_t blk = (size_t)oz::kDigits * oz::kDsADig;
+    const size_t ax = (size_t)((rows + 127) / 128) * ((cols + 31) / 32) * blk;
+    const size_t at = (size_t)((rows + 31) / 32) * ((cols + 127) / 128) * blk;
+    return std::max(ax, at);
+}
 
-cudaError_t launch_oz_convert_rows(const double* A, long rows, long cols, long lda, uint8_t* dig,
-                                   long plane_rows, int* row_ef, int* flag, cudaStream_t st) {
+cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
+                                   long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
+                                   int* flag, cudaStream_t st) {
     if (cols > 16L * 1024 || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1))
         return cudaErrorInvalidValue;
-    const int threads = std::max(32, (int)(((cols + 15) / 16 + 31) / 32 * 32));
-    const long ldd = oz_ldd(cols);
-    // the planes of a row chunk (rows at dig + row offset) keep the full matrix's plane stride
-    unsigned grid = (unsigned)std::min<long>(rows, 148L * (2048 / threads));
-    oz::oz_convert_rows_kernel<<<grid, threads, 0, st>>>(A, rows, cols, lda, dig, ldd,
-                                                        plane_rows * ldd, row_ef, flag);
+    if (r1 >= rows) r1 = (rows + 127) / 128 * 128;  // the last chunk also zeroes the pad rows
+    else if ((r1 & 127) || (r0 & 127)) return cudaErrorInvalidValue;
+    // 16 columns each over whole 128-column blocks, rounded up to whole warps
+    const int threads = (int)(((cols + 127) / 128 * 8 + 31) / 32 * 32);
+    const unsigned grid = (unsigned)std::min<long>(r1 - r0, 148L * std::max(1, 2048 / threads));
+    oz::oz_convert_rows_kernel<<<grid, threads, 0, st>>>(A, r0, r1, rows, cols, lda, dig_ax,
+                                                        dig_atx, row_ef, flag);
     return cudaGetLastError();
 }
 
 cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, long K,
-                                  uint8_t* dig, int* b_ef, cudaStream_t st) {
-    oz::oz_digits_rows_kernel<<<NP, 256, 0, st>>>(Xt, ldx, NP, cols, K, dig, oz_ldb(K), b_ef);
+                                  uint8_t* dig, int* b_ef, cudaStream_t st, int nfirst) {
+    oz::oz_digits_rows_kernel<<<NP, 256, 0, st>>>(Xt, ldx, NP, cols, K, dig, oz_ldb(K), b_ef,
+                                                  nfirst);
     return cudaGetLastError();
 }
 
 cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, long K,
                                   uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st,
-                                  const int* row_ef) {
+                                  const int* row_ef, int nfirst) {
     cudaError_t e = cudaMemsetAsync(colmax, 0, NP * sizeof(int), st);
     if (e != cudaSuccess) return e;
     oz::oz_colmax_kernel<<<oz_grid(K * NP, 2048), 256, 0, st>>>(W, ldw, NP, cols, K, colmax,
@@ -1089,7 +1262,7 @@ cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, l
     if (e != cudaSuccess) return e;
     const long ldb = oz_ldb(K);
     oz::oz_digits_cols_kernel<<<(unsigned)((ldb + 63) / 64), 256, smem, st>>>(
-        W, ldw, NP, cols, K, dig, ldb, colmax, b_ef, row_ef);
+        W, ldw, NP, cols, K, dig, ldb, colmax, b_ef, row_ef, nfirst);
     return cudaGetLastError();
 }
 

@@ -144,34 +144,37 @@ cudaError_t launch_oz_scan(const double* A, long rows, long cols, long lda, int*
                            bool col_acc = false);
 size_t oz_scan_part_ints(long rows, long cols);
 // Digit planes of the rows of Xt (NP x K, ldx; rows >= cols zero), one scale per row.
+// nfirst = 0: plain layout [plane][row][k] (gemm_oz); > 0: the stored-digit GEMM's tiled layout
+// for column chunks of nfirst (oz_chunks).
 cudaError_t launch_oz_digits_rows(const double* Xt, long ldx, int NP, int cols, long K,
-                                  uint8_t* dig, int* b_ef, cudaStream_t st);
+                                  uint8_t* dig, int* b_ef, cudaStream_t st, int nfirst = 0);
 // Digit planes of the columns of W (K x NP, ldw; columns >= cols zero), one scale per column;
 // colmax: NP ints of scratch. row_ef (optional): digitise W' = diag(2^(row_ef[k] - 1076)) W,
-// which carries A's row scales into the stored-digit atx GEMM.
+// which carries A's row scales into the stored-digit atx GEMM. nfirst as above.
 cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, long K,
                                   uint8_t* dig, int* b_ef, int* colmax, cudaStream_t st,
-                                  const int* row_ef = nullptr);
+                                  const int* row_ef = nullptr, int nfirst = 0);
 
-// Stored digits: A (rows x cols <= 16384, lda) -> 7 row-scaled digit planes (plane stride
-// plane_rows * oz_ldd(cols) bytes, rows at dig; a row chunk passes dig offset by its first row),
-// row_ef[rows], NaN/Inf flag. One read of A.
-long oz_ldd(long cols);
-cudaError_t launch_oz_convert_rows(const double* A, long rows, long cols, long lda, uint8_t* dig,
-                                   long plane_rows, int* row_ef, int* flag, cudaStream_t st);
+// Stored digits: rows [r0, r1) of A (rows x cols <= 16384, lda) -> A's 7 row-scaled digit
+// planes, written pre-tiled for both stored-digit GEMM shapes (dig_ax, dig_atx: each
+// oz_tiled_bytes(rows, cols)), row_ef, NaN/Inf flag. One read of A; r0, r1 multiples of 128
+// except r1 = rows (the last chunk, which also zeroes the padding).
+size_t oz_tiled_bytes(long rows, long cols);
+cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
+                                   long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
+                                   int* flag, cudaStream_t st);
 // INT8 GEMM from stored digits (gemm_oz.cu gemm_ozd_kernel):
-//   mn = false: out (M x NP) = A X, adig = A's planes from its first row (plane stride
-//               plane_rows x ldd bytes, M rows used), a_ef[M].
-//   mn = true:  out = A^T W' with A (K x M) as stored (plane_rows = K), W' digits from
-//               launch_oz_digits_cols(..., row_ef); a_ef unused. out_t / splits as GemmOz.
+//   mn = false: out (M x NP) = A X, adig = dig_ax (a_inner = ceil(K / 32)), a_ef[M] (row_ef).
+//   mn = true:  out = A^T W' with A (K x M) as stored, adig = dig_atx (a_inner = ceil(M / 128)),
+//               W' digits from launch_oz_digits_cols(..., row_ef, nfirst); a_ef unused.
+// B digits (bdig) in the tiled layout for oz_chunks(NP). out_t / splits as GemmOz.
 struct GemmOzd {
     bool mn = false;
     const uint8_t* adig = nullptr;
-    long plane_rows = 0, ldd = 0;
+    long a_inner = 0;
     long M = 0, K = 0;
     const int* a_ef = nullptr;
     const uint8_t* bdig = nullptr;
-    long ldb = 0;
     const int* b_ef = nullptr;
     int NP = 0;
     double* out = nullptr;

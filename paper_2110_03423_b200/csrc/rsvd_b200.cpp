@@ -2679,31 +2679,35 @@ rsvd_b200_status rsvd_b200_debug_gemm_ozd(rsvd_b200_handle* h, int mn, const dou
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         // A as stored: arows x acols (ax: M x K; atx: K x M), row-scaled digit planes
         const long arows = mn ? K : M, acols = mn ? M : K;
-        const long ldd = oz_ldd(acols);
-        h->oz_adig.reserve((size_t)7 * arows * ldd);
+        const size_t tb = oz_tiled_bytes(arows, acols);
+        h->oz_adig.reserve(2 * tb);
         h->oz_ef.reserve((size_t)(arows + 2 * NP + 8) * sizeof(int));
         int* row_ef = static_cast<int*>(h->oz_ef.p);
         int* b_ef = row_ef + arows;
         int* scratch = b_ef + NP;
-        uint8_t* adig = static_cast<uint8_t*>(h->oz_adig.p);
-        h->launched(launch_oz_convert_rows(A, arows, acols, lda, adig, arows, row_ef, nullptr,
-                                           h->stream),
+        uint8_t* dax = static_cast<uint8_t*>(h->oz_adig.p);
+        uint8_t* datx = dax + tb;
+        h->launched(launch_oz_convert_rows(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
+                                           nullptr, h->stream),
                     "oz_convert_rows");
+        int nch, nf;
+        oz_chunks(NP, &nch, &nf);
         h->oz_bdig.reserve(oz_digits_bytes(NP, K));
         uint8_t* dig = static_cast<uint8_t*>(h->oz_bdig.p);
         if (mn)
             h->launched(launch_oz_digits_cols(B, ldb, NP, cols, K, dig, b_ef, scratch, h->stream,
-                                              row_ef),
+                                              row_ef, nf),
                         "oz_digits_cols");
         else
-            h->launched(launch_oz_digits_rows(B, ldb, NP, cols, K, dig, b_ef, h->stream),
+            h->launched(launch_oz_digits_rows(B, ldb, NP, cols, K, dig, b_ef, h->stream, nf),
                         "oz_digits_rows");
         GemmOzd g;
         g.mn = mn != 0;
-        g.adig = adig, g.plane_rows = arows, g.ldd = ldd;
+        g.adig = mn ? datx : dax;
+        g.a_inner = mn ? (acols + 127) / 128 : (acols + 31) / 32;
         g.M = M, g.K = K;
         g.a_ef = row_ef;
-        g.bdig = dig, g.ldb = oz_ldb(K), g.b_ef = b_ef, g.NP = NP;
+        g.bdig = dig, g.b_ef = b_ef, g.NP = NP;
         g.out = out, g.ldo = ldo, g.out_t = out_t != 0;
         if (splits > 1) {
             const long slab = out_t ? (long)NP * ldo : M * ldo;

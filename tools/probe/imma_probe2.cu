@@ -83,6 +83,10 @@ __global__ void probe(int N, int iters, int every, long long* out) {
 #pragma unroll
                     for (int j = 0; j < 9; ++j)
                         mma_ts(tmem + (j % 3) * N, ad + (j % 7) * 8, bd, id3, 1);
+                } else if constexpr (P == 5) {  // the Ozaki pattern, A from smem (SW32)
+#pragma unroll
+                    for (int j = 0; j < 9; ++j)
+                        mma_ss(tmem + mdc[j] * N, sdesc(A + (it & 1) * 28672 / 2 + mi[j] * 4096), bd + ((mp0[j] * pb) >> 4), idv[j], 1);
                 } else if constexpr (P == 3) {  // 8 x N=256 SS (peak reference)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) mma_ss(tmem, sdesc(A), bd, id256, 1);
@@ -127,7 +131,9 @@ void run(const char* name, int N, int every, double ops_per_round, long long* d)
 int main() {
     long long* d;
     cudaMalloc(&d, 148 * sizeof(long long));
-    for (int every : {1, 2, 4}) {
+    for (int every : {1}) {
+        run<5>("oz pattern (9 SS MMAs, N=48)", 48, every, 2.0 * 128 * 28 * 48 * 32, d);
+        run<5>("oz pattern (9 SS MMAs, N=32)", 32, every, 2.0 * 128 * 28 * 32 * 32, d);
         run<0>("oz pattern (9 TS MMAs, N=48)", 48, every, 2.0 * 128 * 28 * 48 * 32, d);
         run<0>("oz pattern (9 TS MMAs, N=32)", 32, every, 2.0 * 128 * 28 * 32 * 32, d);
         run<1>("28 single-plane TS MMAs N=48", 48, every, 2.0 * 128 * 28 * 48 * 32, d);

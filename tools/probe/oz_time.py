@@ -10,7 +10,8 @@ import torch
 sys.path.insert(0, ".")
 import paper_2110_03423_b200 as P  # noqa: E402
 
-m, n, NP, cols, splits = (int(x) for x in (sys.argv[1:6] if len(sys.argv) > 5 else
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+m, n, NP, cols, splits = (int(x) for x in (args[:5] if len(args) > 4 else
                                             (202599, 4096, 80, 74, 23)))
 s = P.Solver(0)
 g = torch.Generator(device="cuda").manual_seed(1)
@@ -22,14 +23,15 @@ w[:, :cols] = torch.randn(m, cols, dtype=torch.float64, device="cuda", generator
 y = torch.empty(m, NP, dtype=torch.float64, device="cuda")
 zt = torch.empty(NP, n, dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
+hook = getattr(s.lib, "rsvd_b200_debug_gemm_ozd" if "--stored" in sys.argv else "rsvd_b200_debug_gemm_oz")
 for rep in range(2):
     t0 = time.perf_counter()
-    st = s.lib.rsvd_b200_debug_gemm_oz(s.h, 0, C.c_void_p(a.data_ptr()), m, n, n,
+    st = hook(s.h, 0, C.c_void_p(a.data_ptr()), m, n, n,
                                        C.c_void_p(xt.data_ptr()), n, NP, cols,
                                        C.c_void_p(y.data_ptr()), NP, 0, 1)
     assert st == 0, s.lib.rsvd_b200_last_error().decode()
     t1 = time.perf_counter()
-    st = s.lib.rsvd_b200_debug_gemm_oz(s.h, 1, C.c_void_p(a.data_ptr()), n, m, n,
+    st = hook(s.h, 1, C.c_void_p(a.data_ptr()), n, m, n,
                                        C.c_void_p(w.data_ptr()), NP, NP, cols,
                                        C.c_void_p(zt.data_ptr()), n, 1, splits)
     assert st == 0, s.lib.rsvd_b200_last_error().decode()
