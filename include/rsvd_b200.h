@@ -305,6 +305,9 @@ void rsvd_b200_set_graphs(rsvd_b200_handle* h, int on);
 /* Measured FP64 tensor-core peak of the handle's GPU (TFLOP/s): an issue-bound
  * mma.sync m16n8k16 f64 loop on every SM — the roofline denominator of the GEMMs. */
 rsvd_b200_status rsvd_b200_dmma_peak(rsvd_b200_handle* h, double* tflops);
+/* Measured INT8 tensor-core peak (TOPS; tcgen05 kind::i8 M 128 N 256 K 32 issue loop on every
+ * SM): the roofline denominator of the INT8-emulated FP64 passes over A. */
+rsvd_b200_status rsvd_b200_imma_peak(rsvd_b200_handle* h, double* tops);
 
 /* Test hook for the FP32-input 3xTF32 tcgen05 GEMM (device pointers; see csrc/kernels.h
  * GemmTf32): mn = 0: out = A (M x K) * Bt^T, Bt NP x K; mn = 1: out = A^T W, A K x M,

@@ -25,7 +25,7 @@ EXPORTS = [
     "rsvd_b200_set_robust", "rsvd_b200_set_graphs", "rsvd_b200_nccl_unique_id", "rsvd_b200_comm_init_nccl",
     "rsvd_b200_local_group_create", "rsvd_b200_local_group_destroy", "rsvd_b200_comm_init_local",
     "rsvd_b200_comm_info", "rsvd_b200_comm_free", "rsvd_b200_randomized_ksvd_sharded",
-    "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak",
+    "rsvd_b200_randomized_ksvd_sharded_device", "rsvd_b200_dmma_peak", "rsvd_b200_imma_peak",
     "rsvd_b200_debug_gemm_tf32", "rsvd_b200_debug_cholesky", "rsvd_b200_debug_jacobi",
     "rsvd_b200_debug_gemm_oz", "rsvd_b200_debug_gemm_ozd",
     "rsvd_b200_randomized_ksvd_f32",
@@ -114,6 +114,7 @@ def load() -> C.CDLL:
         "rsvd_b200_set_graphs": (None, [_vp, C.c_int]),
         "rsvd_b200_nccl_unique_id": (C.c_int, [C.c_char_p]),
         "rsvd_b200_dmma_peak": (C.c_int, [_vp, _dp]),
+        "rsvd_b200_imma_peak": (C.c_int, [_vp, _dp]),
         "rsvd_b200_randomized_ksvd_f32": (C.c_int, [_vp, _fp, _sz, _sz, cfgp, _dp, _dp, _dp,
                                                     C.POINTER(_sz)]),
         "rsvd_b200_randomized_ksvd_f32_device": (C.c_int, [_vp, _fp, _sz, _sz, _sz, cfgp, _dp,

@@ -1011,7 +1011,81 @@ __global__ void __launch_bounds__(kDsThreads, 1)
     }
 }
 
+// INT8 tensor-core issue-rate probe: every CTA issues back-to-back M = 128, N = 256, K = 32
+// kind::i8 MMAs from zeroed shared memory (one commit per 8), the roofline denominator of the
+// emulated FP64 passes (MEASURED_PEAKS.json has no INT8 entry).
+__global__ void __launch_bounds__(128, 1) imma_peak_kernel(int iters, int* sink) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* sm = align_smem_1024(smem_raw);
+    __shared__ uint64_t bar[4];
+    __shared__ uint32_t tslot;
+    for (int i = threadIdx.x; i < 12 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+        fence_barrier_init();
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tslot)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tslot;
+    if (threadIdx.x < 32) {
+        const uint64_t a = sdesc(smem_u32(sm)), b = sdesc(smem_u32(sm + 4096));
+        const uint32_t id = idesc(256);
+        // commits waited two rounds later, so the tensor pipe never drains
+        for (int it = 0; it < iters; ++it) {
+            if (elect_one()) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mma_i8(tmem, a, b, id, 1u);
+                commit(&bar[it & 3]);
+            }
+            __syncwarp();
+            if (it >= 2) mbar_wait(&bar[(it - 2) & 3], ((it - 2) >> 2) & 1);
+        }
+        for (int it = iters - 2; it < iters; ++it) mbar_wait(&bar[it & 3], (it >> 2) & 1);
+    }
+    fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    }
+    if (threadIdx.x == 0 && iters < 0) *sink = 1;
+}
+
 }  // namespace oz
+
+cudaError_t measure_imma_peak(cudaStream_t st, double* tops) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4096, smem = 16 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(oz::imma_peak_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    oz::imma_peak_kernel<<<148, 128, smem, st>>>(iters, nullptr);  // warm-up (clocks up)
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0, st);
+        oz::imma_peak_kernel<<<148, 128, smem, st>>>(iters, nullptr);
+        cudaEventRecord(e1, st);
+        e = cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tops = 2.0 * 128 * 256 * 32 * 8.0 * iters * 148 / (best * 1e-3) / 1e12;
+    return e;
+}
 
 // ======================================================================== host side
 namespace {

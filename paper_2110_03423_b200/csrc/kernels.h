@@ -197,6 +197,8 @@ cudaError_t launch_reduce_partials_f32(const float* part, long stride, int split
 
 // FP64 tensor-core (DMMA m16n8k16) issue-rate probe on the whole GPU, TFLOP/s.
 cudaError_t measure_dmma_peak(cudaStream_t st, double* tflops);
+// INT8 tensor-core (tcgen05 kind::i8, M 128 N 256 K 32) issue-rate probe, TOPS.
+cudaError_t measure_imma_peak(cudaStream_t st, double* tops);
 
 // A GaussianSampler state (rng.hpp:21-42): words drawn so far (`counter`) and the cached
 // sine half of an unfinished pair, which the next normal() returns first. A fresh

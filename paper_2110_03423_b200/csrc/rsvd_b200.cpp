@@ -226,6 +226,7 @@ struct rsvd_b200_handle {
     // arrays (A rows, A columns, B columns, scratch) and the scan partials
     DevBuf oz_bdig, oz_ef, oz_part;
     DevBuf oz_adig;  // A's row-scaled digit planes (stored-digit passes)
+    long oz_passes = 0;  // passes over A of the last solve that ran on the INT8 tensor cores
     int* flags_host = nullptr;
     StreamPos omega_pos;  // sampler state the next sketch's Omega continues (default: fresh)
     std::vector<double> omega_host;  // validation mode (n x s row-major)
@@ -619,12 +620,8 @@ void gemm_tf32(rsvd_b200_handle* h, GemmTf32 g, const char* tag = nullptr, doubl
 // DMMA passes save, and the FP64 DMMA kernels keep products such as sketch(I) = Omega
 // bit-exact). RSVD_B200_GEMM=dmma / =oz forces either path (tests, comparisons).
 bool oz_on(const Plan& p) {
-    static const int mode = [] {
-        const char* e = getenv("RSVD_B200_GEMM");
-        if (e && std::string(e) == "dmma") return 0;
-        if (e && std::string(e) == "oz") return 2;
-        return 1;
-    }();
+    const char* e = getenv("RSVD_B200_GEMM");  // read per solve: tests switch it
+    const int mode = (e && std::string(e) == "dmma") ? 0 : (e && std::string(e) == "oz") ? 2 : 1;
     if (mode == 0 || p.f32 || p.NP < 16 || p.NP > 256) return false;
     return mode == 2 || (double)p.m * (double)p.n >= (double)(1L << 26);
 }
@@ -1029,6 +1026,7 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     if (NP <= 96 && !p.f32) h->gpart.reserve((size_t)ax_tiles(p.m, NP) * NP * NP * sizeof(double));
     h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(p.s)) * sizeof(double));
     h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
+    h->oz_passes = 0;
     if (oz_on(p)) {
         h->oz_ef.reserve((size_t)(p.m + p.n + 2 * NP + 8) * sizeof(int));
         h->oz_bdig.reserve(std::max(oz_digits_bytes(NP, p.n), oz_digits_bytes(NP, p.m)));
@@ -1080,6 +1078,7 @@ void oz_ax(const Ctx& c, const double* A, long r0, long rows, double* Y, const c
     g.NP = p.NP;
     g.abort = h->abort_ptr;
     const int splits = oz_splits(rows, p.NP, p.n, false);
+    if (r0 == 0) h->oz_passes += 1;
     h->kernel_begin(tag, flops);
     if (splits == 1) {
         g.out = Y + r0 * p.NP, g.ldo = p.NP;
@@ -1116,6 +1115,7 @@ void oz_atx(const Ctx& c, const double* A, const double* W, double* Zt, const ch
     g.out_t = true;
     g.abort = h->abort_ptr;
     const int splits = oz_splits(p.n, p.NP, p.m, true);
+    h->oz_passes += 1;
     h->kernel_begin(tag, flops);
     if (splits == 1) {
         g.out = Zt, g.ldo = p.ldn;
@@ -2548,6 +2548,7 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
     if (!strcmp(key, "launches")) return h->launches;
     if (!strcmp(key, "graph_launches")) return h->graph_replays;
     if (!strcmp(key, "upload_aty_splits")) return h->upload_aty;
+    if (!strcmp(key, "oz_passes")) return h->oz_passes;
     return -1;
 }
 
@@ -2850,6 +2851,13 @@ rsvd_b200_status rsvd_b200_dmma_peak(rsvd_b200_handle* h, double* tflops) {
     return guarded([&] {
         ck(cudaSetDevice(h->device), "cudaSetDevice");
         ck(measure_dmma_peak(h->stream, tflops), "DMMA peak probe");
+    });
+}
+
+rsvd_b200_status rsvd_b200_imma_peak(rsvd_b200_handle* h, double* tops) {
+    return guarded([&] {
+        ck(cudaSetDevice(h->device), "cudaSetDevice");
+        ck(measure_imma_peak(h->stream, tops), "INT8 tensor peak probe");
     });
 }
 

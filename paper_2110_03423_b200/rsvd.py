@@ -187,6 +187,12 @@ class Solver:
         _check(self.lib, self.lib.rsvd_b200_dmma_peak(self.h, C.byref(t)))
         return t.value
 
+    def imma_peak_tops(self) -> float:
+        """Measured INT8 tensor-core peak of this GPU (rsvd_b200_imma_peak)."""
+        t = C.c_double(0)
+        _check(self.lib, self.lib.rsvd_b200_imma_peak(self.h, C.byref(t)))
+        return t.value
+
     def last_launch_count(self) -> int:
         return int(self.lib.rsvd_b200_last_launch_count(self.h))
 
