@@ -114,7 +114,10 @@ cudaError_t launch_transpose_f32(const float* in, long rows, long cols, long ldi
 //   mn = false (ax):  out (M x NP, ldo) = A (M x K, lda) X,  a_ef[M] per row of A.
 //   mn = true  (atx): out = A^T W, A (K x M, lda); out_t: Z^T (NP x M, ldo) else Z (M x NP);
 //                     a_ef[M] per column of A; split-K slabs at out + s * split_stride.
-// K per split <= kOzMaxKTiles * 32 (int32 accumulator headroom).
+// K per split <= kOzMaxKTiles * 32 (int32 accumulator headroom of a digit group: 7 products of
+// balanced digits, |.| <= 2^14 each, per k). Measured: unsigned two's-complement A digits would
+// save the bias add and XOR (2.6 -> 2.3 ms per C2 pass) but make the dropped low-order products
+// biased (3x the Frobenius error), so the digits stay balanced.
 constexpr int kOzMaxKTiles = 512;
 struct GemmOz {
     bool mn = false;
