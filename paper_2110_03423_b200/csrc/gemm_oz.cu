@@ -679,17 +679,18 @@ __device__ __forceinline__ double row_scale(const int* row_ef, long k) {
 __global__ void __launch_bounds__(256) oz_colmax_kernel(const double* __restrict__ W, long ldw, int NP,
                                                        int cols, long K, int* __restrict__ colmax,
                                                        const int* __restrict__ row_ef) {
+    // thread -> one column of a group of 256 / NP consecutive rows per step (coalesced rows),
+    // running max in a register, one shared atomic per thread at the end
     __shared__ int sm[288];
     for (int i = threadIdx.x; i < NP; i += 256) sm[i] = 0;
     __syncthreads();
-    const long total = K * (long)NP;
-    for (long e = blockIdx.x * 256L + threadIdx.x; e < total; e += (long)gridDim.x * 256) {
-        const long k = e / NP;
-        const int c = (int)(e - k * NP);
-        if (c < cols)
-            atomicMax(&sm[c], (int)((uint32_t)__double2hiint(W[k * ldw + c] * row_scale(row_ef, k)) &
-                                   0x7ff00000u));
-    }
+    const int rpb = max(1, 256 / NP);  // rows per step
+    const int c = threadIdx.x % NP, rl = threadIdx.x / NP;
+    uint32_t m = 0;
+    if (rl < rpb && c < cols)
+        for (long k = (long)blockIdx.x * rpb + rl; k < K; k += (long)gridDim.x * rpb)
+            m = max(m, (uint32_t)__double2hiint(W[k * ldw + c] * row_scale(row_ef, k)) & 0x7ff00000u);
+    if (m) atomicMax(&sm[c], (int)m);
     __syncthreads();
     for (int i = threadIdx.x; i < NP; i += 256)
         if (sm[i]) atomicMax(&colmax[i], sm[i]);
@@ -1328,8 +1329,8 @@ cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, l
                                   const int* row_ef, int nfirst) {
     cudaError_t e = cudaMemsetAsync(colmax, 0, NP * sizeof(int), st);
     if (e != cudaSuccess) return e;
-    oz::oz_colmax_kernel<<<oz_grid(K * NP, 2048), 256, 0, st>>>(W, ldw, NP, cols, K, colmax,
-                                                               row_ef);
+    oz::oz_colmax_kernel<<<(unsigned)std::min<long>(148L * 8, (K + 3) / 4), 256, 0, st>>>(
+        W, ldw, NP, cols, K, colmax, row_ef);
     const size_t smem = 64 * (NP + 1) * sizeof(double);
     e = cudaFuncSetAttribute(oz::oz_digits_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

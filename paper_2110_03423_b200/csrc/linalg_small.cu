@@ -411,13 +411,12 @@ __host__ __device__ inline int jacobi_ld(int s) {
     return 2 * (size_t)s * l16 * sizeof(double) <= 200 * 1024 ? l16 : (s + 1) & ~1;
 }
 
-template <int NQ>
-__global__ void __launch_bounds__(512) jacobi_kernel(
+template <int NQ, int G>
+__global__ void __launch_bounds__(G == 16 ? 1024 : 512) jacobi_kernel(
     const double* __restrict__ Rin, int s, int NP, double* __restrict__ sigma_out,
     double* __restrict__ Uout, double* __restrict__ Wout, int* __restrict__ status,
     const int* __restrict__ abort_flag) {
     extern __shared__ __align__(16) double sh[];
-    constexpr int G = kJacobiGroup;
     const int ls = jacobi_ld(s);
     double* Rc = sh;            // s columns, stride ls (rows s..ls-1 zero)
     double* J = sh + s * ls;    // s columns, stride ls
@@ -465,15 +464,20 @@ __global__ void __launch_bounds__(512) jacobi_kernel(
     while (sweeps < kMaxSweeps) {
         ++sweeps;
         int rotated = 0;
+        // rr_index(slot, round) = slot == 0 ? 0 : 1 + (slot - 1 + round) % (sp - 1), stepped
+        // incrementally (no integer division in the round loop)
+        int ri = k == 0 ? -1 : k - 1, rj = sp - 2 - k;
         for (int round = 0; round < sp - 1; ++round) {
             int i = 0, j = 0;
             bool live = k < sp / 2;
             if (live) {
-                i = rr_index(k, round, sp);
-                j = rr_index(sp - 1 - k, round, sp);
+                i = ri < 0 ? 0 : 1 + ri;
+                j = 1 + rj;
                 if (i > j) { const int t = i; i = j; j = t; }
                 live = j < s;
             }
+            if (ri >= 0 && ++ri == sp - 1) ri = 0;
+            if (++rj == sp - 1) rj = 0;
             double2* ci = reinterpret_cast<double2*>(Rc + i * ls) + gl;
             double2* cj = reinterpret_cast<double2*>(Rc + j * ls) + gl;
             double2 xi[NQ], xj[NQ];
@@ -564,18 +568,31 @@ size_t jacobi_global_scratch_doubles(int s) {
     return block_jacobi_scratch_doubles(s);  // the block Jacobi's scratch
 }
 
+template <int NQ, int G>
+static cudaError_t launch_jacobi_g(const double* R, int s, int NP, double* sigma, double* U,
+                                   double* W, int* status, const int* abort_flag,
+                                   cudaStream_t st) {
+    const size_t smem = 2 * (size_t)s * jacobi_ld(s) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(jacobi_kernel<NQ, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int pairs = ((s + 1) & ~1) / 2;
+    const int threads = std::max(128, (pairs * G + 31) & ~31);
+    jacobi_kernel<NQ, G><<<1, threads, smem, st>>>(R, s, NP, sigma, U, W, status, abort_flag);
+    return cudaGetLastError();
+}
+
+// 16 lanes per column pair when the pairs fit 1024 threads (s <= 128): half the per-lane rows
+// (shorter dependent chains per round) at one more shuffle level; 8 lanes otherwise
 template <int NQ>
 static cudaError_t launch_jacobi_nq(const double* R, int s, int NP, double* sigma, double* U,
                                     double* W, int* status, const int* abort_flag,
                                     cudaStream_t st) {
-    const size_t smem = 2 * (size_t)s * jacobi_ld(s) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(jacobi_kernel<NQ>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static const bool g8 = getenv("RSVD_B200_JACOBI_G8") != nullptr;
     const int pairs = ((s + 1) & ~1) / 2;
-    const int threads = std::max(128, (pairs * kJacobiGroup + 31) & ~31);
-    jacobi_kernel<NQ><<<1, threads, smem, st>>>(R, s, NP, sigma, U, W, status, abort_flag);
-    return cudaGetLastError();
+    if (!g8 && pairs * 16 <= 1024)
+        return launch_jacobi_g<(NQ + 1) / 2, 16>(R, s, NP, sigma, U, W, status, abort_flag, st);
+    return launch_jacobi_g<NQ, kJacobiGroup>(R, s, NP, sigma, U, W, status, abort_flag, st);
 }
 
 cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, double* U, double* W,
