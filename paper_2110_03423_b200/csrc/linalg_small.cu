@@ -395,6 +395,26 @@ cudaError_t launch_small_matmul(const double* X, const double* Y, int s, int NP,
 // shuffles, and the CTA has just the warps the round needs. A sweep without any rotation
 // ends the iteration (svd.cpp:196-199); more than 30 sweeps is a convergence failure
 // (svd.hpp:20). The columns and the rotation accumulator J live in shared memory.
+#ifdef JAC_TRACE  // tools/probe/small_probe.cu: per-phase clock64 stamps of thread 0 of CTA 0
+__device__ long long g_jac_trace[1024];
+__device__ int g_jac_ntrace;
+#define JAC_DECL int jac_n = 0
+#define JAC_MARK(tag)                                                          \
+    do {                                                                       \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && jac_n < 512) {              \
+            g_jac_trace[2 * jac_n] = (tag);                                    \
+            g_jac_trace[2 * jac_n + 1] = clock64();                            \
+            g_jac_ntrace = ++jac_n;                                            \
+        }                                                                      \
+    } while (0)
+#else
+#define JAC_DECL \
+    do {         \
+    } while (0)
+#define JAC_MARK(tag) \
+    do {              \
+    } while (0)
+#endif
 constexpr int kJacobiGroup = 8;
 constexpr int kJacobiMaxNQ = 7;  // row pairs per lane: s <= 8 * 2 * 7 = 112
 // widths beyond (columns + J over 200 KB of shared memory) run the multi-CTA block Jacobi
@@ -562,6 +582,287 @@ __global__ void __launch_bounds__(G == 16 ? 1024 : 512) jacobi_kernel(
     if (tid == 0) status[0] = sweeps;
 }
 
+// ------------------------------------------------- one-sided Jacobi over a thread-block cluster
+// The single-CTA rounds above are bound by the SM's shared-memory pipe (every round reads and
+// writes all of R and J: ~1.8k cycles of LDS/STS/SHFL per round at s = 74). Here the rows are
+// split over a cluster: CTA r holds rows [RPC r, RPC r + RPC) of every column of R and J
+// (RPC = 8 NQ), so each SM moves 1/NC of the bytes. A pair's group (4 lanes, NQ double2 each)
+// reduces its rows' partial (|r_i|^2, |r_j|^2, r_i.r_j), lane 0 stores the partial into every
+// CTA's shared memory, one cluster barrier, and every CTA adds the NC partials in rank order:
+// all CTAs see bit-identical sums, so they take identical skip / rotation decisions (and agree
+// on convergence) without further exchange. Same ordering, rotation formula and thresholds as
+// jacobi_kernel (svd.cpp:35-36,60-90,196-199).
+constexpr int kJcLanes = 4;
+
+// 16 bytes into a cluster peer's shared memory, counted by the peer's mbarrier (complete_tx)
+__device__ __forceinline__ void st_async_f64x2(uint32_t caddr, double a, double b, uint32_t cbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 ::"r"(caddr), "d"(a), "d"(b), "r"(cbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(1024) jacobi_cluster_kernel(
+    const double* __restrict__ Rin, int s, int NP, double* __restrict__ sigma_out,
+    double* __restrict__ Uout, double* __restrict__ Wout, int* __restrict__ status,
+    const int* __restrict__ abort_flag) {
+    constexpr int RPC = 8 * NQ;  // rows per CTA (column stride in shared memory)
+    extern __shared__ __align__(16) double sh[];
+    uint32_t nc, rank;
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(nc));
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int sp = (s + 1) & ~1, pairs = sp / 2;
+    double* Rc = sh;                    // s columns x RPC rows
+    double* J = Rc + (size_t)s * RPC;   // s columns x RPC rows
+    double* part = J + (size_t)s * RPC; // [2][nc][pairs][4]: per-round partials of every CTA
+    __shared__ double red_sh[2];
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (abort_flag && *abort_flag) {  // every CTA reads the same flag: all leave together
+        if (tid == 0 && rank == 0) status[0] = 0;
+        return;
+    }
+    if (warp == 0) {  // scale and skip threshold from the whole matrix, identically in every CTA
+        double mx = 0.0, f2 = 0.0;
+        for (int e = lane; e < s * s; e += 32) {
+            const double v = Rin[(e / s) * NP + e % s];
+            mx = fmax(mx, fabs(v));
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int ex = 0;
+        frexp(mx, &ex);
+        const double scale = mx > 0.0 ? ldexp(1.0, -ex) : 1.0;
+        for (int e = lane; e < s * s; e += 32) {
+            const double v = Rin[(e / s) * NP + e % s] * scale;
+            f2 = fma(v, v, f2);
+        }
+        f2 = warp_sum(f2);
+        if (lane == 0) {
+            red_sh[0] = scale;
+            red_sh[1] = 1e-14 * f2;
+        }
+    }
+    __syncthreads();
+    const double scale = red_sh[0], athr = red_sh[1];
+    const int r0 = (int)rank * RPC;
+    for (int e = tid; e < s * RPC; e += nth) {
+        const int c = e / RPC, rr = e - c * RPC, r = r0 + rr;
+        Rc[e] = r < s ? Rin[(size_t)r * NP + c] * scale : 0.0;
+        J[e] = (r == c) ? 1.0 : 0.0;
+    }
+    const uint32_t part_u32 = smem_u32(part);
+    // full[slot]: round n's partials (slot n & 1) from every CTA have landed here (st.async
+    // complete_tx; thread 0 arms the expected bytes once per round)
+    __shared__ __align__(8) uint64_t full[2];
+    const uint32_t round_bytes = (uint32_t)(nc * pairs * 4 * sizeof(double));
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_barrier_init();
+    }
+    cluster_sync_all();  // every CTA of the cluster is running, barriers initialised
+
+    const int k = tid / kJcLanes, gl = tid % kJcLanes;
+    const bool slot_ok = k < pairs;
+    const int qx = k & 1;  // odd slots walk their double2s in swapped pairs: a quarter-warp's two
+                           // groups touch opposite halves of the banks
+    int sweeps = 0, nround = 0;
+    bool converged = false;
+    JAC_DECL;
+    while (sweeps < kMaxSweeps) {
+        ++sweeps;
+        int rotated = 0;
+        int ri = k == 0 ? -1 : k - 1, rj = sp - 2 - k;
+        for (int round = 0; round < sp - 1; ++round, ++nround) {
+            int i = 0, j = 0;
+            bool live = slot_ok;
+            if (live) {
+                i = ri < 0 ? 0 : 1 + ri;
+                j = 1 + rj;
+                if (i > j) { const int t = i; i = j; j = t; }
+                live = j < s;
+            }
+            if (ri >= 0 && ++ri == sp - 1) ri = 0;
+            if (++rj == sp - 1) rj = 0;
+            JAC_MARK(0);
+            double2* ci = reinterpret_cast<double2*>(Rc + i * RPC);
+            double2* cj = reinterpret_cast<double2*>(Rc + j * RPC);
+            double2 xi[NQ], xj[NQ];
+            double aii = 0.0, ajj = 0.0, d = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int e = gl + kJcLanes * (q ^ qx);
+                xi[q] = live ? ci[e] : make_double2(0.0, 0.0);
+                xj[q] = live ? cj[e] : make_double2(0.0, 0.0);
+                aii = fma(xi[q].x, xi[q].x, fma(xi[q].y, xi[q].y, aii));
+                ajj = fma(xj[q].x, xj[q].x, fma(xj[q].y, xj[q].y, ajj));
+                d = fma(xi[q].x, xj[q].x, fma(xi[q].y, xj[q].y, d));
+            }
+            JAC_MARK(1);
+#pragma unroll
+            for (int o = kJcLanes / 2; o > 0; o >>= 1) {
+                aii += __shfl_xor_sync(0xffffffffu, aii, o);
+                ajj += __shfl_xor_sync(0xffffffffu, ajj, o);
+                d += __shfl_xor_sync(0xffffffffu, d, o);
+            }
+            JAC_MARK(2);
+            const int slot = nround & 1;
+            if (tid == 0) mbar_arrive_expect_tx(&full[slot], round_bytes);
+            if (slot_ok && gl < (int)nc) {  // lane gl (and gl + 4, ...) feeds CTA gl's copy
+                const uint32_t off =
+                    (uint32_t)((((slot * nc + rank) * pairs + k) * 4) * sizeof(double));
+                const uint32_t bar = smem_u32(&full[slot]);
+                for (uint32_t dst = gl; dst < nc; dst += kJcLanes) {
+                    const uint32_t ca = mapa_rank(part_u32 + off, dst);
+                    const uint32_t cb = mapa_rank(bar, dst);
+                    st_async_f64x2(ca, aii, ajj, cb);
+                    st_async_f64x2(ca + 16, d, 0.0, cb);
+                }
+            }
+            mbar_wait_cluster(&full[slot], (uint32_t)(nround >> 1) & 1u);
+            JAC_MARK(3);
+            if (live) {
+                aii = ajj = d = 0.0;
+                for (uint32_t rk = 0; rk < nc; ++rk) {  // rank order: identical in every CTA
+                    const double2* pp =
+                        reinterpret_cast<const double2*>(part + ((slot * nc + rk) * pairs + k) * 4);
+                    const double2 a = pp[0], b = pp[1];
+                    aii += a.x;
+                    ajj += a.y;
+                    d += b.x;
+                }
+            }
+            if (live && !(fabs(d) <= athr && d * d <= (1e-13 * 1e-13) * aii * ajj)) {
+                const double diff = ajj - aii;
+                const double sgn = ((diff >= 0.0) == (d >= 0.0)) || diff == 0.0 ? 1.0 : -1.0;
+                const double t =
+                    sgn * 2.0 * fabs(d) / (fabs(diff) + sqrt(fma(diff, diff, 4.0 * d * d)));
+                const double c = rsqrt(fma(t, t, 1.0));
+                const double sn = c * t;
+                double2* wi = reinterpret_cast<double2*>(J + i * RPC);
+                double2* wj = reinterpret_cast<double2*>(J + j * RPC);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int e = gl + kJcLanes * (q ^ qx);
+                    const double2 yi = wi[e], yj = wj[e];
+                    ci[e] = make_double2(c * xi[q].x - sn * xj[q].x, c * xi[q].y - sn * xj[q].y);
+                    cj[e] = make_double2(sn * xi[q].x + c * xj[q].x, sn * xi[q].y + c * xj[q].y);
+                    wi[e] = make_double2(c * yi.x - sn * yj.x, c * yi.y - sn * yj.y);
+                    wj[e] = make_double2(sn * yi.x + c * yj.x, sn * yi.y + c * yj.y);
+                }
+                rotated = 1;
+            }
+            JAC_MARK(4);
+            // the next round's groups read columns this round rotated; a peer's round-(n+2)
+            // partials reuse slot n & 1 only after it has seen ours of round n + 1, which we
+            // send after these reads
+            __syncthreads();
+            JAC_MARK(5);
+        }
+        if (!__syncthreads_or(rotated)) {  // identical in every CTA (identical decisions)
+            converged = true;
+            break;
+        }
+    }
+    if (!converged) {
+        if (tid == 0 && rank == 0) status[0] = -1;
+        cluster_sync_all();
+        return;
+    }
+    // singular values = column norms (partials of every CTA, added in rank order); stable
+    // descending order (svd.cpp:210-219)
+    double* npart = part;  // [nc][s], reusing the partial buffers: once every CTA has read
+    cluster_sync_all();    // the last round's partials
+    for (int c = tid; c < s; c += nth) {
+        double acc = 0.0;
+        for (int rr = 0; rr < RPC; ++rr) acc = fma(Rc[c * RPC + rr], Rc[c * RPC + rr], acc);
+        for (uint32_t dst = 0; dst < nc; ++dst) {
+            const uint32_t ca =
+                mapa_rank(part_u32 + (uint32_t)((rank * s + c) * sizeof(double)), dst);
+            asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ca), "d"(acc) : "memory");
+        }
+    }
+    cluster_sync_all();
+    __shared__ double norms[kJacobiSmemMax];
+    __shared__ int order[kJacobiSmemMax];
+    for (int c = tid; c < s; c += nth) {
+        double acc = 0.0;
+        for (uint32_t rk = 0; rk < nc; ++rk) acc += npart[rk * s + c];
+        norms[c] = sqrt(acc);
+    }
+    __syncthreads();
+    for (int c = tid; c < s; c += nth) {
+        int rnk = 0;
+        for (int o = 0; o < s; ++o) rnk += (norms[o] > norms[c]) || (norms[o] == norms[c] && o < c);
+        order[rnk] = c;
+    }
+    __syncthreads();
+    const int rend = rank + 1 == nc ? NP : r0 + RPC;  // the last CTA also zero-fills rows >= nc RPC
+    for (int e = tid; e < (rend - r0) * NP; e += nth) {
+        const int r = r0 + e / NP, cc = e % NP;
+        double u = 0.0, w = 0.0;
+        if (r < s && cc < s) {
+            const int src = order[cc];
+            const double sg = norms[src];
+            u = sg > 0.0 ? Rc[src * RPC + (r - r0)] / sg : 0.0;
+            w = J[src * RPC + (r - r0)];
+        }
+        Uout[(size_t)r * NP + cc] = u;
+        Wout[(size_t)r * NP + cc] = w;
+    }
+    if (rank == 0) {
+        for (int c = tid; c < NP; c += nth) sigma_out[c] = c < s ? norms[order[c]] / scale : 0.0;
+        if (tid == 0) status[0] = sweeps;
+    }
+}
+
+template <int NQ>
+static size_t jacobi_cluster_smem(int s, int nc) {
+    const int pairs = ((s + 1) & ~1) / 2;
+    const size_t cols = 2 * (size_t)s * 8 * NQ;
+    const size_t part = std::max((size_t)2 * nc * pairs * 4, (size_t)nc * s);
+    return (cols + part) * sizeof(double);
+}
+
+template <int NQ>
+static cudaError_t launch_jacobi_cluster(const double* R, int s, int NP, double* sigma, double* U,
+                                         double* W, int* status, const int* abort_flag,
+                                         cudaStream_t st) {
+    const int nc = (s + 8 * NQ - 1) / (8 * NQ);
+    const int pairs = ((s + 1) & ~1) / 2;
+    const size_t smem = jacobi_cluster_smem<NQ>(s, nc);
+    if (nc > 8 || smem > 200 * 1024 || pairs * kJcLanes > 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(jacobi_cluster_kernel<NQ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nc);
+    cfg.blockDim = dim3((pairs * kJcLanes + 31) & ~31);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel<NQ>, R, s, NP, sigma, U, W, status,
+                              abort_flag);
+}
+
 size_t jacobi_max_width() { return 320; }
 
 size_t jacobi_global_scratch_doubles(int s) {
@@ -604,6 +905,14 @@ cudaError_t launch_jacobi_svd(const double* R, int s, int NP, double* sigma, dou
                                     : kJacobiSmemMax;
     if (s > std::min(smem_max, kJacobiSmemMax))
         return launch_block_jacobi_svd(R, s, NP, sigma, U, W, status, scratch, abort_flag, st);
+    // the cluster variant pays ~0.5k cycles of DSMEM exchange per round and saves shared-memory
+    // pipe cycles in proportion to s: measured (tools/probe/small_probe.cu, cycles per round)
+    // s = 48: 1686 vs 1438 single-CTA, s = 74: 2209 vs 2318, s = 112: 2925 vs 3634
+    static const int cl_min = getenv("RSVD_B200_JACOBI_CLUSTER_MIN")
+                                  ? atoi(getenv("RSVD_B200_JACOBI_CLUSTER_MIN"))
+                                  : 64;
+    if (s > std::max(cl_min, 16))
+        return launch_jacobi_cluster<2>(R, s, NP, sigma, U, W, status, abort_flag, st);
     switch ((jacobi_ld(s) + 15) / 16) {  // row pairs per lane
         case 1: return launch_jacobi_nq<1>(R, s, NP, sigma, U, W, status, abort_flag, st);
         case 2: return launch_jacobi_nq<2>(R, s, NP, sigma, U, W, status, abort_flag, st);

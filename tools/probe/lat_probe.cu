@@ -40,6 +40,14 @@ __global__ void k(double* out, long long* cyc, double x0) {
     t0 = clock64();
     for (int i = 0; i < N; ++i) x = sqrt(x + 1.0);
     t1 = clock64(); if (lane == 0) cyc[5] = (t1 - t0) / N;
+    // rsqrt chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) x = rsqrt(x + 1.0);
+    t1 = clock64(); if (lane == 0) cyc[9] = (t1 - t0) / N;
+    // MUFU.RSQ64H seed chain
+    t0 = clock64();
+    for (int i = 0; i < N; ++i) asm("rsqrt.approx.ftz.f64 %0, %0;" : "+d"(x));
+    t1 = clock64(); if (lane == 0) cyc[10] = (t1 - t0) / N;
     // LDS dependent (pointer chasing through value)
     int idx = lane;
     t0 = clock64();
@@ -62,7 +70,7 @@ int main() {
     k<<<1, 32>>>(o, c, 1.5);
     k<<<1, 32>>>(o, c, 1.5);
     long long h[16];
-    cudaMemcpy(h, c, 72, cudaMemcpyDeviceToHost);
-    const char* n[] = {"DFMA", "DMUL", "SHFL.64", "rcp_nr", "div", "sqrt", "LDS", "SHFL.32", "bar(1w)"};
-    for (int i = 0; i < 9; ++i) printf("%-8s %lld cycles\n", n[i], h[i]);
+    cudaMemcpy(h, c, 88, cudaMemcpyDeviceToHost);
+    const char* n[] = {"DFMA", "DMUL", "SHFL.64", "rcp_nr", "div", "sqrt", "LDS", "SHFL.32", "bar(1w)", "rsqrt", "rsq.approx"};
+    for (int i = 0; i < 11; ++i) printf("%-8s %lld cycles\n", n[i], h[i]);
 }

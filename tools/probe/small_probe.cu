@@ -102,8 +102,8 @@ static void jacobi_probe(int s, bool transposed) {
             sums[tr[2 * i]] += tr[2 * i + 1] - tr[2 * i - 1];
             cnt[tr[2 * i]] += 1;
         }
-        const char* nm[] = {"sync->next", "load+dots", "shuffles", "rotation", "update"};
-        for (int t = 0; t < 5; ++t)
+        const char* nm[] = {"sync->next", "load+dots", "shuffles", "rotation|send", "update|wait", "rot", "sync"};
+        for (int t = 0; t < 7; ++t)
             if (cnt[t]) printf("   %-12s %8lld cycles avg over %lld\n", nm[t], sums[t] / cnt[t], cnt[t]);
     }
 #endif
