@@ -71,6 +71,33 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
         "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 
+// A operand from TMEM (128 lanes x 8 tf32 columns at a_tmem)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t id,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(id), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+        "r"(v[15])
+        : "memory");
+}
+
+__device__ __forceinline__ bool elect_one_tf32() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -135,9 +162,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 __host__ __device__ __forceinline__ uint32_t b_bytes(int NP, bool mn) {
     return mn ? (uint32_t)((NP + 31) / 32) * kBoxMN : (uint32_t)NP * (BK * 4);
 }
-__host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn) {
-    return 2 * kABytes + 2 * b_bytes(NP, mn);
+__host__ __device__ __forceinline__ uint32_t stage_bytes(int NP, bool mn, bool ts = false) {
+    return (ts ? 1 : 2) * kABytes + 2 * b_bytes(NP, mn);
 }
+// TS: TMEM columns of the accumulator (32-aligned) and of the per-stage A hi / lo buffers
+__host__ __device__ __forceinline__ uint32_t ts_abase(int NP) { return (uint32_t)((NP + 31) & ~31); }
+constexpr uint32_t kTsCols = 2 * BK;  // hi (16 columns) + lo (16 columns) per stage
 
 // Drain the 128 x NP FP32 accumulator (warps 2-5: each its TMEM lane quarter) and store it
 // (FP32 + lo parts, FP64, or transposed), slab blockIdx.y of a split-K launch.
@@ -197,7 +227,15 @@ __device__ __forceinline__ void epilogue(uint32_t tmem, int warp, int lane, int 
 // B operand: each CTA loads half of B and B_lo and multicasts it into both, so B's L2
 // traffic (re-read by every M tile) halves. A stage may then only be refilled once both
 // CTAs' MMAs are done with it: every MMA commit arrives on the empty barrier of both.
-template <bool MN, bool OUT64, bool OUT_T, bool PAIR>
+// TS: the A operand goes to TMEM instead of shared memory. The converter warps (thread = tile
+// row = TMEM lane) read the stage's A tile, write it (the hi part: the tensor core ignores the
+// low mantissa bits) and its lo part into a 32-column TMEM buffer per stage with tcgen05.st,
+// and all three products read A from there: shared memory then carries only the TMA writes
+// and the MMAs' B reads (per 16-wide K stage at NP = 272: ~101 KB instead of ~157 KB: the
+// A tile, read by 3 products x 2 N chunks, and the A_lo writes leave the shared-memory pipe,
+// which bounds the SS form). The MN-major A tile is one unswizzled 128 x 16 box (conflict-free
+// row reads); the MMA warp runs the loop converged and one elected lane issues.
+template <bool MN, bool OUT64, bool OUT_T, bool PAIR, bool TS>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB,
@@ -211,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = align_smem_1024(smem_raw);
     const uint32_t bB = b_bytes(NP, MN);
-    const uint32_t kStage = 2 * kABytes + 2 * bB;
+    const uint32_t kStage = (TS ? 1 : 2) * kABytes + 2 * bB;
+    constexpr uint32_t kAOff = TS ? kABytes : 2 * kABytes;  // B raw offset in a stage
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
     uint64_t* conv = full + kStages;
     uint64_t* empty = conv + kStages;
@@ -223,7 +262,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kt0 = blockIdx.y * k_tiles_per_split;
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
     const int n_iter = max(0, kt1 - kt0);
-    const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
+    const uint32_t tneed = TS ? ts_abase(NP) + kStages * kTsCols : (uint32_t)NP;
+    const uint32_t tmem_cols =
+        tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
     // upper (a symmetric Gram, MN shape): rows m0.. only need columns m0.. (multiple of 128)
     const int c_off = (MN && upper) ? min(m0, (NP - 16) & ~31) : 0;
 
@@ -262,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = it % kStages;
                 if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
                 char* st = smem + s * kStage;
-                char* sb = st + 2 * kABytes;
+                char* sb = st + kAOff;
                 const int k = (kt0 + it) * BK;
                 mbar_arrive_expect_tx(&full[s], kABytes + 2 * bB);
                 if constexpr (!MN) {
@@ -282,9 +323,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 } else {
                     const int nb = (NP + 31) / 32;
+                    if constexpr (TS) {
+                        tma_load_2d(st, &mapA, &full[s], m0, k);  // one 128 x 16 box
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < BM / 32; ++i)
-                        tma_load_2d(st + i * kBoxMN, &mapA, &full[s], m0 + 32 * i, k);
+                        for (int i = 0; i < BM / 32; ++i)
+                            tma_load_2d(st + i * kBoxMN, &mapA, &full[s], m0 + 32 * i, k);
+                    }
                     if constexpr (PAIR) {  // every other 32-wide box of B, to both
                         for (int j = (int)crank; j < nb; j += 2) {
                             tma_load_2d_mc(sb + j * kBoxMN, &mapB, &full[s], 32 * j, k, 3);
@@ -299,6 +344,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if (warp == 1 && TS) {
+        // ------------------------------------------------------- MMA issuer (TS)
+        const uint32_t lbo = MN ? kBoxMN : 16u, sbo = 512u;
+        const uint64_t lay = MN ? 1u : 4u;
+        const int ne = NP - c_off;
+        const int n1 = ne > 256 ? ((ne / 2 + 31) & ~31) : ne, n2 = ne - n1;
+        const uint32_t id1 = idesc(n1, MN) & ~(1u << 15), id2 = n2 > 0 ? idesc(n2, MN) & ~(1u << 15) : 0u;
+        const uint32_t co = (uint32_t)n1 * (MN ? kBoxMN / 32u : BK * 4u);
+        const uint32_t bo = (uint32_t)(c_off / 32) * kBoxMN;
+        const uint32_t abuf = tmem + ts_abase(NP);
+        for (int it = 0; it < n_iter; ++it) {
+            const int s = it % kStages;
+            const uint32_t b_raw = smem_u32(smem + s * kStage) + kAOff + bo, b_lo = b_raw + bB;
+            const uint32_t a_hi = abuf + (uint32_t)s * kTsCols, a_lo = a_hi + BK;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            mbar_wait(&conv[s], (it / kStages) & 1);
+            fence_after();
+            if (elect_one_tf32()) {
+#pragma unroll
+                for (int pr = 0; pr < 3; ++pr) {  // a_hi b_hi, a_hi b_lo, a_lo b_hi
+                    const uint32_t a = pr == 2 ? a_lo : a_hi, b = pr == 1 ? b_lo : b_raw;
+#pragma unroll
+                    for (int ks = 0; ks < BK / 8; ++ks) {
+                        const uint32_t ko = MN ? ks * 1024u : ks * 32u;
+                        const uint32_t acc = (it > 0 || pr > 0 || ks > 0) ? 1u : 0u;
+                        mma_ts(tmem, a + 8u * ks, sdesc(b + ko, lbo, sbo, lay), id1, acc);
+                        if (n2 > 0)
+                            mma_ts(tmem + (uint32_t)n1, a + 8u * ks,
+                                   sdesc(b + co + ko, lbo, sbo, lay), id2, acc);
+                    }
+                }
+                if constexpr (PAIR)
+                    commit_mc(&empty[s], 3);
+                else
+                    commit(&empty[s]);
+            }
+            __syncwarp();
+        }
+        if (n_iter > 0 && elect_one_tf32()) commit(accum);
+        __syncwarp();
     } else if (warp == 1) {
         // ------------------------------------------------------------- MMA issuer
         if (lane == 0) {
@@ -341,6 +426,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (n_iter > 0) commit(accum);
         }
+    } else if (TS) {
+        // ------------------------- A hi / lo into TMEM (warps 2-5: thread = row = lane)
+        const int q = warp & 3;
+        const int r = 32 * q + lane;
+        const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + ts_abase(NP);
+        bool bad = false;
+        for (int it = 0; it < n_iter; ++it) {
+            const int s = it % kStages;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            const char* st = smem + s * kStage;
+            uint32_t hi[16], lo[16];
+            if constexpr (!MN) {  // K-major, SWIZZLE_64B: 16-byte chunk c of row r at c ^ (r/2 % 4)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float4 v = *reinterpret_cast<const float4*>(
+                        st + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+                    hi[4 * c] = __float_as_uint(v.x);
+                    hi[4 * c + 1] = __float_as_uint(v.y);
+                    hi[4 * c + 2] = __float_as_uint(v.z);
+                    hi[4 * c + 3] = __float_as_uint(v.w);
+                }
+            } else {  // MN-major, unswizzled 128 (M) x 16 (K): row k of 512 bytes
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk)
+                    hi[kk] = *reinterpret_cast<const uint32_t*>(st + kk * 512 + r * 4);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+                if (flag) bad |= (hi[kk] & 0x7f800000u) == 0x7f800000u;
+                lo[kk] = __float_as_uint(lo_part(__uint_as_float(hi[kk])));
+            }
+            tmem_st16(tl + (uint32_t)s * kTsCols, hi);
+            tmem_st16(tl + (uint32_t)s * kTsCols + BK, lo);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[s]);
+        }
+        if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
+        if (n_iter > 0) {
+            mbar_wait(accum, 0);
+            fence_after();
+        }
+        epilogue<OUT64, OUT_T>(tmem, warp, lane, m0, M, NP, n_iter > 0, out, out_lo, ldo,
+                               split_stride, c_off);
     } else {
         // ------------------------------------------------- A lo split (warps 2-5)
         const int ct = threadIdx.x - 64;
@@ -648,11 +778,11 @@ int map_f32(CUtensorMap* map, const float* base, long rows, long cols, long ld, 
     return r == CUDA_SUCCESS ? 0 : -3;
 }
 
-template <bool MN, bool OUT64, bool OUT_T, bool PAIR>
+template <bool MN, bool OUT64, bool OUT_T, bool PAIR, bool TS>
 cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
                      const CUtensorMap& mBlo, cudaStream_t st) {
-    const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN) + 16 * 8 + 16 + 1024;
-    auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T, PAIR>;
+    const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN, TS) + 16 * 8 + 16 + 1024;
+    auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T, PAIR, TS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int k_tiles = (int)((p.K + tf32::BK - 1) / tf32::BK);
@@ -724,11 +854,21 @@ bool use_pair(const GemmTf32& p) {
     return pair && tiles > 1 && (tiles % 2 == 0 || tiles >= 16);
 }
 
+// A operand in TMEM (TS) unless RSVD_B200_TF32_SS is set (the shared-memory form, kept for A/B)
+bool use_ts() {
+    static const bool ss = getenv("RSVD_B200_TF32_SS") != nullptr;
+    return !ss;
+}
+
 template <bool MN, bool OUT64, bool OUT_T>
 cudaError_t launch_p(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
                      const CUtensorMap& mBlo, cudaStream_t st) {
-    if (use_pair(p)) return launch_t<MN, OUT64, OUT_T, true>(p, mA, mB, mBlo, st);
-    return launch_t<MN, OUT64, OUT_T, false>(p, mA, mB, mBlo, st);
+    if (use_ts()) {
+        if (use_pair(p)) return launch_t<MN, OUT64, OUT_T, true, true>(p, mA, mB, mBlo, st);
+        return launch_t<MN, OUT64, OUT_T, false, true>(p, mA, mB, mBlo, st);
+    }
+    if (use_pair(p)) return launch_t<MN, OUT64, OUT_T, true, false>(p, mA, mB, mBlo, st);
+    return launch_t<MN, OUT64, OUT_T, false, false>(p, mA, mB, mBlo, st);
 }
 
 }  // namespace
@@ -775,7 +915,9 @@ cudaError_t launch_gemm_tf32(const GemmTf32& p, cudaStream_t st) {
             return cudaErrorInvalidValue;
     } else {  // A: K x M (lda), W: K x NP (ldb); 128-byte rows of M / N
         const auto sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-        if (map_f32(&mA, p.A, p.K, p.M, p.lda, 32, tf32::BK, sw) ||
+        const bool ts = use_ts();  // TS: A is read by the converters only, one plain box
+        if (map_f32(&mA, p.A, p.K, p.M, p.lda, ts ? tf32::BM : 32, tf32::BK,
+                    ts ? CU_TENSOR_MAP_SWIZZLE_NONE : sw) ||
             map_f32(&mB, p.B, p.K, p.NP, p.ldb, 32, tf32::BK, sw) ||
             map_f32(&mBlo, p.Blo, p.K, p.NP, p.ldb, 32, tf32::BK, sw))
             return cudaErrorInvalidValue;
