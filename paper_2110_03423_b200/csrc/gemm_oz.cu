@@ -464,13 +464,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int e = 0; e < 16; ++e)
                     v[e] = *reinterpret_cast<const double*>(box + swz128(h * 16 + e, r & 15));
             }
-            __syncwarp();
-            if (lane == 0) {  // the FP64 tile is in registers: release it in every CTA
-                if (ncl > 1)
-                    for (int rk = 0; rk < ncl; ++rk)
-                        mbar_arrive_remote(mapa_rank(smem_u32(&empty_a[sa]), (uint32_t)rk));
-                else
-                    mbar_arrive(&empty_a[sa]);
+            if (ncl > 1) {
+                // the FP64 tile is in registers: release it in every CTA of the cluster. A
+                // release.cluster arrive costs a GPU-scope fence per warp and stage (measured:
+                // membar stalls doubled the kernel); a relaxed arrive after the registers have
+                // landed (the volatile moves wait on the shared-memory loads' scoreboard)
+                // orders the reads before the producer's refill just the same
+                uint64_t sink = 0;
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    asm volatile("xor.b64 %0, %0, %1;" : "+l"(sink) : "l"(__double_as_longlong(v[e])));
+                asm volatile("" ::"l"(sink));
+                __syncwarp();
+                if (lane < ncl)
+                    asm volatile(
+                        "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                            mapa_rank(smem_u32(&empty_a[sa]), (uint32_t)lane))
+                        : "memory");
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_a[sa]);
             }
             uint32_t pw[kDigits][4];
             if (diag & 4) {

@@ -43,6 +43,7 @@ namespace tf32 {
 constexpr int BM = 128;
 constexpr int BK = 16;
 constexpr int kStages = 4;
+constexpr int kStagesTs = 4;  // TS (a fifth stage fits without the A_lo region: measured equal)
 constexpr int kThreads = 192;
 constexpr uint32_t kABytes = BM * BK * 4;  // 8 KB per A tile (raw or lo)
 constexpr uint32_t kBoxMN = 32 * BK * 4;   // 2 KB: one MN-major box (32 M/N x 16 K)
@@ -248,13 +249,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (abort_flag && *(const volatile int*)abort_flag) return;
     extern __shared__ __align__(1024) char smem_raw[];
     char* smem = align_smem_1024(smem_raw);
+    constexpr int NS = TS ? kStagesTs : kStages;
     const uint32_t bB = b_bytes(NP, MN);
     const uint32_t kStage = (TS ? 1 : 2) * kABytes + 2 * bB;
     constexpr uint32_t kAOff = TS ? kABytes : 2 * kABytes;  // B raw offset in a stage
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
-    uint64_t* conv = full + kStages;
-    uint64_t* empty = conv + kStages;
-    uint64_t* accum = empty + kStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * kStage);
+    uint64_t* conv = full + NS;
+    uint64_t* empty = conv + NS;
+    uint64_t* accum = empty + NS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -262,14 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kt0 = blockIdx.y * k_tiles_per_split;
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
     const int n_iter = max(0, kt1 - kt0);
-    const uint32_t tneed = TS ? ts_abase(NP) + kStages * kTsCols : (uint32_t)NP;
+    const uint32_t tneed = TS ? ts_abase(NP) + NS * kTsCols : (uint32_t)NP;
     const uint32_t tmem_cols =
         tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
     // upper (a symmetric Gram, MN shape): rows m0.. only need columns m0.. (multiple of 128)
     const int c_off = (MN && upper) ? min(m0, (NP - 16) & ~31) : 0;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&conv[s], 4);
             mbar_init(&empty[s], PAIR ? 2 : 1);
@@ -300,8 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_prefetch_desc(&mapB);
             tma_prefetch_desc(&mapBlo);
             for (int it = 0; it < n_iter; ++it) {
-                const int s = it % kStages;
-                if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+                const int s = it % NS;
+                if (it >= NS) mbar_wait(&empty[s], ((it / NS) - 1) & 1);
                 char* st = smem + s * kStage;
                 char* sb = st + kAOff;
                 const int k = (kt0 + it) * BK;
@@ -355,11 +357,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t bo = (uint32_t)(c_off / 32) * kBoxMN;
         const uint32_t abuf = tmem + ts_abase(NP);
         for (int it = 0; it < n_iter; ++it) {
-            const int s = it % kStages;
+            const int s = it % NS;
             const uint32_t b_raw = smem_u32(smem + s * kStage) + kAOff + bo, b_lo = b_raw + bB;
             const uint32_t a_hi = abuf + (uint32_t)s * kTsCols, a_lo = a_hi + BK;
-            mbar_wait(&full[s], (it / kStages) & 1);
-            mbar_wait(&conv[s], (it / kStages) & 1);
+            mbar_wait(&full[s], (it / NS) & 1);
+            mbar_wait(&conv[s], (it / NS) & 1);
             fence_after();
             if (elect_one_tf32()) {
 #pragma unroll
@@ -408,15 +410,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             };
             for (int it = 0; it < n_iter; ++it) {
-                const int s = it % kStages;
+                const int s = it % NS;
                 const uint32_t st = smem_u32(smem + s * kStage);
                 const uint32_t a_raw = st, a_lo = st + kABytes;
                 const uint32_t b_raw = st + 2 * kABytes + bo, b_lo = b_raw + bB;
-                mbar_wait(&full[s], (it / kStages) & 1);
+                mbar_wait(&full[s], (it / NS) & 1);
                 fence_after();
                 issue(a_raw, b_raw, it > 0 ? 1u : 0u);  // a_hi b_hi
                 issue(a_raw, b_lo, 1u);                 // a_hi b_lo
-                mbar_wait(&conv[s], (it / kStages) & 1);
+                mbar_wait(&conv[s], (it / NS) & 1);
                 fence_after();
                 issue(a_lo, b_raw, 1u);                 // a_lo b_hi
                 if constexpr (PAIR)
@@ -433,8 +435,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + ts_abase(NP);
         bool bad = false;
         for (int it = 0; it < n_iter; ++it) {
-            const int s = it % kStages;
-            mbar_wait(&full[s], (it / kStages) & 1);
+            const int s = it % NS;
+            mbar_wait(&full[s], (it / NS) & 1);
             const char* st = smem + s * kStage;
             uint32_t hi[16], lo[16];
             if constexpr (!MN) {  // K-major, SWIZZLE_64B: 16-byte chunk c of row r at c ^ (r/2 % 4)
@@ -476,8 +478,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ct = threadIdx.x - 64;
         bool bad = false;
         for (int it = 0; it < n_iter; ++it) {
-            const int s = it % kStages;
-            mbar_wait(&full[s], (it / kStages) & 1);
+            const int s = it % NS;
+            mbar_wait(&full[s], (it / NS) & 1);
             char* st = smem + s * kStage;
             const float4* ar = reinterpret_cast<const float4*>(st);
             float4* al = reinterpret_cast<float4*>(st + kABytes);
@@ -781,7 +783,8 @@ int map_f32(CUtensorMap* map, const float* base, long rows, long cols, long ld, 
 template <bool MN, bool OUT64, bool OUT_T, bool PAIR, bool TS>
 cudaError_t launch_t(const GemmTf32& p, const CUtensorMap& mA, const CUtensorMap& mB,
                      const CUtensorMap& mBlo, cudaStream_t st) {
-    const size_t smem = tf32::kStages * tf32::stage_bytes(p.NP, MN, TS) + 16 * 8 + 16 + 1024;
+    const int ns = TS ? tf32::kStagesTs : tf32::kStages;
+    const size_t smem = ns * tf32::stage_bytes(p.NP, MN, TS) + (3 * ns + 1) * 8 + 16 + 1024;
     auto kern = tf32::gemm_tf32_kernel<MN, OUT64, OUT_T, PAIR, TS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

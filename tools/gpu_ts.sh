@@ -1,12 +1,8 @@
-# 3xTF32 GEMM with A in TMEM (TS) vs shared memory (SS): tests, C4 launch lists, bench
-OUT=gpurun_out/ts
+# 3xTF32 GEMM (TS): tests, C4 launch list, bench
+OUT=gpurun_out/ts2
 mkdir -p $OUT
-timeout 900 python -m pytest tests/test_gpu_tf32.py tests/test_gpu_f32.py -q -x 2>&1 | tail -3
-for v in ts ss; do
-  if [ $v = ss ]; then export RSVD_B200_TF32_SS=1; else unset RSVD_B200_TF32_SS; fi
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-      --log-file $OUT/launches_$v.csv python tools/profile_config.py c4 > /dev/null 2>&1
-  echo "== $v"; python tools/launch_summary.py $OUT/launches_$v.csv 2>&1 | head -8
-done
-unset RSVD_B200_TF32_SS
-timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu 2>&1 | tail -1 | cut -c1-400
+timeout 900 python -m pytest tests/test_gpu_tf32.py tests/test_gpu_f32.py -q -x 2>&1 | tail -2
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches.csv python tools/profile_config.py c4 > /dev/null 2>&1
+python tools/launch_summary.py $OUT/launches.csv 2>&1 | head -6
+timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu 2>&1 | tail -1 | cut -c1-300
