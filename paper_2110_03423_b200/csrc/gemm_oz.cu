@@ -47,9 +47,15 @@ constexpr int kDigits = 7;        // S
 constexpr int kGroups = 7;        // g = i + j in [S - 1, 2S - 2]
 constexpr int BM = 128;           // MMA M (rows of the tile)
 constexpr int BK = 32;            // K per stage = one kind::i8 MMA
-constexpr int kFStages = 4;       // FP64 A ring (TMA -> converters)
+#ifndef OZ_FSTAGES
+#define OZ_FSTAGES 4
+#endif
+#ifndef OZ_BSTAGES
+#define OZ_BSTAGES 4
+#endif
+constexpr int kFStages = OZ_FSTAGES;  // FP64 A ring (TMA -> converters)
 constexpr int kDStages = 3;       // A digits in TMEM (converters -> MMA): 7 N + 3 x 56 <= 512 columns
-constexpr int kBStages = 4;       // B digit planes in shared memory (TMA -> MMA)
+constexpr int kBStages = OZ_BSTAGES;  // B digit planes in shared memory (TMA -> MMA)
 constexpr int kConvWarps = 8;     // warps 3..10: (row, k-half) per thread
 constexpr int kThreads = 96 + 32 * kConvWarps;
 constexpr int kMaxN = 48;         // columns per CTA: 7 accumulators of N + 3 x 56 digit columns

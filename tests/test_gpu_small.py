@@ -90,10 +90,14 @@ def jacobi(solver, r, NP):
     return sig, U, W, sw.value
 
 
-@pytest.mark.parametrize("s", [1, 2, 5, 8, 9, 42, 74, 112, 113, 148, 200, 272, 320])
-def test_jacobi_sizes(solver, s):
-    """Both Jacobi kernels (single CTA s <= 112, block Jacobi beyond) on a graded triangular
-    R (the shape the pipeline hands over: R_B of B^T = Q_B R_B): sigma against torch's SVD,
+@pytest.mark.parametrize("s,NP", [(s, (s + 15) // 16 * 16) for s in
+                                  [1, 2, 5, 8, 9, 42, 64, 65, 74, 80, 81, 96, 97, 112, 113, 148,
+                                   200, 272, 320]] + [(70, 112), (100, 128)])
+def test_jacobi_sizes(solver, s, NP):
+    """All three Jacobi kernels (single CTA s <= 64, the cluster of ceil(s / 16) CTAs for
+    64 < s <= 112 — every cluster size from 5 to 7, and NP beyond 16 ceil(s / 16) so the last
+    CTA zero-fills the extra rows — and the block Jacobi beyond) on a graded triangular R (the
+    shape the pipeline hands over: R_B of B^T = Q_B R_B): sigma against torch's SVD,
     R W = U diag(sigma), orthonormal U and W, descending order, zero padding."""
     import torch
     gen = torch.Generator(device="cuda").manual_seed(1000 + s)
@@ -101,13 +105,14 @@ def test_jacobi_sizes(solver, s):
     a = a * torch.logspace(0, -4, s, dtype=torch.float64, device="cuda")
     r = torch.linalg.qr(a.T).R.T.contiguous().T.contiguous()  # upper triangular, graded
     r = torch.triu(r)
-    NP = (s + 15) // 16 * 16
     sig, U, W, sweeps = jacobi(solver, r, NP)
     assert 1 <= sweeps <= 30
     ref = torch.linalg.svdvals(r)
     got = sig[:s]
     assert torch.all(got[:-1] >= got[1:])
     assert torch.all(sig[s:] == 0)
+    assert torch.all(U[s:] == 0) and torch.all(U[:, s:] == 0)
+    assert torch.all(W[s:] == 0) and torch.all(W[:, s:] == 0)
     rel = ((got - ref).abs() / ref).max().item()
     assert rel < 1e-12, rel
     Us, Ws = U[:s, :s], W[:s, :s]
@@ -118,13 +123,14 @@ def test_jacobi_sizes(solver, s):
     assert recon < 1e-13, recon
 
 
-def test_jacobi_rank_deficient(solver):
-    """Zero columns: sigma exactly 0 there, U column 0 (completed later by the pipeline)."""
+@pytest.mark.parametrize("s,zero_from", [(20, 15), (90, 70)])
+def test_jacobi_rank_deficient(solver, s, zero_from):
+    """Zero columns: sigma exactly 0 there, U column 0 (completed later by the pipeline);
+    s = 90 runs on the cluster kernel."""
     import torch
-    s = 20
     r = torch.triu(torch.randn(s, s, dtype=torch.float64, device="cuda"))
-    r[:, 15:] = 0
-    sig, U, W, sweeps = jacobi(solver, r, 32)
+    r[:, zero_from:] = 0
+    sig, U, W, sweeps = jacobi(solver, r, (s + 15) // 16 * 16)
     assert sweeps >= 1
-    assert torch.all(sig[15:s] == 0)
-    assert torch.all(U[:s, 15:s] == 0)
+    assert torch.all(sig[zero_from:s] == 0)
+    assert torch.all(U[:s, zero_from:s] == 0)
