@@ -819,6 +819,66 @@ __global__ void __launch_bounds__(1024) oz_convert_rows_kernel(
     if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
 }
 
+// Streaming form of the same conversion, with the row exponents given (oz_scan): one CTA per
+// 128-row x 128-column block of A (256 threads; thread -> 16-column chunk t & 7 of row
+// 32 it + t / 8, it = 0..3), so that every warp store lands on contiguous bytes of both tiled
+// layouts (4 rows x 128 B of a SW32 ax tile, 4 rows x 128 B of an atx block) instead of 32
+// scattered 16-byte pieces (oz_convert_rows_kernel: 3.2 TB/s of combined traffic). Rows
+// >= `rows` and columns >= `cols` are zero digits; row block rb = blockIdx.y + r0 / 128.
+// dig_ax may be null (only the atx blocks: the pipeline's stored-digit atx passes).
+__global__ void __launch_bounds__(256) oz_convert_tiles_kernel(
+    const double* __restrict__ A, long r0, long rows, long cols, long lda,
+    uint8_t* __restrict__ dig_ax, uint8_t* __restrict__ dig_atx, const int* __restrict__ row_ef) {
+    const int t = threadIdx.x, chunk = t & 7, rq = t >> 3;
+    const long KT = (cols + 31) / 32, JB = (cols + 127) / 128;
+    const long jb = blockIdx.x, rb = (r0 >> 7) + blockIdx.y;
+    const long c0 = jb * 128 + chunk * 16;
+    const long kt = c0 >> 5;
+    const uint32_t half = (uint32_t)(chunk & 1);
+#pragma unroll 1
+    for (int it = 0; it < 4; ++it) {
+        const uint32_t rl = (uint32_t)(it * 32 + rq);
+        const long r = rb * 128 + rl;
+        double v[16];
+        if (r < rows && c0 + 16 <= cols) {
+            const double* row = A + r * lda + c0;
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+                const double2 x = __ldcs(reinterpret_cast<const double2*>(row + e));
+                v[e] = x.x;
+                v[e + 1] = x.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                v[e] = (r < rows && c0 + e < cols) ? A[r * lda + c0 + e] : 0.0;
+        }
+        double f1, f2;
+        fixed_scale(r < rows ? row_ef[r] : 0, f1, f2);
+        uint32_t pw[kDigits][4];
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            uint64_t wd[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) wd[e] = digits_scaled(v[4 * qd + e], f1, f2);
+            uint32_t pl[kDigits];
+            planes4(wd, pl);
+#pragma unroll
+            for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
+        }
+        const uint32_t kl = rl & 31;
+        uint8_t* ax = dig_ax + ((rb * KT + kt) * kDigits) * 4096 + sw32(rl, half);
+        uint8_t* at = dig_atx + ((((r >> 5) * JB) + jb) * kDigits) * 4096 + kl * 128 +
+                      (((uint32_t)chunk ^ (kl & 7)) << 4);
+#pragma unroll
+        for (int i = 0; i < kDigits; ++i) {
+            const uint4 q = make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
+            if (dig_ax && kt < KT) __stcs(reinterpret_cast<uint4*>(ax + i * 4096), q);
+            __stcs(reinterpret_cast<uint4*>(at + i * 4096), q);
+        }
+    }
+}
+
 // ------------------------------------------------------------ GEMM from stored digits
 // Both pass shapes from A's row-scaled digit planes (oz_convert_rows) and the small operand's
 // digit planes:
@@ -1305,6 +1365,10 @@ size_t oz_scan_part_ints(long rows, long cols) {
     return (size_t)(cb * rows + rb * cols);
 }
 
+size_t oz_atx_bytes(long rows, long cols) {  // rows padded to whole 128-row blocks (convert)
+    return (size_t)((rows + 127) / 128 * 4) * ((cols + 127) / 128) * oz::kDigits * oz::kDsADig;
+}
+
 size_t oz_tiled_bytes(long rows, long cols) {
     const size_t blk = (size_t)oz::kDigits * oz::kDsADig;
     const size_t ax = (size_t)((rows + 127) / 128) * ((cols + 31) / 32) * blk;
@@ -1324,6 +1388,19 @@ cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows,
     const unsigned grid = (unsigned)std::min<long>(r1 - r0, 148L * std::max(1, 2048 / threads));
     oz::oz_convert_rows_kernel<<<grid, threads, 0, st>>>(A, r0, r1, rows, cols, lda, dig_ax,
                                                         dig_atx, row_ef, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows, long cols,
+                                    long lda, uint8_t* dig_ax, uint8_t* dig_atx,
+                                    const int* row_ef, cudaStream_t st) {
+    if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1) || (r0 & 127)) return cudaErrorInvalidValue;
+    if (r1 >= rows) r1 = (rows + 127) / 128 * 128;  // the last chunk also zeroes the pad rows
+    else if (r1 & 127) return cudaErrorInvalidValue;
+    if (r1 <= r0) return cudaSuccess;
+    const dim3 grid((unsigned)((cols + 127) / 128), (unsigned)((r1 - r0) / 128));
+    oz::oz_convert_tiles_kernel<<<grid, 256, 0, st>>>(A, r0, rows, cols, lda, dig_ax, dig_atx,
+                                                      row_ef);
     return cudaGetLastError();
 }
 

@@ -163,6 +163,11 @@ cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, l
 // oz_tiled_bytes(rows, cols)), row_ef, NaN/Inf flag. One read of A; r0, r1 multiples of 128
 // except r1 = rows (the last chunk, which also zeroes the padding).
 size_t oz_tiled_bytes(long rows, long cols);
+// the same digit layouts from a scan's row exponents (row_ef input), coalesced tile writes;
+// dig_ax may be null (atx blocks only)
+cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows, long cols,
+                                    long lda, uint8_t* dig_ax, uint8_t* dig_atx,
+                                    const int* row_ef, cudaStream_t st);
 cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
                                    long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
                                    int* flag, cudaStream_t st);
@@ -188,6 +193,8 @@ struct GemmOzd {
     const int* abort = nullptr;
 };
 cudaError_t launch_gemm_ozd(const GemmOzd& p, cudaStream_t st);
+// bytes of the stored atx blocks of A (rows x cols): 4 ceil(rows / 128) x ceil(cols / 128) blocks
+size_t oz_atx_bytes(long rows, long cols);  // rows rounded up to 128
 
 cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
 cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);

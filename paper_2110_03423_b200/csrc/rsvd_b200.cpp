@@ -169,11 +169,12 @@ struct GraphKey {
     int profiling = 0;
     unsigned long gen = 0;
     const void* comm = nullptr;  // sharded solves: the communicator the graph's all-reduces use
+    int apass = 0;               // A-pass datapath (oz_mode: DMMA / emulated / stored digits)
     bool operator==(const GraphKey& o) const {
         return a == o.a && m == o.m && n == o.n && lda == o.lda && s == o.s && NP == o.NP &&
                f32 == o.f32 && k == o.k && q == o.q && seed == o.seed && u == o.u &&
                sigma == o.sigma && v == o.v && ldu == o.ldu && ldv == o.ldv &&
-               profiling == o.profiling && gen == o.gen && comm == o.comm;
+               profiling == o.profiling && gen == o.gen && comm == o.comm && apass == o.apass;
     }
 };
 
@@ -226,7 +227,9 @@ struct rsvd_b200_handle {
     // arrays (A rows, A columns, B columns, scratch) and the scan partials
     DevBuf oz_bdig, oz_ef, oz_part;
     DevBuf oz_adig;  // A's row-scaled digit planes (stored-digit passes)
+    bool oz_stored = false;  // this run's passes after the sketch read A's stored digits
     long oz_passes = 0;  // passes over A of the last solve that ran on the INT8 tensor cores
+    long oz_stored_passes = 0;  // of those, atx passes from A's stored digits
     int* flags_host = nullptr;
     StreamPos omega_pos;  // sampler state the next sketch's Omega continues (default: fresh)
     std::vector<double> omega_host;  // validation mode (n x s row-major)
@@ -624,6 +627,31 @@ bool oz_on(const Plan& p) {
     const int mode = (e && std::string(e) == "dmma") ? 0 : (e && std::string(e) == "oz") ? 2 : 1;
     if (mode == 0 || p.f32 || p.NP < 16 || p.NP > 256) return false;
     return mode == 2 || (double)p.m * (double)p.n >= (double)(1L << 26);
+}
+
+// Stored digits for the atx passes (default for the emulated path; RSVD_B200_OZ_STORED=0
+// disables): right after each row chunk's scan, oz_convert_tiles writes A's row-scaled digits
+// in the atx block layout of gemm_ozd (one streaming pass, ~0.9 of HBM bandwidth), and the atx
+// passes ((A^T Q)^T, Q^T A) read those with A's row scales folded into W — no FP64 tile, no
+// conversion, no duplicated conversion by the column-chunk CTAs (1.59 against 2.64 ms per C2
+// pass). The ax passes keep the in-kernel digits: their stored form saved too little to pay
+// for writing a second layout. Needs oz_atx_bytes (0.88 x the FP64 A) of HBM; without the room
+// the atx passes stay in-kernel. Accuracy: normwise FP64 per column of W' (the row scales
+// folded in), against per column of A for the in-kernel digits.
+bool oz_stored_fits(rsvd_b200_handle* h, const Plan& p) {
+    const char* e = getenv("RSVD_B200_OZ_STORED");
+    if (e && atoi(e) == 0) return false;
+    const size_t need = oz_atx_bytes(p.m, p.n);
+    if (need <= h->oz_adig.bytes) return true;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+    return need + (size_t)(2ull << 30) <= free_b + h->oz_adig.bytes;
+}
+
+// 0: DMMA passes, 1: emulated with in-kernel digits, 2: emulated with stored digits
+int oz_mode(rsvd_b200_handle* h, const Plan& p) {
+    if (!oz_on(p)) return 0;
+    return oz_stored_fits(h, p) ? 2 : 1;
 }
 
 long oz_tiles(long N, int NP) {
@@ -1027,10 +1055,20 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
     h->jscratch.reserve(std::max<size_t>(1, jacobi_global_scratch_doubles(p.s)) * sizeof(double));
     h->cwork.reserve(complete_basis_work_doubles(p.n) * sizeof(double));
     h->oz_passes = 0;
+    h->oz_stored_passes = 0;
+    h->oz_stored = false;
     if (oz_on(p)) {
         h->oz_ef.reserve((size_t)(p.m + p.n + 2 * NP + 8) * sizeof(int));
         h->oz_bdig.reserve(std::max(oz_digits_bytes(NP, p.n), oz_digits_bytes(NP, p.m)));
         h->oz_part.reserve(oz_scan_part_ints(p.m, p.n) * sizeof(int));
+        // optimistic path only: the robust rerun (inputs that break CholeskyQR, i.e. strongly
+        // graded spectra) keeps the in-kernel digits, whose per-column scales of A hold the
+        // small singular values' relative accuracy better (tools/probe/stored_accuracy.py:
+        // 5.4e-11 against 1.8e-10 at sigma ratio 2.5e-8)
+        if (!robust && oz_mode(h, p) == 2) {
+            h->oz_adig.reserve(oz_atx_bytes(p.m, p.n));
+            h->oz_stored = true;
+        }
     }
     ck(cudaMemsetAsync(h->flags.p, 0, kNumFlags * sizeof(int), h->stream), "memset flags");
     h->aty_pending = false;
@@ -1065,6 +1103,9 @@ void oz_digits_xt(const Ctx& c, const double* Xt) {
                                         c.h->stream),
                   "oz_digits_rows");
 }
+
+// A's stored digits (oz_adig): the atx blocks of gemm_ozd
+uint8_t* oz_dig_atx(const Ctx& c) { return static_cast<uint8_t*>(c.h->oz_adig.p); }
 
 // Y (rows x NP) = A[r0 : r0 + rows] X with the digits of Xt already prepared.
 void oz_ax(const Ctx& c, const double* A, long r0, long rows, double* Y, const char* tag,
@@ -1102,6 +1143,40 @@ void oz_atx(const Ctx& c, const double* A, const double* W, double* Zt, const ch
     rsvd_b200_handle* h = c.h;
     const Plan& p = c.p;
     int* colmax = oz_b_ef(c) + p.NP;
+    if (h->oz_stored) {  // W' = diag(2^(E_row - 53)) W digitised per column, A's stored digits
+        int nch, nf;
+        oz_chunks(p.NP, &nch, &nf);
+        h->launched(launch_oz_digits_cols(W, p.NP, p.NP, p.s, p.m,
+                                          static_cast<uint8_t*>(h->oz_bdig.p), oz_b_ef(c),
+                                          colmax, h->stream, oz_row_ef(c), nf),
+                    "oz_digits_cols");
+        GemmOzd g;
+        g.mn = true;
+        g.adig = oz_dig_atx(c), g.a_inner = (p.n + 127) / 128;
+        g.M = p.n, g.K = p.m, g.a_ef = oz_row_ef(c);
+        g.bdig = static_cast<const uint8_t*>(h->oz_bdig.p), g.b_ef = oz_b_ef(c), g.NP = p.NP;
+        g.out_t = true;
+        g.abort = h->abort_ptr;
+        const int splits = oz_splits(p.n, p.NP, p.m, true);
+        h->oz_passes += 1;
+        h->oz_stored_passes += 1;
+        h->kernel_begin(tag, flops);
+        if (splits == 1) {
+            g.out = Zt, g.ldo = p.ldn;
+            h->launched(launch_gemm_ozd(g, h->stream), "gemm_ozd");
+            h->kernel_end(tag);
+            return;
+        }
+        const long slab = (long)p.NP * p.ldn;
+        if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+            fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
+        g.out = h->part.d(), g.ldo = p.ldn, g.splits = splits, g.split_stride = slab;
+        h->launched(launch_gemm_ozd(g, h->stream), "gemm_ozd(split)");
+        h->kernel_end(tag);
+        h->launched(launch_reduce_partials(h->part.d(), slab, splits, Zt, slab, h->stream),
+                    "reduce_partials");
+        return;
+    }
     h->launched(launch_oz_digits_cols(W, p.NP, p.NP, p.s, p.m,
                                       static_cast<uint8_t*>(h->oz_bdig.p), oz_b_ef(c), colmax,
                                       h->stream),
@@ -1256,6 +1331,10 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
             if (chunked)
                 ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
             oz_scan(c, A, r0, rows, ci == 0, check);
+            if (h->oz_stored)  // the chunk's rows in the atx block layout
+                h->launched(launch_oz_convert_tiles(A, r0, r0 + rows, p.m, p.n, p.lda, nullptr,
+                                                    oz_dig_atx(c), oz_row_ef(c), h->stream),
+                            "oz_convert_tiles");
             oz_ax(c, A, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
         }
         if (chunked) h->up_active = false;
@@ -1493,6 +1572,7 @@ int solve_tall_graph(rsvd_b200_handle* h, const double* A, const Plan& p,
     key.profiling = h->profiling;
     key.comm = p.sharded ? static_cast<const void*>(h->comm.get()) : nullptr;
     key.gen = g_ws_gen.load();
+    key.apass = oz_mode(h, p);
     rsvd_b200_handle::SolveGraph* hit = nullptr;
     rsvd_b200_handle::SolveGraph* lru = &h->graphs[0];
     for (auto& cand : h->graphs) {
@@ -2549,6 +2629,7 @@ long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key) {
     if (!strcmp(key, "graph_launches")) return h->graph_replays;
     if (!strcmp(key, "upload_aty_splits")) return h->upload_aty;
     if (!strcmp(key, "oz_passes")) return h->oz_passes;
+    if (!strcmp(key, "oz_stored_passes")) return h->oz_stored_passes;
     return -1;
 }
 
@@ -2682,15 +2763,27 @@ rsvd_b200_status rsvd_b200_debug_gemm_ozd(rsvd_b200_handle* h, int mn, const dou
         const long arows = mn ? K : M, acols = mn ? M : K;
         const size_t tb = oz_tiled_bytes(arows, acols);
         h->oz_adig.reserve(2 * tb);
-        h->oz_ef.reserve((size_t)(arows + 2 * NP + 8) * sizeof(int));
+        h->oz_ef.reserve((size_t)(arows + acols + 2 * NP + 8) * sizeof(int));
         int* row_ef = static_cast<int*>(h->oz_ef.p);
-        int* b_ef = row_ef + arows;
+        int* col_ef = row_ef + arows;
+        int* b_ef = col_ef + acols;
         int* scratch = b_ef + NP;
         uint8_t* dax = static_cast<uint8_t*>(h->oz_adig.p);
         uint8_t* datx = dax + tb;
-        h->launched(launch_oz_convert_rows(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
-                                           nullptr, h->stream),
-                    "oz_convert_rows");
+        static const bool rows_conv = getenv("RSVD_B200_OZD_CONVERT_ROWS") != nullptr;
+        if (rows_conv) {
+            h->launched(launch_oz_convert_rows(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
+                                               nullptr, h->stream),
+                        "oz_convert_rows");
+        } else {
+            h->oz_part.reserve(oz_scan_part_ints(arows, acols) * sizeof(int));
+            h->launched(launch_oz_scan(A, arows, acols, lda, row_ef, col_ef,
+                                       static_cast<int*>(h->oz_part.p), nullptr, h->stream, false),
+                        "oz_scan");
+            h->launched(launch_oz_convert_tiles(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
+                                                h->stream),
+                        "oz_convert_tiles");
+        }
         int nch, nf;
         oz_chunks(NP, &nch, &nf);
         h->oz_bdig.reserve(oz_digits_bytes(NP, K));

@@ -40,6 +40,33 @@ def test_oz_solve_vs_oracle(solver, port, m, n, k, p, q):
     check_against(res, ref.sigma, ref.u, ref.v, f"oz {m}x{n} k={k}")
 
 
+@pytest.mark.parametrize("stored", ["1", "0"])
+def test_oz_stored_digit_atx_passes(solver, port, monkeypatch, stored):
+    """The atx passes read A's stored digits (written by oz_convert_tiles right after the scan)
+    on the optimistic path, or form them in-kernel (RSVD_B200_OZ_STORED=0): both meet the
+    oracle bar, and the pass counts say which ran."""
+    import paper_2110_03423_b200 as P
+    monkeypatch.setenv("RSVD_B200_OZ_STORED", stored)
+    a = planted(3000, 640, 40, 1e5, 77)
+    q = 2
+    res = solver.randomized_ksvd(a, P.RsvdConfig(k=40, power_q=q, seed=11))
+    assert solver.last_info("robust_reruns") == 0
+    assert solver.last_info("oz_passes") == 2 * q + 2
+    assert solver.last_info("oz_stored_passes") == (q + 1 if stored == "1" else 0)
+    ref = port.randomized_ksvd(a, 40, power_q=q, seed=11)
+    check_against(res, ref.sigma, ref.u, ref.v, f"stored={stored}")
+
+
+def test_oz_robust_rerun_keeps_in_kernel_digits(solver):
+    """A CholeskyQR breakdown reruns robustly with the column-scaled in-kernel digits (better
+    relative accuracy of the small singular values than the stored, row-scaled ones)."""
+    import paper_2110_03423_b200 as P
+    a = planted(3000, 400, 20, 1e12, 13)
+    solver.randomized_ksvd(a, P.RsvdConfig(k=20, oversample=10, power_q=3, seed=1))
+    assert solver.last_info("robust_reruns") == 1
+    assert solver.last_info("oz_stored_passes") == 0
+
+
 def test_oz_badly_scaled_rows_and_columns(solver, port):
     """Rows and columns spanning 12 orders of magnitude: the per-row / per-column fixed-point
     scales keep every pass FP64-accurate in the normwise sense the SVD depends on."""
