@@ -168,6 +168,11 @@ size_t oz_tiled_bytes(long rows, long cols);
 cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows, long cols,
                                     long lda, uint8_t* dig_ax, uint8_t* dig_atx,
                                     const int* row_ef, cudaStream_t st);
+// row exponents + NaN/Inf flag + the atx-block digits of rows [r0, r1) in one pass over A
+// (row_ef output; no column maxima)
+cudaError_t launch_oz_scan_convert(const double* A, long r0, long r1, long rows, long cols,
+                                   long lda, uint8_t* dig_atx, int* row_ef, int* flag,
+                                   cudaStream_t st);
 cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
                                    long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
                                    int* flag, cudaStream_t st);

@@ -1330,11 +1330,14 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
             const long r0 = ci * rows_per, rows = std::min(p.m - r0, rows_per);
             if (chunked)
                 ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
-            oz_scan(c, A, r0, rows, ci == 0, check);
-            if (h->oz_stored)  // the chunk's rows in the atx block layout
-                h->launched(launch_oz_convert_tiles(A, r0, r0 + rows, p.m, p.n, p.lda, nullptr,
-                                                    oz_dig_atx(c), oz_row_ef(c), h->stream),
-                            "oz_convert_tiles");
+            if (h->oz_stored)  // row scales, NaN check and the atx-block digits in one pass
+                h->launched(launch_oz_scan_convert(A, r0, r0 + rows, p.m, p.n, p.lda,
+                                                   oz_dig_atx(c), oz_row_ef(c),
+                                                   check ? c.flags + kFlagNonfinite : nullptr,
+                                                   h->stream),
+                            "oz_scan_convert");
+            else
+                oz_scan(c, A, r0, rows, ci == 0, check);
             oz_ax(c, A, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
         }
         if (chunked) h->up_active = false;
