@@ -879,7 +879,8 @@ __global__ void __launch_bounds__(256) oz_convert_tiles_kernel(
     }
 }
 
-// Row exponents, NaN/Inf check and the atx-block digits in one pass over A (the optimistic
+// Row exponents, NaN/Inf check and the stored digits (atx blocks, optionally ax tiles) in one
+// pass over A (the optimistic
 // pipeline's stored-digit atx passes need no column maxima): persistent CTAs (3 per SM) take
 // 4-row groups; pass 1 (two warps per row) reduces each row's maximum exponent, pass 2
 // re-reads the group — 128 KB per CTA, 57 MB in flight, so from L2 — and writes every warp's
@@ -894,12 +895,13 @@ constexpr int kScRows = OZ_SC_ROWS;            // rows per group: 8 (2 CTAs / SM
 constexpr int kScCtas = kScRows == 8 ? 2 : 3;  // resident CTAs per SM (the L2 working set)
 __global__ void __launch_bounds__(256, kScCtas) oz_scan_convert_kernel(
     const double* __restrict__ A, long r0, long r1, long rows, long cols, long lda,
-    uint8_t* __restrict__ dig_atx, int* __restrict__ row_ef, int* __restrict__ flag) {
+    uint8_t* __restrict__ dig_ax, uint8_t* __restrict__ dig_atx, int* __restrict__ row_ef,
+    int* __restrict__ flag) {
     __shared__ int ef_sh[kScRows];
     __shared__ uint32_t mx_sh[8];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     constexpr int kWpr = 8 / kScRows;  // warps per row in pass 1
-    const long JB = (cols + 127) / 128;
+    const long JB = (cols + 127) / 128, KT = (cols + 31) / 32;
     bool bad = false;
     for (long g0 = r0 + (long)blockIdx.x * kScRows; g0 < r1; g0 += (long)gridDim.x * kScRows) {
         {  // pass 1: warps w, w + kScRows, ... -> row g0 + w % kScRows, interleaved columns
@@ -972,6 +974,15 @@ __global__ void __launch_bounds__(256, kScCtas) oz_scan_convert_kernel(
             for (int i = 0; i < kDigits; ++i)
                 __stcs(reinterpret_cast<uint4*>(at + i * 4096),
                        make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]));
+            const long kt = c0 >> 5;
+            if (dig_ax && kt < KT) {  // the ax tile (4 rows x 32 B of each plane per k-tile)
+                uint8_t* ax = dig_ax + (((r >> 7) * KT + kt) * kDigits) * 4096 +
+                              sw32((uint32_t)(r & 127), (uint32_t)(chunk & 1));
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i)
+                    __stcs(reinterpret_cast<uint4*>(ax + i * 4096),
+                           make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]));
+            }
         }
         __syncthreads();  // ef_sh is rewritten by the next group
     }
@@ -1102,10 +1113,20 @@ __global__ void __launch_bounds__(kDsThreads, 1)
             mbar_wait(&full[s], (it / kDsStages) & 1);
             fence_after();
             if (elect_one()) {
+#ifndef OZD_AX_CP
                 if constexpr (!MN) {
-                    // K-major A digits: copy the 7 tiles into a TMEM buffer (3 after the
-                    // accumulators, in-order with the MMAs) and run the MMAs with A from TMEM,
-                    // which the tensor core reads faster than shared memory at these widths
+                    // K-major A digits straight from shared memory (SW32): 1.81 ms per C2 pass,
+                    // against 2.26 ms copying the 7 tiles into TMEM first (tcgen05.cp bound)
+#pragma unroll
+                    for (int j = 0; j < kNM; ++j)
+                        mma_i8(tmem + (uint32_t)(mdc[j] * N), sdesc(st + (uint32_t)mi[j] * kDsADig),
+                               bd + (((uint64_t)mp0[j] * pb) >> 4), idv[j],
+                               (it > 0 || j > 1) ? 1u : 0u);
+                } else
+#endif
+                if constexpr (!MN) {
+                    // (OZD_AX_CP) K-major A digits: copy the 7 tiles into a TMEM buffer (3 after
+                    // the accumulators, in-order with the MMAs) and run the MMAs with A from TMEM
                     const uint32_t tb = tmem + (uint32_t)(kGroups * N) + (uint32_t)(it % 3) * 56u;
 #pragma unroll
                     for (int i = 0; i < kDigits; ++i)
@@ -1464,6 +1485,10 @@ size_t oz_scan_part_ints(long rows, long cols) {
     return (size_t)(cb * rows + rb * cols);
 }
 
+size_t oz_ax_bytes(long rows, long cols) {
+    return (size_t)((rows + 127) / 128) * ((cols + 31) / 32) * oz::kDigits * oz::kDsADig;
+}
+
 size_t oz_atx_bytes(long rows, long cols) {  // rows padded to whole 128-row blocks (convert)
     return (size_t)((rows + 127) / 128 * 4) * ((cols + 127) / 128) * oz::kDigits * oz::kDsADig;
 }
@@ -1504,16 +1529,16 @@ cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows
 }
 
 cudaError_t launch_oz_scan_convert(const double* A, long r0, long r1, long rows, long cols,
-                                   long lda, uint8_t* dig_atx, int* row_ef, int* flag,
-                                   cudaStream_t st) {
+                                   long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
+                                   int* flag, cudaStream_t st) {
     if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1) || (r0 & 127)) return cudaErrorInvalidValue;
     if (r1 >= rows) r1 = (rows + 127) / 128 * 128;  // the last chunk also zeroes the pad rows
     else if (r1 & 127) return cudaErrorInvalidValue;
     if (r1 <= r0) return cudaSuccess;
     const long groups = (r1 - r0) / oz::kScRows;
     const unsigned grid = (unsigned)std::min<long>(groups, (long)oz::kScCtas * 148);
-    oz::oz_scan_convert_kernel<<<grid, 256, 0, st>>>(A, r0, r1, rows, cols, lda, dig_atx, row_ef,
-                                                     flag);
+    oz::oz_scan_convert_kernel<<<grid, 256, 0, st>>>(A, r0, r1, rows, cols, lda, dig_ax,
+                                                     dig_atx, row_ef, flag);
     return cudaGetLastError();
 }
 

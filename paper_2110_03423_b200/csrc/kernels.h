@@ -168,11 +168,11 @@ size_t oz_tiled_bytes(long rows, long cols);
 cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows, long cols,
                                     long lda, uint8_t* dig_ax, uint8_t* dig_atx,
                                     const int* row_ef, cudaStream_t st);
-// row exponents + NaN/Inf flag + the atx-block digits of rows [r0, r1) in one pass over A
-// (row_ef output; no column maxima)
+// row exponents + NaN/Inf flag + the stored digits (atx blocks; ax tiles unless dig_ax is
+// null) of rows [r0, r1) in one pass over A (row_ef output; no column maxima)
 cudaError_t launch_oz_scan_convert(const double* A, long r0, long r1, long rows, long cols,
-                                   long lda, uint8_t* dig_atx, int* row_ef, int* flag,
-                                   cudaStream_t st);
+                                   long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
+                                   int* flag, cudaStream_t st);
 cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
                                    long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
                                    int* flag, cudaStream_t st);
@@ -199,7 +199,9 @@ struct GemmOzd {
 };
 cudaError_t launch_gemm_ozd(const GemmOzd& p, cudaStream_t st);
 // bytes of the stored atx blocks of A (rows x cols): 4 ceil(rows / 128) x ceil(cols / 128) blocks
-size_t oz_atx_bytes(long rows, long cols);  // rows rounded up to 128
+size_t oz_atx_bytes(long rows, long cols);
+// bytes of the stored ax tiles of A: ceil(rows / 128) x ceil(cols / 32) blocks
+size_t oz_ax_bytes(long rows, long cols);  // rows rounded up to 128
 
 cudaError_t launch_gemm_ax(const GemmAx& p, cudaStream_t st);
 cudaError_t launch_gemm_atx(const GemmAtx& p, cudaStream_t st);

@@ -629,19 +629,19 @@ bool oz_on(const Plan& p) {
     return mode == 2 || (double)p.m * (double)p.n >= (double)(1L << 26);
 }
 
-// Stored digits for the atx passes (default for the emulated path; RSVD_B200_OZ_STORED=0
-// disables): right after each row chunk's scan, oz_convert_tiles writes A's row-scaled digits
-// in the atx block layout of gemm_ozd (one streaming pass, ~0.9 of HBM bandwidth), and the atx
-// passes ((A^T Q)^T, Q^T A) read those with A's row scales folded into W — no FP64 tile, no
-// conversion, no duplicated conversion by the column-chunk CTAs (1.59 against 2.64 ms per C2
-// pass). The ax passes keep the in-kernel digits: their stored form saved too little to pay
-// for writing a second layout. Needs oz_atx_bytes (0.88 x the FP64 A) of HBM; without the room
-// the atx passes stay in-kernel. Accuracy: normwise FP64 per column of W' (the row scales
-// folded in), against per column of A for the in-kernel digits.
+// Stored digits (default for the emulated path; RSVD_B200_OZ_STORED=0 disables): one fused
+// pass over A (oz_scan_convert, per row chunk as it lands) yields the row scales, the NaN/Inf
+// check and A's row-scaled digits in the two tiled layouts of gemm_ozd, and every pass over A
+// then reads digits instead of FP64 — no conversion inside the GEMMs, none duplicated by the
+// column-chunk CTAs (C2: 1.81 / 1.59 ms per ax / atx pass against 2.61 / 2.64 in-kernel; the
+// atx passes fold A's row scales into W). Needs oz_ax_bytes + oz_atx_bytes (1.75 x the FP64 A)
+// of HBM; without the room the passes stay in-kernel. Accuracy of the atx passes: normwise
+// FP64 per column of W' (the row scales folded in), against per column of A in-kernel — so the
+// robust rerun (inputs that break CholeskyQR) keeps the in-kernel digits.
 bool oz_stored_fits(rsvd_b200_handle* h, const Plan& p) {
     const char* e = getenv("RSVD_B200_OZ_STORED");
     if (e && atoi(e) == 0) return false;
-    const size_t need = oz_atx_bytes(p.m, p.n);
+    const size_t need = oz_ax_bytes(p.m, p.n) + oz_atx_bytes(p.m, p.n);
     if (need <= h->oz_adig.bytes) return true;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
@@ -1066,7 +1066,7 @@ Ctx begin_run(rsvd_b200_handle* h, const Plan& p, bool robust) {
         // small singular values' relative accuracy better (tools/probe/stored_accuracy.py:
         // 5.4e-11 against 1.8e-10 at sigma ratio 2.5e-8)
         if (!robust && oz_mode(h, p) == 2) {
-            h->oz_adig.reserve(oz_atx_bytes(p.m, p.n));
+            h->oz_adig.reserve(oz_ax_bytes(p.m, p.n) + oz_atx_bytes(p.m, p.n));
             h->oz_stored = true;
         }
     }
@@ -1098,14 +1098,50 @@ void oz_scan(const Ctx& c, const double* A, long r0, long rows, bool first, bool
 
 // Digits of the n-side operand Xt (NP x ldn; rows >= s zero) for the ax passes.
 void oz_digits_xt(const Ctx& c, const double* Xt) {
+    int nch, nf;  // the stored-digit GEMM reads the planes tiled per column chunk
+    oz_chunks(c.p.NP, &nch, &nf);
     c.h->launched(launch_oz_digits_rows(Xt, c.p.ldn, c.p.NP, c.p.s, c.p.n,
                                         static_cast<uint8_t*>(c.h->oz_bdig.p), oz_b_ef(c),
-                                        c.h->stream),
+                                        c.h->stream, c.h->oz_stored ? nf : 0),
                   "oz_digits_rows");
 }
 
-// A's stored digits (oz_adig): the atx blocks of gemm_ozd
-uint8_t* oz_dig_atx(const Ctx& c) { return static_cast<uint8_t*>(c.h->oz_adig.p); }
+// A's stored digits (oz_adig): the ax tiles, then the atx blocks of gemm_ozd
+uint8_t* oz_dig_ax(const Ctx& c) { return static_cast<uint8_t*>(c.h->oz_adig.p); }
+uint8_t* oz_dig_atx(const Ctx& c) { return oz_dig_ax(c) + oz_ax_bytes(c.p.m, c.p.n); }
+
+// Y[r0 : r0 + rows] (NP wide) = A[r0 : r0 + rows] X from the stored ax tiles (r0 % 128 == 0),
+// Xt's digits prepared tiled (oz_digits_xt).
+void ozd_ax(const Ctx& c, long r0, long rows, double* Y, const char* tag, double flops) {
+    rsvd_b200_handle* h = c.h;
+    const Plan& p = c.p;
+    GemmOzd g;
+    g.a_inner = (p.n + 31) / 32;
+    g.adig = oz_dig_ax(c) + (size_t)(r0 / 128) * g.a_inner * oz_ax_bytes(128, 32);
+    g.M = rows, g.K = p.n, g.a_ef = oz_row_ef(c) + r0;
+    g.bdig = static_cast<const uint8_t*>(h->oz_bdig.p), g.b_ef = oz_b_ef(c), g.NP = p.NP;
+    g.abort = h->abort_ptr;
+    const int splits = oz_splits(rows, p.NP, p.n, false);
+    if (r0 == 0) {
+        h->oz_passes += 1;
+        h->oz_stored_passes += 1;
+    }
+    h->kernel_begin(tag, flops);
+    if (splits == 1) {
+        g.out = Y + r0 * p.NP, g.ldo = p.NP;
+        h->launched(launch_gemm_ozd(g, h->stream), "gemm_ozd");
+        h->kernel_end(tag);
+        return;
+    }
+    const long slab = rows * p.NP;
+    if (h->part.bytes < (size_t)splits * slab * sizeof(double))
+        fail(RSVD_B200_ALLOC_ERROR, "split-K workspace too small");
+    g.out = h->part.d(), g.ldo = p.NP, g.splits = splits, g.split_stride = slab;
+    h->launched(launch_gemm_ozd(g, h->stream), "gemm_ozd(split)");
+    h->kernel_end(tag);
+    h->launched(launch_reduce_partials(h->part.d(), slab, splits, Y + r0 * p.NP, slab, h->stream),
+                "reduce_partials");
+}
 
 // Y (rows x NP) = A[r0 : r0 + rows] X with the digits of Xt already prepared.
 void oz_ax(const Ctx& c, const double* A, long r0, long rows, double* Y, const char* tag,
@@ -1330,15 +1366,17 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
             const long r0 = ci * rows_per, rows = std::min(p.m - r0, rows_per);
             if (chunked)
                 ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
-            if (h->oz_stored)  // row scales, NaN check and the atx-block digits in one pass
+            if (h->oz_stored) {  // row scales, NaN check and both digit layouts in one pass
                 h->launched(launch_oz_scan_convert(A, r0, r0 + rows, p.m, p.n, p.lda,
-                                                   oz_dig_atx(c), oz_row_ef(c),
+                                                   oz_dig_ax(c), oz_dig_atx(c), oz_row_ef(c),
                                                    check ? c.flags + kFlagNonfinite : nullptr,
                                                    h->stream),
                             "oz_scan_convert");
-            else
+                ozd_ax(c, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
+            } else {
                 oz_scan(c, A, r0, rows, ci == 0, check);
-            oz_ax(c, A, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
+                oz_ax(c, A, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
+            }
         }
         if (chunked) h->up_active = false;
         h->gram_ready = false;
@@ -1419,7 +1457,10 @@ void power_iterate_dev(const Ctx& c, const double* A, size_t q, bool materialize
         h->mark("power_ax");
         if (oz_on(p)) {
             oz_digits_xt(c, h->xt.d());
-            oz_ax(c, A, 0, p.m, h->y.d(), "gemm_A", 2.0 * p.m * p.n * p.s);  // Y = A Z
+            if (h->oz_stored)
+                ozd_ax(c, 0, p.m, h->y.d(), "gemm_A", 2.0 * p.m * p.n * p.s);  // Y = A Z
+            else
+                oz_ax(c, A, 0, p.m, h->y.d(), "gemm_A", 2.0 * p.m * p.n * p.s);  // Y = A Z
             h->gram_ready = false;
         } else {
             h->gram_ready = gemm_ax(h, A, p.m, p.n, p.lda, h->xt.d(), p.ldn, p.NP, h->y.d(),
