@@ -565,6 +565,7 @@ def run_ours(args):
     p1.synchronize()
     prof_ms = p0.elapsed_time(p1)
     stats = solver.kernel_stats("gemm_A")
+    conv_stats = solver.kernel_stats("oz_convert")
     solver.set_profiling(0)
     barrier()
     step_ms = dev_ms / args.steps
@@ -632,8 +633,18 @@ def run_ours(args):
             peak = peak_i8
             peak_src = ("tcgen05 kind::i8 M128 N256 K32 issue-rate probe (rsvd_b200_imma_peak), "
                         "measured in this run; MEASURED_PEAKS.json has no INT8 entry")
+            stored = solver.last_info("oz_stored_passes") > 0
             kernel = ("gemm_A (FP64 passes over A emulated on the INT8 tensor cores: Ozaki "
-                      "scheme, 7 balanced base-256 digits, 28 digit products; ax + atx)")
+                      "scheme, 7 balanced base-256 digits, 28 digit products; ax + atx"
+                      + (", from A's digit planes stored once per solve)" if stored else ")"))
+            if stored and conv_stats["count"]:
+                fp64_equiv["digit_conversion"] = {
+                    "kernel": "oz_scan_convert (row scales, NaN/Inf check and both stored "
+                              "digit layouts in one pass over A; HBM-bound)",
+                    "ms_per_solve": round(conv_stats["ms"] / args.steps, 4),
+                    "bytes_per_solve": m * n * 8 + 2 * m * n * 7,
+                    "GBps": round((m * n * 8 + 2 * m * n * 7) / (conv_stats["ms"] / args.steps * 1e-3)
+                                  / 1e9, 1)}
         roof = {"bound": "tensor", "kernel": kernel,
                 "achieved": round(achieved, 3) if achieved else None, "peak": round(peak, 3),
                 "unit": "TOPS (INT8)" if oz else "TFLOP/s",

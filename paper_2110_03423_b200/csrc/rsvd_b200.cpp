@@ -1367,11 +1367,13 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
             if (chunked)
                 ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
             if (h->oz_stored) {  // row scales, NaN check and both digit layouts in one pass
+                h->kernel_begin("oz_convert", 0.0);
                 h->launched(launch_oz_scan_convert(A, r0, r0 + rows, p.m, p.n, p.lda,
                                                    oz_dig_ax(c), oz_dig_atx(c), oz_row_ef(c),
                                                    check ? c.flags + kFlagNonfinite : nullptr,
                                                    h->stream),
                             "oz_scan_convert");
+                h->kernel_end("oz_convert");
                 ozd_ax(c, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
             } else {
                 oz_scan(c, A, r0, rows, ci == 0, check);
