@@ -650,7 +650,8 @@ def run_ours(args):
                 "unit": "TOPS (INT8)" if oz else "TFLOP/s",
                 "frac": round(achieved / peak, 4) if achieved else None,
                 "traffic": traffic.get("gemm_A_bytes_per_launch") if traffic else None,
-                "traffic_algorithmic": m * n * (4 if f32 else 8),
+                "traffic_algorithmic": m * n * (4 if f32 else 7 if (oz and solver.last_info(
+                    "oz_stored_passes") > 0) else 8),
                 "peak_source": peak_src,
                 "launches_timed": stats["count"], "ms_per_launch": round(per_launch_ms, 4),
                 "share_of_step": round(stats["ms"] / prof_ms, 4) if prof_ms else None,
