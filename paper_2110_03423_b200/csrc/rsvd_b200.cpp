@@ -1366,13 +1366,21 @@ void sketch_dev(const Ctx& c, const double* A, uint64_t seed, bool check, bool p
             const long r0 = ci * rows_per, rows = std::min(p.m - r0, rows_per);
             if (chunked)
                 ck(cudaStreamWaitEvent(h->stream, h->up_ev[ci], 0), "wait for chunk upload");
-            if (h->oz_stored) {  // row scales, NaN check and both digit layouts in one pass
+            if (h->oz_stored) {  // row scales, NaN check and both digit layouts
                 h->kernel_begin("oz_convert", 0.0);
-                h->launched(launch_oz_scan_convert(A, r0, r0 + rows, p.m, p.n, p.lda,
-                                                   oz_dig_ax(c), oz_dig_atx(c), oz_row_ef(c),
-                                                   check ? c.flags + kFlagNonfinite : nullptr,
-                                                   h->stream),
-                            "oz_scan_convert");
+                if (p.n <= 4608) {  // one pass: the re-read of 4-row groups stays in L2
+                    h->launched(launch_oz_scan_convert(A, r0, r0 + rows, p.m, p.n, p.lda,
+                                                       oz_dig_ax(c), oz_dig_atx(c), oz_row_ef(c),
+                                                       check ? c.flags + kFlagNonfinite : nullptr,
+                                                       h->stream),
+                                "oz_scan_convert");
+                } else {  // wide rows (C3, C5): scan, then the streaming tile conversion
+                    oz_scan(c, A, r0, rows, ci == 0, check);
+                    h->launched(launch_oz_convert_tiles(A, r0, r0 + rows, p.m, p.n, p.lda,
+                                                        oz_dig_ax(c), oz_dig_atx(c), oz_row_ef(c),
+                                                        h->stream),
+                                "oz_convert_tiles");
+                }
                 h->kernel_end("oz_convert");
                 ozd_ax(c, r0, rows, h->y.d(), "gemm_A", 2.0 * rows * n * s);
             } else {
