@@ -892,7 +892,10 @@ __global__ void __launch_bounds__(256) oz_convert_tiles_kernel(
 #define OZ_SC_ROWS 4
 #endif
 constexpr int kScRows = OZ_SC_ROWS;            // rows per group: 8 (2 CTAs / SM) or 4 (3 / SM)
-constexpr int kScCtas = kScRows == 8 ? 2 : 3;  // resident CTAs per SM (the L2 working set)
+#ifndef OZ_SC_CTAS
+#define OZ_SC_CTAS (kScRows == 8 ? 2 : 3)
+#endif
+constexpr int kScCtas = OZ_SC_CTAS;  // resident CTAs per SM (the L2 working set)
 __global__ void __launch_bounds__(256, kScCtas) oz_scan_convert_kernel(
     const double* __restrict__ A, long r0, long r1, long rows, long cols, long lda,
     uint8_t* __restrict__ dig_ax, uint8_t* __restrict__ dig_atx, int* __restrict__ row_ef,
