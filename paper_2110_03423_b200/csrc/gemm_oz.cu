@@ -742,88 +742,12 @@ __global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __res
     }
 }
 
-// ======================================================= stored digits (convert once per solve)
-// A (rows x cols, lda) -> 7 row-scaled digit planes, written twice, pre-tiled and pre-swizzled
-// for the two pass shapes so that a pass stage is one contiguous 28 KB bulk copy:
-//   ax  tiles: row block rb (128 rows) x k-tile kt (32 columns): [plane][128 rows x 32 B] in
-//              the SW32 K-major layout, block (rb * KT + kt), KT = ceil(cols / 32);
-//   atx tiles: k block kb (32 rows) x column block jb (128 columns): [plane][32 rows x 128 B]
-//              in the SW128 MN-major layout, block (kb * JB + jb), JB = ceil(cols / 128).
-// Also row_ef[r] and the NaN/Inf flag. Rows [r0, r1) (absolute); rows >= `rows` (up to the
-// next 128) and columns >= cols (up to the next 128) are written as zero digits. Thread t holds
-// elements [16 t, 16 t + 16) of a row in registers, so A is read once.
-__global__ void __launch_bounds__(1024) oz_convert_rows_kernel(
-    const double* __restrict__ A, long r0, long r1, long rows, long cols, long lda,
-    uint8_t* __restrict__ dig_ax, uint8_t* __restrict__ dig_atx, int* __restrict__ row_ef,
-    int* __restrict__ flag) {
-    __shared__ uint32_t red[32];
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5, nw = (blockDim.x + 31) >> 5;
-    const long KT = (cols + 31) / 32, JB = (cols + 127) / 128;
-    // whole warps; each layout is written up to its own block edge (KT 32 <= JB 128 columns)
-    const bool w_ax = 16L * t < KT * 32, w_at = 16L * t < JB * 128;
-    bool bad = false;
-    for (long r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
-        const double* row = A + r * lda;
-        const long c0 = 16L * t;
-        double v[16];
-        if (r < rows && c0 + 16 <= cols) {
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-                const double2 x = __ldcs(reinterpret_cast<const double2*>(row + c0 + e));
-                v[e] = x.x;
-                v[e + 1] = x.y;
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = (r < rows && c0 + e < cols) ? row[c0 + e] : 0.0;
-        }
-        uint32_t m = 0;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) m = max(m, (uint32_t)__double2hiint(v[e]) & 0x7ff00000u);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) red[w] = m;
-        __syncthreads();
-        uint32_t mm = 0;
-        for (int i = 0; i < nw; ++i) mm = max(mm, red[i]);
-        __syncthreads();
-        const int ef = (int)(mm >> 20);
-        bad |= ef == 0x7ff;
-        if (t == 0 && r < rows) row_ef[r] = ef;
-        double f1, f2;
-        fixed_scale(ef, f1, f2);
-        uint32_t pw[kDigits][4];
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-            uint64_t wd[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) wd[e] = digits_scaled(v[4 * qd + e], f1, f2);
-            uint32_t pl[kDigits];
-            planes4(wd, pl);
-#pragma unroll
-            for (int i = 0; i < kDigits; ++i) pw[i][qd] = pl[i] ^ 0x80808080u;
-        }
-        const long rb = r >> 7, kb = r >> 5;
-        const uint32_t rl = (uint32_t)(r & 127), kl = (uint32_t)(r & 31);
-        uint8_t* ax = dig_ax + ((rb * KT + (c0 >> 5)) * kDigits) * 4096 + sw32(rl, (c0 >> 4) & 1);
-        const uint32_t chunk = (uint32_t)((c0 >> 4) & 7);
-        uint8_t* at = dig_atx + ((kb * JB + (c0 >> 7)) * kDigits) * 4096 + kl * 128 +
-                      ((chunk ^ (kl & 7)) << 4);
-#pragma unroll
-        for (int i = 0; i < kDigits; ++i) {
-            const uint4 q = make_uint4(pw[i][0], pw[i][1], pw[i][2], pw[i][3]);
-            if (w_ax) __stcs(reinterpret_cast<uint4*>(ax + i * 4096), q);
-            if (w_at) __stcs(reinterpret_cast<uint4*>(at + i * 4096), q);
-        }
-    }
-    if (flag && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flag, 1);
-}
 
 // Streaming form of the same conversion, with the row exponents given (oz_scan): one CTA per
 // 128-row x 128-column block of A (256 threads; thread -> 16-column chunk t & 7 of row
 // 32 it + t / 8, it = 0..3), so that every warp store lands on contiguous bytes of both tiled
 // layouts (4 rows x 128 B of a SW32 ax tile, 4 rows x 128 B of an atx block) instead of 32
-// scattered 16-byte pieces (oz_convert_rows_kernel: 3.2 TB/s of combined traffic). Rows
+// scattered 16-byte pieces (a row-per-CTA conversion measured 3.2 TB/s of combined traffic). Rows
 // >= `rows` and columns >= `cols` are zero digits; row block rb = blockIdx.y + r0 / 128.
 // dig_ax may be null (only the atx blocks: the pipeline's stored-digit atx passes).
 __global__ void __launch_bounds__(256) oz_convert_tiles_kernel(
@@ -993,7 +917,8 @@ __global__ void __launch_bounds__(256, kScCtas) oz_scan_convert_kernel(
 }
 
 // ------------------------------------------------------------ GEMM from stored digits
-// Both pass shapes from A's row-scaled digit planes (oz_convert_rows) and the small operand's
+// Both pass shapes from A's row-scaled digit planes (oz_scan_convert / oz_convert_tiles) and the
+// small operand's
 // digit planes:
 //   MN = false (ax):  Y (M x NP) = A X. A operand = 128 rows x 32 k of each plane (K-major,
 //                     SW32 TMA boxes); out = T 2^(a_ef[row] + b_ef[c] - 2104).
@@ -1503,20 +1428,6 @@ size_t oz_tiled_bytes(long rows, long cols) {
     return std::max(ax, at);
 }
 
-cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
-                                   long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
-                                   int* flag, cudaStream_t st) {
-    if (cols > 16L * 1024 || (reinterpret_cast<uintptr_t>(A) & 15) || (lda & 1))
-        return cudaErrorInvalidValue;
-    if (r1 >= rows) r1 = (rows + 127) / 128 * 128;  // the last chunk also zeroes the pad rows
-    else if ((r1 & 127) || (r0 & 127)) return cudaErrorInvalidValue;
-    // 16 columns each over whole 128-column blocks, rounded up to whole warps
-    const int threads = (int)(((cols + 127) / 128 * 8 + 31) / 32 * 32);
-    const unsigned grid = (unsigned)std::min<long>(r1 - r0, 148L * std::max(1, 2048 / threads));
-    oz::oz_convert_rows_kernel<<<grid, threads, 0, st>>>(A, r0, r1, rows, cols, lda, dig_ax,
-                                                        dig_atx, row_ef, flag);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows, long cols,
                                     long lda, uint8_t* dig_ax, uint8_t* dig_atx,

@@ -173,9 +173,7 @@ cudaError_t launch_oz_convert_tiles(const double* A, long r0, long r1, long rows
 cudaError_t launch_oz_scan_convert(const double* A, long r0, long r1, long rows, long cols,
                                    long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
                                    int* flag, cudaStream_t st);
-cudaError_t launch_oz_convert_rows(const double* A, long r0, long r1, long rows, long cols,
-                                   long lda, uint8_t* dig_ax, uint8_t* dig_atx, int* row_ef,
-                                   int* flag, cudaStream_t st);
+
 // INT8 GEMM from stored digits (gemm_oz.cu gemm_ozd_kernel):
 //   mn = false: out (M x NP) = A X, adig = dig_ax (a_inner = ceil(K / 32)), a_ef[M] (row_ef).
 //   mn = true:  out = A^T W' with A (K x M) as stored, adig = dig_atx (a_inner = ceil(M / 128)),

@@ -2824,20 +2824,13 @@ rsvd_b200_status rsvd_b200_debug_gemm_ozd(rsvd_b200_handle* h, int mn, const dou
         int* scratch = b_ef + NP;
         uint8_t* dax = static_cast<uint8_t*>(h->oz_adig.p);
         uint8_t* datx = dax + tb;
-        static const bool rows_conv = getenv("RSVD_B200_OZD_CONVERT_ROWS") != nullptr;
-        if (rows_conv) {
-            h->launched(launch_oz_convert_rows(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
-                                               nullptr, h->stream),
-                        "oz_convert_rows");
-        } else {
-            h->oz_part.reserve(oz_scan_part_ints(arows, acols) * sizeof(int));
-            h->launched(launch_oz_scan(A, arows, acols, lda, row_ef, col_ef,
-                                       static_cast<int*>(h->oz_part.p), nullptr, h->stream, false),
-                        "oz_scan");
-            h->launched(launch_oz_convert_tiles(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
-                                                h->stream),
-                        "oz_convert_tiles");
-        }
+        h->oz_part.reserve(oz_scan_part_ints(arows, acols) * sizeof(int));
+        h->launched(launch_oz_scan(A, arows, acols, lda, row_ef, col_ef,
+                                   static_cast<int*>(h->oz_part.p), nullptr, h->stream, false),
+                    "oz_scan");
+        h->launched(launch_oz_convert_tiles(A, 0, arows, arows, acols, lda, dax, datx, row_ef,
+                                            h->stream),
+                    "oz_convert_tiles");
         int nch, nf;
         oz_chunks(NP, &nch, &nf);
         h->oz_bdig.reserve(oz_digits_bytes(NP, K));

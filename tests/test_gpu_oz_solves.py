@@ -57,6 +57,20 @@ def test_oz_stored_digit_atx_passes(solver, port, monkeypatch, stored):
     check_against(res, ref.sigma, ref.u, ref.v, f"stored={stored}")
 
 
+def test_oz_wide_rows_scan_then_tile_conversion(solver, port):
+    """Rows wider than 4608 columns are converted by the scan + the streaming tile kernel (the
+    fused pass's L2 re-read would not fit); same oracle bar."""
+    import paper_2110_03423_b200 as P
+    rng = np.random.default_rng(31)
+    r = 120
+    a = (rng.standard_normal((6000, r)) * np.exp(-np.arange(r) / 12.0)) @ rng.standard_normal(
+        (r, 4736)) + 1e-9 * rng.standard_normal((6000, 4736))
+    res = solver.randomized_ksvd(a, P.RsvdConfig(k=24, power_q=1, seed=5))
+    assert solver.last_info("oz_stored_passes") == 4
+    ref = port.randomized_ksvd(a, 24, power_q=1, seed=5)
+    check_against(res, ref.sigma, ref.u, ref.v, "wide rows")
+
+
 def test_oz_robust_rerun_keeps_in_kernel_digits(solver):
     """A CholeskyQR breakdown reruns robustly with the column-scaled in-kernel digits (better
     relative accuracy of the small singular values than the stored, row-scaled ones)."""
