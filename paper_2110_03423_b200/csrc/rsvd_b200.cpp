@@ -1110,6 +1110,19 @@ void oz_digits_xt(const Ctx& c, const double* Xt) {
 uint8_t* oz_dig_ax(const Ctx& c) { return static_cast<uint8_t*>(c.h->oz_adig.p); }
 uint8_t* oz_dig_atx(const Ctx& c) { return oz_dig_ax(c) + oz_ax_bytes(c.p.m, c.p.n); }
 
+// the side stream (copy_stream: host uploads) and `events` chunk events on it
+void ensure_side_stream(rsvd_b200_handle* h, long events) {
+    if (!h->copy_stream) {
+        ck(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "stream create");
+        ck(cudaEventCreateWithFlags(&h->up_start, cudaEventDisableTiming), "event create");
+    }
+    while ((long)h->up_ev.size() < events) {
+        cudaEvent_t e;
+        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+        h->up_ev.push_back(e);
+    }
+}
+
 // Y[r0 : r0 + rows] (NP wide) = A[r0 : r0 + rows] X from the stored ax tiles (r0 % 128 == 0),
 // Xt's digits prepared tiled (oz_digits_xt).
 void ozd_ax(const Ctx& c, long r0, long rows, double* Y, const char* tag, double flops) {
@@ -2102,16 +2115,8 @@ static void upload_a(rsvd_b200_handle* h, const void* av, long m, long n, long l
            "H2D of A");
         return;
     }
-    if (!h->copy_stream) {
-        ck(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "stream create");
-        ck(cudaEventCreateWithFlags(&h->up_start, cudaEventDisableTiming), "event create");
-    }
     const long chunks = (m + chunk_rows - 1) / chunk_rows;
-    while ((long)h->up_ev.size() < chunks) {
-        cudaEvent_t e;
-        ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
-        h->up_ev.push_back(e);
-    }
+    ensure_side_stream(h, chunks);
     // the copies must not overtake earlier work on the solve stream that reads a_copy
     ck(cudaEventRecord(h->up_start, h->stream), "event record");
     ck(cudaStreamWaitEvent(h->copy_stream, h->up_start, 0), "stream wait");
