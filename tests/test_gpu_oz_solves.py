@@ -104,12 +104,14 @@ def test_oz_sharded_matches_oracle(port):
     check_sharded(out, 3, ref, 4000)
 
 
-def test_oz_chunked_upload_bit_identical(solver, monkeypatch):
-    """Host-buffer solves scan and sketch A chunk by chunk as it lands; the row scales are
-    chunk-local and the chunks are whole tiles, so the result equals the device solve's."""
+@pytest.mark.parametrize("m", [37888, 37000])
+def test_oz_chunked_upload_bit_identical(solver, monkeypatch, m):
+    """Host-buffer solves convert and sketch A chunk by chunk as it lands; the row scales are
+    chunk-local and the chunks are whole tiles (the last one partial when m % 128 != 0, its
+    pad rows zero digits), so the result equals the device solve's."""
     import torch
     import paper_2110_03423_b200 as P
-    a = planted(37888, 512, 64, 1e4, 4)
+    a = planted(m, 512, 64, 1e4, 4)
     cfg = P.RsvdConfig(k=64, oversample=10, power_q=2, seed=5)
     monkeypatch.setenv("RSVD_B200_UPLOAD_CHUNK_MB", "4")
     res = solver.randomized_ksvd(a, cfg)
