@@ -933,7 +933,6 @@ constexpr int kDsThreads = 192;
 constexpr uint32_t kDsADig = BM * BK;                       // 4 KB per A digit tile
 constexpr uint32_t kDsBPlane = 64 * BK;                     // N <= 64
 constexpr uint32_t kDsStage = kDigits * kDsADig + kDigits * kDsBPlane;  // 43008 B
-constexpr int kDsMaxN = 64;
 
 __device__ __forceinline__ uint64_t sdesc_mn128(uint32_t saddr) {
     // MN-major SWIZZLE_128B: 128 B of M per row (one atom wide), 8-row (K) atoms 1024 B apart
