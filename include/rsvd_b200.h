@@ -294,7 +294,9 @@ long rsvd_b200_last_launch_count(rsvd_b200_handle* h);
  * cumulative over the handle, "graph_launches" (device-resident solves that ran as one
  * launch of the handle's cached CUDA graph of the pipeline; RSVD_B200_NO_GRAPH disables it),
  * "upload_aty_splits" (host-buffer solves: split count of the first power iteration's A^T Y0
- * produced during the chunked upload, 0 if that pass ran after it).
+ * produced during the chunked upload, 0 if that pass ran after it), "oz_passes" (passes over A
+ * of the last solve that ran as INT8-emulated FP64 products) and "oz_stored_passes" (of those,
+ * the ones that read A's digit planes converted once per solve).
  * Returns -1 for an unknown key. */
 long rsvd_b200_last_info(rsvd_b200_handle* h, const char* key);
 /* Force the robust path (host-checked Cholesky, Householder fallback) for every solve. */
