@@ -249,7 +249,7 @@ cudaError_t launch_gaussian_rowmajor(uint64_t seed, long rows, long cols, double
 cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
                             int* status, int* abort_flag, double tol, cudaStream_t st,
                             const double* Gref = nullptr, long ldref = 0, int sref = 0,
-                            bool accumulate = false);
+                            bool accumulate = false, int out_n = 0);  // out_n: written block (0: NP)
 int cholesky_max_width();
 // C (M x N, ldc) = alpha op(A) op(B) + beta Cin; ta/tb: operand stored transposed.
 // Cin == nullptr means Cin = C.

@@ -158,7 +158,8 @@ __device__ __forceinline__ void chol_diag_factor(double* S, int ld, int j0, doub
 __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
     const double* __restrict__ G, long ldg, int s, int NP, double* __restrict__ R,
     double* __restrict__ RinvT, int* __restrict__ status, int* __restrict__ abort_flag,
-    double tol, const double* __restrict__ Gref, long ldref, int sref, bool accumulate) {
+    double tol, const double* __restrict__ Gref, long ldref, int sref, bool accumulate,
+    int out_n) {
     extern __shared__ __align__(16) double S[];
     const int sp = chol_pad(s), ld = sp + 2;
     double* rdiag = S + (size_t)sp * ld;
@@ -316,9 +317,10 @@ __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
         __syncthreads();
         CHOL_MARK(6);
     }
-    // R[r][c] (c > r) and Rinv^T[r][c] = X[c][r] (c < r) both live at S[c][r]
-    for (int e = tid; e < NP * NP; e += nth) {
-        const int r = e / NP, c = e - r * NP;
+    // R[r][c] (c > r) and Rinv^T[r][c] = X[c][r] (c < r) both live at S[c][r]; the output is
+    // the out_n x out_n block at R / RinvT (leading dimension NP), zero outside s x s
+    for (int e = tid; e < out_n * out_n; e += nth) {
+        const int r = e / out_n, c = e - r * out_n;
         double rv = 0.0, xv = 0.0;
         if (r < s && c < s) {
             const double v = S[c * ld + r];
@@ -329,8 +331,8 @@ __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(
                 xv = v;
             }
         }
-        R[e] = rv;
-        RinvT[e] = xv;
+        R[(size_t)r * NP + c] = rv;
+        RinvT[(size_t)r * NP + c] = xv;
     }
     if (tid == 0 && !accumulate) status[0] = 0;
     CHOL_MARK(7);
@@ -349,7 +351,9 @@ int cholesky_max_width() {
 
 cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R, double* RinvT,
                             int* status, int* abort_flag, double tol, cudaStream_t st,
-                            const double* Gref, long ldref, int sref, bool accumulate) {
+                            const double* Gref, long ldref, int sref, bool accumulate,
+                            int out_n) {
+    if (out_n <= 0) out_n = NP;
     if (!Gref) {
         Gref = G;
         ldref = ldg;
@@ -361,7 +365,7 @@ cudaError_t launch_cholesky(const double* G, long ldg, int s, int NP, double* R,
         cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cholesky_kernel<<<1, kCholThreads, smem, st>>>(G, ldg, s, NP, R, RinvT, status, abort_flag, tol,
-                                                   Gref, ldref, sref, accumulate);
+                                                   Gref, ldref, sref, accumulate, out_n);
     return cudaGetLastError();
 }
 

@@ -733,31 +733,27 @@ void cholesky(const Ctx& c, int g_slot, int r_slot, int rit_slot) {
         h->launched(launch_cholesky(G, NP, s, NP, R, RiT, status, abort, tol, st), "cholesky");
         return;
     }
+    // 2 x 2 blocks: the two Cholesky CTAs write their factors straight into R / R^-T (the first
+    // one the whole NP x NP region, zeros included; the second only its s2 x s2 block)
     const int s1 = (s + 1) / 2, s2 = s - s1;
-    double *R11 = c.slot(kB1), *R11iT = c.slot(kB2), *S = c.slot(kB3), *R22 = c.slot(kB4),
-           *R22iT = c.slot(kB5);
-    h->launched(launch_fill(R, (long)NP * NP, 0.0, st), "fill");
-    h->launched(launch_fill(RiT, (long)NP * NP, 0.0, st), "fill");
-    h->launched(launch_cholesky(G, NP, s1, NP, R11, R11iT, status, abort, tol, st, G, NP, s,
-                                false),
+    double* S = c.slot(kB3);
+    double* R22 = R + (size_t)s1 * NP + s1;
+    double* R22iT = RiT + (size_t)s1 * NP + s1;
+    h->launched(launch_cholesky(G, NP, s1, NP, R, RiT, status, abort, tol, st, G, NP, s, false),
                 "cholesky");
     // R12 = R11^-T G12 -> R[0:s1, s1:s]
-    h->launched(launch_small_gemm(s1, s2, s1, 1.0, R11iT, NP, false, G + s1, NP, false, 0.0,
+    h->launched(launch_small_gemm(s1, s2, s1, 1.0, RiT, NP, false, G + s1, NP, false, 0.0,
                                   nullptr, 0, R + s1, NP, st),
                 "small_gemm");
     // S = G22 - R12^T R12
     h->launched(launch_small_gemm(s2, s2, s1, -1.0, R + s1, NP, true, R + s1, NP, false, 1.0,
                                   G + (size_t)s1 * NP + s1, NP, S, NP, st),
                 "small_gemm");
-    h->launched(launch_cholesky(S, NP, s2, NP, R22, R22iT, status, abort, tol, st, G, NP, s,
-                                true),
+    h->launched(launch_cholesky(S, NP, s2, NP, R22, R22iT, status, abort, tol, st, G, NP, s, true,
+                                s2),
                 "cholesky");
-    h->launched(launch_copy2d(R11, NP, R, NP, s1, s1, st), "copy2d");
-    h->launched(launch_copy2d(R22, NP, R + (size_t)s1 * NP + s1, NP, s2, s2, st), "copy2d");
-    h->launched(launch_copy2d(R11iT, NP, RiT, NP, s1, s1, st), "copy2d");
-    h->launched(launch_copy2d(R22iT, NP, RiT + (size_t)s1 * NP + s1, NP, s2, s2, st), "copy2d");
     // T = R12^T R11^-T (s2 x s1) into S; RiT[s1:, 0:s1] = -R22^-T T
-    h->launched(launch_small_gemm(s2, s1, s1, 1.0, R + s1, NP, true, R11iT, NP, false, 0.0,
+    h->launched(launch_small_gemm(s2, s1, s1, 1.0, R + s1, NP, true, RiT, NP, false, 0.0,
                                   nullptr, 0, S, NP, st),
                 "small_gemm");
     h->launched(launch_small_gemm(s2, s1, s2, -1.0, R22iT, NP, false, S, NP, false, 0.0, nullptr,
