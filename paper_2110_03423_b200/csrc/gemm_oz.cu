@@ -234,7 +234,8 @@ __device__ __forceinline__ void fixed_scale(int ef_max, double& f1, double& f2) 
 }
 
 // digits_of with the scale applied on the FP64 pipe: (x f1) f2 is x 2^(53 - E) exactly, and
-// the conversion rounds it to the nearest integer X (the same X as the integer path above).
+// the conversion rounds it to the nearest integer X (ties to even, where the integer path above
+// rounds ties away from zero; the same X otherwise).
 __device__ __forceinline__ uint64_t digits_scaled(double x, double f1, double f2) {
     const long long X = __double2ll_rn((x * f1) * f2);
     return (uint64_t)X + kDigitBias;  // the bias XOR is applied to the packed plane words
@@ -715,25 +716,35 @@ __global__ void __launch_bounds__(256) oz_digits_cols_kernel(const double* __res
                                                             int* __restrict__ b_ef,
                                                             const int* __restrict__ row_ef,
                                                             int nfirst) {
-    extern __shared__ double slab[];  // 64 x (NP + 1)
-    const long k0 = (long)blockIdx.x * 64;
-    const int ld = NP + 1;
-    for (int e = threadIdx.x; e < 64 * NP; e += 256) {
-        const int kk = e / NP, c = e - kk * NP;
-        const long k = k0 + kk;
-        slab[kk * ld + c] = (k < K && c < cols) ? W[k * ldw + c] * row_scale(row_ef, k) : 0.0;
+    // one k-tile (32 rows of W) per CTA; the slab is column-major (33-double stride) so that
+    // every thread's 4 consecutive k of one column are contiguous, and the row scales of W' are
+    // read once per row (the digits keep the integer path's rounding: ties away from zero)
+    extern __shared__ double slab[];  // NP x 33
+    __shared__ double rs[32];
+    constexpr int ld = 33;
+    const long k0 = (long)blockIdx.x * 32;
+    if (threadIdx.x < 32) {
+        const long k = k0 + threadIdx.x;
+        rs[threadIdx.x] = k < K ? row_scale(row_ef, k) : 0.0;
     }
     if (blockIdx.x == 0)
         for (int c = threadIdx.x; c < NP; c += 256) b_ef[c] = colmax[c] >> 20;
     __syncthreads();
-    // thread -> (c, 4 consecutive k): 16 k-quads per column
-    for (int e = threadIdx.x; e < NP * 16; e += 256) {
-        const int c = e >> 4, kq = (e & 15) * 4;
+    for (int e = threadIdx.x; e < 32 * NP; e += 256) {
+        const int kk = e / NP, c = e - kk * NP;
+        const long k = k0 + kk;
+        slab[c * ld + kk] = (k < K && c < cols) ? W[k * ldw + c] * rs[kk] : 0.0;
+    }
+    __syncthreads();
+    // thread -> (column c, 4 consecutive k): 8 k-quads per column; a warp writes 4 columns'
+    // 32-byte rows of each plane
+    for (int e = threadIdx.x; e < NP * 8; e += 256) {
+        const int c = e >> 3, kq = (e & 7) * 4;
         if (k0 + kq >= ldb) continue;
         const int ef = colmax[c] >> 20;
         uint64_t w[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = digits_of(slab[(kq + j) * ld + c], ef);
+        for (int j = 0; j < 4; ++j) w[j] = digits_of(slab[c * ld + kq + j], ef);
         uint32_t pl[kDigits];
         planes4(w, pl);
 #pragma unroll
@@ -1469,12 +1480,12 @@ cudaError_t launch_oz_digits_cols(const double* W, long ldw, int NP, int cols, l
     if (e != cudaSuccess) return e;
     oz::oz_colmax_kernel<<<(unsigned)std::min<long>(148L * 8, (K + 3) / 4), 256, 0, st>>>(
         W, ldw, NP, cols, K, colmax, row_ef);
-    const size_t smem = 64 * (NP + 1) * sizeof(double);
+    const size_t smem = (size_t)NP * 33 * sizeof(double);
     e = cudaFuncSetAttribute(oz::oz_digits_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
     const long ldb = oz_ldb(K);
-    oz::oz_digits_cols_kernel<<<(unsigned)((ldb + 63) / 64), 256, smem, st>>>(
+    oz::oz_digits_cols_kernel<<<(unsigned)((ldb + 31) / 32), 256, smem, st>>>(
         W, ldw, NP, cols, K, dig, ldb, colmax, b_ef, row_ef, nfirst);
     return cudaGetLastError();
 }
