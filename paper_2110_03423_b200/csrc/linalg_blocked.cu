@@ -34,8 +34,8 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 // C (M x N, ldc) = alpha * op(A) op(B) + beta * Cin (ldcin); op(A) is M x K,
 // op(B) K x N; ta / tb: the operand is stored transposed (row-major K x M / N x K).
 // Cin may alias C (each element is read before it is written by the same thread).
-// 16 x 16 output tiles (one output per thread, so an s = 136 block spans 81 CTAs), K in
-// chunks of 32; both operand tiles are loaded along their contiguous dimension whatever the
+// 16 x 16 output tiles (one output per thread, so an s = 136 block spans 81 CTAs), K in chunks
+// of up to 144; both operand tiles are loaded along their contiguous dimension whatever the
 // transposition (coalesced), and transposed on the way into shared memory.
 __global__ void __launch_bounds__(256) small_gemm_kernel(int M, int N, int K, double alpha,
                                                          const double* __restrict__ A, long lda,
@@ -43,31 +43,39 @@ __global__ void __launch_bounds__(256) small_gemm_kernel(int M, int N, int K, do
                                                          long ldb, bool tb, double beta,
                                                          const double* Cin, long ldcin,
                                                          double* C, long ldc) {
-    __shared__ double As[16][33];  // As[r][k] = op(A)[i0 + r][k0 + k]
-    __shared__ double Bs[32][17];  // Bs[k][c] = op(B)[k0 + k][j0 + c]
+    // K in chunks of up to 144 (the blocked Cholesky's 136-wide products in one chunk: one
+    // load phase and one barrier instead of five 32-wide rounds), two accumulators
+    constexpr int KC = 144;
+    __shared__ double As[16][KC + 1];  // As[r][k] = op(A)[i0 + r][k0 + k]
+    __shared__ double Bs[KC][17];      // Bs[k][c] = op(B)[k0 + k][j0 + c]
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int i0 = blockIdx.y * 16, j0 = blockIdx.x * 16;
-    double acc = 0.0;
-    for (int k0 = 0; k0 < K; k0 += 32) {
-#pragma unroll
-        for (int e = tid; e < 512; e += 256) {
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int k0 = 0; k0 < K; k0 += KC) {
+        const int kc = min(KC, K - k0);
+        // both operands loaded along their contiguous dimension (coalesced)
+        for (int e = tid; e < 16 * kc; e += 256) {
             int r, k;
-            if (ta) { k = e >> 4; r = e & 15; } else { r = e >> 5; k = e & 31; }
+            if (ta) { k = e >> 4; r = e & 15; } else { r = e / kc; k = e - r * kc; }
             const int i = i0 + r, kk = k0 + k;
-            As[r][k] = (i < M && kk < K) ? (ta ? A[(long)kk * lda + i] : A[(long)i * lda + kk]) : 0.0;
+            As[r][k] = i < M ? (ta ? A[(long)kk * lda + i] : A[(long)i * lda + kk]) : 0.0;
             int c, kb;
-            if (tb) { c = e >> 5; kb = e & 31; } else { kb = e >> 4; c = e & 15; }
+            if (tb) { c = e / kc; kb = e - c * kc; } else { kb = e >> 4; c = e & 15; }
             const int j = j0 + c, kj = k0 + kb;
-            Bs[kb][c] = (kj < K && j < N) ? (tb ? B[(long)j * ldb + kj] : B[(long)kj * ldb + j]) : 0.0;
+            Bs[kb][c] = j < N ? (tb ? B[(long)j * ldb + kj] : B[(long)kj * ldb + j]) : 0.0;
         }
         __syncthreads();
-#pragma unroll 8
-        for (int kk = 0; kk < 32; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
+        int kk = 0;
+        for (; kk + 1 < kc; kk += 2) {
+            acc0 = fma(As[ty][kk], Bs[kk][tx], acc0);
+            acc1 = fma(As[ty][kk + 1], Bs[kk + 1][tx], acc1);
+        }
+        if (kk < kc) acc0 = fma(As[ty][kk], Bs[kk][tx], acc0);
         __syncthreads();
     }
     const int i = i0 + ty, j = j0 + tx;
     if (i < M && j < N) {
-        double v = alpha * acc;
+        double v = alpha * (acc0 + acc1);
         if (beta != 0.0) v += beta * Cin[(long)i * ldcin + j];
         C[(long)i * ldc + j] = v;
     }
