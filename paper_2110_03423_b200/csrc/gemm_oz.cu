@@ -14,25 +14,32 @@
 // tile needs 7 accumulators of N columns in TMEM. Error: the fixed-point rounding of each
 // operand (2^-54 of the row / column maximum) plus the truncation, i.e. the normwise error of
 // an FP64 GEMM (measured against an exact long-double product: Frobenius-relative 1.1e-15
-// against 6.6e-16 for FP64 BLAS on the C2 operand shapes, tools/probe/ozaki_model.py), with no
+// against 6.6e-16 for FP64 BLAS on the C2 operand shapes, tests/test_gpu_oz.py), with no
 // rounding at all along K.
 //
 // Shapes (the two the FP64 path has):
 //   ax  : Y (M x NP) = A (M x K row-major) X, per-row scales of A (a_ef[M]); X as digit
 //         planes of X^T (NP x K) with per-column scales (b_ef[NP]).
-//   atx : Z = A^T W, A (K x M row-major) read in place; per-column scales of A (a_ef over the
-//         M = A's columns); W as digit planes of W^T (NP x K). Output Z^T (NP x M) or Z.
-// The digits of A are formed in shared memory by converter warps from the FP64 tile TMA
-// brought in (never stored in HBM: A is read exactly once per pass, like the DMMA kernels);
-// the digits of the small operand come from a prep kernel (launch_oz_digits_*).
+//   atx : Z = A^T W, A (K x M row-major) read in place; W as digit planes of W^T (NP x K).
+//         Output Z^T (NP x M) or Z.
+// Two forms of A's digits:
+//   * stored (the optimistic pipeline's default, gemm_ozd_kernel): one pass over A per row
+//     chunk (oz_scan_convert_kernel, or oz_scan + oz_convert_tiles for rows wider than 4608)
+//     writes A's row-scaled digits pre-tiled for both shapes, and every pass bulk-copies them
+//     (no FP64 tile, no conversion in the GEMM). The atx shape folds A's row scales into W
+//     (W' = diag(2^(E_k - 53)) W, exact powers of two).
+//   * in-kernel (gemm_oz_kernel: the robust rerun, or when the stored planes do not fit HBM):
+//     converter warps form the digits of the TMA'd FP64 tile and write them straight into TMEM
+//     for TS MMAs; per-column scales of A for the atx shape (oz_scan).
+// The small operand's digits come from a prep kernel (launch_oz_digits_*).
 //
-// TMEM holds 7 x N int32 columns, so N <= 64 per CTA: wider sketches are split into column
-// chunks of <= 64 whose CTAs are adjacent in the grid (both read the same A tile, the second
-// from L2). CTA = 6 warps: warp 0 TMA, warp 1 TMEM owner + MMA issuer (one lane), warps 2-5
-// converters (one A row / column each) and epilogue (one TMEM lane each).
-// UMMA operands: K-major, SWIZZLE_32B (rows of 32 int8 = one K = 32 MMA step, 8-row atoms of
-// 256 B, 16-byte chunk c of row r stored at chunk c ^ ((r >> 2) & 1)) for both the digits
-// written by the converters and the B digits TMA writes with CU_TENSOR_MAP_SWIZZLE_32B.
+// TMEM holds 7 x N int32 accumulator columns (plus, in-kernel, the A-digit buffers), so N <= 48
+// per CTA: wider sketches run as column chunks of <= 48 whose CTAs share the A tile (stored:
+// cluster multicast of the digit blocks; in-kernel: L2). MMAs: the 28 digit products issued as
+// 9 wide MMAs (digit i of A against B's planes 6 - i .. 6 laid out back to back), one elected
+// lane of a converged warp issuing. UMMA operands: K-major SWIZZLE_32B (rows of 32 int8 = one
+// K = 32 MMA step, 8-row atoms of 256 B, 16-byte chunk c of row r stored at chunk
+// c ^ ((r >> 2) & 1)); the stored atx blocks are MN-major SWIZZLE_128B.
 #include <stdlib.h>
 
 #include <algorithm>
