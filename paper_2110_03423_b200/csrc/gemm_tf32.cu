@@ -19,13 +19,15 @@
 // FP32 epilogue below writes it next to every tall FP32 output, cvt_f64_f32 for the
 // small operands); only A's lo part is formed in shared memory.
 //
-// CTA = 6 warps: warp 0 issues TMA, warp 1 owns the TMEM allocation and one elected
-// lane issues the MMAs (M = 128, N = NP in chunks of at most 256), warps 2-5 form A_lo
-// (and scan A for NaN/Inf when asked), then drain the accumulator (tcgen05.ld 32x32b)
-// in the epilogue. Four pipeline stages of K = 16; per stage the MMA issuer runs the two
-// products that need no conversion (a b, a b_lo) as soon as TMA lands and the third
-// (a_lo b) once the converters signal, so the conversion hides behind 2/3 of the math.
-// mbarriers: full (TMA tx), conv (4 converter warps), empty (tcgen05.commit), accum.
+// CTA = 6 warps: warp 0 issues TMA, warp 1 owns the TMEM allocation and issues the MMAs
+// (M = 128, N = NP in chunks of at most 256), warps 2-5 split A (and scan it for NaN/Inf when
+// asked), then drain the accumulator (tcgen05.ld 32x32b) in the epilogue. Four pipeline
+// stages of K = 16. Default (TS): the converter warps write A and A_lo into a TMEM buffer per
+// stage and all three products read A from TMEM, so shared memory carries only the TMA writes
+// and the B reads (profiles/r2_ncu_tf32_ts.md). The shared-memory form (RSVD_B200_TF32_SS)
+// writes A_lo next to A in the stage and runs a b, a b_lo as soon as TMA lands and a_lo b
+// once the converters signal. mbarriers: full (TMA tx), conv (4 converter warps), empty
+// (tcgen05.commit), accum.
 //
 // UMMA shared-memory descriptors (version 1):
 //   K-major : SWIZZLE_64B (layout 4): rows of 64 B (16 fp32 along K), 8-row atoms of
