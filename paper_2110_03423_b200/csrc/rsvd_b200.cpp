@@ -11,15 +11,19 @@
 //   B      = Q^T A; (U_B, sigma, V) = svd(B); U = Q U_B[:, :k]    (rsvd.cpp:89-109)
 // with these B200 substitutions:
 //   * every product is a TMA-fed FP64 tensor-core GEMM (gemm_f64.cu) reading A
-//     in place (no transposed copy); split-K partials are reduced in fixed order;
+//     in place (no transposed copy); split-K partials are reduced in fixed order.
+//     For A with at least 2^26 elements the passes over A run as exact INT8 digit
+//     products on tcgen05 (gemm_oz.cu, Ozaki scheme): on the optimistic path from A's
+//     digit planes converted once per solve, on the robust rerun with in-kernel digits;
+//     FP32 A runs every m-sized product as 3xTF32 on tcgen05 (gemm_tf32.cu);
 //   * thin QR is CholeskyQR2 (Gram by the same GEMMs, s x s Cholesky in shared
-//     memory, TRSM as a GEMM against R^-1), with the unblocked Householder QR
-//     (householder.cu, the reference's own algorithm) as the fallback when a
-//     Cholesky pivot signals an ill-conditioned input;
+//     memory, TRSM as a GEMM against R^-1), with a blocked Householder QR
+//     (householder.cu, the reference's algorithm in compact-WY panels) as the
+//     fallback when a Cholesky pivot signals an ill-conditioned input;
 //   * the SVD of the s x n matrix B runs as CholeskyQR2 of B^T = Q_B R_B followed
-//     by one-sided Jacobi on the s x s R_B in shared memory (same rotation rule and
-//     thresholds as svd.cpp), V = Q_B U_R, U_B = W_R, then the reference's sort and
-//     sign convention.
+//     by one-sided Jacobi on the s x s R_B (one CTA, a thread-block cluster, or a
+//     cooperative block Jacobi by width; same rotation rule and thresholds as
+//     svd.cpp), V = Q_B U_R, U_B = W_R, then the reference's sort and sign convention.
 // range_basis inside the pipeline: power_iterate always returns orthonormal
 // columns (Householder or CholeskyQR2 Q), whose R factor has |R_jj| = 1 + O(eps),
 // so the drop rule |R_jj| <= 1e-13 ||W||_F (<= 1e-13 sqrt(s)) can never fire and
