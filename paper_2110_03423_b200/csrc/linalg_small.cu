@@ -1,5 +1,5 @@
-// Small dense linear algebra on the (k+p) x (k+p) side of the rSVD, one CTA each,
-// operands held in shared memory:
+// Small dense linear algebra on the (k+p) x (k+p) side of the rSVD, one CTA (or, for the
+// Jacobi at 64 < s <= 112, one thread-block cluster) each, operands held in shared memory:
 //   * Cholesky of a Gram matrix + the triangular inverse (CholeskyQR, replaces the
 //     reference's Householder QR, qr.cpp:27-102, on the well-conditioned path),
 //   * one-sided Jacobi SVD of the small triangular factor R_B of B^T (replaces the
